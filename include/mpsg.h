@@ -1,0 +1,168 @@
+/*
+ * mpsg.h — C ABI of the B200-native MPS sampling sweep (FastMPS, arxiv 2512.20064).
+ *
+ * This is the drop-in boundary for the reference's sampling entry point.  The reference
+ * (`mpsamp`, a C++20 library) has no FFI of its own; what a maintainer binds is
+ *
+ *   SampleBatch mpsamp::sample_batch(const MpsState&, const BatchPlan&, const SamplerOptions&,
+ *                                    RunStats* = nullptr)             proj/include/mpsamp/sampler.hpp:84-85
+ *   void mpsamp::detail::sample_micro_serial(const MpsState&, uint64_t first, size_t count,
+ *                                            const SamplerOptions&, uint8_t* rows, RunStats&)
+ *                                                                     proj/include/mpsamp/sampler.hpp:103-104
+ *
+ * Every entry point below replaces one of those (or one of the pieces the reference's
+ * executors re-drive, sampler.hpp:98-102), takes only plain pointers and sizes, and returns an
+ * error code that maps 1:1 onto the reference's exception hierarchy (errors.hpp:8-27):
+ *
+ *   MPSG_OK 0, MPSG_ERR_CONFIG 2 (ConfigError / DimensionError), MPSG_ERR_NUMERIC 3
+ *   (NumericError), MPSG_ERR_IO 4 (IoError), MPSG_ERR_CUDA 5 (CUDA / NCCL failure),
+ *   MPSG_ERR_INTERNAL 1.  mpsg_last_error() returns the thread-local message.
+ *
+ * Data layouts are the reference's, unchanged (tensor.hpp:56-61, mps.hpp:10-19):
+ *   gamma[i]  complex128 interleaved (re, im), shape (bond[i], bond[i+1], d) row-major, d fastest
+ *   lambda[i] float64, length bond[i+1], nonnegative and nonincreasing
+ *   rows      uint8, count x num_sites row-major (stride num_sites), 0xFF = dead sample
+ *   draws     keyed splitmix64 (rng.hpp:12-37), key(seed, 0x6d656173, global sample, site)
+ *
+ * The library is CUDA-only (sm_100a).  There is no CPU fallback: on a host without a B200 every
+ * compute entry point returns MPSG_ERR_CUDA.
+ */
+#ifndef MPSG_H
+#define MPSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPSG_ABI_VERSION 1
+
+enum {
+  MPSG_OK = 0,
+  MPSG_ERR_INTERNAL = 1,
+  MPSG_ERR_CONFIG = 2,
+  MPSG_ERR_NUMERIC = 3,
+  MPSG_ERR_IO = 4,
+  MPSG_ERR_CUDA = 5
+};
+
+/* Precision / ScalingMode values are the reference's enums (precision.hpp:15-17). */
+enum { MPSG_F64 = 0, MPSG_F32 = 1, MPSG_TF32 = 2, MPSG_F16 = 3 };
+enum { MPSG_SCALE_NONE = 0, MPSG_SCALE_GLOBAL_MAX = 1, MPSG_SCALE_PER_SAMPLE_MAX = 2 };
+
+/* GPU contraction schemes:
+ *   MPSG_MODE_SPLIT   fp16 Gamma x (hi + lo) fp16 environment, fp32 accumulate; F32-class
+ *                     accuracy, 2x issued MMAs.  Used for compute = F64 / F32.
+ *   MPSG_MODE_SINGLE  fp16 Gamma x fp16 environment, one MMA pass; F16-class accuracy.
+ *                     Used for compute = TF32 / F16.
+ *   MPSG_MODE_AUTO    pick from policy.compute. */
+enum { MPSG_MODE_AUTO = 0, MPSG_MODE_SPLIT = 1, MPSG_MODE_SINGLE = 2 };
+
+#define MPSG_DEAD 0xFF
+
+/* Mirrors mpsamp::MpsState (mps.hpp:14-22) as plain pointers into caller-owned memory. */
+typedef struct mpsg_mps_view {
+  uint64_t num_sites;              /* M */
+  uint64_t phys_dim;               /* d */
+  const uint64_t* bond_dims;       /* M + 1, boundaries 1 */
+  const double* const* gamma;      /* M pointers, complex128 interleaved (chiL, chiR, d) */
+  const double* const* lambda;     /* M pointers, length bond_dims[i + 1] */
+} mpsg_mps_view;
+
+/* Mirrors mpsamp::PrecisionPolicy (precision.hpp:27-33). */
+typedef struct mpsg_policy {
+  int compute;                     /* MPSG_F64 .. MPSG_F16 */
+  int storage;                     /* MPSG_F64 / F32 / F16 (TF32 rejected, precision.cpp:98-102) */
+  int scaling;                     /* MPSG_SCALE_* */
+} mpsg_policy;
+
+/* Engine options (no reference counterpart; zero-initialise for defaults). */
+typedef struct mpsg_options {
+  int mode;                        /* MPSG_MODE_*, default AUTO */
+  uint64_t pass_samples;           /* samples per device pass (the GEMM M extent); 0 = auto */
+  int record_site_times;           /* fill mpsg_stats.site_seconds (adds one event per site) */
+  int reserved[5];
+} mpsg_options;
+
+/* Mirrors mpsamp::RunStats + FlopCounters (sampler.hpp:46-54, contract.hpp:12-25). */
+typedef struct mpsg_stats {
+  uint64_t contraction_macs;       /* sum_i count * chiL_i * chiR_i * d (contract.cpp:97-100) */
+  uint64_t measure_weight_macs;    /* sum_i count * chiR_i * d (sampler.cpp:113-116) */
+  uint64_t dead_samples;
+  double seconds;                  /* wall time of the call */
+  double* site_seconds;            /* optional caller array of length M (device time per site) */
+  uint64_t issued_mma_flops;       /* real flops issued to the tensor cores (incl. padding, split) */
+  uint64_t h2d_bytes, d2h_bytes;
+} mpsg_stats;
+
+typedef struct mpsg_handle_s* mpsg_handle;
+
+/* ---- library -------------------------------------------------------------------------- */
+int mpsg_abi_version(void);
+const char* mpsg_last_error(void);
+/* Number of visible sm_100 devices (0 when none; never an error). */
+int mpsg_device_count(void);
+
+/* ---- state ----------------------------------------------------------------------------- */
+/* Validates like MpsState::validate (mps.cpp:12-38) and PrecisionPolicy::validate
+ * (precision.cpp:98-102), rejects non-finite Gamma like contract_site at F64
+ * (contract.cpp:117-119), compresses every site to the device format (fp16 planes with
+ * power-of-two row/column scales) and keeps it resident on each listed device (data-parallel
+ * replicas).  devices == NULL / ndev == 0 means device 0. */
+int mpsg_create(const mpsg_mps_view* mps, const mpsg_policy* policy, const mpsg_options* opts,
+                const int* devices, int ndev, mpsg_handle* out);
+
+/* Incremental builder for states too large for host memory (e.g. generated on the device).
+ * gamma may be a host pointer or a device pointer on the first listed device; dtype is
+ * MPSG_F64 (complex128) or MPSG_F32 (complex64). */
+int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bond_dims,
+                       const mpsg_policy* policy, const mpsg_options* opts, const int* devices,
+                       int ndev, mpsg_handle* out);
+int mpsg_builder_set_site(mpsg_handle h, uint64_t site, const void* gamma, int gamma_is_device,
+                          int dtype, const double* lambda);
+int mpsg_builder_finish(mpsg_handle h);
+
+void mpsg_destroy(mpsg_handle h);
+
+/* Device bytes held for the compressed state on one device (algorithmic Gamma bytes). */
+uint64_t mpsg_state_bytes(mpsg_handle h);
+
+/* The Gamma values the GPU actually samples (decoded compressed format), reference layout:
+ * complex128 interleaved (chiL, chiR, d).  The CPU oracle consumes these. */
+int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out);
+
+/* ---- sampling: replaces sample_batch / sample_micro_serial ------------------------------ */
+/* Samples global indices [first, first + count) with measurement seed `seed` and writes
+ * rows (count x M, host memory).  Equivalent to detail::sample_micro_serial over that range
+ * (sampler.cpp:129-162); with first = 0, count = N it is sample_batch (sampler.cpp:164-205)
+ * for any BatchPlan, since outcomes are keyed by global sample index.  Work is split across
+ * the handle's devices (one host thread each). */
+int mpsg_sample(mpsg_handle h, uint64_t seed, uint64_t first, uint64_t count, uint8_t* rows,
+                mpsg_stats* stats);
+
+/* Same, writing into device memory on the first listed device (no D2H). */
+int mpsg_sample_device(mpsg_handle h, uint64_t seed, uint64_t first, uint64_t count,
+                       uint8_t* rows_dev, mpsg_stats* stats);
+
+/* Teacher-forced per-site marginals: walks the GPU sweep along the given outcome strings
+ * (count x M, 0xFF = dead) and writes p[n, i, k] = w[n,k] / sum_k w[n,k] (sampler.cpp:83-100)
+ * as float64 count x M x d (-1 for dead).  Used for the 1e-4 marginal parity check. */
+int mpsg_marginals(mpsg_handle h, uint64_t first, uint64_t count, const uint8_t* forced,
+                   double* marg);
+
+/* The device RNG: draws[j] = uniform(seed, 0x6d656173, first + j, site) computed by the GPU
+ * (detail::measurement_draws, sampler.cpp:120-127). */
+int mpsg_device_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, double* out);
+
+/* One contraction through the tcgen05 GEMM (contract_site, contract.cpp:109-121): env is
+ * complex128 (count, chiL) in the reference scaling; temp receives complex128
+ * (count, chiR, d) in the same scaling.  Exposed for numerics tests. */
+int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t count,
+                       double* temp);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPSG_H */

@@ -1,0 +1,29 @@
+"""B200-native MPS sampling sweep (FastMPS, arxiv 2512.20064).
+
+The hot path — contract L[N, chi] x Gamma_i, Born weights, keyed draw, gather + renormalise — runs
+in hand-written sm_100a kernels (libmpsg.so, tcgen05/TMEM/TMA) behind the C ABI in
+include/mpsg.h.  This package is the host-side mirror of the reference's ``mpsamp`` interface.
+"""
+from .sampler import (  # noqa: F401
+    DEAD_OUTCOME,
+    BatchPlan,
+    ConfigError,
+    DeviceError,
+    DimensionError,
+    Error,
+    GpuSampler,
+    IoError,
+    Mode,
+    MpsState,
+    NumericError,
+    Precision,
+    PrecisionPolicy,
+    RunStats,
+    SampleBatch,
+    SamplerOptions,
+    ScalingMode,
+    capped_bond_dims,
+    device_draws,
+    sample_batch,
+    sample_micro_serial,
+)

@@ -1,0 +1,89 @@
+"""ctypes binding of libmpsg.so (include/mpsg.h).  The CUDA library is the only compute path:
+if it is missing or no B200 is visible, calls fail loudly — there is no CPU fallback."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmpsg.so")
+
+MPSG_OK, MPSG_ERR_INTERNAL, MPSG_ERR_CONFIG, MPSG_ERR_NUMERIC, MPSG_ERR_IO, MPSG_ERR_CUDA = 0, 1, 2, 3, 4, 5
+
+_u64, _int, _dbl = C.c_uint64, C.c_int, C.c_double
+_pd = C.POINTER(C.c_double)
+_pu8 = C.POINTER(C.c_uint8)
+_pu64 = C.POINTER(C.c_uint64)
+
+
+class MpsView(C.Structure):
+    _fields_ = [("num_sites", _u64), ("phys_dim", _u64), ("bond_dims", _pu64),
+                ("gamma", C.POINTER(_pd)), ("lambda_", C.POINTER(_pd))]
+
+
+class Policy(C.Structure):
+    _fields_ = [("compute", _int), ("storage", _int), ("scaling", _int)]
+
+
+class Options(C.Structure):
+    _fields_ = [("mode", _int), ("pass_samples", _u64), ("record_site_times", _int),
+                ("reserved", _int * 5)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("contraction_macs", _u64), ("measure_weight_macs", _u64), ("dead_samples", _u64),
+                ("seconds", _dbl), ("site_seconds", _pd), ("issued_mma_flops", _u64),
+                ("h2d_bytes", _u64), ("d2h_bytes", _u64)]
+
+
+# (name, restype, argtypes) for every entry point of include/mpsg.h
+SIGNATURES = [
+    ("mpsg_abi_version", _int, []),
+    ("mpsg_last_error", C.c_char_p, []),
+    ("mpsg_device_count", _int, []),
+    ("mpsg_create", _int, [C.POINTER(MpsView), C.POINTER(Policy), C.POINTER(Options),
+                           C.POINTER(_int), _int, C.POINTER(C.c_void_p)]),
+    ("mpsg_builder_begin", _int, [_u64, _u64, _pu64, C.POINTER(Policy), C.POINTER(Options),
+                                  C.POINTER(_int), _int, C.POINTER(C.c_void_p)]),
+    ("mpsg_builder_set_site", _int, [C.c_void_p, _u64, C.c_void_p, _int, _int, _pd]),
+    ("mpsg_builder_finish", _int, [C.c_void_p]),
+    ("mpsg_destroy", None, [C.c_void_p]),
+    ("mpsg_state_bytes", _u64, [C.c_void_p]),
+    ("mpsg_decoded_gamma", _int, [C.c_void_p, _u64, _pd]),
+    ("mpsg_sample", _int, [C.c_void_p, _u64, _u64, _u64, _pu8, C.POINTER(Stats)]),
+    ("mpsg_sample_device", _int, [C.c_void_p, _u64, _u64, _u64, C.c_void_p, C.POINTER(Stats)]),
+    ("mpsg_marginals", _int, [C.c_void_p, _u64, _u64, _pu8, _pd]),
+    ("mpsg_device_draws", _int, [_u64, _u64, _u64, _u64, _pd]),
+    ("mpsg_contract_site", _int, [C.c_void_p, _u64, _pd, _u64, _pd]),
+]
+
+_lib = None
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", os.path.join(HERE, "csrc")], check=True)
+
+
+def lib():
+    """Load the in-tree libmpsg.so (building it if a toolchain is present)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            try:
+                build()
+            except Exception as e:  # pragma: no cover
+                raise RuntimeError(f"libmpsg.so missing and could not be built: {e}") from e
+        L = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        if L.mpsg_abi_version() != 1:
+            raise RuntimeError("libmpsg ABI mismatch")
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().mpsg_last_error().decode(errors="replace")

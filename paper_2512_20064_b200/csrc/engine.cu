@@ -1,0 +1,782 @@
+// Host runtime of the B200 sampling sweep and the C ABI declared in include/mpsg.h.
+//
+// One handle holds the compressed MPS resident on each listed device (data-parallel replicas,
+// the reference's run_data_parallel, parallel.cpp:240-330, without the per-site broadcast since
+// every replica keeps the whole chain in HBM).  mpsg_sample splits [first, first+count) into
+// contiguous per-device ranges, each driven by its own host thread and CUDA stream; per device the
+// range is cut into passes of `cap` samples and each pass runs the site loop of
+// detail::sample_micro_serial (sampler.cpp:129-162) as two kernels per site:
+//   K1 site_gemm (tcgen05 contraction + fused weight/max epilogue), K2 select (draw, CDF, gather,
+//   renormalise, split).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/mpsg.h"
+#include "sweep.cuh"
+
+namespace mpsg {
+
+// ---------------------------------------------------------------------------------------------
+// errors (errors.hpp:8-27 mapped to codes)
+// ---------------------------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+static thread_local std::string g_last_error;
+
+#define CUDA_OK(expr)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw Error(MPSG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+static void config_check(bool ok, const std::string& msg) {
+  if (!ok) throw Error(MPSG_ERR_CONFIG, msg);
+}
+
+// ---------------------------------------------------------------------------------------------
+// TMA descriptor encoding through the driver entry point (no -lcuda link dependency)
+// ---------------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) throw Error(MPSG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// fp16 matrix [rows][cols] (cols contiguous), box 32 cols x 128 rows, 64 B swizzle.
+static CUtensorMap make_tma_2d(const void* base, uint64_t cols, uint64_t rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(kBM)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(MPSG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
+// ---------------------------------------------------------------------------------------------
+// power-of-two bond scales gamma_i[r] ~ Lambda_i[r]
+// ---------------------------------------------------------------------------------------------
+static double pow2_near(double x) {
+  int e;
+  std::frexp(x, &e);  // x = f 2^e, f in [0.5,1)
+  e = std::max(-60, std::min(60, e - 1));
+  return std::ldexp(1.0, e);
+}
+static std::vector<double> bond_scales(const double* lambda, size_t n) {
+  std::vector<double> g(n, 1.0);
+  double last = 1.0;
+  for (size_t r = 0; r < n; ++r) {
+    if (lambda[r] > 0.0 && std::isfinite(lambda[r])) last = pow2_near(lambda[r]);
+    g[r] = last;
+  }
+  return g;
+}
+
+// ---------------------------------------------------------------------------------------------
+// state
+// ---------------------------------------------------------------------------------------------
+struct SiteDev {
+  int chil = 0, chir = 0, kp = 0, chirp = 0, np = 0, nt = 0;
+  __half* g = nullptr;       // [2][np][kp]
+  float2* cinfo = nullptr;   // [np]
+  double* cs = nullptr;      // [chir * d]
+  CUtensorMap tma_g{}, tma_env{};
+};
+
+struct DevCtx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::vector<SiteDev> sites;
+  int cap = 0;               // pass capacity (rows), multiple of 128
+  __half* env = nullptr;     // [4][cap][kmax]
+  float2* temp = nullptr;    // [cap][d][chirp_max]
+  float2* pstat = nullptr;   // [cap][nt_max]
+  uint8_t* alive = nullptr;  // [cap]
+  uint8_t* rows = nullptr;   // [cap][M]
+  uint8_t* forced = nullptr; // [cap][M] (lazy)
+  double* marg = nullptr;    // [cap][M][d] (lazy)
+  double* scratch = nullptr; // compress: gl, gr, wl
+  void* src = nullptr;       // compress staging (device)
+  size_t src_bytes = 0;
+  int* err = nullptr;
+  uint8_t* host_rows = nullptr;  // pinned [cap][M]
+  std::vector<cudaEvent_t> ev;
+};
+
+}  // namespace mpsg
+
+struct mpsg_handle_s {
+  uint64_t M = 0, d = 0;
+  std::vector<uint64_t> bonds;
+  mpsg_policy policy{};
+  mpsg_options opts{};
+  bool split = true;
+  std::vector<std::vector<double>> gl, gr;  // per site: left / right bond scales
+  std::vector<mpsg::DevCtx> devs;
+  std::vector<char> site_set;
+  bool finished = false;
+  std::mutex mu;
+};
+
+namespace mpsg {
+
+static int kmax_of(const mpsg_handle_s& h) {
+  int k = kBK;
+  for (uint64_t b : h.bonds) k = std::max(k, round_up(static_cast<int>(b), kBK));
+  return k;
+}
+static int chirp_max_of(const mpsg_handle_s& h) {
+  int c = kBN;
+  for (uint64_t i = 1; i <= h.M; ++i) c = std::max(c, round_up(static_cast<int>(h.bonds[i]), kBN));
+  return c;
+}
+
+static void validate_shape(uint64_t m, uint64_t d, const uint64_t* bonds) {
+  // MpsState::validate (mps.cpp:12-20) + GPU-path limits
+  config_check(m > 0, "mps has no sites");
+  config_check(d >= 1, "mps physical dimension must be >= 1");
+  config_check(d <= 254, "phys_dim must fit the u8 outcome encoding (<= 254)");
+  config_check(bonds != nullptr, "bond_dims is null");
+  config_check(bonds[0] == 1 && bonds[m] == 1, "boundary bonds must be 1");
+  for (uint64_t i = 0; i <= m; ++i) {
+    config_check(bonds[i] >= 1, "bond dimensions must be >= 1");
+    config_check(bonds[i] <= (1u << 20), "bond dimension too large for the device format");
+  }
+}
+
+static void validate_policy(const mpsg_policy& p) {
+  config_check(p.compute >= MPSG_F64 && p.compute <= MPSG_F16, "unknown compute precision");
+  config_check(p.storage >= MPSG_F64 && p.storage <= MPSG_F16, "unknown storage precision");
+  // PrecisionPolicy::validate (precision.cpp:98-102)
+  config_check(p.storage != MPSG_TF32, "storage precision must be one of f64/f32/f16");
+  config_check(p.scaling >= MPSG_SCALE_NONE && p.scaling <= MPSG_SCALE_PER_SAMPLE_MAX,
+               "unknown scaling mode");
+}
+
+static void validate_lambda(const double* lam, size_t n) {
+  // mps.cpp:30-36
+  for (size_t j = 0; j < n; ++j) {
+    if (lam[j] < 0.0) throw Error(MPSG_ERR_NUMERIC, "lambda entries must be nonnegative");
+    if (j > 0 && lam[j] > lam[j - 1])
+      throw Error(MPSG_ERR_NUMERIC, "lambda vectors must be nonincreasing");
+  }
+}
+
+static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
+  CUDA_OK(cudaSetDevice(dc.device));
+  int major = 0;
+  CUDA_OK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dc.device));
+  if (major != 10) throw Error(MPSG_ERR_CUDA, "device is not sm_100 (B200)");
+  CUDA_OK(cudaDeviceGetAttribute(&dc.num_sms, cudaDevAttrMultiProcessorCount, dc.device));
+  CUDA_OK(cudaStreamCreateWithFlags(&dc.stream, cudaStreamNonBlocking));
+  const int kmax = kmax_of(h), chirpm = chirp_max_of(h);
+  const size_t row_bytes = 8ull * kmax + 8ull * h.d * chirpm + 8ull * h.d * (chirpm / kBN) + 1 + h.M;
+  uint64_t want = h.opts.pass_samples;
+  if (want == 0) {
+    const double budget = 6.0e9;  // bytes of per-pass working set
+    want = std::min<uint64_t>(65536, static_cast<uint64_t>(budget / row_bytes));
+  }
+  dc.cap = std::max(kBM, round_up(static_cast<int>(std::min<uint64_t>(want, 1u << 22)), kBM));
+  dc.sites.resize(h.M);
+  CUDA_OK(cudaMalloc(&dc.env, 4ull * dc.cap * kmax * sizeof(__half)));
+  CUDA_OK(cudaMalloc(&dc.temp, 1ull * dc.cap * h.d * chirpm * sizeof(float2)));
+  CUDA_OK(cudaMalloc(&dc.pstat, 1ull * dc.cap * h.d * (chirpm / kBN) * sizeof(float2)));
+  CUDA_OK(cudaMalloc(&dc.alive, dc.cap));
+  CUDA_OK(cudaMalloc(&dc.rows, 1ull * dc.cap * h.M));
+  CUDA_OK(cudaMalloc(&dc.err, sizeof(int)));
+  CUDA_OK(cudaMemset(dc.err, 0, sizeof(int)));
+  CUDA_OK(cudaMalloc(&dc.scratch, sizeof(double) * (kmax + 2ull * chirpm)));
+  CUDA_OK(cudaMallocHost(&dc.host_rows, 1ull * dc.cap * h.M));
+}
+
+static void free_device(DevCtx& dc) {
+  cudaSetDevice(dc.device);
+  if (dc.stream) cudaStreamSynchronize(dc.stream);
+  for (auto& s : dc.sites) {
+    cudaFree(s.g);
+    cudaFree(s.cinfo);
+    cudaFree(s.cs);
+  }
+  cudaFree(dc.env);
+  cudaFree(dc.temp);
+  cudaFree(dc.pstat);
+  cudaFree(dc.alive);
+  cudaFree(dc.rows);
+  cudaFree(dc.forced);
+  cudaFree(dc.marg);
+  cudaFree(dc.scratch);
+  cudaFree(dc.src);
+  cudaFree(dc.err);
+  if (dc.host_rows) cudaFreeHost(dc.host_rows);
+  for (auto e : dc.ev) cudaEventDestroy(e);
+  if (dc.stream) cudaStreamDestroy(dc.stream);
+}
+
+// Compress site i on device dc from `src` (device pointer on dc.device).
+static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* src_dev,
+                          bool f64, const double* lambda) {
+  SiteDev& s = dc.sites[i];
+  s.chil = static_cast<int>(h.bonds[i]);
+  s.chir = static_cast<int>(h.bonds[i + 1]);
+  s.kp = round_up(s.chil, kBK);
+  s.chirp = round_up(s.chir, kBN);
+  s.np = static_cast<int>(h.d) * s.chirp;
+  s.nt = s.np / kBN;
+  if (!s.g) {
+    CUDA_OK(cudaMalloc(&s.g, 2ull * s.np * s.kp * sizeof(__half)));
+    CUDA_OK(cudaMalloc(&s.cinfo, 1ull * s.np * sizeof(float2)));
+    CUDA_OK(cudaMalloc(&s.cs, 1ull * s.chir * h.d * sizeof(double)));
+  }
+  std::vector<double> wl(s.chir);
+  for (int r = 0; r < s.chir; ++r) {
+    const double q = lambda[r] / h.gr[i][r];
+    wl[r] = q * q;
+  }
+  double* d_gl = dc.scratch;
+  double* d_gr = d_gl + s.chil;
+  double* d_wl = d_gr + s.chir;
+  CUDA_OK(cudaMemcpyAsync(d_gl, h.gl[i].data(), sizeof(double) * s.chil, cudaMemcpyHostToDevice, dc.stream));
+  CUDA_OK(cudaMemcpyAsync(d_gr, h.gr[i].data(), sizeof(double) * s.chir, cudaMemcpyHostToDevice, dc.stream));
+  CUDA_OK(cudaMemcpyAsync(d_wl, wl.data(), sizeof(double) * s.chir, cudaMemcpyHostToDevice, dc.stream));
+  CUDA_OK(cudaMemsetAsync(s.g, 0, 2ull * s.np * s.kp * sizeof(__half), dc.stream));
+  CUDA_OK(cudaMemsetAsync(s.cinfo, 0, 1ull * s.np * sizeof(float2), dc.stream));
+  launch_compress_site(src_dev, f64, s.chil, s.chir, static_cast<int>(h.d), s.kp, s.chirp, d_gl,
+                       d_gr, d_wl, s.g, s.cinfo, s.cs, dc.err, dc.stream);
+  CUDA_OK(cudaGetLastError());
+  int err = 0;
+  CUDA_OK(cudaMemcpyAsync(&err, dc.err, sizeof(int), cudaMemcpyDeviceToHost, dc.stream));
+  CUDA_OK(cudaStreamSynchronize(dc.stream));
+  if (err != 0) {
+    cudaMemset(dc.err, 0, sizeof(int));
+    throw Error(MPSG_ERR_NUMERIC, "contract_site: non-finite input (site " + std::to_string(i) +
+                                      ") or dynamic range beyond the compressed format");
+  }
+  s.tma_g = make_tma_2d(s.g, s.kp, 2ull * s.np);
+  s.tma_env = make_tma_2d(dc.env, s.kp, 4ull * dc.cap);
+}
+
+static void ensure_src(DevCtx& dc, size_t bytes) {
+  if (dc.src_bytes >= bytes) return;
+  cudaFree(dc.src);
+  dc.src = nullptr;
+  CUDA_OK(cudaMalloc(&dc.src, bytes));
+  dc.src_bytes = bytes;
+}
+
+static void set_site(mpsg_handle_s& h, uint64_t i, const void* gamma, bool is_device, int dtype,
+                     const double* lambda) {
+  config_check(!h.finished, "builder already finished");
+  config_check(i < h.M, "site index out of range");
+  config_check(gamma != nullptr && lambda != nullptr, "null gamma / lambda");
+  config_check(dtype == MPSG_F64 || dtype == MPSG_F32, "gamma dtype must be f64 or f32");
+  // the left bond scales of site i derive from Lambda_{i-1}: sites are set in chain order
+  config_check(i == 0 || h.site_set[i - 1], "sites must be set in increasing order");
+  const size_t chir = h.bonds[i + 1];
+  validate_lambda(lambda, chir);
+  h.gr[i] = bond_scales(lambda, chir);
+  if (i + 1 < h.M) h.gl[i + 1] = h.gr[i];
+  const size_t elems = 2ull * h.bonds[i] * chir * h.d;
+  const size_t bytes = elems * (dtype == MPSG_F64 ? 8 : 4);
+  for (size_t di = 0; di < h.devs.size(); ++di) {
+    DevCtx& dc = h.devs[di];
+    CUDA_OK(cudaSetDevice(dc.device));
+    const void* src = gamma;
+    if (!is_device || di > 0) {
+      ensure_src(dc, bytes);
+      if (!is_device) {
+        CUDA_OK(cudaMemcpyAsync(dc.src, gamma, bytes, cudaMemcpyHostToDevice, dc.stream));
+      } else {
+        CUDA_OK(cudaMemcpyPeerAsync(dc.src, dc.device, gamma, h.devs[0].device, bytes, dc.stream));
+      }
+      src = dc.src;
+    }
+    compress_site(h, dc, i, src, dtype == MPSG_F64, lambda);
+  }
+  h.site_set[i] = 1;
+}
+
+// ---------------------------------------------------------------------------------------------
+// the sweep
+// ---------------------------------------------------------------------------------------------
+struct PassOut {
+  uint64_t macs = 0, wmacs = 0, issued = 0;
+};
+
+// Runs one pass of `count` (<= cap) samples starting at global index `first` on dc.
+static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first, int count,
+                     const uint8_t* forced_dev, double* marg_dev, PassOut& po, bool timing) {
+  const int rows = round_up(count, kBM);
+  launch_init_env(dc.env, dc.cap, dc.sites[0].kp, rows, count, dc.alive, dc.stream);
+  for (uint64_t i = 0; i < h.M; ++i) {
+    const SiteDev& s = dc.sites[i];
+    SiteGemmArgs ga;
+    ga.m_tiles = rows / kBM;
+    ga.n_tiles = s.nt;
+    ga.k_blocks = s.kp / kBK;
+    ga.plane_rows_a = dc.cap;
+    ga.np = s.np;
+    ga.chirp = s.chirp;
+    ga.d = static_cast<int>(h.d);
+    ga.group_n = std::min(s.nt, 8);
+    ga.cinfo = s.cinfo;
+    ga.temp = dc.temp;
+    ga.pstat = dc.pstat;
+    const int tiles = ga.m_tiles * ga.n_tiles;
+    launch_site_gemm(h.split, s.tma_env, s.tma_g, ga, std::min(tiles, dc.num_sms), dc.stream);
+
+    SelectArgs sa;
+    sa.site = static_cast<int>(i);
+    sa.num_sites = static_cast<int>(h.M);
+    sa.d = static_cast<int>(h.d);
+    sa.chir = s.chir;
+    sa.chirp = s.chirp;
+    sa.n_tiles = s.nt;
+    sa.tiles_per_k = s.chirp / kBN;
+    sa.rows = rows;
+    sa.count = count;
+    sa.kp_next = (i + 1 < h.M) ? dc.sites[i + 1].kp : 0;
+    sa.env_cap = dc.cap;
+    sa.seed = seed;
+    sa.first = first;
+    sa.temp = dc.temp;
+    sa.pstat = dc.pstat;
+    sa.alive = dc.alive;
+    sa.rows_out = dc.rows;
+    sa.env_next = dc.env;
+    sa.forced = forced_dev;
+    sa.marg = marg_dev;
+    launch_select(sa, dc.stream);
+    if (timing) CUDA_OK(cudaEventRecord(dc.ev[i + 1], dc.stream));
+    po.macs += static_cast<uint64_t>(count) * s.chil * s.chir * h.d;
+    po.wmacs += static_cast<uint64_t>(count) * s.chir * h.d;
+    po.issued += 8ull * rows * s.np * s.kp * (h.split ? 2 : 1);
+  }
+  CUDA_OK(cudaGetLastError());
+}
+
+struct RangeResult {
+  PassOut po;
+  std::vector<double> site_ms;
+  std::exception_ptr err;
+};
+
+// Samples [first, first+count) on one device; rows_host may be null when rows_dev_out is set.
+static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first,
+                      uint64_t count, uint8_t* rows_host, uint8_t* rows_dev_out,
+                      const uint8_t* forced_host, double* marg_host, RangeResult& rr) {
+  try {
+    CUDA_OK(cudaSetDevice(dc.device));
+    const bool timing = h.opts.record_site_times != 0;
+    if (timing && dc.ev.empty()) {
+      dc.ev.resize(h.M + 1);
+      for (auto& e : dc.ev) CUDA_OK(cudaEventCreate(&e));
+    }
+    if (timing) rr.site_ms.assign(h.M, 0.0);
+    if ((forced_host || marg_host) && !dc.forced) {
+      CUDA_OK(cudaMalloc(&dc.forced, 1ull * dc.cap * h.M));
+      CUDA_OK(cudaMalloc(&dc.marg, 1ull * dc.cap * h.M * h.d * sizeof(double)));
+    }
+    for (uint64_t off = 0; off < count; off += dc.cap) {
+      const int n = static_cast<int>(std::min<uint64_t>(dc.cap, count - off));
+      if (forced_host)
+        CUDA_OK(cudaMemcpyAsync(dc.forced, forced_host + off * h.M, 1ull * n * h.M,
+                                cudaMemcpyHostToDevice, dc.stream));
+      if (timing) CUDA_OK(cudaEventRecord(dc.ev[0], dc.stream));
+      run_pass(h, dc, seed, first + off, n, forced_host ? dc.forced : nullptr,
+               marg_host ? dc.marg : nullptr, rr.po, timing);
+      if (rows_dev_out) {
+        CUDA_OK(cudaMemcpyAsync(rows_dev_out + off * h.M, dc.rows, 1ull * n * h.M,
+                                cudaMemcpyDeviceToDevice, dc.stream));
+      }
+      if (rows_host) {
+        CUDA_OK(cudaMemcpyAsync(dc.host_rows, dc.rows, 1ull * n * h.M, cudaMemcpyDeviceToHost,
+                                dc.stream));
+      }
+      if (marg_host) {
+        CUDA_OK(cudaMemcpyAsync(marg_host + off * h.M * h.d, dc.marg,
+                                1ull * n * h.M * h.d * sizeof(double), cudaMemcpyDeviceToHost,
+                                dc.stream));
+      }
+      CUDA_OK(cudaStreamSynchronize(dc.stream));
+      if (rows_host) std::memcpy(rows_host + off * h.M, dc.host_rows, 1ull * n * h.M);
+      if (timing) {
+        for (uint64_t i = 0; i < h.M; ++i) {
+          float ms = 0.f;
+          CUDA_OK(cudaEventElapsedTime(&ms, dc.ev[i], dc.ev[i + 1]));
+          rr.site_ms[i] += ms;
+        }
+      }
+    }
+  } catch (...) {
+    rr.err = std::current_exception();
+  }
+}
+
+static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_t count,
+                        uint8_t* rows_host, uint8_t* rows_dev, const uint8_t* forced,
+                        double* marg, mpsg_stats* st) {
+  config_check(h.finished, "state not finished (mpsg_builder_finish)");
+  std::lock_guard<std::mutex> lk(h.mu);
+  const auto t0 = std::chrono::steady_clock::now();
+  const size_t nd = rows_dev ? 1 : h.devs.size();
+  std::vector<RangeResult> rr(nd);
+  std::vector<std::thread> th;
+  for (size_t k = 0; k < nd; ++k) {
+    const uint64_t a = count * k / nd, b = count * (k + 1) / nd;
+    if (b <= a) continue;
+    auto body = [&, k, a, b] {
+      run_range(h, h.devs[k], seed, first + a, b - a, rows_host ? rows_host + a * h.M : nullptr,
+                rows_dev ? rows_dev + a * h.M : nullptr, forced ? forced + a * h.M : nullptr,
+                marg ? marg + a * h.M * h.d : nullptr, rr[k]);
+    };
+    if (nd == 1)
+      body();
+    else
+      th.emplace_back(body);
+  }
+  for (auto& t : th) t.join();
+  for (auto& r : rr)
+    if (r.err) std::rethrow_exception(r.err);
+  if (st) {
+    st->contraction_macs = st->measure_weight_macs = st->issued_mma_flops = 0;
+    for (auto& r : rr) {
+      st->contraction_macs += r.po.macs;
+      st->measure_weight_macs += r.po.wmacs;
+      st->issued_mma_flops += r.po.issued;
+    }
+    st->dead_samples = 0;
+    if (rows_host)
+      for (uint64_t n = 0; n < count; ++n) st->dead_samples += rows_host[n * h.M + h.M - 1] == kDead;
+    st->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    st->h2d_bytes = forced ? count * h.M : 0;
+    st->d2h_bytes = rows_host ? count * h.M : 0;
+    if (st->site_seconds) {
+      for (uint64_t i = 0; i < h.M; ++i) {
+        double mx = 0.0;  // devices run concurrently: report the slowest
+        for (auto& r : rr)
+          if (!r.site_ms.empty()) mx = std::max(mx, r.site_ms[i] * 1e-3);
+        st->site_seconds[i] = mx;
+      }
+    }
+  }
+}
+
+}  // namespace mpsg
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+using namespace mpsg;
+
+template <typename F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return MPSG_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_last_error = std::string("out of memory: ") + e.what();
+    return MPSG_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MPSG_ERR_INTERNAL;
+  }
+}
+
+extern "C" {
+#pragma GCC visibility push(default)
+
+int mpsg_abi_version(void) { return MPSG_ABI_VERSION; }
+const char* mpsg_last_error(void) { return g_last_error.c_str(); }
+
+int mpsg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int c = 0;
+  for (int i = 0; i < n; ++i) {
+    int major = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, i) == cudaSuccess &&
+        major == 10)
+      ++c;
+  }
+  return c;
+}
+
+int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bond_dims,
+                       const mpsg_policy* policy, const mpsg_options* opts, const int* devices,
+                       int ndev, mpsg_handle* out) {
+  return guarded([&] {
+    config_check(out != nullptr, "null output handle");
+    *out = nullptr;
+    validate_shape(num_sites, phys_dim, bond_dims);
+    mpsg_policy pol{MPSG_F64, MPSG_F64, MPSG_SCALE_NONE};
+    if (policy) pol = *policy;
+    validate_policy(pol);
+    auto h = std::make_unique<mpsg_handle_s>();
+    h->M = num_sites;
+    h->d = phys_dim;
+    h->bonds.assign(bond_dims, bond_dims + num_sites + 1);
+    h->policy = pol;
+    if (opts) h->opts = *opts;
+    config_check(h->opts.mode >= MPSG_MODE_AUTO && h->opts.mode <= MPSG_MODE_SINGLE, "unknown mode");
+    h->split = h->opts.mode == MPSG_MODE_SPLIT ||
+               (h->opts.mode == MPSG_MODE_AUTO && (pol.compute == MPSG_F64 || pol.compute == MPSG_F32));
+    h->gl.resize(num_sites);
+    h->gr.resize(num_sites);
+    for (uint64_t i = 0; i < num_sites; ++i) {
+      h->gl[i].assign(h->bonds[i], 1.0);
+      h->gr[i].assign(h->bonds[i + 1], 1.0);
+    }
+    h->site_set.assign(num_sites, 0);
+    if (ndev <= 0 || devices == nullptr) {
+      h->devs.resize(1);
+      h->devs[0].device = 0;
+    } else {
+      h->devs.resize(ndev);
+      for (int k = 0; k < ndev; ++k) h->devs[k].device = devices[k];
+    }
+    if (mpsg_device_count() == 0) throw Error(MPSG_ERR_CUDA, "no sm_100 CUDA device visible");
+    try {
+      for (auto& dc : h->devs) alloc_device(*h, dc);
+    } catch (...) {
+      for (auto& dc : h->devs) free_device(dc);
+      throw;
+    }
+    *out = h.release();
+  });
+}
+
+int mpsg_builder_set_site(mpsg_handle h, uint64_t site, const void* gamma, int gamma_is_device,
+                          int dtype, const double* lambda) {
+  return guarded([&] {
+    config_check(h != nullptr, "null handle");
+    set_site(*h, site, gamma, gamma_is_device != 0, dtype, lambda);
+  });
+}
+
+int mpsg_builder_finish(mpsg_handle h) {
+  return guarded([&] {
+    config_check(h != nullptr, "null handle");
+    for (uint64_t i = 0; i < h->M; ++i)
+      config_check(h->site_set[i] != 0, "site " + std::to_string(i) + " was never set");
+    h->finished = true;
+  });
+}
+
+int mpsg_create(const mpsg_mps_view* mps, const mpsg_policy* policy, const mpsg_options* opts,
+                const int* devices, int ndev, mpsg_handle* out) {
+  int rc = guarded([&] {
+    config_check(mps != nullptr && out != nullptr, "null argument");
+    config_check(mps->gamma != nullptr && mps->lambda != nullptr, "null gamma / lambda arrays");
+  });
+  if (rc) return rc;
+  rc = mpsg_builder_begin(mps->num_sites, mps->phys_dim, mps->bond_dims, policy, opts, devices,
+                          ndev, out);
+  if (rc) return rc;
+  for (uint64_t i = 0; i < mps->num_sites; ++i) {
+    rc = mpsg_builder_set_site(*out, i, mps->gamma[i], 0, MPSG_F64, mps->lambda[i]);
+    if (rc) {
+      mpsg_destroy(*out);
+      *out = nullptr;
+      return rc;
+    }
+  }
+  rc = mpsg_builder_finish(*out);
+  if (rc) {
+    mpsg_destroy(*out);
+    *out = nullptr;
+  }
+  return rc;
+}
+
+void mpsg_destroy(mpsg_handle h) {
+  if (!h) return;
+  for (auto& dc : h->devs) free_device(dc);
+  delete h;
+}
+
+uint64_t mpsg_state_bytes(mpsg_handle h) {
+  if (!h || h->devs.empty()) return 0;
+  uint64_t b = 0;
+  for (const auto& s : h->devs[0].sites) b += 2ull * s.np * s.kp * sizeof(__half);
+  return b;
+}
+
+int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
+  return guarded([&] {
+    config_check(h != nullptr && out != nullptr, "null argument");
+    config_check(site < h->M && h->site_set[site], "site not set");
+    DevCtx& dc = h->devs[0];
+    CUDA_OK(cudaSetDevice(dc.device));
+    const SiteDev& s = dc.sites[site];
+    std::vector<__half> g(2ull * s.np * s.kp);
+    std::vector<double> cs(1ull * s.chir * h->d);
+    CUDA_OK(cudaMemcpy(g.data(), s.g, g.size() * sizeof(__half), cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(cs.data(), s.cs, cs.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    const size_t d = h->d;
+    for (int l = 0; l < s.chil; ++l)
+      for (int r = 0; r < s.chir; ++r)
+        for (size_t k = 0; k < d; ++k) {
+          const size_t row = k * s.chirp + r;
+          const double f = static_cast<double>(static_cast<float>(cs[r * d + k])) * h->gl[site][l] /
+                           h->gr[site][r];
+          const size_t o = 2 * ((static_cast<size_t>(l) * s.chir + r) * d + k);
+          out[o] = static_cast<double>(__half2float(g[row * s.kp + l])) * f;
+          out[o + 1] = static_cast<double>(__half2float(g[(s.np + row) * s.kp + l])) * f;
+        }
+  });
+}
+
+int mpsg_sample(mpsg_handle h, uint64_t seed, uint64_t first, uint64_t count, uint8_t* rows,
+                mpsg_stats* stats) {
+  return guarded([&] {
+    config_check(h != nullptr, "null handle");
+    config_check(count == 0 || rows != nullptr, "null rows");
+    config_check(count >= 1, "batch plan: total samples must be >= 1");  // sampler.cpp:21
+    sample_impl(*h, seed, first, count, rows, nullptr, nullptr, nullptr, stats);
+  });
+}
+
+int mpsg_sample_device(mpsg_handle h, uint64_t seed, uint64_t first, uint64_t count,
+                       uint8_t* rows_dev, mpsg_stats* stats) {
+  return guarded([&] {
+    config_check(h != nullptr && rows_dev != nullptr, "null argument");
+    config_check(count >= 1, "batch plan: total samples must be >= 1");
+    sample_impl(*h, seed, first, count, nullptr, rows_dev, nullptr, nullptr, stats);
+  });
+}
+
+int mpsg_marginals(mpsg_handle h, uint64_t first, uint64_t count, const uint8_t* forced,
+                   double* marg) {
+  return guarded([&] {
+    config_check(h != nullptr && forced != nullptr && marg != nullptr, "null argument");
+    config_check(count >= 1, "count must be >= 1");
+    std::vector<uint8_t> rows(count * h->M);
+    sample_impl(*h, 0, first, count, rows.data(), nullptr, forced, marg, nullptr);
+  });
+}
+
+int mpsg_device_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, double* out) {
+  return guarded([&] {
+    config_check(out != nullptr, "null output");
+    if (mpsg_device_count() == 0) throw Error(MPSG_ERR_CUDA, "no sm_100 CUDA device visible");
+    double* d = nullptr;
+    CUDA_OK(cudaMalloc(&d, sizeof(double) * std::max<uint64_t>(count, 1)));
+    launch_draws(seed, first, count, site, d, nullptr);
+    cudaError_t e = cudaMemcpy(out, d, sizeof(double) * count, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    CUDA_OK(e);
+  });
+}
+
+int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t count,
+                       double* temp) {
+  return guarded([&] {
+    config_check(h != nullptr && env != nullptr && temp != nullptr, "null argument");
+    config_check(site < h->M && h->finished, "bad site / unfinished state");
+    DevCtx& dc = h->devs[0];
+    config_check(count >= 1 && count <= static_cast<uint64_t>(dc.cap), "count exceeds pass capacity");
+    CUDA_OK(cudaSetDevice(dc.device));
+    std::lock_guard<std::mutex> lk(h->mu);
+    const SiteDev& s = dc.sites[site];
+    const int n = static_cast<int>(count);
+    const int rows = round_up(n, kBM);
+    // host: internal env E = env * gl * sigma_n (sigma_n power of two), hi/lo fp16 planes
+    const size_t plane = 1ull * dc.cap * s.kp;
+    std::vector<__half> e(4 * plane, __float2half_rn(0.f));
+    std::vector<double> sig(n, 1.0);
+    for (int r = 0; r < n; ++r) {
+      double mx = 0.0;
+      for (int l = 0; l < s.chil; ++l) {
+        const double* v = env + 2 * (static_cast<size_t>(r) * s.chil + l);
+        mx = std::max(mx, std::max(std::fabs(v[0]), std::fabs(v[1])) * h->gl[site][l]);
+      }
+      int ex = 0;
+      if (mx > 0.0) std::frexp(mx, &ex);
+      sig[r] = std::ldexp(1.0, -ex);
+      for (int l = 0; l < s.chil; ++l) {
+        const double* v = env + 2 * (static_cast<size_t>(r) * s.chil + l);
+        const float fr = static_cast<float>(v[0] * h->gl[site][l] * sig[r]);
+        const float fi = static_cast<float>(v[1] * h->gl[site][l] * sig[r]);
+        const __half hr = __float2half_rn(fr), hi = __float2half_rn(fi);
+        const size_t o = static_cast<size_t>(r) * s.kp + l;
+        e[o] = hr;
+        e[plane + o] = hi;
+        e[2 * plane + o] = __float2half_rn(fr - __half2float(hr));
+        e[3 * plane + o] = __float2half_rn(fi - __half2float(hi));
+      }
+    }
+    CUDA_OK(cudaMemcpy(dc.env, e.data(), e.size() * sizeof(__half), cudaMemcpyHostToDevice));
+    SiteGemmArgs ga;
+    ga.m_tiles = rows / kBM;
+    ga.n_tiles = s.nt;
+    ga.k_blocks = s.kp / kBK;
+    ga.plane_rows_a = dc.cap;
+    ga.np = s.np;
+    ga.chirp = s.chirp;
+    ga.d = static_cast<int>(h->d);
+    ga.group_n = std::min(s.nt, 8);
+    ga.cinfo = s.cinfo;
+    ga.temp = dc.temp;
+    ga.pstat = dc.pstat;
+    launch_site_gemm(h->split, s.tma_env, s.tma_g, ga, std::min(ga.m_tiles * ga.n_tiles, dc.num_sms),
+                     dc.stream);
+    CUDA_OK(cudaGetLastError());
+    std::vector<float2> t(1ull * n * h->d * s.chirp);
+    CUDA_OK(cudaMemcpyAsync(t.data(), dc.temp, t.size() * sizeof(float2), cudaMemcpyDeviceToHost,
+                            dc.stream));
+    CUDA_OK(cudaStreamSynchronize(dc.stream));
+    const size_t d = h->d;
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c < s.chir; ++c)
+        for (size_t k = 0; k < d; ++k) {
+          const float2 v = t[(static_cast<size_t>(r) * d + k) * s.chirp + c];
+          const double f = 1.0 / (h->gr[site][c] * sig[r]);
+          const size_t o = 2 * ((static_cast<size_t>(r) * s.chir + c) * d + k);
+          temp[o] = v.x * f;
+          temp[o + 1] = v.y * f;
+        }
+  });
+}
+
+#pragma GCC visibility pop
+}  // extern "C"

@@ -1,0 +1,72 @@
+// Kernel interface of the per-site sweep step (host engine <-> device kernels).
+//
+// Device data layout:
+//   G    fp16  [2 planes (re, im)][Np][Kp]   compressed site tensor, K-major (l contiguous);
+//              output column j = k * chirp + r  (k-major so a 128-column tile is one outcome k)
+//   cinfo float2 [Np]  (column scale cs_j, weight factor wl_r = (Lambda_r / gamma_r)^2)
+//   env  fp16  [4 planes (hi.re, hi.im, lo.re, lo.im)][cap rows][Kp]   internal environment
+//   temp float2 [rows][d][chirp]  contracted site, internal scaling, complex fp32
+//   pstat float2 [rows][ntiles]   per (sample, 128-column tile): (sum wl*|t|^2, max |t| comp.)
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mpsg {
+
+constexpr int kBM = 128;  // samples per tile (UMMA M)
+constexpr int kBN = 128;  // complex output columns per tile (UMMA N per real plane)
+constexpr int kBK = 32;   // K elements per pipeline stage (64 B rows, SWIZZLE_64B)
+constexpr int kGemmThreads = 256;
+constexpr uint64_t kMeasureStream = 0x6d656173ull;  // rng.hpp:19
+constexpr uint8_t kDead = 0xFF;                      // sampler.hpp:17
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+struct SiteGemmArgs {
+  int m_tiles;      // rows / 128
+  int n_tiles;      // Np / 128
+  int k_blocks;     // Kp / 32
+  int plane_rows_a; // row offset between env planes (= env capacity rows)
+  int np;           // Np (row offset between G planes)
+  int chirp;        // padded chiR (multiple of 128)
+  int d;
+  int group_n;      // N-tiles per raster group
+  const float2* cinfo;
+  float2* temp;
+  float2* pstat;
+};
+
+struct SelectArgs {
+  int site, num_sites, d, chir, chirp, n_tiles, tiles_per_k;
+  int rows;                 // samples handled this pass (multiple of 128 >= count)
+  int count;                // live samples this pass
+  int kp_next;              // K extent of the next site's env (0 on the last site)
+  int env_cap;              // env plane stride in rows
+  uint64_t seed, first;
+  const float2* temp;
+  const float2* pstat;
+  uint8_t* alive;
+  uint8_t* rows_out;        // [count][num_sites] (device)
+  __half* env_next;         // next site's env planes (may alias the current env buffer)
+  const uint8_t* forced;    // optional [count][num_sites] teacher forcing
+  double* marg;             // optional [count][num_sites][d]
+};
+
+// host launchers (sweep_kernels.cu)
+void launch_site_gemm(bool split, const CUtensorMap& tma_env, const CUtensorMap& tma_g,
+                      const SiteGemmArgs& a, int grid, cudaStream_t s);
+void launch_select(const SelectArgs& a, cudaStream_t s);
+void launch_init_env(__half* env, int env_cap, int kp0, int rows, int count, uint8_t* alive,
+                     cudaStream_t s);
+void launch_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, double* out,
+                  cudaStream_t s);
+// Compression of one site: src complex (chiL, chiR, d) f64 or f32 interleaved on device.
+void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int kp,
+                          int chirp, const double* gl, const double* gr, const double* wl,
+                          __half* g_out, float2* cinfo_out, double* cs_out, int* err,
+                          cudaStream_t s);
+int gemm_smem_bytes(bool split);
+
+}  // namespace mpsg

@@ -1,0 +1,501 @@
+// Per-site sweep kernels for sm_100a.
+//
+//   K1 site_gemm_kernel   temp = env x Gamma_i on tcgen05 (TMA -> smem -> UMMA -> TMEM), complex
+//                         4M decomposition with the sign folded into the instruction descriptor,
+//                         fused measurement epilogue: per (sample, 128-column tile) partial Born
+//                         weight sum wl_r |t|^2 and max component, temp stored k-major.
+//                         Reference: contract_site (contract.cpp:18-41,109-121) + the weight loop
+//                         of measure (sampler.cpp:83-90) + partial_measure_stats (parallel.cpp:90-114).
+//   K2 select_kernel      per sample: reduce partials (f64), keyed draw (rng.hpp:22-37), f64 CDF
+//                         search with strict '>' and clamp (sampler.cpp:92-107), dead handling,
+//                         gather of the chosen slice (sampler.cpp:110-111), power-of-two
+//                         renormalisation (precision.cpp:152-163) and hi/lo fp16 split into the
+//                         next site's GEMM operand.
+//   init / draws / compress helpers.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ptx.cuh"
+#include "sweep.cuh"
+
+namespace mpsg {
+
+// ============================================================================================
+// RNG (rng.hpp:12-37), bit-exact with the reference.
+// ============================================================================================
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double keyed_uniform(uint64_t seed, uint64_t stream, uint64_t sample,
+                                                uint64_t site) {
+  uint64_t h = mix64(seed ^ (stream * 0xD6E8FEB86659FD93ull));
+  h = mix64(h ^ (sample * 0xA5A5A5A5A5A5A5A5ull));
+  h = mix64(h ^ (site * 0xC2B2AE3D27D4EB4Full));
+  return static_cast<double>(h >> 11) * 0x1.0p-53;
+}
+
+// ============================================================================================
+// K1: tcgen05 complex GEMM + fused measurement epilogue
+// ============================================================================================
+template <bool kSplit>
+struct GemmCfg {
+  static constexpr int kAPlanes = kSplit ? 4 : 2;  // env planes: hi.re hi.im [lo.re lo.im]
+  static constexpr int kTile = kBM * kBK * 2;      // 8 KiB: 128 rows x 64 B (A and B alike)
+  static constexpr int kStageBytes = (kAPlanes + 2) * kTile;
+  static constexpr int kStages = kSplit ? 4 : 6;
+  static constexpr int kBarrierBytes = 256;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + kBarrierBytes;
+  static_assert(kBM == 128 && kBN == 128 && kBK == 32, "tile shape baked into descriptors");
+};
+
+int gemm_smem_bytes(bool split) { return split ? GemmCfg<true>::kSmem : GemmCfg<false>::kSmem; }
+
+__device__ __forceinline__ void tile_coords(int t, const SiteGemmArgs& a, int& m, int& n) {
+  const int per_group = a.group_n * a.m_tiles;
+  const int g = t / per_group;
+  const int n0 = g * a.group_n;
+  const int gw = min(a.group_n, a.n_tiles - n0);
+  const int r = t - g * per_group;
+  m = r / gw;
+  n = n0 + (r - m * gw);
+}
+
+template <bool kSplit>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    site_gemm_kernel(const __grid_constant__ CUtensorMap tma_env,
+                     const __grid_constant__ CUtensorMap tma_g, const SiteGemmArgs a) {
+  using C = GemmCfg<kSplit>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int j = 0; j < 2; ++j) {
+      ptx::mbar_init(&tfull[j], 1);
+      ptx::mbar_init(&tempty[j], 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tma_env);
+    ptx::tma_prefetch_desc(&tma_g);
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(tmem_slot, 512);  // 2 accumulator stages x (re 128 + im 128) fp32 columns
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = a.m_tiles * a.n_tiles;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const uint64_t pol_env = ptx::l2_policy_evict_first();
+      const uint64_t pol_g = ptx::l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int m, n;
+        tile_coords(t, a, m, n);
+        for (int kb = 0; kb < a.k_blocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * C::kStageBytes;
+          ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+#pragma unroll
+          for (int q = 0; q < C::kAPlanes; ++q)
+            ptx::tma_load_2d(&tma_env, &full[stage], st + q * C::kTile, kb * kBK,
+                             q * a.plane_rows_a + m * kBM, pol_env);
+#pragma unroll
+          for (int p = 0; p < 2; ++p)
+            ptx::tma_load_2d(&tma_g, &full[stage], st + (C::kAPlanes + p) * C::kTile, kb * kBK,
+                             p * a.np + n * kBN, pol_g);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread) ----------------
+    if (lane == 0) {
+      constexpr uint32_t kId = ptx::idesc_f16_f32(kBM, kBN, false);
+      constexpr uint32_t kIdNeg = ptx::idesc_f16_f32(kBM, kBN, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_re = tmem_base + acc * 256;
+        const uint32_t d_im = d_re + 128;
+        for (int kb = 0; kb < a.k_blocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t st = ptx::smem_u32(smem + stage * C::kStageBytes);
+#pragma unroll
+          for (int ks = 0; ks < kBK / 16; ++ks) {
+            const uint32_t off = ks * 32;  // 16 fp16 along K
+            const uint64_t br = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 0) * C::kTile + off);
+            const uint64_t bi = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 1) * C::kTile + off);
+            const uint32_t accum = (kb | ks) ? 1u : 0u;
+            {
+              const uint64_t ar = ptx::sdesc_kmajor_sw64(st + 0 * C::kTile + off);
+              const uint64_t ai = ptx::sdesc_kmajor_sw64(st + 1 * C::kTile + off);
+              // Re += Er.Gr - Ei.Gi ; Im += Er.Gi + Ei.Gr
+              ptx::umma_f16_ss(d_re, ar, br, kId, accum);
+              ptx::umma_f16_ss(d_re, ai, bi, kIdNeg, 1u);
+              ptx::umma_f16_ss(d_im, ar, bi, kId, accum);
+              ptx::umma_f16_ss(d_im, ai, br, kId, 1u);
+            }
+            if constexpr (kSplit) {
+              const uint64_t ar = ptx::sdesc_kmajor_sw64(st + 2 * C::kTile + off);
+              const uint64_t ai = ptx::sdesc_kmajor_sw64(st + 3 * C::kTile + off);
+              ptx::umma_f16_ss(d_re, ar, br, kId, 1u);
+              ptx::umma_f16_ss(d_re, ai, bi, kIdNeg, 1u);
+              ptx::umma_f16_ss(d_im, ar, bi, kId, 1u);
+              ptx::umma_f16_ss(d_im, ai, br, kId, 1u);
+            }
+          }
+          ptx::umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> (weights, max, temp) ----------------
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int m, n;
+      tile_coords(t, a, m, n);
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row = m * kBM + q * 32 + lane;
+      const int col0 = n * kBN;
+      const int k = col0 / a.chirp;
+      const int r0 = col0 - k * a.chirp;
+      float2* dst = a.temp + (static_cast<size_t>(row) * a.d + k) * a.chirp + r0;
+      const float2* ci = a.cinfo + col0;
+      const uint32_t tb = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
+      float w = 0.f, mx = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < kBN / 32; ++c) {
+        float re[32], im[32];
+        ptx::tmem_ld_32x32b_x32(tb + c * 32, re);
+        ptx::tmem_ld_32x32b_x32(tb + 128 + c * 32, im);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const float4 cc = *reinterpret_cast<const float4*>(ci + c * 32 + j);  // (cs0, wl0, cs1, wl1)
+          const float tr0 = re[j] * cc.x, ti0 = im[j] * cc.x;
+          const float tr1 = re[j + 1] * cc.z, ti1 = im[j + 1] * cc.z;
+          w = fmaf(cc.y, fmaf(tr0, tr0, ti0 * ti0), w);
+          w = fmaf(cc.w, fmaf(tr1, tr1, ti1 * ti1), w);
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(tr0), fabsf(ti0)), fmaxf(fabsf(tr1), fabsf(ti1))));
+          *reinterpret_cast<float4*>(dst + c * 32 + j) = make_float4(tr0, ti0, tr1, ti1);
+        }
+      }
+      a.pstat[static_cast<size_t>(row) * a.n_tiles + n] = make_float2(w, mx);
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, 512);
+  }
+}
+
+void launch_site_gemm(bool split, const CUtensorMap& tma_env, const CUtensorMap& tma_g,
+                      const SiteGemmArgs& a, int grid, cudaStream_t s) {
+  if (split) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(site_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           GemmCfg<true>::kSmem);
+      attr = true;
+    }
+    site_gemm_kernel<true><<<grid, kGemmThreads, GemmCfg<true>::kSmem, s>>>(tma_env, tma_g, a);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(site_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           GemmCfg<false>::kSmem);
+      attr = true;
+    }
+    site_gemm_kernel<false><<<grid, kGemmThreads, GemmCfg<false>::kSmem, s>>>(tma_env, tma_g, a);
+  }
+}
+
+// ============================================================================================
+// K2: measurement select + gather + renormalise + split (one warp per sample)
+// ============================================================================================
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Born weight of outcome k for sample row: fixed-order f64 reduction of the tile partials.
+__device__ __forceinline__ double outcome_weight(const float2* ps, int k, int tiles_per_k,
+                                                 int lane) {
+  double s = 0.0;
+  for (int t = lane; t < tiles_per_k; t += 32) s += static_cast<double>(ps[k * tiles_per_k + t].x);
+  return warp_sum(s);
+}
+
+__global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (n >= a.rows) return;
+  const bool live_in = n < a.count && a.alive[n];
+  const float2* ps = a.pstat + static_cast<size_t>(n) * a.n_tiles;
+  int outcome = kDead;   // recorded at this site
+  bool live_out = false; // carries into the next site
+  float scale = 0.f;
+  if (live_in) {
+    double total = 0.0;  // sampler.cpp:92-93, ascending k
+    for (int k = 0; k < a.d; ++k) total += outcome_weight(ps, k, a.tiles_per_k, lane);
+    if (a.marg != nullptr) {
+      double* mrow = a.marg + (static_cast<size_t>(n) * a.num_sites + a.site) * a.d;
+      for (int k = 0; k < a.d; ++k) {
+        const double wk = outcome_weight(ps, k, a.tiles_per_k, lane);
+        if (lane == 0) mrow[k] = total == 0.0 ? -1.0 : wk / total;
+      }
+    }
+    if (total != 0.0) {  // total == 0 -> dead (sampler.cpp:94-98)
+      int kk;
+      if (a.forced != nullptr) {
+        kk = a.forced[static_cast<size_t>(n) * a.num_sites + a.site];
+      } else {
+        const double draw = keyed_uniform(a.seed, kMeasureStream, a.first + n, a.site);
+        double cum = 0.0;
+        kk = 0;
+        for (int k = 0; k < a.d; ++k) {  // sampler.cpp:100-106: strict '>', no early break
+          cum += outcome_weight(ps, k, a.tiles_per_k, lane) / total;
+          if (draw > cum) ++kk;
+        }
+        if (kk >= a.d) kk = a.d - 1;  // :107
+      }
+      if (kk != kDead) {
+        outcome = kk;
+        // per-sample max of the chosen slice (precision.cpp:155-160); 0 -> dead from here on
+        float mx = 0.f;
+        for (int t = lane; t < a.tiles_per_k; t += 32) mx = fmaxf(mx, ps[kk * a.tiles_per_k + t].y);
+        mx = warp_max(mx);
+        if (mx > 0.f) {
+          int e;
+          frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
+          scale = ldexpf(1.0f, -e);
+          live_out = true;
+        }
+      }
+    }
+  }
+  if (!live_in && a.marg != nullptr && lane == 0 && n < a.count) {
+    double* mrow = a.marg + (static_cast<size_t>(n) * a.num_sites + a.site) * a.d;
+    for (int k = 0; k < a.d; ++k) mrow[k] = -1.0;
+  }
+  if (lane == 0 && n < a.count) {
+    a.rows_out[static_cast<size_t>(n) * a.num_sites + a.site] = static_cast<uint8_t>(outcome);
+    a.alive[n] = live_out ? 1 : 0;
+  }
+  if (a.kp_next > 0) {
+    // next env row: E[n, r] = temp[n, k, r] * 2^-e, split hi/lo fp16 (zeros for dead / pad)
+    const size_t plane = static_cast<size_t>(a.env_cap) * a.kp_next;
+    __half* e0 = a.env_next + static_cast<size_t>(n) * a.kp_next;
+    const float2* src = a.temp + (static_cast<size_t>(n) * a.d + (live_out ? outcome : 0)) * a.chirp;
+    for (int r = lane; r < a.kp_next; r += 32) {
+      float2 v = make_float2(0.f, 0.f);
+      if (live_out && r < a.chir) {
+        v = src[r];
+        v.x *= scale;
+        v.y *= scale;
+      }
+      const __half hr = __float2half_rn(v.x), hi = __float2half_rn(v.y);
+      e0[r] = hr;
+      e0[plane + r] = hi;
+      e0[2 * plane + r] = __float2half_rn(v.x - __half2float(hr));
+      e0[3 * plane + r] = __float2half_rn(v.y - __half2float(hi));
+    }
+  }
+}
+
+void launch_select(const SelectArgs& a, cudaStream_t s) {
+  const int threads = 256;
+  const int blocks = (a.rows * 32 + threads - 1) / threads;
+  select_kernel<<<blocks, threads, 0, s>>>(a);
+}
+
+// ============================================================================================
+// site-0 environment (sampler.cpp:136-138: env = ones(count, 1), all alive)
+// ============================================================================================
+__global__ void init_env_kernel(__half* env, int env_cap, int kp0, int rows, int count,
+                                uint8_t* alive) {
+  const size_t plane = static_cast<size_t>(env_cap) * kp0;
+  const size_t total = 4 * plane;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t p = i / plane, rem = i - p * plane;
+    const size_t n = rem / kp0, c = rem - n * kp0;
+    env[i] = __float2half_rn((p == 0 && c == 0 && n < static_cast<size_t>(count)) ? 1.0f : 0.0f);
+  }
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < rows; n += gridDim.x * blockDim.x)
+    alive[n] = n < count ? 1 : 0;
+}
+
+void launch_init_env(__half* env, int env_cap, int kp0, int rows, int count, uint8_t* alive,
+                     cudaStream_t s) {
+  init_env_kernel<<<296, 256, 0, s>>>(env, env_cap, kp0, rows, count, alive);
+}
+
+__global__ void draws_kernel(uint64_t seed, uint64_t first, uint64_t count, uint64_t site,
+                             double* out) {
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < count;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[j] = keyed_uniform(seed, kMeasureStream, first + j, site);
+}
+
+void launch_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, double* out,
+                  cudaStream_t s) {
+  draws_kernel<<<148, 256, 0, s>>>(seed, first, count, site, out);
+}
+
+// ============================================================================================
+// Compression: Gamma (chiL, chiR, d) -> fp16 planes [2][Np][Kp] with power-of-two scales
+//   Ghat[l, r, k] = Gamma[l, r, k] * gr[r] / gl[l] / cs[r, k],  |Ghat| <= 1
+// ============================================================================================
+template <typename T>
+__device__ __forceinline__ void load_c(const void* src, size_t idx, double& re, double& im) {
+  const T* p = static_cast<const T*>(src) + 2 * idx;
+  re = static_cast<double>(p[0]);
+  im = static_cast<double>(p[1]);
+}
+
+template <typename T>
+__global__ void colscale_kernel(const void* src, int chil, int chir, int d, int chirp,
+                                const double* gl, const double* gr, const double* wl,
+                                float2* cinfo, double* cs_out, int* err) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;  // column j = r * d + k
+  const int width = chir * d;
+  if (j >= width) return;
+  const int r = j / d, k = j - r * d;
+  double mx = 0.0;
+  bool finite = true;
+  for (int l = 0; l < chil; ++l) {
+    double re, im;
+    load_c<T>(src, static_cast<size_t>(l) * width + j, re, im);
+    if (!isfinite(re) || !isfinite(im)) finite = false;
+    const double f = gr[r] / gl[l];
+    mx = fmax(mx, fmax(fabs(re * f), fabs(im * f)));
+  }
+  if (!finite) atomicExch(err, 3);  // NumericError: non-finite Gamma (contract.cpp:117-119)
+  double cs = 1.0;
+  if (mx > 0.0) {
+    int e;
+    frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)
+    if (e > 120) {
+      atomicExch(err, 3);  // outside the compressed format's range
+      e = 120;
+    }
+    if (e < -120) e = -120;
+    cs = ldexp(1.0, e);
+  }
+  cs_out[j] = cs;
+  cinfo[k * chirp + r] = make_float2(static_cast<float>(cs), static_cast<float>(wl[r]));
+}
+
+template <typename T>
+__global__ void pack_kernel(const void* src, int chil, int chir, int d, int kp, int chirp,
+                            const double* gl, const double* gr, const double* cs, __half* g_out) {
+  __shared__ __half tre[32][33], tim[32][33];
+  const int width = chir * d;
+  const int np = d * chirp;
+  const int j0 = blockIdx.x * 32, l0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int l = l0 + yy, j = j0 + tx;
+    __half hr = __float2half_rn(0.f), hi = hr;
+    if (l < chil && j < width) {
+      double re, im;
+      load_c<T>(src, static_cast<size_t>(l) * width + j, re, im);
+      const int r = j / d;
+      const double f = gr[r] / gl[l] / cs[j];
+      hr = __double2half(re * f);
+      hi = __double2half(im * f);
+    }
+    tre[yy][tx] = hr;
+    tim[yy][tx] = hi;
+  }
+  __syncthreads();
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int j = j0 + yy, l = l0 + tx;
+    if (j < width && l < kp) {
+      const int r = j / d, k = j - r * d;
+      const size_t row = static_cast<size_t>(k) * chirp + r;
+      g_out[row * kp + l] = tre[tx][yy];
+      g_out[(static_cast<size_t>(np) + row) * kp + l] = tim[tx][yy];
+    }
+  }
+}
+
+void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int kp,
+                          int chirp, const double* gl, const double* gr, const double* wl,
+                          __half* g_out, float2* cinfo_out, double* cs_out, int* err,
+                          cudaStream_t s) {
+  const int width = chir * d;
+  const dim3 cb((width + 127) / 128);
+  const dim3 pb((width + 31) / 32, (chil + 31) / 32);
+  if (src_f64) {
+    colscale_kernel<double><<<cb, 128, 0, s>>>(src, chil, chir, d, chirp, gl, gr, wl, cinfo_out,
+                                               cs_out, err);
+    pack_kernel<double><<<pb, dim3(32, 8), 0, s>>>(src, chil, chir, d, kp, chirp, gl, gr, cs_out,
+                                                   g_out);
+  } else {
+    colscale_kernel<float><<<cb, 128, 0, s>>>(src, chil, chir, d, chirp, gl, gr, wl, cinfo_out,
+                                              cs_out, err);
+    pack_kernel<float><<<pb, dim3(32, 8), 0, s>>>(src, chil, chir, d, kp, chirp, gl, gr, cs_out,
+                                                  g_out);
+  }
+}
+
+}  // namespace mpsg

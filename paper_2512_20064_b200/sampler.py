@@ -1,0 +1,370 @@
+"""Host-side mirror of the reference's sampling interface (``mpsamp``), backed by libmpsg.so.
+
+Names, argument meaning and error behaviour follow the reference headers so that code written
+against ``mpsamp::sample_batch`` reads the same here:
+
+=========================  ======================================================================
+this module                reference (proj/include/mpsamp/…)
+=========================  ======================================================================
+``Precision``              ``enum class Precision``           precision.hpp:15
+``ScalingMode``            ``enum class ScalingMode``         precision.hpp:17
+``PrecisionPolicy``        ``struct PrecisionPolicy``         precision.hpp:27-33 (validate :98-102)
+``MpsState``               ``struct MpsState``                mps.hpp:14-22 (validate mps.cpp:12-38)
+``BatchPlan``              ``struct BatchPlan``               sampler.hpp:22-31 (normalize sampler.cpp:20-25)
+``SamplerOptions``         ``struct SamplerOptions``          sampler.hpp:75-81
+``SampleBatch``            ``struct SampleBatch``             sampler.hpp:33-44
+``RunStats``               ``struct RunStats``                sampler.hpp:46-54
+``sample_batch``           ``sample_batch``                   sampler.hpp:84-85 (sampler.cpp:164-205)
+``sample_micro_serial``    ``detail::sample_micro_serial``    sampler.hpp:103-104
+``Error`` & subclasses     ``errors.hpp:8-27``
+=========================  ======================================================================
+
+The compute runs on the B200 through the C ABI; this layer only validates, marshals pointers and
+maps return codes onto the exception hierarchy.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import time
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+DEAD_OUTCOME = 0xFF  # sampler.hpp:17
+
+
+# ---- errors.hpp:8-27 -----------------------------------------------------------------------
+class Error(RuntimeError):
+    """mpsamp::Error"""
+
+
+class ConfigError(Error):
+    """mpsamp::ConfigError (exit code 2)"""
+
+
+class DimensionError(ConfigError):
+    """mpsamp::DimensionError"""
+
+
+class NumericError(Error):
+    """mpsamp::NumericError (exit code 3)"""
+
+
+class IoError(Error):
+    """mpsamp::IoError (exit code 4)"""
+
+
+class DeviceError(Error):
+    """CUDA / NCCL failure (no reference counterpart; the reference has no device)."""
+
+
+def _check(rc: int) -> None:
+    if rc == _lib.MPSG_OK:
+        return
+    msg = _lib.last_error()
+    cls = {_lib.MPSG_ERR_CONFIG: ConfigError, _lib.MPSG_ERR_NUMERIC: NumericError,
+           _lib.MPSG_ERR_IO: IoError, _lib.MPSG_ERR_CUDA: DeviceError}.get(rc, Error)
+    if cls is ConfigError and ("shape" in msg or "length" in msg or "bond" in msg or "dimension" in msg):
+        cls = DimensionError
+    raise cls(msg)
+
+
+# ---- precision.hpp ---------------------------------------------------------------------------
+class Precision(enum.IntEnum):
+    F64 = 0
+    F32 = 1
+    TF32 = 2
+    F16 = 3
+
+    @staticmethod
+    def from_string(s: str) -> "Precision":  # precision.cpp:78-84
+        m = {"f64": Precision.F64, "f32": Precision.F32, "tf32": Precision.TF32, "f16": Precision.F16}
+        if s not in m:
+            raise ConfigError("unknown precision tag: " + s)
+        return m[s]
+
+
+class ScalingMode(enum.IntEnum):
+    NONE = 0
+    GLOBAL_MAX = 1
+    PER_SAMPLE_MAX = 2
+
+    @staticmethod
+    def from_string(s: str) -> "ScalingMode":  # precision.cpp:86-91
+        m = {"none": ScalingMode.NONE, "global-max": ScalingMode.GLOBAL_MAX,
+             "per-sample-max": ScalingMode.PER_SAMPLE_MAX}
+        if s not in m:
+            raise ConfigError("unknown scaling mode: " + s)
+        return m[s]
+
+
+@dataclass
+class PrecisionPolicy:
+    compute: Precision = Precision.F64
+    storage: Precision = Precision.F64
+    scaling: ScalingMode = ScalingMode.NONE
+
+    def validate(self) -> None:  # precision.cpp:98-102
+        if self.storage == Precision.TF32:
+            raise ConfigError("storage precision must be one of f64/f32/f16")
+
+
+class Mode(enum.IntEnum):
+    """GPU contraction scheme; AUTO picks SPLIT for F64/F32 compute."""
+    AUTO = 0
+    SPLIT = 1
+    SINGLE = 2
+
+
+# ---- mps.hpp ---------------------------------------------------------------------------------
+@dataclass
+class MpsState:
+    """gammas[i]: complex128 (bond[i], bond[i+1], d); lambdas[i]: float64 (bond[i+1],)."""
+
+    num_sites: int = 0
+    phys_dim: int = 0
+    bond_dims: list = field(default_factory=list)
+    gammas: list = field(default_factory=list)
+    lambdas: list = field(default_factory=list)
+
+    def validate(self) -> None:  # mps.cpp:12-38
+        if self.num_sites == 0:
+            raise DimensionError("mps has no sites")
+        if self.phys_dim < 1:
+            raise DimensionError("mps physical dimension must be >= 1")
+        if len(self.bond_dims) != self.num_sites + 1:
+            raise DimensionError("bond_dims length mismatch")
+        if self.bond_dims[0] != 1 or self.bond_dims[-1] != 1:
+            raise DimensionError("boundary bonds must be 1")
+        if len(self.gammas) != self.num_sites or len(self.lambdas) != self.num_sites:
+            raise DimensionError("site tensor count mismatch")
+        for i in range(self.num_sites):
+            g = self.gammas[i]
+            if g.ndim != 3 or g.shape != (self.bond_dims[i], self.bond_dims[i + 1], self.phys_dim):
+                raise DimensionError("gamma shape disagrees with bond dimension chain")
+            lam = np.asarray(self.lambdas[i])
+            if lam.shape != (self.bond_dims[i + 1],):
+                raise DimensionError("lambda length disagrees with bond dimension chain")
+            if (lam < 0).any():
+                raise NumericError("lambda entries must be nonnegative")
+            if lam.size > 1 and (np.diff(lam) > 0).any():
+                raise NumericError("lambda vectors must be nonincreasing")
+
+
+def capped_bond_dims(num_sites: int, phys_dim: int, chi_max: int) -> list:
+    """mps.cpp:78-88: min(d^i, d^(M-i), chi_max) (double arithmetic, truncated)."""
+    out = []
+    for i in range(num_sites + 1):
+        cap = min(float(phys_dim) ** i, float(phys_dim) ** (num_sites - i), float(chi_max))
+        out.append(int(cap))
+    return out
+
+
+# ---- sampler.hpp -----------------------------------------------------------------------------
+@dataclass
+class BatchPlan:
+    total_samples: int = 0
+    macro_batch: int = 0
+    micro_batch: int = 5000
+
+    def normalize(self) -> None:  # sampler.cpp:20-25
+        if self.total_samples == 0:
+            raise ConfigError("batch plan: total samples must be >= 1")
+        if self.macro_batch == 0 or self.macro_batch > self.total_samples:
+            self.macro_batch = self.total_samples
+        if self.micro_batch == 0:
+            self.micro_batch = 5000
+        if self.micro_batch > self.macro_batch:
+            self.micro_batch = self.macro_batch
+
+    def macro_count(self) -> int:
+        return (self.total_samples + self.macro_batch - 1) // self.macro_batch
+
+    @staticmethod
+    def simple(n: int, n2: int = 5000) -> "BatchPlan":
+        p = BatchPlan(n, n, n2)
+        p.normalize()
+        return p
+
+
+@dataclass
+class SamplerOptions:
+    policy: PrecisionPolicy = field(default_factory=PrecisionPolicy)
+    seed: int = 0
+    schedule: Optional[object] = None        # BondSchedule: not supported on the GPU path
+    site_transform: Optional[object] = None  # SiteTransform hook: not supported on the GPU path
+    record_decay_trace: bool = False
+    mode: Mode = Mode.AUTO
+    pass_samples: int = 0
+
+
+@dataclass
+class SampleBatch:
+    num_samples: int = 0
+    num_sites: int = 0
+    phys_dim: int = 0
+    seed: int = 0
+    outcomes: np.ndarray = None  # (N, M) uint8
+
+    def outcome(self, sample: int, site: int) -> int:
+        return int(self.outcomes[sample, site])
+
+    def dead_count(self) -> int:  # sampler.cpp:40-47
+        return int((self.outcomes[:, -1] == DEAD_OUTCOME).sum())
+
+
+@dataclass
+class RunStats:
+    contraction_macs: int = 0
+    measure_weight_macs: int = 0
+    dead_samples: int = 0
+    site_seconds: list = field(default_factory=list)
+    total_seconds: float = 0.0
+    issued_mma_flops: int = 0
+
+
+# ---- the device-resident sampler -------------------------------------------------------------
+class GpuSampler:
+    """A compressed MPS resident on one or more B200s (libmpsg handle)."""
+
+    def __init__(self, mps: MpsState, policy: Optional[PrecisionPolicy] = None, mode: Mode = Mode.AUTO,
+                 devices: Optional[Sequence[int]] = None, pass_samples: int = 0,
+                 record_site_times: bool = False):
+        L = _lib.lib()
+        mps.validate()
+        self.policy = policy or PrecisionPolicy()
+        self.policy.validate()
+        self.num_sites, self.phys_dim = mps.num_sites, mps.phys_dim
+        self.bond_dims = list(mps.bond_dims)
+        self._h = C.c_void_p()
+        bonds = (C.c_uint64 * len(mps.bond_dims))(*mps.bond_dims)
+        g = [np.ascontiguousarray(x, np.complex128) for x in mps.gammas]
+        lam = [np.ascontiguousarray(x, np.float64) for x in mps.lambdas]
+        view = _lib.MpsView(mps.num_sites, mps.phys_dim, bonds,
+                            (_lib._pd * len(g))(*[x.ctypes.data_as(_lib._pd) for x in g]),
+                            (_lib._pd * len(lam))(*[x.ctypes.data_as(_lib._pd) for x in lam]))
+        pol = _lib.Policy(int(self.policy.compute), int(self.policy.storage), int(self.policy.scaling))
+        opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times))
+        devs, nd = self._devices(devices)
+        _check(L.mpsg_create(C.byref(view), C.byref(pol), C.byref(opt), devs, nd, C.byref(self._h)))
+
+    @staticmethod
+    def _devices(devices):
+        if not devices:
+            return None, 0
+        arr = (C.c_int * len(devices))(*devices)
+        return arr, len(devices)
+
+    @classmethod
+    def from_builder(cls, handle: C.c_void_p, num_sites: int, phys_dim: int, bond_dims: list,
+                     policy: PrecisionPolicy) -> "GpuSampler":
+        self = cls.__new__(cls)
+        self._h = handle
+        self.num_sites, self.phys_dim, self.bond_dims = num_sites, phys_dim, list(bond_dims)
+        self.policy = policy
+        return self
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            _lib.lib().mpsg_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def state_bytes(self) -> int:
+        return int(_lib.lib().mpsg_state_bytes(self._h))
+
+    def sample(self, first: int, count: int, seed: int, stats: Optional[RunStats] = None,
+               out: Optional[np.ndarray] = None) -> np.ndarray:
+        """detail::sample_micro_serial over global samples [first, first+count)."""
+        rows = out if out is not None else np.empty((count, self.num_sites), np.uint8)
+        st = _lib.Stats()
+        site_s = None
+        if stats is not None:
+            site_s = np.zeros(self.num_sites, np.float64)
+            st.site_seconds = site_s.ctypes.data_as(_lib._pd)
+        _check(_lib.lib().mpsg_sample(self._h, seed, first, count, rows.ctypes.data_as(_lib._pu8),
+                                      C.byref(st)))
+        if stats is not None:
+            stats.contraction_macs += st.contraction_macs
+            stats.measure_weight_macs += st.measure_weight_macs
+            stats.dead_samples += st.dead_samples
+            stats.total_seconds += st.seconds
+            stats.issued_mma_flops += st.issued_mma_flops
+            stats.site_seconds = list(np.asarray(stats.site_seconds or np.zeros(self.num_sites)) + site_s)
+        return rows
+
+    def sample_device(self, first: int, count: int, seed: int, rows_dev_ptr: int) -> None:
+        _check(_lib.lib().mpsg_sample_device(self._h, seed, first, count, C.c_void_p(rows_dev_ptr), None))
+
+    def marginals(self, first: int, forced: np.ndarray) -> np.ndarray:
+        forced = np.ascontiguousarray(forced, np.uint8)
+        n = forced.shape[0]
+        marg = np.empty((n, self.num_sites, self.phys_dim), np.float64)
+        _check(_lib.lib().mpsg_marginals(self._h, first, n, forced.ctypes.data_as(_lib._pu8),
+                                         marg.ctypes.data_as(_lib._pd)))
+        return marg
+
+    def decoded_gamma(self, site: int) -> np.ndarray:
+        b = self.bond_dims
+        out = np.empty((b[site], b[site + 1], self.phys_dim), np.complex128)
+        _check(_lib.lib().mpsg_decoded_gamma(self._h, site, out.ctypes.data_as(_lib._pd)))
+        return out
+
+    def contract_site(self, site: int, env: np.ndarray) -> np.ndarray:
+        env = np.ascontiguousarray(env, np.complex128)
+        b = self.bond_dims
+        out = np.empty((env.shape[0], b[site + 1], self.phys_dim), np.complex128)
+        _check(_lib.lib().mpsg_contract_site(self._h, site, env.ctypes.data_as(_lib._pd), env.shape[0],
+                                             out.ctypes.data_as(_lib._pd)))
+        return out
+
+
+def device_draws(seed: int, first: int, count: int, site: int) -> np.ndarray:
+    """detail::measurement_draws (sampler.cpp:120-127) computed on the GPU."""
+    out = np.empty(count, np.float64)
+    _check(_lib.lib().mpsg_device_draws(seed, first, count, site, out.ctypes.data_as(_lib._pd)))
+    return out
+
+
+def sample_micro_serial(sampler: GpuSampler, first: int, count: int, opts: SamplerOptions,
+                        rows: np.ndarray, stats: RunStats) -> None:
+    """detail::sample_micro_serial (sampler.hpp:103-104) on a resident GpuSampler."""
+    sampler.sample(first, count, opts.seed, stats=stats, out=rows)
+
+
+def sample_batch(mps: MpsState, plan: BatchPlan, opts: SamplerOptions,
+                 stats: Optional[RunStats] = None, devices: Optional[Sequence[int]] = None) -> SampleBatch:
+    """mpsamp::sample_batch (sampler.cpp:164-205) on the B200.
+
+    The batch plan is validated and normalised exactly like the reference; outcomes do not depend
+    on N1/N2 (keyed RNG), so the GPU processes the whole range in passes of its own size.
+    """
+    mps.validate()
+    opts.policy.validate()
+    plan = BatchPlan(plan.total_samples, plan.macro_batch, plan.micro_batch)
+    plan.normalize()
+    if opts.schedule is not None:
+        raise ConfigError("bond schedules are not supported by the GPU sweep (out of scope)")
+    if opts.site_transform is not None:
+        raise ConfigError("site transforms are not supported by the GPU sweep (out of scope)")
+    t0 = time.perf_counter()
+    smp = GpuSampler(mps, opts.policy, opts.mode, devices, opts.pass_samples,
+                     record_site_times=stats is not None)
+    try:
+        st = stats if stats is not None else RunStats()
+        rows = smp.sample(0, plan.total_samples, opts.seed, stats=st)
+    finally:
+        smp.close()
+    if stats is not None:
+        stats.total_seconds = time.perf_counter() - t0
+    return SampleBatch(plan.total_samples, mps.num_sites, mps.phys_dim, opts.seed, rows)

@@ -1,0 +1,133 @@
+"""GPU parity: the CUDA sweep (through the C ABI) against the CPU oracle on the same MPS and seed.
+
+The oracle consumes the *decoded* compressed Gamma (mpsg_decoded_gamma), i.e. exactly the values
+the GPU samples.  Tolerances (north star, BASELINE.json):
+  * per-site marginals: relative 1e-4 (absolute 1e-7 for p < 1e-3);
+  * outcome strings identical except draws within EPS_BOUNDARY of a CDF boundary, which are
+    counted and reported (north-star rule: 1e-6).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+MARG_RTOL = 1e-4
+MARG_ATOL_SMALL = 1e-7
+EPS_BOUNDARY = 1e-6
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2512_20064_b200 as P
+    if P.sampler._lib.lib().mpsg_device_count() == 0:
+        pytest.fail("no B200 visible to libmpsg (GPU test on a non-GPU host)")
+    return P
+
+
+def to_state(P, mps: O.Mps):
+    return P.MpsState(mps.num_sites, mps.phys_dim, list(mps.bond_dims), list(mps.gammas), list(mps.lambdas))
+
+
+def decoded_mps(smp, mps: O.Mps) -> O.Mps:
+    out = O.Mps(mps.phys_dim, list(mps.bond_dims))
+    for i in range(mps.num_sites):
+        out.gammas.append(smp.decoded_gamma(i))
+        out.lambdas.append(mps.lambdas[i])
+    return out
+
+
+def boundary_distance(marg_row: np.ndarray, u: float) -> float:
+    """Distance of draw u to the nearest interior CDF boundary of one site's distribution."""
+    cum = np.cumsum(marg_row)[:-1]
+    return float(np.min(np.abs(cum - u))) if cum.size else 1.0
+
+
+def compare_strings(gpu_rows, ref_rows, marg_ref, seed, first=0):
+    """Returns (#differing samples, #explained by boundary draws).  A sample's string may differ
+    only from the first site whose draw lies within EPS_BOUNDARY of a reference CDF boundary."""
+    diff = np.nonzero((gpu_rows != ref_rows).any(axis=1))[0]
+    explained = 0
+    for n in diff:
+        i = int(np.argmax(gpu_rows[n] != ref_rows[n]))
+        u = O.orc().orc_uniform(seed, O.MEASURE_STREAM, first + int(n), i)
+        if boundary_distance(marg_ref[n, i], u) < EPS_BOUNDARY:
+            explained += 1
+    return len(diff), explained
+
+
+def test_device_rng_bit_exact(pkg):
+    L = O.orc()
+    for seed, first, site in [(7, 0, 0), (7, 0, 1), (123456789, 999990, 1023), (2**64 - 1, 2**63, 5)]:
+        got = pkg.device_draws(seed, first, 64, site)
+        want = np.array([L.orc_uniform(seed, O.MEASURE_STREAM, first + j, site) for j in range(64)])
+        assert np.array_equal(got, want)
+    assert pkg.device_draws(7, 0, 1, 0)[0] == 0.91427399614005611
+
+
+def test_decode_close_to_input(pkg, gold):
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    smp = pkg.GpuSampler(to_state(pkg, mps))
+    for i in range(mps.num_sites):
+        g, dg = mps.gammas[i], smp.decoded_gamma(i)
+        # per-column relative error <= fp16 half-ulp of the column max (plus subnormal floor)
+        colmax = np.maximum(np.abs(g.real), np.abs(g.imag)).max(axis=0, keepdims=True)
+        err = np.maximum(np.abs(g.real - dg.real), np.abs(g.imag - dg.imag))
+        assert (err <= colmax * 2.0 ** -10 + 1e-300).all(), i
+
+
+@pytest.mark.parametrize("mode", ["split", "single"])
+def test_contract_site_numerics(pkg, gold, mode):
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    smp = pkg.GpuSampler(to_state(pkg, mps), mode=pkg.Mode.SPLIT if mode == "split" else pkg.Mode.SINGLE)
+    rng = np.random.default_rng(3)
+    tol = 2e-6 if mode == "split" else 2e-3
+    for i in [0, 1, 2, 5, 13, 14, 15]:
+        gd = smp.decoded_gamma(i)
+        cl = gd.shape[0]
+        env = rng.standard_normal((300, cl)) + 1j * rng.standard_normal((300, cl))
+        got = smp.contract_site(i, env)
+        want = np.einsum("nl,lrk->nrk", env, gd)
+        scale = np.abs(want).max(axis=(1, 2), keepdims=True)
+        rel = (np.abs(got - want) / scale).max()
+        assert rel < tol, (i, rel)
+
+
+@pytest.mark.parametrize("name", ["c1", "c1b"])
+def test_c1_strings_and_marginals(pkg, gold, name):
+    z = np.load(f"{gold}/{name}.npz")
+    mps = O.load_npz_mps(z)
+    n, seed = int(z["n"]), int(z["seed"])
+    smp = pkg.GpuSampler(to_state(pkg, mps), pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX))
+    dec = decoded_mps(smp, mps)
+    ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, n, seed, want_marginals=True)
+    gpu_rows = smp.sample(0, n, seed)
+    # teacher-forced GPU marginals along the reference's own outcome strings
+    gpu_marg = smp.marginals(0, ref_rows)
+    live = ref_marg >= 0
+    big = live & (ref_marg >= 1e-3)
+    small = live & (ref_marg < 1e-3)
+    rel = np.abs(gpu_marg[big] - ref_marg[big]) / ref_marg[big]
+    assert rel.max() < MARG_RTOL, rel.max()
+    assert np.abs(gpu_marg[small] - ref_marg[small]).max() < MARG_ATOL_SMALL
+    ndiff, explained = compare_strings(gpu_rows, ref_rows, ref_marg, seed)
+    assert ndiff == explained, (ndiff, explained)
+
+
+def test_c1_sample_batch_api(pkg, gold):
+    """sample_batch through the reference-shaped API; batching plan must not change outcomes."""
+    z = np.load(f"{gold}/c1.npz")
+    mps = O.load_npz_mps(z)
+    st = to_state(pkg, mps)
+    opts = pkg.SamplerOptions(policy=pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX), seed=7)
+    a = pkg.sample_batch(st, pkg.BatchPlan(1000, 0, 5000), opts)
+    opts.pass_samples = 128
+    b = pkg.sample_batch(st, pkg.BatchPlan(1000, 300, 77), opts)
+    assert np.array_equal(a.outcomes, b.outcomes)
+    assert a.dead_count() == 0
+    smp = pkg.GpuSampler(st, opts.policy)
+    part = smp.sample(300, 77, 7)
+    assert np.array_equal(part, a.outcomes[300:377])
