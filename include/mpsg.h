@@ -82,7 +82,8 @@ typedef struct mpsg_policy {
 typedef struct mpsg_options {
   int mode;                        /* MPSG_MODE_*, default AUTO */
   uint64_t pass_samples;           /* samples per device pass (the GEMM M extent); 0 = auto */
-  int record_site_times;           /* fill mpsg_stats.site_seconds (adds one event per site) */
+  int record_site_times;           /* 1: fill mpsg_stats.site_seconds (one event per site);
+                                      2: also time every contraction kernel (gemm_seconds) */
   int reserved[5];
 } mpsg_options;
 
@@ -95,6 +96,9 @@ typedef struct mpsg_stats {
   double* site_seconds;            /* optional caller array of length M (device time per site) */
   uint64_t issued_mma_flops;       /* real flops issued to the tensor cores (incl. padding, split) */
   uint64_t h2d_bytes, d2h_bytes;
+  double gemm_seconds;             /* device time of the contraction kernels (record_site_times 2) */
+  uint64_t gemm_flops;             /* algorithmic flops of those launches: 8 * contraction_macs */
+  uint64_t kernel_launches;        /* CUDA kernels launched by this call */
 } mpsg_stats;
 
 typedef struct mpsg_handle_s* mpsg_handle;

@@ -7,7 +7,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmpsg.so")
+LIB_PATH = os.environ.get("MPSG_LIB_PATH") or os.path.join(HERE, "libmpsg.so")
 
 MPSG_OK, MPSG_ERR_INTERNAL, MPSG_ERR_CONFIG, MPSG_ERR_NUMERIC, MPSG_ERR_IO, MPSG_ERR_CUDA = 0, 1, 2, 3, 4, 5
 
@@ -34,7 +34,8 @@ class Options(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("contraction_macs", _u64), ("measure_weight_macs", _u64), ("dead_samples", _u64),
                 ("seconds", _dbl), ("site_seconds", _pd), ("issued_mma_flops", _u64),
-                ("h2d_bytes", _u64), ("d2h_bytes", _u64)]
+                ("h2d_bytes", _u64), ("d2h_bytes", _u64), ("gemm_seconds", _dbl),
+                ("gemm_flops", _u64), ("kernel_launches", _u64)]
 
 
 # (name, restype, argtypes) for every entry point of include/mpsg.h

@@ -134,7 +134,8 @@ struct DevCtx {
   size_t src_bytes = 0;
   int* err = nullptr;
   uint8_t* host_rows = nullptr;  // pinned [cap][M]
-  std::vector<cudaEvent_t> ev;
+  std::vector<cudaEvent_t> ev;   // per-site boundaries (M + 1)
+  std::vector<cudaEvent_t> gev;  // per-site GEMM start/stop (2 M)
 };
 
 }  // namespace mpsg
@@ -204,7 +205,8 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
   CUDA_OK(cudaDeviceGetAttribute(&dc.num_sms, cudaDevAttrMultiProcessorCount, dc.device));
   CUDA_OK(cudaStreamCreateWithFlags(&dc.stream, cudaStreamNonBlocking));
   const int kmax = kmax_of(h), chirpm = chirp_max_of(h);
-  const size_t row_bytes = 8ull * kmax + 8ull * h.d * chirpm + 8ull * h.d * (chirpm / kBN) + 1 + h.M;
+  const size_t nt_max = h.d * (chirpm / kBN) + 1;  // + the pair-padding tile
+  const size_t row_bytes = 8ull * kmax + 8ull * h.d * chirpm + 8ull * nt_max + 1 + h.M;
   uint64_t want = h.opts.pass_samples;
   if (want == 0) {
     const double budget = 6.0e9;  // bytes of per-pass working set
@@ -214,7 +216,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
   dc.sites.resize(h.M);
   CUDA_OK(cudaMalloc(&dc.env, 4ull * dc.cap * kmax * sizeof(__half)));
   CUDA_OK(cudaMalloc(&dc.temp, 1ull * dc.cap * h.d * chirpm * sizeof(float2)));
-  CUDA_OK(cudaMalloc(&dc.pstat, 1ull * dc.cap * h.d * (chirpm / kBN) * sizeof(float2)));
+  CUDA_OK(cudaMalloc(&dc.pstat, 1ull * dc.cap * nt_max * sizeof(float2)));
   CUDA_OK(cudaMalloc(&dc.alive, dc.cap));
   CUDA_OK(cudaMalloc(&dc.rows, 1ull * dc.cap * h.M));
   CUDA_OK(cudaMalloc(&dc.err, sizeof(int)));
@@ -243,6 +245,7 @@ static void free_device(DevCtx& dc) {
   cudaFree(dc.err);
   if (dc.host_rows) cudaFreeHost(dc.host_rows);
   for (auto e : dc.ev) cudaEventDestroy(e);
+  for (auto e : dc.gev) cudaEventDestroy(e);
   if (dc.stream) cudaStreamDestroy(dc.stream);
 }
 
@@ -254,7 +257,7 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
   s.chir = static_cast<int>(h.bonds[i + 1]);
   s.kp = round_up(s.chil, kBK);
   s.chirp = round_up(s.chir, kBN);
-  s.np = static_cast<int>(h.d) * s.chirp;
+  s.np = round_up(static_cast<int>(h.d) * s.chirp, 2 * kBN);  // whole N-tile pairs (CTA pairs)
   s.nt = s.np / kBN;
   if (!s.g) {
     CUDA_OK(cudaMalloc(&s.g, 2ull * s.np * s.kp * sizeof(__half)));
@@ -333,14 +336,16 @@ static void set_site(mpsg_handle_s& h, uint64_t i, const void* gamma, bool is_de
 // the sweep
 // ---------------------------------------------------------------------------------------------
 struct PassOut {
-  uint64_t macs = 0, wmacs = 0, issued = 0;
+  uint64_t macs = 0, wmacs = 0, issued = 0, launches = 0;
+  double gemm_s = 0.0;
 };
 
 // Runs one pass of `count` (<= cap) samples starting at global index `first` on dc.
 static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first, int count,
-                     const uint8_t* forced_dev, double* marg_dev, PassOut& po, bool timing) {
+                     const uint8_t* forced_dev, double* marg_dev, PassOut& po, int timing) {
   const int rows = round_up(count, kBM);
   launch_init_env(dc.env, dc.cap, dc.sites[0].kp, rows, count, dc.alive, dc.stream);
+  po.launches += 1;
   for (uint64_t i = 0; i < h.M; ++i) {
     const SiteDev& s = dc.sites[i];
     SiteGemmArgs ga;
@@ -351,12 +356,14 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
     ga.np = s.np;
     ga.chirp = s.chirp;
     ga.d = static_cast<int>(h.d);
-    ga.group_n = std::min(s.nt, 8);
+    ga.group_n = std::min(s.nt / 2, 4);
     ga.cinfo = s.cinfo;
     ga.temp = dc.temp;
     ga.pstat = dc.pstat;
-    const int tiles = ga.m_tiles * ga.n_tiles;
+    const int tiles = ga.m_tiles * ga.n_tiles;  // = 2 x (tile-pair units)
+    if (timing >= 2) CUDA_OK(cudaEventRecord(dc.gev[2 * i], dc.stream));
     launch_site_gemm(h.split, s.tma_env, s.tma_g, ga, std::min(tiles, dc.num_sms), dc.stream);
+    if (timing >= 2) CUDA_OK(cudaEventRecord(dc.gev[2 * i + 1], dc.stream));
 
     SelectArgs sa;
     sa.site = static_cast<int>(i);
@@ -381,6 +388,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
     sa.marg = marg_dev;
     launch_select(sa, dc.stream);
     if (timing) CUDA_OK(cudaEventRecord(dc.ev[i + 1], dc.stream));
+    po.launches += 2;
     po.macs += static_cast<uint64_t>(count) * s.chil * s.chir * h.d;
     po.wmacs += static_cast<uint64_t>(count) * s.chir * h.d;
     po.issued += 8ull * rows * s.np * s.kp * (h.split ? 2 : 1);
@@ -400,10 +408,14 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
                       const uint8_t* forced_host, double* marg_host, RangeResult& rr) {
   try {
     CUDA_OK(cudaSetDevice(dc.device));
-    const bool timing = h.opts.record_site_times != 0;
+    const int timing = h.opts.record_site_times;
     if (timing && dc.ev.empty()) {
       dc.ev.resize(h.M + 1);
       for (auto& e : dc.ev) CUDA_OK(cudaEventCreate(&e));
+    }
+    if (timing >= 2 && dc.gev.empty()) {
+      dc.gev.resize(2 * h.M);
+      for (auto& e : dc.gev) CUDA_OK(cudaEventCreate(&e));
     }
     if (timing) rr.site_ms.assign(h.M, 0.0);
     if ((forced_host || marg_host) && !dc.forced) {
@@ -438,6 +450,10 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
           float ms = 0.f;
           CUDA_OK(cudaEventElapsedTime(&ms, dc.ev[i], dc.ev[i + 1]));
           rr.site_ms[i] += ms;
+          if (timing >= 2) {
+            CUDA_OK(cudaEventElapsedTime(&ms, dc.gev[2 * i], dc.gev[2 * i + 1]));
+            rr.po.gemm_s += ms * 1e-3;
+          }
         }
       }
     }
@@ -473,11 +489,16 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
     if (r.err) std::rethrow_exception(r.err);
   if (st) {
     st->contraction_macs = st->measure_weight_macs = st->issued_mma_flops = 0;
+    st->kernel_launches = 0;
+    st->gemm_seconds = 0.0;
     for (auto& r : rr) {
       st->contraction_macs += r.po.macs;
       st->measure_weight_macs += r.po.wmacs;
       st->issued_mma_flops += r.po.issued;
+      st->kernel_launches += r.po.launches;
+      st->gemm_seconds = std::max(st->gemm_seconds, r.po.gemm_s);  // devices run concurrently
     }
+    st->gemm_flops = 8 * st->contraction_macs;
     st->dead_samples = 0;
     if (rows_host)
       for (uint64_t n = 0; n < count; ++n) st->dead_samples += rows_host[n * h.M + h.M - 1] == kDead;
@@ -754,7 +775,7 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
     ga.np = s.np;
     ga.chirp = s.chirp;
     ga.d = static_cast<int>(h->d);
-    ga.group_n = std::min(s.nt, 8);
+    ga.group_n = std::min(s.nt / 2, 4);
     ga.cinfo = s.cinfo;
     ga.temp = dc.temp;
     ga.pstat = dc.pstat;

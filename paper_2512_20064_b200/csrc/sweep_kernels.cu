@@ -18,6 +18,8 @@
 #include <stdint.h>
 
 #include "ptx.cuh"
+
+
 #include "sweep.cuh"
 
 namespace mpsg {
@@ -55,14 +57,18 @@ struct GemmCfg {
 
 int gemm_smem_bytes(bool split) { return split ? GemmCfg<true>::kSmem : GemmCfg<false>::kSmem; }
 
-__device__ __forceinline__ void tile_coords(int t, const SiteGemmArgs& a, int& m, int& n) {
+// Work unit = (M tile, pair of N tiles); the two CTAs of a cluster share the unit's env (A) tiles
+// through TMA multicast and each computes one of the two N tiles.  Units are rastered in groups
+// of `group_n` N-tile pairs so concurrently running clusters reuse Gamma tiles from L2.
+__device__ __forceinline__ void unit_coords(int u, const SiteGemmArgs& a, int& m, int& np) {
+  const int pairs = a.n_tiles >> 1;
   const int per_group = a.group_n * a.m_tiles;
-  const int g = t / per_group;
+  const int g = u / per_group;
   const int n0 = g * a.group_n;
-  const int gw = min(a.group_n, a.n_tiles - n0);
-  const int r = t - g * per_group;
+  const int gw = min(a.group_n, pairs - n0);
+  const int r = u - g * per_group;
   m = r / gw;
-  n = n0 + (r - m * gw);
+  np = n0 + (r - m * gw);
 }
 
 template <bool kSplit>
@@ -81,11 +87,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int rank = static_cast<int>(ptx::cluster_ctarank());  // 0 / 1 within the CTA pair
+  const int cluster = blockIdx.x >> 1;
+  const int num_clusters = gridDim.x >> 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&full[s], 1);   // own producer's expect_tx; bytes arrive from both CTAs
+      ptx::mbar_init(&empty[s], 2);  // released by the MMA commits of both CTAs
     }
     for (int j = 0; j < 2; ++j) {
       ptx::mbar_init(&tfull[j], 1);
@@ -103,9 +112,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
+  ptx::cluster_sync();  // peer barriers initialised before any multicast / remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int total = a.m_tiles * a.n_tiles;
+  const int units = a.m_tiles * (a.n_tiles >> 1);
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -114,17 +124,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_g = ptx::l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        int m, n;
-        tile_coords(t, a, m, n);
+      for (int u = cluster; u < units; u += num_clusters) {
+        int m, np;
+        unit_coords(u, a, m, np);
+        const int n = 2 * np + rank;
         for (int kb = 0; kb < a.k_blocks; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_wait(&empty[stage], phase ^ 1);  // free in both CTAs
           uint8_t* st = smem + stage * C::kStageBytes;
           ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
 #pragma unroll
-          for (int q = 0; q < C::kAPlanes; ++q)
-            ptx::tma_load_2d(&tma_env, &full[stage], st + q * C::kTile, kb * kBK,
-                             q * a.plane_rows_a + m * kBM, pol_env);
+          for (int q = rank; q < C::kAPlanes; q += 2)  // this CTA's half of the env planes
+            ptx::tma_load_2d_mc(&tma_env, &full[stage], st + q * C::kTile, kb * kBK,
+                                q * a.plane_rows_a + m * kBM, 0x3, pol_env);
 #pragma unroll
           for (int p = 0; p < 2; ++p)
             ptx::tma_load_2d(&tma_g, &full[stage], st + (C::kAPlanes + p) * C::kTile, kb * kBK,
@@ -145,7 +156,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int u = cluster; u < units; u += num_clusters) {
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_re = tmem_base + acc * 256;
@@ -160,25 +171,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint64_t br = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 0) * C::kTile + off);
             const uint64_t bi = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 1) * C::kTile + off);
             const uint32_t accum = (kb | ks) ? 1u : 0u;
-            {
-              const uint64_t ar = ptx::sdesc_kmajor_sw64(st + 0 * C::kTile + off);
-              const uint64_t ai = ptx::sdesc_kmajor_sw64(st + 1 * C::kTile + off);
-              // Re += Er.Gr - Ei.Gi ; Im += Er.Gi + Ei.Gr
-              ptx::umma_f16_ss(d_re, ar, br, kId, accum);
+            // Re += Er.Gr - Ei.Gi ; Im += Er.Gi + Ei.Gr.  The Er tile feeds two consecutive MMAs
+            // through the A collector (read from shared memory once).  The collector is not used
+            // for the Ei pair: reuse combined with an operand negation gives wrong results.
+#pragma unroll
+            for (int h = 0; h < (kSplit ? 2 : 1); ++h) {
+              const uint32_t acc0 = h ? 1u : accum;
+              const uint64_t ar = ptx::sdesc_kmajor_sw64(st + (2 * h + 0) * C::kTile + off);
+              const uint64_t ai = ptx::sdesc_kmajor_sw64(st + (2 * h + 1) * C::kTile + off);
+              ptx::umma_f16_ss_afill(d_re, ar, br, kId, acc0);
+              ptx::umma_f16_ss_alast(d_im, ar, bi, kId, acc0);
               ptx::umma_f16_ss(d_re, ai, bi, kIdNeg, 1u);
-              ptx::umma_f16_ss(d_im, ar, bi, kId, accum);
-              ptx::umma_f16_ss(d_im, ai, br, kId, 1u);
-            }
-            if constexpr (kSplit) {
-              const uint64_t ar = ptx::sdesc_kmajor_sw64(st + 2 * C::kTile + off);
-              const uint64_t ai = ptx::sdesc_kmajor_sw64(st + 3 * C::kTile + off);
-              ptx::umma_f16_ss(d_re, ar, br, kId, 1u);
-              ptx::umma_f16_ss(d_re, ai, bi, kIdNeg, 1u);
-              ptx::umma_f16_ss(d_im, ar, bi, kId, 1u);
               ptx::umma_f16_ss(d_im, ai, br, kId, 1u);
             }
           }
-          ptx::umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+          ptx::umma_commit_mc(&empty[stage], 0x3);  // slot free in both CTAs once MMAs retire
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
@@ -194,37 +201,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      int m, n;
-      tile_coords(t, a, m, n);
+    for (int u = cluster; u < units; u += num_clusters) {
+      int m, np;
+      unit_coords(u, a, m, np);
+      const int n = 2 * np + rank;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       const int row = m * kBM + q * 32 + lane;
       const int col0 = n * kBN;
       const int k = col0 / a.chirp;
-      const int r0 = col0 - k * a.chirp;
-      float2* dst = a.temp + (static_cast<size_t>(row) * a.d + k) * a.chirp + r0;
-      const float2* ci = a.cinfo + col0;
-      const uint32_t tb = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
-      float w = 0.f, mx = 0.f;
+      if (k < a.d) {  // the N padding tile (odd tile count) has nothing to store
+        const int r0 = col0 - k * a.chirp;
+        float2* dst = a.temp + (static_cast<size_t>(row) * a.d + k) * a.chirp + r0;
+        const float2* ci = a.cinfo + col0;
+        const uint32_t tb = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
+        float w = 0.f, mx = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < kBN / 32; ++c) {
-        float re[32], im[32];
-        ptx::tmem_ld_32x32b_x32(tb + c * 32, re);
-        ptx::tmem_ld_32x32b_x32(tb + 128 + c * 32, im);
-        ptx::tmem_wait_ld();
+        for (int c = 0; c < kBN / 32; ++c) {
+          float re[32], im[32];
+          ptx::tmem_ld_32x32b_x32(tb + c * 32, re);
+          ptx::tmem_ld_32x32b_x32(tb + 128 + c * 32, im);
+          ptx::tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const float4 cc = *reinterpret_cast<const float4*>(ci + c * 32 + j);  // (cs0, wl0, cs1, wl1)
-          const float tr0 = re[j] * cc.x, ti0 = im[j] * cc.x;
-          const float tr1 = re[j + 1] * cc.z, ti1 = im[j + 1] * cc.z;
-          w = fmaf(cc.y, fmaf(tr0, tr0, ti0 * ti0), w);
-          w = fmaf(cc.w, fmaf(tr1, tr1, ti1 * ti1), w);
-          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(tr0), fabsf(ti0)), fmaxf(fabsf(tr1), fabsf(ti1))));
-          *reinterpret_cast<float4*>(dst + c * 32 + j) = make_float4(tr0, ti0, tr1, ti1);
+          for (int j = 0; j < 32; j += 2) {
+            const float4 cc = *reinterpret_cast<const float4*>(ci + c * 32 + j);  // (cs0, wl0, cs1, wl1)
+            const float tr0 = re[j] * cc.x, ti0 = im[j] * cc.x;
+            const float tr1 = re[j + 1] * cc.z, ti1 = im[j + 1] * cc.z;
+            w = fmaf(cc.y, fmaf(tr0, tr0, ti0 * ti0), w);
+            w = fmaf(cc.w, fmaf(tr1, tr1, ti1 * ti1), w);
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(tr0), fabsf(ti0)), fmaxf(fabsf(tr1), fabsf(ti1))));
+            *reinterpret_cast<float4*>(dst + c * 32 + j) = make_float4(tr0, ti0, tr1, ti1);
+          }
         }
+        a.pstat[static_cast<size_t>(row) * a.n_tiles + n] = make_float2(w, mx);
       }
-      a.pstat[static_cast<size_t>(row) * a.n_tiles + n] = make_float2(w, mx);
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
       acc ^= 1;
@@ -234,31 +244,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  ptx::cluster_sync();  // no remote arrive / multicast may target an exited peer
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, 512);
   }
 }
 
+template <bool kSplit>
+static void launch_gemm_t(const CUtensorMap& tma_env, const CUtensorMap& tma_g,
+                          const SiteGemmArgs& a, int grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(site_gemm_kernel<kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         GemmCfg<kSplit>::kSmem);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = GemmCfg<kSplit>::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, site_gemm_kernel<kSplit>, tma_env, tma_g, a);
+}
+
 void launch_site_gemm(bool split, const CUtensorMap& tma_env, const CUtensorMap& tma_g,
                       const SiteGemmArgs& a, int grid, cudaStream_t s) {
-  if (split) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(site_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           GemmCfg<true>::kSmem);
-      attr = true;
-    }
-    site_gemm_kernel<true><<<grid, kGemmThreads, GemmCfg<true>::kSmem, s>>>(tma_env, tma_g, a);
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(site_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           GemmCfg<false>::kSmem);
-      attr = true;
-    }
-    site_gemm_kernel<false><<<grid, kGemmThreads, GemmCfg<false>::kSmem, s>>>(tma_env, tma_g, a);
-  }
+  grid = (grid + 1) & ~1;  // whole CTA pairs
+  if (split)
+    launch_gemm_t<true>(tma_env, tma_g, a, grid, s);
+  else
+    launch_gemm_t<false>(tma_env, tma_g, a, grid, s);
 }
 
 // ============================================================================================

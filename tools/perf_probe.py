@@ -1,0 +1,41 @@
+"""Perf probe: per-site device times and algorithmic TFLOP/s for a synthetic chain.
+
+usage: python tools/perf_probe.py M CHI D N [mode] [pass]
+"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2512_20064_b200 as P  # noqa: E402
+from paper_2512_20064_b200.synthetic import build_synthetic  # noqa: E402
+
+M, chi, d, N = (int(x) for x in sys.argv[1:5])
+mode = P.Mode.SINGLE if len(sys.argv) > 5 and sys.argv[5] == "single" else P.Mode.SPLIT
+ps = int(sys.argv[6]) if len(sys.argv) > 6 else 0
+t = time.time()
+smp, lams = build_synthetic(M, chi, d, mode=mode, pass_samples=ps or N, record_site_times=True)
+print(f"build {time.time()-t:.1f}s state {smp.state_bytes/1e9:.2f} GB", flush=True)
+bonds = smp.bond_dims
+rows = torch.empty((N, M), dtype=torch.uint8, device="cuda")
+for rep in range(3):
+    st = P.RunStats()
+    torch.cuda.synchronize()
+    t = time.time()
+    out = smp.sample(0, N, 7, stats=st)
+    el = time.time() - t
+    flops = 8.0 * N * sum(bonds[i] * bonds[i + 1] * d for i in range(M))
+    ss = np.array(st.site_seconds)
+    print(f"rep {rep}: {el:.3f}s  {N/el:.0f} samples/s  alg {flops/el/1e12:.1f} TF/s  issued {st.issued_mma_flops/el/1e12:.1f} TF/s"
+          f"  sum(site) {ss.sum():.3f}s  dead {st.dead_samples}", flush=True)
+full = [i for i in range(M) if bonds[i] == chi and bonds[i + 1] == chi]
+if full:
+    i = full[len(full) // 2]
+    f_site = 8.0 * N * chi * chi * d
+    print(f"interior site {i}: {ss[i]*1e3:.2f} ms -> alg {f_site/ss[i]/1e12:.1f} TF/s", flush=True)
+print("first rows", out[:2], flush=True)
+print("outcome histogram site 10:", np.bincount(out[:, min(10, M - 1)], minlength=d), flush=True)
