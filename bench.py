@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MPS sampling sweep (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--pass P] [--impl ours|reference]
+
+A *step* is one pass of the hot path — the full left-to-right sweep over all M sites (contract,
+Born weights, keyed draw, gather + renormalise) — for P samples per GPU.  Inputs (the compressed
+MPS) are resident in HBM before the timed region; the MPS (102 GB at c3) is far larger than L2,
+so no flush is needed between steps.  `value` = samples/s of the whole job (all ranks), device
+time from CUDA events on the engine's stream, max over ranks.  Multi-GPU: one process per GPU
+(torchrun), data-parallel over disjoint global sample ranges with no data-path collective
+(the keyed RNG makes outcomes partition-independent), so scaling is "weak".
+
+--impl reference times the reference's own CPU sampler (oracle/_ref, the unmodified reference
+compiled from its sources) on this host's cores for the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/sec (M=1024, χ=2048) at 1/2/4/8 B200; % of tensor-core roofline"
+CONFIGS = {
+    "c1": dict(M=16, chi=32, d=4, job=1000, desc="c1: M=16, chi=32, d=4, N=1000"),
+    "c2": dict(M=256, chi=512, d=6, job=100_000, desc="c2: M=256, chi=512, d=6, N=1e5 (whole MPS in HBM)"),
+    "c3": dict(M=1024, chi=2048, d=6, job=1_000_000, desc="c3: M=1024, chi=2048, d=6, N=1e6 data-parallel"),
+    "c5_1024": dict(M=512, chi=1024, d=4, job=100_000, desc="c5: M=512, chi=1024, d=4, N=1e5"),
+    "c5_4096": dict(M=512, chi=4096, d=4, job=100_000, desc="c5: M=512, chi=4096, d=4, N=1e5"),
+}
+DEFAULT_PASS = {"c1": 1000, "c2": 32768, "c3": 16384, "c5_1024": 32768, "c5_4096": 8192}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p["bf16_tflops_sustained"], p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def chain_macs(M, chi, d):
+    from paper_2512_20064_b200.sampler import capped_bond_dims
+    b = capped_bond_dims(M, d, chi)
+    return sum(b[i] * b[i + 1] * d for i in range(M)), b
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [l.split(", ") for l in self.lines if l and l[0].isdigit()]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4)
+                          if len(r) > 5 + j and r[5 + j].strip() == "Active"})
+        load = sorted(sm)[len(sm) // 2:] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU reference timing (oracle/_ref = the reference compiled from its own sources)
+# ---------------------------------------------------------------------------------------------
+def cpu_reference_rate(chi: int, d: int, target_s: float = 8.0, threads: int | None = None):
+    """Times the reference hot step (contract_site + measure + scale, sampler.cpp:140-158) on a
+    full-chi interior site with all host threads; returns (complex MAC/s, threads, kind, sample)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ctypes as C
+
+    import oracle as O
+
+    threads = threads or os.cpu_count() or 1
+    rng = np.random.default_rng(5)
+    g = (rng.standard_normal((chi, chi, d)) + 1j * rng.standard_normal((chi, chi, d))) / np.sqrt(chi * d)
+    lam = np.sort(rng.uniform(0.1, 1.0, chi))[::-1].copy()
+    lam /= np.sqrt((lam * lam).sum())
+    mps = O.Mps(d, [chi, chi], [g], [lam])
+    if O.have_ref():
+        kind = "reference"
+        rs = O.RefState(mps)
+        t1, m1 = rs.time_site_step(0, 1, threads)
+        count = max(1, int(target_s / max(t1, 1e-3)))
+        secs, macs = rs.time_site_step(0, count, threads)
+    else:  # the plain-C restatement (oracle/mpsamp_oracle.c), one thread
+        kind = "port"
+        threads = 1
+        t1, _ = O.orc_time_site_step(g, lam, 1)
+        count = max(1, int(target_s / max(t1, 1e-3)))
+        secs, macs = O.orc_time_site_step(g, lam, count)
+    sample = (f"contract_site+measure+scale at one chi={chi}, d={d} interior site, {count} samples x "
+              f"{threads} threads, extrapolated over the chain's complex MACs")
+    return macs / secs, threads, kind, sample, secs
+
+
+def run_reference_arm(args, cfg):
+    """--impl reference: the reference CPU sampler on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    macs_per_sample, _ = chain_macs(cfg["M"], cfg["chi"], cfg["d"])
+    vals = []
+    for step in range(args.warmup + args.steps):
+        rate, threads, kind, sample, secs = cpu_reference_rate(cfg["chi"], cfg["d"], target_s=args.ref_seconds)
+        if step >= args.warmup:
+            vals.append(rate / macs_per_sample)
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (random dense site)",
+            "config": {"workload": cfg["desc"], "M": cfg["M"], "chi": cfg["chi"], "d": cfg["d"],
+                       "parallelism": f"host threads x{threads}"},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": kind, "sample": sample},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--pass", dest="pass_samples", type=int, default=0)
+    ap.add_argument("--mode", default="split", choices=["split", "single"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2512_20064_b200 as P
+    from paper_2512_20064_b200.synthetic import build_synthetic
+
+    P_pass = args.pass_samples or DEFAULT_PASS[args.config]
+    mode = P.Mode.SPLIT if args.mode == "split" else P.Mode.SINGLE
+    t0 = time.perf_counter()
+    smp, _ = build_synthetic(cfg["M"], cfg["chi"], cfg["d"], seed=42, mode=mode, devices=[local],
+                             pass_samples=P_pass, record_site_times=2,
+                             policy=P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX))
+    build_s = time.perf_counter() - t0
+    macs_per_sample, bonds = chain_macs(cfg["M"], cfg["chi"], cfg["d"])
+    rows_dev = torch.empty((P_pass, cfg["M"]), dtype=torch.uint8, device="cuda")
+
+    def step(it):
+        st = P.RunStats()
+        first = (it * world + rank) * P_pass
+        rows = smp.sample(first, P_pass, 7, stats=st)  # host rows; device time from events
+        return st, rows
+
+    def device_step(it):
+        st = P.RunStats()
+        first = (it * world + rank) * P_pass
+        L = P.sampler._lib
+        s = L.Stats()
+        site = np.zeros(cfg["M"], np.float64)
+        s.site_seconds = site.ctypes.data_as(L._pd)
+        P.sampler._check(L.lib().mpsg_sample_device(smp._h, 7, first, P_pass, __import__("ctypes").c_void_p(rows_dev.data_ptr()),
+                                                    __import__("ctypes").byref(s)))
+        st.contraction_macs = s.contraction_macs
+        st.issued_mma_flops = s.issued_mma_flops
+        st.site_seconds = site
+        return st, s
+
+    for w in range(args.warmup):
+        device_step(w)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    dev_s, gemm_s, gemm_flops, issued, launches = 0.0, 0.0, 0, 0, 0
+    wall0 = time.perf_counter()
+    for it in range(args.steps):
+        st, s = device_step(args.warmup + it)
+        dev_s += float(np.sum(st.site_seconds))
+        gemm_s += s.gemm_seconds
+        gemm_flops += s.gemm_flops
+        issued += s.issued_mma_flops
+        launches += s.kernel_launches
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    clocks = clk.stop()
+    t_max = dev_s
+    if dist:
+        tt = torch.tensor([dev_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+        dist.barrier()
+
+    # e2e through the C ABI with host buffers (rows D2H inside the timed region)
+    e2e_s = 0.0
+    for it in range(args.e2e_steps):
+        t = time.perf_counter()
+        step(args.warmup + args.steps + it)
+        e2e_s += time.perf_counter() - t
+    e2e = P_pass * args.e2e_steps * world / e2e_s if e2e_s > 0 else None
+    if dist and e2e_s > 0:
+        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = P_pass * args.e2e_steps * world / float(tt.item())
+
+    value = P_pass * world * args.steps / t_max
+    burst, sustained, hbm, src = peaks()
+    achieved = gemm_flops / gemm_s / 1e12 if gemm_s > 0 else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.mode}_p{P_pass}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, threads, kind, sample, secs = cpu_reference_rate(cfg["chi"], cfg["d"], target_s=args.ref_seconds)
+        cpu = {"value": rate / macs_per_sample, "unit": "samples/s", "cores": threads, "kind": kind,
+               "sample": sample, "seconds": round(secs, 2)}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f16 x (f16 hi + f16 lo) -> f32 accumulate; f64 CDF" if args.mode == "split" else
+                     "f16 x f16 -> f32 accumulate; f64 CDF",
+            "data": "synthetic random right-canonical MPS generated on device (seed 42), measurement seed 7",
+            "config": {"workload": cfg["desc"] + f"; step = one sweep of {P_pass} samples/GPU over all M sites",
+                       "M": cfg["M"], "chi": cfg["chi"], "d": cfg["d"], "pass_samples_per_gpu": P_pass,
+                       "job_samples": cfg["job"], "job_seconds_at_value": cfg["job"] / value,
+                       "mode": args.mode, "parallelism": f"dp{world}",
+                       "l2": f"inputs larger than L2 (resident compressed MPS {smp.state_bytes / 1e9:.1f} GB)",
+                       "build_seconds": round(build_s, 1)},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
+                         "frac": achieved / sustained if achieved else None, "traffic": traffic,
+                         "peak_kind": f"bf16 dense sustained ({src})",
+                         "kernel": "site_gemm_kernel (tcgen05, all sites of the sweep)",
+                         "flops_per_unit": "8*chiL*chiR*d per sample per site (4M, = 8 x contraction_macs)",
+                         "issued_tflops": issued / gemm_s / 1e12 if gemm_s > 0 else None,
+                         "issued_frac": issued / gemm_s / 1e12 / sustained if gemm_s > 0 else None,
+                         "frac_of_burst": achieved / burst if achieved else None,
+                         "gemm_share_of_step": gemm_s / dev_s if dev_s > 0 else None},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": P_pass * cfg["M"],
+                    "note": "mpsg_sample with host output rows; step inputs are (seed, first, count) scalars, "
+                            "the compressed MPS is resident"},
+            "clocks": clocks, "gpu_launches": launches, "wall_seconds": wall,
+        }
+        print(json.dumps(line), flush=True)
+    smp.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -355,3 +355,31 @@ uint64_t orc_fnv1a(const uint8_t* p, size_t n) {
     }
     return h;
 }
+
+/* CPU baseline probe for the port: one iteration of the site loop (sampler.cpp:140-158) at a
+ * single site for `count` samples from a seeded random environment, f64 + PerSampleMax.
+ * Returns the complex MACs performed (time it from the caller). */
+uint64_t orc_site_step(const double* gamma, size_t chil, size_t chir, size_t d, const double* lambda,
+                       size_t count, uint64_t seed) {
+    double* env = (double*)malloc(sizeof(double) * 2 * count * chil);
+    double* temp = (double*)malloc(sizeof(double) * 2 * count * chir * d);
+    double* next = (double*)malloc(sizeof(double) * 2 * count * chir);
+    double* draws = (double*)malloc(sizeof(double) * count);
+    uint8_t* alive = (uint8_t*)malloc(count);
+    uint8_t* oc = (uint8_t*)malloc(count);
+    for (size_t j = 0; j < 2 * count * chil; ++j) env[j] = orc_uniform(99, 1, 0, j) - 0.5;
+    for (size_t n = 0; n < count; ++n) {
+        alive[n] = 1;
+        draws[n] = orc_uniform(seed, ORC_MEASURE_STREAM, n, 0);
+    }
+    contract_f64(env, count, chil, gamma, chir, d, temp);
+    orc_measure(temp, count, chir, d, lambda, draws, alive, oc, next, NULL);
+    orc_scale_rows(next, count, chir, ORC_SCALE_PER_SAMPLE, alive);
+    free(env);
+    free(temp);
+    free(next);
+    free(draws);
+    free(alive);
+    free(oc);
+    return (uint64_t)count * chil * chir * d;
+}

@@ -33,6 +33,8 @@ int orc_sample_range(size_t m, size_t d, const size_t* bonds, const double* cons
                      double* marg, uint64_t* contraction_macs);
 void orc_capped_bond_dims(size_t m, size_t d, size_t chi_max, size_t* out);
 uint64_t orc_fnv1a(const uint8_t* p, size_t n);
+uint64_t orc_site_step(const double* gamma, size_t chil, size_t chir, size_t d, const double* lambda,
+                       size_t count, uint64_t seed);
 
 #ifdef __cplusplus
 }

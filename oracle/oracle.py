@@ -66,6 +66,8 @@ def orc():
         L.orc_capped_bond_dims.argtypes = [_sz, _sz, _sz, C.POINTER(_sz)]
         L.orc_fnv1a.restype = _u64
         L.orc_fnv1a.argtypes = [_pu8, _sz]
+        L.orc_site_step.restype = _u64
+        L.orc_site_step.argtypes = [_pd, _sz, _sz, _sz, _pd, _sz, _u64]
     return _orc
 
 
@@ -275,3 +277,14 @@ def load_npz_mps(npz, prefix: str = "") -> Mps:
         mps.gammas.append(npz[f"{prefix}gamma_{i}"])
         mps.lambdas.append(npz[f"{prefix}lambda_{i}"])
     return mps
+
+
+def orc_time_site_step(gamma: np.ndarray, lam: np.ndarray, count: int):
+    """Port CPU probe: one site step for `count` samples on one thread -> (seconds, complex MACs)."""
+    import time as _t
+    g = np.ascontiguousarray(gamma, np.complex128)
+    lam = np.ascontiguousarray(lam, np.float64)
+    cl, cr, d = g.shape
+    t0 = _t.perf_counter()
+    macs = orc().orc_site_step(g.ctypes.data_as(_pd), cl, cr, d, lam.ctypes.data_as(_pd), count, 7)
+    return _t.perf_counter() - t0, macs

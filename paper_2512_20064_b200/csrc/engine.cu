@@ -155,6 +155,10 @@ struct mpsg_handle_s {
 
 namespace mpsg {
 
+// N-tile pairs per raster group: the group's Gamma tiles (<= 2 x 16 x 1 MiB at chi = 2048) stay in
+// L2 across the M sweep while the env tiles are re-read once per group.
+constexpr int kGroupPairs = 16;
+
 static int kmax_of(const mpsg_handle_s& h) {
   int k = kBK;
   for (uint64_t b : h.bonds) k = std::max(k, round_up(static_cast<int>(b), kBK));
@@ -356,7 +360,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
     ga.np = s.np;
     ga.chirp = s.chirp;
     ga.d = static_cast<int>(h.d);
-    ga.group_n = std::min(s.nt / 2, 4);
+    ga.group_n = std::min(s.nt / 2, kGroupPairs);
     ga.cinfo = s.cinfo;
     ga.temp = dc.temp;
     ga.pstat = dc.pstat;
@@ -775,7 +779,7 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
     ga.np = s.np;
     ga.chirp = s.chirp;
     ga.d = static_cast<int>(h->d);
-    ga.group_n = std::min(s.nt / 2, 4);
+    ga.group_n = std::min(s.nt / 2, kGroupPairs);
     ga.cinfo = s.cinfo;
     ga.temp = dc.temp;
     ga.pstat = dc.pstat;

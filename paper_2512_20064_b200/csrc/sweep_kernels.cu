@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      const uint64_t pol_env = ptx::l2_policy_evict_first();
+      const uint64_t pol_env = ptx::l2_policy_evict_normal();  // re-read by every N pair of the group
       const uint64_t pol_g = ptx::l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;

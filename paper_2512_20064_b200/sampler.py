@@ -157,11 +157,13 @@ class MpsState:
 
 def capped_bond_dims(num_sites: int, phys_dim: int, chi_max: int) -> list:
     """mps.cpp:78-88: min(d^i, d^(M-i), chi_max) (double arithmetic, truncated)."""
-    out = []
-    for i in range(num_sites + 1):
-        cap = min(float(phys_dim) ** i, float(phys_dim) ** (num_sites - i), float(chi_max))
-        out.append(int(cap))
-    return out
+    def p(e):  # std::pow(double, double), +inf on overflow
+        try:
+            return float(phys_dim) ** e
+        except OverflowError:
+            return float("inf")
+
+    return [int(min(p(i), p(num_sites - i), float(chi_max))) for i in range(num_sites + 1)]
 
 
 # ---- sampler.hpp -----------------------------------------------------------------------------

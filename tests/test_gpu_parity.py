@@ -131,3 +131,15 @@ def test_c1_sample_batch_api(pkg, gold):
     smp = pkg.GpuSampler(st, opts.policy)
     part = smp.sample(300, 77, 7)
     assert np.array_equal(part, a.outcomes[300:377])
+
+
+def test_cpp_dropin_adapter_gpu():
+    """mpsg_mpsamp::sample_batch (C++ drop-in, built against the reference headers) on the B200."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "adapter_test")
+    if not os.path.exists(exe):
+        pytest.skip("adapter_test not built (needs the reference headers at build time)")
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=120)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -1,0 +1,165 @@
+"""CPU tests: the C ABI library, the host-side mirror of the reference interface, and the
+multi-rank data-parallel driver (gloo, world_size 2)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2512_20064_b200 as P
+from paper_2512_20064_b200 import _lib
+from paper_2512_20064_b200.parallel import balanced_partition, rank_range, run_data_parallel
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+# ---- C ABI ------------------------------------------------------------------------------------
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "mpsg.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(mpsg_[a-z_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    syms = header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(L, s), s
+    assert {name for name, _, _ in _lib.SIGNATURES} == set(syms)
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump --list-elf {_lib.LIB_PATH} 2>/dev/null").read()
+    assert "sm_100a" in out
+    sass = os.popen(f"cuobjdump -sass {_lib.LIB_PATH} 2>/dev/null").read()
+    assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass  # tcgen05 + TMA + TMEM
+
+
+def test_abi_basics_without_gpu():
+    L = _lib.lib()
+    assert L.mpsg_abi_version() == 1
+    if L.mpsg_device_count() == 0:
+        # no CPU fallback: a compute call fails loudly with the CUDA code
+        out = np.empty(4)
+        assert L.mpsg_device_draws(1, 0, 4, 0, out.ctypes.data_as(_lib._pd)) == _lib.MPSG_ERR_CUDA
+        assert "device" in _lib.last_error()
+
+
+def _begin(bonds, d=2, policy=(0, 0, 0)):
+    L = _lib.lib()
+    h = C.c_void_p()
+    bd = (C.c_uint64 * len(bonds))(*bonds)
+    pol = _lib.Policy(*policy)
+    rc = L.mpsg_builder_begin(len(bonds) - 1, d, bd, C.byref(pol), None, None, 0, C.byref(h))
+    if rc == 0:
+        L.mpsg_destroy(h)
+    return rc
+
+
+def test_abi_config_validation_precedes_device():
+    # MpsState::validate (mps.cpp:12-38) and PrecisionPolicy::validate (precision.cpp:98-102)
+    assert _begin([2, 2]) == _lib.MPSG_ERR_CONFIG            # boundary bonds must be 1
+    assert _begin([1, 4, 1], d=0) == _lib.MPSG_ERR_CONFIG     # phys_dim >= 1
+    assert _begin([1, 4, 1], policy=(0, 2, 0)) == _lib.MPSG_ERR_CONFIG  # tf32 storage
+    assert _begin([1, 0, 1]) == _lib.MPSG_ERR_CONFIG          # zero bond
+    assert _begin([1, 4, 1], d=300) == _lib.MPSG_ERR_CONFIG   # u8 outcomes
+
+
+# ---- host mirror of the reference interface ----------------------------------------------------
+def test_batch_plan_normalize_matches_reference():
+    p = P.BatchPlan(1000, 0, 5000)
+    p.normalize()
+    assert (p.total_samples, p.macro_batch, p.micro_batch) == (1000, 1000, 1000)
+    p = P.BatchPlan(1000, 300, 0)
+    p.normalize()
+    assert (p.macro_batch, p.micro_batch, p.macro_count()) == (300, 300, 4)
+    with pytest.raises(P.ConfigError):
+        P.BatchPlan(0).normalize()
+
+
+def test_policy_and_enums():
+    assert P.Precision.from_string("tf32") == P.Precision.TF32
+    assert P.ScalingMode.from_string("per-sample-max") == P.ScalingMode.PER_SAMPLE_MAX
+    with pytest.raises(P.ConfigError):
+        P.Precision.from_string("bf16")
+    with pytest.raises(P.ConfigError):
+        P.PrecisionPolicy(storage=P.Precision.TF32).validate()
+
+
+def test_mps_state_validation(gold):
+    z = np.load(os.path.join(gold, "c1.npz"))
+    mps = O.load_npz_mps(z)
+    st = P.MpsState(mps.num_sites, mps.phys_dim, list(mps.bond_dims), list(mps.gammas), list(mps.lambdas))
+    st.validate()
+    bad = P.MpsState(st.num_sites, st.phys_dim, list(st.bond_dims), list(st.gammas), list(st.lambdas))
+    bad.lambdas[3] = bad.lambdas[3][::-1].copy()
+    with pytest.raises(P.NumericError):
+        bad.validate()
+    bad = P.MpsState(st.num_sites, st.phys_dim, [2] + list(st.bond_dims[1:]), list(st.gammas), list(st.lambdas))
+    with pytest.raises(P.DimensionError):
+        bad.validate()
+
+
+def test_capped_bond_dims_matches_oracle():
+    for m, d, chi in [(16, 4, 32), (1024, 6, 2048), (8176, 4, 10000), (5, 7, 3)]:
+        assert P.capped_bond_dims(m, d, chi) == O.capped_bond_dims(m, d, chi)
+
+
+def test_sample_batch_rejects_out_of_scope_options(gold):
+    z = np.load(os.path.join(gold, "c1.npz"))
+    mps = O.load_npz_mps(z)
+    st = P.MpsState(mps.num_sites, mps.phys_dim, list(mps.bond_dims), list(mps.gammas), list(mps.lambdas))
+    with pytest.raises(P.ConfigError):
+        P.sample_batch(st, P.BatchPlan(10), P.SamplerOptions(schedule=object()))
+
+
+# ---- data-parallel driver ----------------------------------------------------------------------
+def test_balanced_partition_matches_reference():
+    assert balanced_partition(10, 4) == [(0, 3), (3, 6), (6, 8), (8, 10)]
+    assert rank_range(100, 7, 2, 3) == (105, 2)
+
+
+def _dp_worker(rank, world, port, gold, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    z = np.load(os.path.join(gold, "c1.npz"))
+    mps = O.load_npz_mps(z)
+    # per-rank sampler = the CPU oracle (this test checks the orchestration, not the kernels)
+    fn = lambda f, n, s: O.orc_sample_range(mps, f, n, s)[0]  # noqa: E731
+    out = run_data_parallel(fn, 0, 1000, 7, mps.num_sites)
+    if rank == 0:
+        q.put(O.fnv1a(out))
+    dist.destroy_process_group()
+
+
+def test_data_parallel_gloo_world2(gold):
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_dp_worker, args=(r, 2, port, gold, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in ps)
+    assert q.get(timeout=5) == 0x991D873B454AB515  # == serial reference (tests/golden/c1.npz)
+
+
+ADAPTER = os.path.join(ROOT, "oracle", "_ref", "adapter_test")
+
+
+@pytest.mark.skipif(not os.path.exists(ADAPTER), reason="adapter_test needs the reference headers to build")
+def test_cpp_dropin_adapter_cpu():
+    """include/mpsg_mpsamp.hpp compiled against the reference headers: validation and error mapping."""
+    import subprocess
+    r = subprocess.run([ADAPTER, "cpu"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stdout + r.stderr
