@@ -84,7 +84,12 @@ typedef struct mpsg_options {
   uint64_t pass_samples;           /* samples per device pass (the GEMM M extent); 0 = auto */
   int record_site_times;           /* 1: fill mpsg_stats.site_seconds (one event per site);
                                       2: also time every contraction kernel (gemm_seconds) */
-  int reserved[5];
+  int tp_size;                     /* tensor-parallel group size (0/1 = none): this handle holds
+                                      column shard tp_rank of every Gamma_i (balanced_partition of
+                                      chiR, collective.cpp:80-92), the even-site pattern of
+                                      parallel.cpp:420-443 applied at every site */
+  int tp_rank;
+  int reserved[3];
 } mpsg_options;
 
 /* Mirrors mpsamp::RunStats + FlopCounters (sampler.hpp:46-54, contract.hpp:12-25). */
@@ -134,8 +139,22 @@ void mpsg_destroy(mpsg_handle h);
 uint64_t mpsg_state_bytes(mpsg_handle h);
 
 /* The Gamma values the GPU actually samples (decoded compressed format), reference layout:
- * complex128 interleaved (chiL, chiR, d).  The CPU oracle consumes these. */
+ * complex128 interleaved (chiL, chiR, d).  The CPU oracle consumes these.  A tensor-parallel
+ * handle writes only its own column shard (other entries are left untouched). */
 int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out);
+
+/* ---- tensor parallelism ------------------------------------------------------------------ */
+/* Per site every rank contracts its Gamma column shard with the full environment, the per-
+ * (sample, outcome) (weight, max) partials are all-gathered and summed in rank order (so every
+ * rank draws the same outcome), and the environment shards are all-gathered for the next site.
+ * All ranks call mpsg_sample with the same range and obtain identical rows. */
+/* 128-byte NCCL unique id, created on one rank and shared with the others out of band. */
+int mpsg_nccl_unique_id(uint8_t id[128]);
+/* Join the NCCL communicator of tp_size ranks (one process or thread per rank and device). */
+int mpsg_tp_connect_nccl(mpsg_handle h, const uint8_t id[128]);
+/* Group n handles of one process (ranks 0..n-1, any devices, possibly the same one) with an
+ * in-process exchange instead of NCCL; each rank's mpsg_sample must run on its own thread. */
+int mpsg_tp_connect_local(mpsg_handle* handles, int n);
 
 /* ---- sampling: replaces sample_batch / sample_micro_serial ------------------------------ */
 /* Samples global indices [first, first + count) with measurement seed `seed` and writes

@@ -28,7 +28,7 @@ class Policy(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("mode", _int), ("pass_samples", _u64), ("record_site_times", _int),
-                ("reserved", _int * 5)]
+                ("tp_size", _int), ("tp_rank", _int), ("reserved", _int * 3)]
 
 
 class Stats(C.Structure):
@@ -57,6 +57,9 @@ SIGNATURES = [
     ("mpsg_marginals", _int, [C.c_void_p, _u64, _u64, _pu8, _pd]),
     ("mpsg_device_draws", _int, [_u64, _u64, _u64, _u64, _pd]),
     ("mpsg_contract_site", _int, [C.c_void_p, _u64, _pd, _u64, _pd]),
+    ("mpsg_nccl_unique_id", _int, [C.POINTER(C.c_uint8)]),
+    ("mpsg_tp_connect_nccl", _int, [C.c_void_p, C.POINTER(C.c_uint8)]),
+    ("mpsg_tp_connect_local", _int, [C.POINTER(C.c_void_p), _int]),
 ]
 
 _lib = None

@@ -11,8 +11,12 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <memory>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -86,6 +90,134 @@ static CUtensorMap make_tma_2d(const void* base, uint64_t cols, uint64_t rows) {
   return m;
 }
 
+// Shard-major env [shards][4 planes * cap rows][kshard]: box 32 k x 128 rows x 1 shard.
+static CUtensorMap make_tma_env(const void* base, uint64_t kshard, uint64_t rows, uint64_t shards) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {kshard, rows, shards};
+  cuuint64_t strides[2] = {kshard * 2, rows * kshard * 2};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(kBM), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(MPSG_ERR_CUDA, "cuTensorMapEncodeTiled (3d) failed");
+  return m;
+}
+
+// balanced_partition (collective.cpp:80-92): [begin, end) of part `i` of `extent` over `parts`.
+static void part_range(int extent, int parts, int i, int& b, int& e) {
+  const int base = extent / parts, rem = extent % parts;
+  b = i * base + std::min(i, rem);
+  e = b + base + (i < rem ? 1 : 0);
+}
+
+// ---------------------------------------------------------------------------------------------
+// collectives for tensor parallelism: NCCL (dlopen'd) or an in-process group of handles
+// ---------------------------------------------------------------------------------------------
+struct Comm {
+  virtual ~Comm() = default;
+  // In place: this rank's chunk sits at buf + rank * chunk; afterwards every slot is filled.
+  virtual void allgather(void* buf, size_t chunk, cudaStream_t s) = 0;
+};
+
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+static const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(h, "ncclAllGather"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+  });
+  if (!api.allGather || !api.commInitRank || !api.getUniqueId)
+    throw Error(MPSG_ERR_CUDA, "NCCL (libnccl.so.2) not available");
+  return api;
+}
+
+#define NCCL_OK(expr)                                                                 \
+  do {                                                                                \
+    ncclResult_t r_ = (expr);                                                         \
+    if (r_ != ncclSuccess)                                                            \
+      throw Error(MPSG_ERR_CUDA, std::string(#expr) + ": " + nccl().getErrorString(r_)); \
+  } while (0)
+
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0;
+  NcclComm(const ncclUniqueId& id, int nranks, int r) : rank(r) {
+    NCCL_OK(nccl().commInitRank(&comm, nranks, id, r));
+  }
+  ~NcclComm() override {
+    if (comm && nccl().commDestroy) nccl().commDestroy(comm);
+  }
+  void allgather(void* buf, size_t chunk, cudaStream_t s) override {
+    NCCL_OK(nccl().allGather(static_cast<char*>(buf) + rank * chunk, buf, chunk, ncclUint8, comm, s));
+  }
+};
+
+// Several handles in one process (one per rank, possibly on the same device): the all-gather is
+// peer/device copies ordered with events; host threads meet at a barrier twice per call.
+struct LocalGroup {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t generation = 0;
+  std::vector<void*> bufs;
+  std::vector<int> devices;
+  std::vector<cudaEvent_t> ready, done;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = generation;
+    if (++arrived == n) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != g; });
+    }
+  }
+  ~LocalGroup() {
+    for (auto e : ready) cudaEventDestroy(e);
+    for (auto e : done) cudaEventDestroy(e);
+  }
+};
+
+struct LocalComm : Comm {
+  std::shared_ptr<LocalGroup> g;
+  int rank;
+  LocalComm(std::shared_ptr<LocalGroup> grp, int r) : g(std::move(grp)), rank(r) {}
+  void allgather(void* buf, size_t chunk, cudaStream_t s) override {
+    LocalGroup& G = *g;
+    G.bufs[rank] = buf;
+    CUDA_OK(cudaEventRecord(G.ready[rank], s));
+    G.barrier();
+    for (int q = 0; q < G.n; ++q) {
+      if (q == rank) continue;
+      CUDA_OK(cudaStreamWaitEvent(s, G.ready[q], 0));
+      CUDA_OK(cudaMemcpyPeerAsync(static_cast<char*>(buf) + q * chunk, G.devices[rank],
+                                  static_cast<char*>(G.bufs[q]) + q * chunk, G.devices[q], chunk, s));
+    }
+    CUDA_OK(cudaEventRecord(G.done[rank], s));
+    G.barrier();
+    for (int q = 0; q < G.n; ++q)
+      if (q != rank) CUDA_OK(cudaStreamWaitEvent(s, G.done[q], 0));
+  }
+};
+
 // ---------------------------------------------------------------------------------------------
 // power-of-two bond scales gamma_i[r] ~ Lambda_i[r]
 // ---------------------------------------------------------------------------------------------
@@ -110,6 +242,8 @@ static std::vector<double> bond_scales(const double* lambda, size_t n) {
 // ---------------------------------------------------------------------------------------------
 struct SiteDev {
   int chil = 0, chir = 0, kp = 0, chirp = 0, np = 0, nt = 0;
+  int b0 = 0, width = 0;     // this rank's column shard [b0, b0 + width) of chiR
+  int kshard = 0;            // env K extent per shard (kp = shards * kshard)
   __half* g = nullptr;       // [2][np][kp]
   float2* cinfo = nullptr;   // [np]
   double* cs = nullptr;      // [chir * d]
@@ -125,6 +259,7 @@ struct DevCtx {
   __half* env = nullptr;     // [4][cap][kmax]
   float2* temp = nullptr;    // [cap][d][chirp_max]
   float2* pstat = nullptr;   // [cap][nt_max]
+  float2* part = nullptr;    // [tp][cap][d] exchanged (weight, max) partials (TP only)
   uint8_t* alive = nullptr;  // [cap]
   uint8_t* rows = nullptr;   // [cap][M]
   uint8_t* forced = nullptr; // [cap][M] (lazy)
@@ -150,6 +285,8 @@ struct mpsg_handle_s {
   std::vector<mpsg::DevCtx> devs;
   std::vector<char> site_set;
   bool finished = false;
+  int tp = 1, tp_rank = 0;                 // tensor-parallel group (column-sharded Gamma)
+  std::unique_ptr<mpsg::Comm> comm;
   std::mutex mu;
 };
 
@@ -159,14 +296,20 @@ namespace mpsg {
 // L2 across the M sweep while the env tiles are re-read once per group.
 constexpr int kGroupPairs = 16;
 
-static int kmax_of(const mpsg_handle_s& h) {
+static int kshard_of(const mpsg_handle_s& h, uint64_t bond) {
+  return round_up((static_cast<int>(bond) + h.tp - 1) / h.tp, kBK);
+}
+static int kshard_max_of(const mpsg_handle_s& h) {
   int k = kBK;
-  for (uint64_t b : h.bonds) k = std::max(k, round_up(static_cast<int>(b), kBK));
+  for (uint64_t i = 0; i < h.M; ++i) k = std::max(k, kshard_of(h, h.bonds[i]));
   return k;
+}
+static int chirp_of(const mpsg_handle_s& h, uint64_t bond) {
+  return round_up((static_cast<int>(bond) + h.tp - 1) / h.tp, kBN);
 }
 static int chirp_max_of(const mpsg_handle_s& h) {
   int c = kBN;
-  for (uint64_t i = 1; i <= h.M; ++i) c = std::max(c, round_up(static_cast<int>(h.bonds[i]), kBN));
+  for (uint64_t i = 1; i <= h.M; ++i) c = std::max(c, chirp_of(h, h.bonds[i]));
   return c;
 }
 
@@ -208,9 +351,10 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
   if (major != 10) throw Error(MPSG_ERR_CUDA, "device is not sm_100 (B200)");
   CUDA_OK(cudaDeviceGetAttribute(&dc.num_sms, cudaDevAttrMultiProcessorCount, dc.device));
   CUDA_OK(cudaStreamCreateWithFlags(&dc.stream, cudaStreamNonBlocking));
-  const int kmax = kmax_of(h), chirpm = chirp_max_of(h);
+  const int kmax = h.tp * kshard_max_of(h), chirpm = chirp_max_of(h);
   const size_t nt_max = h.d * (chirpm / kBN) + 1;  // + the pair-padding tile
-  const size_t row_bytes = 8ull * kmax + 8ull * h.d * chirpm + 8ull * nt_max + 1 + h.M;
+  const size_t row_bytes = 8ull * kmax + 8ull * h.d * chirpm + 8ull * nt_max + 1 + h.M +
+                           (h.tp > 1 ? 8ull * h.tp * h.d : 0);
   uint64_t want = h.opts.pass_samples;
   if (want == 0) {
     const double budget = 6.0e9;  // bytes of per-pass working set
@@ -221,11 +365,12 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
   CUDA_OK(cudaMalloc(&dc.env, 4ull * dc.cap * kmax * sizeof(__half)));
   CUDA_OK(cudaMalloc(&dc.temp, 1ull * dc.cap * h.d * chirpm * sizeof(float2)));
   CUDA_OK(cudaMalloc(&dc.pstat, 1ull * dc.cap * nt_max * sizeof(float2)));
+  if (h.tp > 1) CUDA_OK(cudaMalloc(&dc.part, 1ull * h.tp * dc.cap * h.d * sizeof(float2)));
   CUDA_OK(cudaMalloc(&dc.alive, dc.cap));
   CUDA_OK(cudaMalloc(&dc.rows, 1ull * dc.cap * h.M));
   CUDA_OK(cudaMalloc(&dc.err, sizeof(int)));
   CUDA_OK(cudaMemset(dc.err, 0, sizeof(int)));
-  CUDA_OK(cudaMalloc(&dc.scratch, sizeof(double) * (kmax + 2ull * chirpm)));
+  CUDA_OK(cudaMalloc(&dc.scratch, sizeof(double) * (kmax + 2ull * h.tp * chirpm) + sizeof(int) * kmax));
   CUDA_OK(cudaMallocHost(&dc.host_rows, 1ull * dc.cap * h.M));
 }
 
@@ -240,6 +385,7 @@ static void free_device(DevCtx& dc) {
   cudaFree(dc.env);
   cudaFree(dc.temp);
   cudaFree(dc.pstat);
+  cudaFree(dc.part);
   cudaFree(dc.alive);
   cudaFree(dc.rows);
   cudaFree(dc.forced);
@@ -253,36 +399,48 @@ static void free_device(DevCtx& dc) {
   if (dc.stream) cudaStreamDestroy(dc.stream);
 }
 
-// Compress site i on device dc from `src` (device pointer on dc.device).
+// Compress this rank's column shard of site i on device dc from `src` (device pointer).
 static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* src_dev,
                           bool f64, const double* lambda) {
   SiteDev& s = dc.sites[i];
   s.chil = static_cast<int>(h.bonds[i]);
   s.chir = static_cast<int>(h.bonds[i + 1]);
-  s.kp = round_up(s.chil, kBK);
-  s.chirp = round_up(s.chir, kBN);
+  part_range(s.chir, h.tp, h.tp_rank, s.b0, s.width);
+  s.width -= s.b0;
+  s.kshard = kshard_of(h, h.bonds[i]);
+  s.kp = h.tp * s.kshard;
+  s.chirp = chirp_of(h, h.bonds[i + 1]);
   s.np = round_up(static_cast<int>(h.d) * s.chirp, 2 * kBN);  // whole N-tile pairs (CTA pairs)
   s.nt = s.np / kBN;
   if (!s.g) {
     CUDA_OK(cudaMalloc(&s.g, 2ull * s.np * s.kp * sizeof(__half)));
     CUDA_OK(cudaMalloc(&s.cinfo, 1ull * s.np * sizeof(float2)));
-    CUDA_OK(cudaMalloc(&s.cs, 1ull * s.chir * h.d * sizeof(double)));
+    CUDA_OK(cudaMalloc(&s.cs, std::max<size_t>(1, 1ull * s.width * h.d) * sizeof(double)));
   }
   std::vector<double> wl(s.chir);
   for (int r = 0; r < s.chir; ++r) {
     const double q = lambda[r] / h.gr[i][r];
     wl[r] = q * q;
   }
+  // K position of row l: the previous site's column shards, each padded to kshard
+  std::vector<int> lpos(s.chil);
+  for (int q = 0; q < h.tp; ++q) {
+    int b, e;
+    part_range(s.chil, h.tp, q, b, e);
+    for (int l = b; l < e; ++l) lpos[l] = q * s.kshard + (l - b);
+  }
   double* d_gl = dc.scratch;
   double* d_gr = d_gl + s.chil;
   double* d_wl = d_gr + s.chir;
+  int* d_lpos = reinterpret_cast<int*>(d_wl + s.chir);
   CUDA_OK(cudaMemcpyAsync(d_gl, h.gl[i].data(), sizeof(double) * s.chil, cudaMemcpyHostToDevice, dc.stream));
   CUDA_OK(cudaMemcpyAsync(d_gr, h.gr[i].data(), sizeof(double) * s.chir, cudaMemcpyHostToDevice, dc.stream));
   CUDA_OK(cudaMemcpyAsync(d_wl, wl.data(), sizeof(double) * s.chir, cudaMemcpyHostToDevice, dc.stream));
+  CUDA_OK(cudaMemcpyAsync(d_lpos, lpos.data(), sizeof(int) * s.chil, cudaMemcpyHostToDevice, dc.stream));
   CUDA_OK(cudaMemsetAsync(s.g, 0, 2ull * s.np * s.kp * sizeof(__half), dc.stream));
   CUDA_OK(cudaMemsetAsync(s.cinfo, 0, 1ull * s.np * sizeof(float2), dc.stream));
-  launch_compress_site(src_dev, f64, s.chil, s.chir, static_cast<int>(h.d), s.kp, s.chirp, d_gl,
-                       d_gr, d_wl, s.g, s.cinfo, s.cs, dc.err, dc.stream);
+  launch_compress_site(src_dev, f64, s.chil, s.chir, static_cast<int>(h.d), s.b0, s.width, s.kp,
+                       s.chirp, d_lpos, d_gl, d_gr, d_wl, s.g, s.cinfo, s.cs, dc.err, dc.stream);
   CUDA_OK(cudaGetLastError());
   int err = 0;
   CUDA_OK(cudaMemcpyAsync(&err, dc.err, sizeof(int), cudaMemcpyDeviceToHost, dc.stream));
@@ -293,7 +451,7 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
                                       ") or dynamic range beyond the compressed format");
   }
   s.tma_g = make_tma_2d(s.g, s.kp, 2ull * s.np);
-  s.tma_env = make_tma_2d(dc.env, s.kp, 4ull * dc.cap);
+  s.tma_env = make_tma_env(dc.env, s.kshard, 4ull * dc.cap, h.tp);
 }
 
 static void ensure_src(DevCtx& dc, size_t bytes) {
@@ -348,7 +506,7 @@ struct PassOut {
 static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first, int count,
                      const uint8_t* forced_dev, double* marg_dev, PassOut& po, int timing) {
   const int rows = round_up(count, kBM);
-  launch_init_env(dc.env, dc.cap, dc.sites[0].kp, rows, count, dc.alive, dc.stream);
+  launch_init_env(dc.env, dc.cap, dc.sites[0].kshard, h.tp, rows, count, dc.alive, dc.stream);
   po.launches += 1;
   for (uint64_t i = 0; i < h.M; ++i) {
     const SiteDev& s = dc.sites[i];
@@ -356,6 +514,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
     ga.m_tiles = rows / kBM;
     ga.n_tiles = s.nt;
     ga.k_blocks = s.kp / kBK;
+    ga.kshard_blocks = s.kshard / kBK;
     ga.plane_rows_a = dc.cap;
     ga.np = s.np;
     ga.chirp = s.chirp;
@@ -373,28 +532,46 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
     sa.site = static_cast<int>(i);
     sa.num_sites = static_cast<int>(h.M);
     sa.d = static_cast<int>(h.d);
-    sa.chir = s.chir;
+    sa.chir_loc = s.width;
     sa.chirp = s.chirp;
-    sa.n_tiles = s.nt;
-    sa.tiles_per_k = s.chirp / kBN;
+    if (h.tp == 1) {  // partials straight from the tiles: (tile t of outcome k) at pstat[n][k*tpk+t]
+      sa.parts = s.chirp / kBN;
+      sa.part_base = dc.pstat;
+      sa.part_stride = 1;
+      sa.row_stride = s.nt;
+      sa.k_stride = s.chirp / kBN;
+    } else {  // per-rank (weight, max) per outcome, exchanged, summed in rank order on every rank
+      launch_reduce_tiles(dc.pstat, s.nt, s.chirp / kBN, sa.d, rows,
+                          dc.part + 1ull * h.tp_rank * dc.cap * h.d, dc.stream);
+      h.comm->allgather(dc.part, 1ull * dc.cap * h.d * sizeof(float2), dc.stream);
+      sa.parts = h.tp;
+      sa.part_base = dc.part;
+      sa.part_stride = 1ll * dc.cap * static_cast<long long>(h.d);
+      sa.row_stride = static_cast<long long>(h.d);
+      sa.k_stride = 1;
+      po.launches += 1;
+    }
     sa.rows = rows;
     sa.count = count;
-    sa.kp_next = (i + 1 < h.M) ? dc.sites[i + 1].kp : 0;
+    const bool has_next = i + 1 < h.M;
+    const int kn = has_next ? dc.sites[i + 1].kshard : 0;
+    sa.kp_next = kn;
     sa.env_cap = dc.cap;
     sa.seed = seed;
     sa.first = first;
     sa.temp = dc.temp;
-    sa.pstat = dc.pstat;
     sa.alive = dc.alive;
     sa.rows_out = dc.rows;
-    sa.env_next = dc.env;
+    sa.env_next = dc.env + 4ull * dc.cap * kn * h.tp_rank;
     sa.forced = forced_dev;
     sa.marg = marg_dev;
     launch_select(sa, dc.stream);
+    if (h.tp > 1 && has_next)  // rebuild the full environment from the column shards
+      h.comm->allgather(dc.env, 4ull * dc.cap * kn * sizeof(__half), dc.stream);
     if (timing) CUDA_OK(cudaEventRecord(dc.ev[i + 1], dc.stream));
     po.launches += 2;
-    po.macs += static_cast<uint64_t>(count) * s.chil * s.chir * h.d;
-    po.wmacs += static_cast<uint64_t>(count) * s.chir * h.d;
+    po.macs += static_cast<uint64_t>(count) * s.chil * s.width * h.d;
+    po.wmacs += static_cast<uint64_t>(count) * s.width * h.d;
     po.issued += 8ull * rows * s.np * s.kp * (h.split ? 2 : 1);
   }
   CUDA_OK(cudaGetLastError());
@@ -470,6 +647,8 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
                         uint8_t* rows_host, uint8_t* rows_dev, const uint8_t* forced,
                         double* marg, mpsg_stats* st) {
   config_check(h.finished, "state not finished (mpsg_builder_finish)");
+  config_check(h.tp == 1 || h.comm != nullptr, "tensor-parallel handle not connected (mpsg_tp_connect_*)");
+  config_check(h.tp == 1 || h.devs.size() == 1, "a tensor-parallel rank drives exactly one device");
   std::lock_guard<std::mutex> lk(h.mu);
   const auto t0 = std::chrono::steady_clock::now();
   const size_t nd = rows_dev ? 1 : h.devs.size();
@@ -583,6 +762,10 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
     h->policy = pol;
     if (opts) h->opts = *opts;
     config_check(h->opts.mode >= MPSG_MODE_AUTO && h->opts.mode <= MPSG_MODE_SINGLE, "unknown mode");
+    h->tp = std::max(1, h->opts.tp_size);
+    h->tp_rank = h->opts.tp_rank;
+    config_check(h->tp_rank >= 0 && h->tp_rank < h->tp, "tp_rank out of range");
+    config_check(h->tp == 1 || ndev <= 1, "a tensor-parallel rank drives exactly one device");
     h->split = h->opts.mode == MPSG_MODE_SPLIT ||
                (h->opts.mode == MPSG_MODE_AUTO && (pol.compute == MPSG_F64 || pol.compute == MPSG_F32));
     h->gl.resize(num_sites);
@@ -674,20 +857,67 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
     CUDA_OK(cudaSetDevice(dc.device));
     const SiteDev& s = dc.sites[site];
     std::vector<__half> g(2ull * s.np * s.kp);
-    std::vector<double> cs(1ull * s.chir * h->d);
+    std::vector<double> cs(std::max<size_t>(1, 1ull * s.width * h->d));
     CUDA_OK(cudaMemcpy(g.data(), s.g, g.size() * sizeof(__half), cudaMemcpyDeviceToHost));
     CUDA_OK(cudaMemcpy(cs.data(), s.cs, cs.size() * sizeof(double), cudaMemcpyDeviceToHost));
     const size_t d = h->d;
+    std::vector<int> lpos(s.chil);
+    for (int q = 0; q < h->tp; ++q) {
+      int b, e;
+      part_range(s.chil, h->tp, q, b, e);
+      for (int l = b; l < e; ++l) lpos[l] = q * s.kshard + (l - b);
+    }
     for (int l = 0; l < s.chil; ++l)
-      for (int r = 0; r < s.chir; ++r)
+      for (int rl = 0; rl < s.width; ++rl)
         for (size_t k = 0; k < d; ++k) {
-          const size_t row = k * s.chirp + r;
-          const double f = static_cast<double>(static_cast<float>(cs[r * d + k])) * h->gl[site][l] /
+          const int r = s.b0 + rl;
+          const size_t row = k * s.chirp + rl;
+          const double f = static_cast<double>(static_cast<float>(cs[rl * d + k])) * h->gl[site][l] /
                            h->gr[site][r];
           const size_t o = 2 * ((static_cast<size_t>(l) * s.chir + r) * d + k);
-          out[o] = static_cast<double>(__half2float(g[row * s.kp + l])) * f;
-          out[o + 1] = static_cast<double>(__half2float(g[(s.np + row) * s.kp + l])) * f;
+          out[o] = static_cast<double>(__half2float(g[row * s.kp + lpos[l]])) * f;
+          out[o + 1] = static_cast<double>(__half2float(g[(s.np + row) * s.kp + lpos[l]])) * f;
         }
+  });
+}
+
+int mpsg_nccl_unique_id(uint8_t id[128]) {
+  return guarded([&] {
+    config_check(id != nullptr, "null id");
+    ncclUniqueId u;
+    NCCL_OK(nccl().getUniqueId(&u));
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+int mpsg_tp_connect_nccl(mpsg_handle h, const uint8_t id[128]) {
+  return guarded([&] {
+    config_check(h != nullptr && id != nullptr, "null argument");
+    config_check(h->tp > 1, "handle was not created with tp_size > 1");
+    CUDA_OK(cudaSetDevice(h->devs[0].device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    h->comm = std::make_unique<NcclComm>(u, h->tp, h->tp_rank);
+  });
+}
+
+int mpsg_tp_connect_local(mpsg_handle* hs, int n) {
+  return guarded([&] {
+    config_check(hs != nullptr && n >= 1, "null / empty handle list");
+    auto g = std::make_shared<LocalGroup>();
+    g->n = n;
+    g->bufs.assign(n, nullptr);
+    g->ready.resize(n);
+    g->done.resize(n);
+    for (int r = 0; r < n; ++r) {
+      config_check(hs[r] != nullptr, "null handle");
+      config_check(hs[r]->tp == n && hs[r]->tp_rank == r, "handle r must have tp_size n, tp_rank r");
+      g->devices.push_back(hs[r]->devs[0].device);
+      CUDA_OK(cudaSetDevice(hs[r]->devs[0].device));
+      CUDA_OK(cudaEventCreateWithFlags(&g->ready[r], cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&g->done[r], cudaEventDisableTiming));
+    }
+    for (int r = 0; r < n; ++r) hs[r]->comm = std::make_unique<LocalComm>(g, r);
   });
 }
 
@@ -738,6 +968,7 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
   return guarded([&] {
     config_check(h != nullptr && env != nullptr && temp != nullptr, "null argument");
     config_check(site < h->M && h->finished, "bad site / unfinished state");
+    config_check(h->tp == 1, "mpsg_contract_site: not available on a tensor-parallel handle");
     DevCtx& dc = h->devs[0];
     config_check(count >= 1 && count <= static_cast<uint64_t>(dc.cap), "count exceeds pass capacity");
     CUDA_OK(cudaSetDevice(dc.device));
@@ -775,6 +1006,7 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
     ga.m_tiles = rows / kBM;
     ga.n_tiles = s.nt;
     ga.k_blocks = s.kp / kBK;
+    ga.kshard_blocks = s.kshard / kBK;
     ga.plane_rows_a = dc.cap;
     ga.np = s.np;
     ga.chirp = s.chirp;

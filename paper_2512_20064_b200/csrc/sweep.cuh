@@ -25,31 +25,38 @@ constexpr uint8_t kDead = 0xFF;                      // sampler.hpp:17
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 struct SiteGemmArgs {
-  int m_tiles;      // rows / 128
-  int n_tiles;      // Np / 128
-  int k_blocks;     // Kp / 32
-  int plane_rows_a; // row offset between env planes (= env capacity rows)
-  int np;           // Np (row offset between G planes)
-  int chirp;        // padded chiR (multiple of 128)
+  int m_tiles;       // rows / 128
+  int n_tiles;       // Np / 128 (even)
+  int k_blocks;      // total K blocks = shards * kshard_blocks
+  int kshard_blocks; // K blocks per env shard (Kshard / 32); env TMA map is 3-D (k, row, shard)
+  int plane_rows_a;  // row offset between env planes (= env capacity rows)
+  int np;            // Np (row offset between G planes)
+  int chirp;         // padded local chiR (multiple of 128)
   int d;
-  int group_n;      // N-tiles per raster group
+  int group_n;       // N-tile pairs per raster group
   const float2* cinfo;
   float2* temp;
   float2* pstat;
 };
 
+// Per-(sample, outcome) partials read by the select kernel: element (part, n, k) lives at
+// part_base[part * part_stride + n * row_stride + k * k_stride]; parts are summed in order.
 struct SelectArgs {
-  int site, num_sites, d, chir, chirp, n_tiles, tiles_per_k;
+  int site, num_sites, d;
+  int chir_loc;             // live local columns of the slice (this rank's shard width)
+  int chirp;                // padded local chiR (temp row stride per outcome)
+  int parts;                // number of partials per (n, k)
+  long long part_stride, row_stride, k_stride;
   int rows;                 // samples handled this pass (multiple of 128 >= count)
   int count;                // live samples this pass
-  int kp_next;              // K extent of the next site's env (0 on the last site)
+  int kp_next;              // width of this rank's next-env shard (0 on the last site)
   int env_cap;              // env plane stride in rows
   uint64_t seed, first;
   const float2* temp;
-  const float2* pstat;
+  const float2* part_base;
   uint8_t* alive;
   uint8_t* rows_out;        // [count][num_sites] (device)
-  __half* env_next;         // next site's env planes (may alias the current env buffer)
+  __half* env_next;         // this rank's shard of the next env: [4][env_cap][kp_next]
   const uint8_t* forced;    // optional [count][num_sites] teacher forcing
   double* marg;             // optional [count][num_sites][d]
 };
@@ -58,15 +65,20 @@ struct SelectArgs {
 void launch_site_gemm(bool split, const CUtensorMap& tma_env, const CUtensorMap& tma_g,
                       const SiteGemmArgs& a, int grid, cudaStream_t s);
 void launch_select(const SelectArgs& a, cudaStream_t s);
-void launch_init_env(__half* env, int env_cap, int kp0, int rows, int count, uint8_t* alive,
-                     cudaStream_t s);
+// pstat [rows][nt] -> out [rows][d]: (sum of weights, max) over the tiles of each outcome
+void launch_reduce_tiles(const float2* pstat, int nt, int tiles_per_k, int d, int rows,
+                         float2* out, cudaStream_t s);
+// Site-0 env in the shard-major layout [shards][4][cap][kshard]: E[n][0] = 1 (shard 0).
+void launch_init_env(__half* env, int env_cap, int kshard0, int shards, int rows, int count,
+                     uint8_t* alive, cudaStream_t s);
 void launch_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, double* out,
                   cudaStream_t s);
-// Compression of one site: src complex (chiL, chiR, d) f64 or f32 interleaved on device.
-void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int kp,
-                          int chirp, const double* gl, const double* gr, const double* wl,
-                          __half* g_out, float2* cinfo_out, double* cs_out, int* err,
-                          cudaStream_t s);
+// Compression of one site's column shard [b0, b0 + width) of chiR: src complex (chiL, chiR, d)
+// f64 or f32 interleaved on device; row l goes to padded K position lpos[l].
+void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
+                          int width, int kp, int chirp, const int* lpos, const double* gl,
+                          const double* gr, const double* wl, __half* g_out, float2* cinfo_out,
+                          double* cs_out, int* err, cudaStream_t s);
 int gemm_smem_bytes(bool split);
 
 }  // namespace mpsg

@@ -128,14 +128,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         int m, np;
         unit_coords(u, a, m, np);
         const int n = 2 * np + rank;
+        int shard = 0, kin = 0;  // K block kb = shard * kshard_blocks + kin
         for (int kb = 0; kb < a.k_blocks; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);  // free in both CTAs
           uint8_t* st = smem + stage * C::kStageBytes;
           ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
 #pragma unroll
           for (int q = rank; q < C::kAPlanes; q += 2)  // this CTA's half of the env planes
-            ptx::tma_load_2d_mc(&tma_env, &full[stage], st + q * C::kTile, kb * kBK,
-                                q * a.plane_rows_a + m * kBM, 0x3, pol_env);
+            ptx::tma_load_3d_mc(&tma_env, &full[stage], st + q * C::kTile, kin * kBK,
+                                q * a.plane_rows_a + m * kBM, shard, 0x3, pol_env);
 #pragma unroll
           for (int p = 0; p < 2; ++p)
             ptx::tma_load_2d(&tma_g, &full[stage], st + (C::kAPlanes + p) * C::kTile, kb * kBK,
@@ -143,6 +144,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
+          }
+          if (++kin == a.kshard_blocks) {
+            kin = 0;
+            ++shard;
           }
         }
       }
@@ -298,12 +303,18 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-// Born weight of outcome k for sample row: fixed-order f64 reduction of the tile partials.
-__device__ __forceinline__ double outcome_weight(const float2* ps, int k, int tiles_per_k,
-                                                 int lane) {
+// Born weight of outcome k for sample n: fixed-order f64 reduction of its partials.
+__device__ __forceinline__ double outcome_weight(const SelectArgs& a, int n, int k, int lane) {
+  const float2* base = a.part_base + n * a.row_stride + k * a.k_stride;
   double s = 0.0;
-  for (int t = lane; t < tiles_per_k; t += 32) s += static_cast<double>(ps[k * tiles_per_k + t].x);
+  for (int t = lane; t < a.parts; t += 32) s += static_cast<double>(base[t * a.part_stride].x);
   return warp_sum(s);
+}
+__device__ __forceinline__ float outcome_max(const SelectArgs& a, int n, int k, int lane) {
+  const float2* base = a.part_base + n * a.row_stride + k * a.k_stride;
+  float m = 0.f;
+  for (int t = lane; t < a.parts; t += 32) m = fmaxf(m, base[t * a.part_stride].y);
+  return warp_max(m);
 }
 
 __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
@@ -311,17 +322,16 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
   const int lane = threadIdx.x & 31;
   if (n >= a.rows) return;
   const bool live_in = n < a.count && a.alive[n];
-  const float2* ps = a.pstat + static_cast<size_t>(n) * a.n_tiles;
   int outcome = kDead;   // recorded at this site
   bool live_out = false; // carries into the next site
   float scale = 0.f;
   if (live_in) {
     double total = 0.0;  // sampler.cpp:92-93, ascending k
-    for (int k = 0; k < a.d; ++k) total += outcome_weight(ps, k, a.tiles_per_k, lane);
+    for (int k = 0; k < a.d; ++k) total += outcome_weight(a, n, k, lane);
     if (a.marg != nullptr) {
       double* mrow = a.marg + (static_cast<size_t>(n) * a.num_sites + a.site) * a.d;
       for (int k = 0; k < a.d; ++k) {
-        const double wk = outcome_weight(ps, k, a.tiles_per_k, lane);
+        const double wk = outcome_weight(a, n, k, lane);
         if (lane == 0) mrow[k] = total == 0.0 ? -1.0 : wk / total;
       }
     }
@@ -334,7 +344,7 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
         double cum = 0.0;
         kk = 0;
         for (int k = 0; k < a.d; ++k) {  // sampler.cpp:100-106: strict '>', no early break
-          cum += outcome_weight(ps, k, a.tiles_per_k, lane) / total;
+          cum += outcome_weight(a, n, k, lane) / total;
           if (draw > cum) ++kk;
         }
         if (kk >= a.d) kk = a.d - 1;  // :107
@@ -342,9 +352,7 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
       if (kk != kDead) {
         outcome = kk;
         // per-sample max of the chosen slice (precision.cpp:155-160); 0 -> dead from here on
-        float mx = 0.f;
-        for (int t = lane; t < a.tiles_per_k; t += 32) mx = fmaxf(mx, ps[kk * a.tiles_per_k + t].y);
-        mx = warp_max(mx);
+        const float mx = outcome_max(a, n, kk, lane);
         if (mx > 0.f) {
           int e;
           frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
@@ -369,7 +377,7 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
     const float2* src = a.temp + (static_cast<size_t>(n) * a.d + (live_out ? outcome : 0)) * a.chirp;
     for (int r = lane; r < a.kp_next; r += 32) {
       float2 v = make_float2(0.f, 0.f);
-      if (live_out && r < a.chir) {
+      if (live_out && r < a.chir_loc) {
         v = src[r];
         v.x *= scale;
         v.y *= scale;
@@ -383,6 +391,34 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
   }
 }
 
+// pstat [rows][nt] -> out [rows][d]: per outcome k the sum of its tiles' weights (fixed-order f64
+// reduction, rounded to fp32 for the exchange) and the max; one warp per sample.
+__global__ void reduce_tiles_kernel(const float2* pstat, int nt, int tpk, int d, int rows,
+                                    float2* out) {
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (n >= rows) return;
+  for (int k = 0; k < d; ++k) {
+    double s = 0.0;
+    float m = 0.f;
+    for (int t = lane; t < tpk; t += 32) {
+      const float2 v = pstat[static_cast<size_t>(n) * nt + k * tpk + t];
+      s += static_cast<double>(v.x);
+      m = fmaxf(m, v.y);
+    }
+    s = warp_sum(s);
+    m = warp_max(m);
+    if (lane == 0) out[static_cast<size_t>(n) * d + k] = make_float2(static_cast<float>(s), m);
+  }
+}
+
+void launch_reduce_tiles(const float2* pstat, int nt, int tiles_per_k, int d, int rows,
+                         float2* out, cudaStream_t s) {
+  const int threads = 256;
+  reduce_tiles_kernel<<<(rows * 32 + threads - 1) / threads, threads, 0, s>>>(pstat, nt, tiles_per_k,
+                                                                             d, rows, out);
+}
+
 void launch_select(const SelectArgs& a, cudaStream_t s) {
   const int threads = 256;
   const int blocks = (a.rows * 32 + threads - 1) / threads;
@@ -392,23 +428,23 @@ void launch_select(const SelectArgs& a, cudaStream_t s) {
 // ============================================================================================
 // site-0 environment (sampler.cpp:136-138: env = ones(count, 1), all alive)
 // ============================================================================================
-__global__ void init_env_kernel(__half* env, int env_cap, int kp0, int rows, int count,
-                                uint8_t* alive) {
-  const size_t plane = static_cast<size_t>(env_cap) * kp0;
-  const size_t total = 4 * plane;
+__global__ void init_env_kernel(__half* env, int env_cap, int kshard0, int shards, int rows,
+                                int count, uint8_t* alive) {
+  const size_t plane = static_cast<size_t>(env_cap) * kshard0;
+  const size_t total = static_cast<size_t>(shards) * 4 * plane;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t p = i / plane, rem = i - p * plane;
-    const size_t n = rem / kp0, c = rem - n * kp0;
+    const size_t p = i / plane, rem = i - p * plane;  // p = shard * 4 + plane
+    const size_t n = rem / kshard0, c = rem - n * kshard0;
     env[i] = __float2half_rn((p == 0 && c == 0 && n < static_cast<size_t>(count)) ? 1.0f : 0.0f);
   }
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < rows; n += gridDim.x * blockDim.x)
     alive[n] = n < count ? 1 : 0;
 }
 
-void launch_init_env(__half* env, int env_cap, int kp0, int rows, int count, uint8_t* alive,
-                     cudaStream_t s) {
-  init_env_kernel<<<296, 256, 0, s>>>(env, env_cap, kp0, rows, count, alive);
+void launch_init_env(__half* env, int env_cap, int kshard0, int shards, int rows, int count,
+                     uint8_t* alive, cudaStream_t s) {
+  init_env_kernel<<<296, 256, 0, s>>>(env, env_cap, kshard0, shards, rows, count, alive);
 }
 
 __global__ void draws_kernel(uint64_t seed, uint64_t first, uint64_t count, uint64_t site,
@@ -435,18 +471,20 @@ __device__ __forceinline__ void load_c(const void* src, size_t idx, double& re, 
 }
 
 template <typename T>
-__global__ void colscale_kernel(const void* src, int chil, int chir, int d, int chirp,
-                                const double* gl, const double* gr, const double* wl,
+__global__ void colscale_kernel(const void* src, int chil, int chir, int d, int b0, int width,
+                                int chirp, const double* gl, const double* gr, const double* wl,
                                 float2* cinfo, double* cs_out, int* err) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;  // column j = r * d + k
-  const int width = chir * d;
-  if (j >= width) return;
-  const int r = j / d, k = j - r * d;
+  const int jl = blockIdx.x * blockDim.x + threadIdx.x;  // local column jl = r_loc * d + k
+  if (jl >= width * d) return;
+  const int rl = jl / d, k = jl - rl * d;
+  const int r = b0 + rl;
+  const size_t j = static_cast<size_t>(r) * d + k;
+  const size_t stride = static_cast<size_t>(chir) * d;
   double mx = 0.0;
   bool finite = true;
   for (int l = 0; l < chil; ++l) {
     double re, im;
-    load_c<T>(src, static_cast<size_t>(l) * width + j, re, im);
+    load_c<T>(src, static_cast<size_t>(l) * stride + j, re, im);
     if (!isfinite(re) || !isfinite(im)) finite = false;
     const double f = gr[r] / gl[l];
     mx = fmax(mx, fmax(fabs(re * f), fabs(im * f)));
@@ -463,26 +501,27 @@ __global__ void colscale_kernel(const void* src, int chil, int chir, int d, int 
     if (e < -120) e = -120;
     cs = ldexp(1.0, e);
   }
-  cs_out[j] = cs;
-  cinfo[k * chirp + r] = make_float2(static_cast<float>(cs), static_cast<float>(wl[r]));
+  cs_out[jl] = cs;
+  cinfo[k * chirp + rl] = make_float2(static_cast<float>(cs), static_cast<float>(wl[r]));
 }
 
 template <typename T>
-__global__ void pack_kernel(const void* src, int chil, int chir, int d, int kp, int chirp,
-                            const double* gl, const double* gr, const double* cs, __half* g_out) {
+__global__ void pack_kernel(const void* src, int chil, int chir, int d, int b0, int width, int kp,
+                            int chirp, const int* lpos, const double* gl, const double* gr,
+                            const double* cs, __half* g_out, int np) {
   __shared__ __half tre[32][33], tim[32][33];
-  const int width = chir * d;
-  const int np = d * chirp;
+  const int wcols = width * d;
+  const size_t stride = static_cast<size_t>(chir) * d;
   const int j0 = blockIdx.x * 32, l0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
   for (int yy = ty; yy < 32; yy += 8) {
-    const int l = l0 + yy, j = j0 + tx;
+    const int l = l0 + yy, jl = j0 + tx;
     __half hr = __float2half_rn(0.f), hi = hr;
-    if (l < chil && j < width) {
+    if (l < chil && jl < wcols) {
+      const int rl = jl / d, k = jl - rl * d;
       double re, im;
-      load_c<T>(src, static_cast<size_t>(l) * width + j, re, im);
-      const int r = j / d;
-      const double f = gr[r] / gl[l] / cs[j];
+      load_c<T>(src, static_cast<size_t>(l) * stride + static_cast<size_t>(b0 + rl) * d + k, re, im);
+      const double f = gr[b0 + rl] / gl[l] / cs[jl];
       hr = __double2half(re * f);
       hi = __double2half(im * f);
     }
@@ -491,33 +530,36 @@ __global__ void pack_kernel(const void* src, int chil, int chir, int d, int kp, 
   }
   __syncthreads();
   for (int yy = ty; yy < 32; yy += 8) {
-    const int j = j0 + yy, l = l0 + tx;
-    if (j < width && l < kp) {
-      const int r = j / d, k = j - r * d;
-      const size_t row = static_cast<size_t>(k) * chirp + r;
-      g_out[row * kp + l] = tre[tx][yy];
-      g_out[(static_cast<size_t>(np) + row) * kp + l] = tim[tx][yy];
+    const int jl = j0 + yy, l = l0 + tx;
+    if (jl < wcols && l < chil) {
+      const int rl = jl / d, k = jl - rl * d;
+      const size_t row = static_cast<size_t>(k) * chirp + rl;
+      const size_t col = static_cast<size_t>(lpos[l]);
+      g_out[row * kp + col] = tre[tx][yy];
+      g_out[(static_cast<size_t>(np) + row) * kp + col] = tim[tx][yy];
     }
   }
 }
 
-void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int kp,
-                          int chirp, const double* gl, const double* gr, const double* wl,
-                          __half* g_out, float2* cinfo_out, double* cs_out, int* err,
-                          cudaStream_t s) {
-  const int width = chir * d;
-  const dim3 cb((width + 127) / 128);
-  const dim3 pb((width + 31) / 32, (chil + 31) / 32);
+void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
+                          int width, int kp, int chirp, const int* lpos, const double* gl,
+                          const double* gr, const double* wl, __half* g_out, float2* cinfo_out,
+                          double* cs_out, int* err, cudaStream_t s) {
+  if (width <= 0) return;
+  const int wcols = width * d;
+  const int np = round_up(d * chirp, 2 * kBN);
+  const dim3 cb((wcols + 127) / 128);
+  const dim3 pb((wcols + 31) / 32, (chil + 31) / 32);
   if (src_f64) {
-    colscale_kernel<double><<<cb, 128, 0, s>>>(src, chil, chir, d, chirp, gl, gr, wl, cinfo_out,
-                                               cs_out, err);
-    pack_kernel<double><<<pb, dim3(32, 8), 0, s>>>(src, chil, chir, d, kp, chirp, gl, gr, cs_out,
-                                                   g_out);
+    colscale_kernel<double><<<cb, 128, 0, s>>>(src, chil, chir, d, b0, width, chirp, gl, gr, wl,
+                                               cinfo_out, cs_out, err);
+    pack_kernel<double><<<pb, dim3(32, 8), 0, s>>>(src, chil, chir, d, b0, width, kp, chirp, lpos,
+                                                   gl, gr, cs_out, g_out, np);
   } else {
-    colscale_kernel<float><<<cb, 128, 0, s>>>(src, chil, chir, d, chirp, gl, gr, wl, cinfo_out,
-                                              cs_out, err);
-    pack_kernel<float><<<pb, dim3(32, 8), 0, s>>>(src, chil, chir, d, kp, chirp, gl, gr, cs_out,
-                                                  g_out);
+    colscale_kernel<float><<<cb, 128, 0, s>>>(src, chil, chir, d, b0, width, chirp, gl, gr, wl,
+                                              cinfo_out, cs_out, err);
+    pack_kernel<float><<<pb, dim3(32, 8), 0, s>>>(src, chil, chir, d, b0, width, kp, chirp, lpos, gl,
+                                                  gr, cs_out, g_out, np);
   }
 }
 

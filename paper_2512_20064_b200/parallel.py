@@ -1,5 +1,13 @@
 """Multi-GPU executors (one process per GPU, torch.distributed for the plumbing).
 
+Tensor parallel — the reference's even-site double-site scheme (parallel.cpp:420-443) applied at
+every site: each rank of a group of p2 holds the column shard balanced_partition(chiR, p2)[rank]
+of every Gamma_i (so chi >= 4096 chains are split across HBMs), contracts it against the full
+environment, exchanges the small per-(sample, outcome) (weight, max) partials and draws the same
+outcome on every rank, then all-gathers the environment shards.  The exchange runs inside libmpsg
+(NCCL, or an in-process group for ranks sharing a process); ``tp_connect_nccl`` shares the NCCL id
+through torch.distributed and ``TensorParallelLocal`` drives p2 ranks from threads of one process.
+
 Data parallel — the reference's ``run_data_parallel`` (parallel.cpp:240-330).  The reference
 round-robins macro batches over simulated workers and has worker 0 broadcast every site payload
 (parallel.cpp:271-289).  Here every rank keeps the whole compressed MPS resident in its own HBM,
@@ -60,3 +68,68 @@ def run_data_parallel(sample_fn: Callable[[int, int, int], np.ndarray], first: i
     for r, (a, b) in enumerate(parts):
         out[a:b] = gathered[r][: b - a].cpu().numpy()
     return out
+
+
+def tp_connect_nccl(sampler, group=None) -> None:
+    """Share an NCCL unique id over torch.distributed and connect this rank's TP sampler."""
+    import torch.distributed as dist
+
+    from .sampler import nccl_unique_id
+    obj = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    sampler.connect_nccl(obj[0])
+
+
+class TensorParallelLocal:
+    """p2 tensor-parallel ranks in one process (one thread each), e.g. several GPUs without NCCL or
+    p2 ranks on a single GPU for testing the sharded path."""
+
+    def __init__(self, mps, p2: int, devices=None, **kw):
+        from .sampler import GpuSampler, connect_local
+        devices = devices or [0] * p2
+        self.ranks = [GpuSampler(mps, devices=[devices[r]], tp_size=p2, tp_rank=r, **kw) for r in range(p2)]
+        connect_local(self.ranks)
+
+    def _all(self, fn):
+        import threading
+        out = [None] * len(self.ranks)
+        err = []
+
+        def run(r):
+            try:
+                out[r] = fn(self.ranks[r])
+            except Exception as e:  # pragma: no cover
+                err.append(e)
+
+        ts = [threading.Thread(target=run, args=(r,)) for r in range(len(self.ranks))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if err:
+            raise err[0]
+        return out
+
+    def sample(self, first: int, count: int, seed: int):
+        """Returns every rank's rows (they are identical)."""
+        return self._all(lambda s: s.sample(first, count, seed))
+
+    def marginals(self, first: int, forced):
+        return self._all(lambda s: s.marginals(first, forced))
+
+    def decoded_gamma(self, site: int):
+        """The full decoded Gamma_i assembled from every rank's column shard."""
+        from . import _lib
+        from .sampler import _check
+        b = self.ranks[0].bond_dims
+        full = np.zeros((b[site], b[site + 1], self.ranks[0].phys_dim), np.complex128)
+        for r, s in enumerate(self.ranks):
+            part = np.zeros_like(full)
+            _check(_lib.lib().mpsg_decoded_gamma(s._h, site, part.ctypes.data_as(_lib._pd)))
+            c0, c1 = balanced_partition(b[site + 1], len(self.ranks))[r]
+            full[:, c0:c1, :] = part[:, c0:c1, :]
+        return full
+
+    def close(self):
+        for s in self.ranks:
+            s.close()

@@ -235,7 +235,7 @@ class GpuSampler:
 
     def __init__(self, mps: MpsState, policy: Optional[PrecisionPolicy] = None, mode: Mode = Mode.AUTO,
                  devices: Optional[Sequence[int]] = None, pass_samples: int = 0,
-                 record_site_times: bool = False):
+                 record_site_times: bool = False, tp_size: int = 1, tp_rank: int = 0):
         L = _lib.lib()
         mps.validate()
         self.policy = policy or PrecisionPolicy()
@@ -250,7 +250,8 @@ class GpuSampler:
                             (_lib._pd * len(g))(*[x.ctypes.data_as(_lib._pd) for x in g]),
                             (_lib._pd * len(lam))(*[x.ctypes.data_as(_lib._pd) for x in lam]))
         pol = _lib.Policy(int(self.policy.compute), int(self.policy.storage), int(self.policy.scaling))
-        opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times))
+        opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), int(tp_size), int(tp_rank))
+        self.tp_size, self.tp_rank = tp_size, tp_rank
         devs, nd = self._devices(devices)
         _check(L.mpsg_create(C.byref(view), C.byref(pol), C.byref(opt), devs, nd, C.byref(self._h)))
 
@@ -266,6 +267,7 @@ class GpuSampler:
                      policy: PrecisionPolicy) -> "GpuSampler":
         self = cls.__new__(cls)
         self._h = handle
+        self.tp_size, self.tp_rank = 1, 0
         self.num_sites, self.phys_dim, self.bond_dims = num_sites, phys_dim, list(bond_dims)
         self.policy = policy
         return self
@@ -280,6 +282,11 @@ class GpuSampler:
             self.close()
         except Exception:
             pass
+
+    def connect_nccl(self, unique_id: bytes) -> None:
+        """Join the tensor-parallel NCCL communicator (see mpsg_tp_connect_nccl)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(_lib.lib().mpsg_tp_connect_nccl(self._h, buf))
 
     @property
     def state_bytes(self) -> int:
@@ -329,6 +336,18 @@ class GpuSampler:
         _check(_lib.lib().mpsg_contract_site(self._h, site, env.ctypes.data_as(_lib._pd), env.shape[0],
                                              out.ctypes.data_as(_lib._pd)))
         return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(_lib.lib().mpsg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def connect_local(samplers: Sequence["GpuSampler"]) -> None:
+    """Group tensor-parallel ranks living in this process (mpsg_tp_connect_local)."""
+    arr = (C.c_void_p * len(samplers))(*[s._h.value for s in samplers])
+    _check(_lib.lib().mpsg_tp_connect_local(arr, len(samplers)))
 
 
 def device_draws(seed: int, first: int, count: int, site: int) -> np.ndarray:

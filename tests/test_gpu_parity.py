@@ -143,3 +143,30 @@ def test_cpp_dropin_adapter_gpu():
     r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=120)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("p2", [2, 3])
+def test_tensor_parallel_local(pkg, gold, p2):
+    """Column-sharded Gamma + per-site exchange (p2 ranks on one device, in-process exchange):
+    rows identical on every rank and equal to the unsharded sweep except boundary draws;
+    marginals within 1e-4 of the oracle."""
+    from paper_2512_20064_b200.parallel import TensorParallelLocal
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    st = to_state(pkg, mps)
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    tp = TensorParallelLocal(st, p2, policy=pol)
+    one = pkg.GpuSampler(st, pol)
+    for i in range(mps.num_sites):
+        assert np.array_equal(tp.decoded_gamma(i), one.decoded_gamma(i)), i
+    rows = tp.sample(0, 1000, 7)
+    for r in rows[1:]:
+        assert np.array_equal(r, rows[0])
+    dec = decoded_mps(one, mps)
+    ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, 1000, 7, want_marginals=True)
+    ndiff, explained = compare_strings(rows[0], ref_rows, ref_marg, 7)
+    assert ndiff == explained, (ndiff, explained)
+    marg = tp.marginals(0, ref_rows)[0]
+    big = ref_marg >= 1e-3
+    assert (np.abs(marg[big] - ref_marg[big]) / ref_marg[big]).max() < MARG_RTOL
+    tp.close()
