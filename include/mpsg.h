@@ -89,7 +89,11 @@ typedef struct mpsg_options {
                                       chiR, collective.cpp:80-92), the even-site pattern of
                                       parallel.cpp:420-443 applied at every site */
   int tp_rank;
-  int reserved[3];
+  int host_stream_slots;           /* 0: compressed Gamma resident in HBM.  >= 2: Gamma kept in
+                                      pinned host memory and streamed per site through this many
+                                      device slots by a copy stream overlapping the compute
+                                      (the reference's SiteStream prefetch, mps_io.cpp:294-350) */
+  int reserved[2];
 } mpsg_options;
 
 /* Mirrors mpsamp::RunStats + FlopCounters (sampler.hpp:46-54, contract.hpp:12-25). */

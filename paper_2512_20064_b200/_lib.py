@@ -28,7 +28,8 @@ class Policy(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("mode", _int), ("pass_samples", _u64), ("record_site_times", _int),
-                ("tp_size", _int), ("tp_rank", _int), ("reserved", _int * 3)]
+                ("tp_size", _int), ("tp_rank", _int), ("host_stream_slots", _int),
+                ("reserved", _int * 2)]
 
 
 class Stats(C.Structure):

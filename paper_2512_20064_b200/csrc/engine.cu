@@ -248,6 +248,10 @@ struct SiteDev {
   float2* cinfo = nullptr;   // [np]
   double* cs = nullptr;      // [chir * d]
   CUtensorMap tma_g{}, tma_env{};
+  // host-streamed mode: the compressed site lives in pinned host memory
+  __half* g_host = nullptr;
+  float2* cinfo_host = nullptr;
+  std::vector<CUtensorMap> tma_slot;  // G map per device slot
 };
 
 struct DevCtx {
@@ -269,6 +273,14 @@ struct DevCtx {
   size_t src_bytes = 0;
   int* err = nullptr;
   uint8_t* host_rows = nullptr;  // pinned [cap][M]
+  // host-streamed Gamma: ring of device slots filled by a copy stream (sequence q -> slot q % R)
+  int slots = 0;
+  std::vector<__half*> slot_g;
+  std::vector<float2*> slot_cinfo;
+  std::vector<cudaEvent_t> loaded, freed;
+  cudaStream_t copy_stream = nullptr;
+  uint64_t issued = 0, consumed = 0;  // rolling site-load sequence (sites 0..M-1, repeated)
+  uint64_t h2d_bytes = 0;
   std::vector<cudaEvent_t> ev;   // per-site boundaries (M + 1)
   std::vector<cudaEvent_t> gev;  // per-site GEMM start/stop (2 M)
 };
@@ -372,14 +384,38 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
   CUDA_OK(cudaMemset(dc.err, 0, sizeof(int)));
   CUDA_OK(cudaMalloc(&dc.scratch, sizeof(double) * (kmax + 2ull * h.tp * chirpm) + sizeof(int) * kmax));
   CUDA_OK(cudaMallocHost(&dc.host_rows, 1ull * dc.cap * h.M));
+  if (h.opts.host_stream_slots > 0) {
+    config_check(h.opts.host_stream_slots >= 2, "host_stream_slots must be 0 or >= 2");
+    dc.slots = h.opts.host_stream_slots;
+    size_t gmax = 0, nmax = 0;
+    for (uint64_t i = 0; i < h.M; ++i) {
+      const size_t kp = static_cast<size_t>(h.tp) * kshard_of(h, h.bonds[i]);
+      const size_t np = round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN);
+      gmax = std::max(gmax, 2 * np * kp);
+      nmax = std::max(nmax, np);
+    }
+    CUDA_OK(cudaStreamCreateWithFlags(&dc.copy_stream, cudaStreamNonBlocking));
+    dc.slot_g.resize(dc.slots);
+    dc.slot_cinfo.resize(dc.slots);
+    dc.loaded.resize(dc.slots);
+    dc.freed.resize(dc.slots);
+    for (int q = 0; q < dc.slots; ++q) {
+      CUDA_OK(cudaMalloc(&dc.slot_g[q], gmax * sizeof(__half)));
+      CUDA_OK(cudaMalloc(&dc.slot_cinfo[q], nmax * sizeof(float2)));
+      CUDA_OK(cudaEventCreateWithFlags(&dc.loaded[q], cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&dc.freed[q], cudaEventDisableTiming));
+    }
+  }
 }
 
 static void free_device(DevCtx& dc) {
   cudaSetDevice(dc.device);
   if (dc.stream) cudaStreamSynchronize(dc.stream);
   for (auto& s : dc.sites) {
-    cudaFree(s.g);
-    cudaFree(s.cinfo);
+    if (!dc.slots) {
+      cudaFree(s.g);
+      cudaFree(s.cinfo);
+    }
     cudaFree(s.cs);
   }
   cudaFree(dc.env);
@@ -396,6 +432,17 @@ static void free_device(DevCtx& dc) {
   if (dc.host_rows) cudaFreeHost(dc.host_rows);
   for (auto e : dc.ev) cudaEventDestroy(e);
   for (auto e : dc.gev) cudaEventDestroy(e);
+  if (dc.copy_stream) cudaStreamSynchronize(dc.copy_stream);
+  for (auto& s : dc.sites) {
+    if (s.g_host) cudaFreeHost(s.g_host);
+    if (s.cinfo_host) cudaFreeHost(s.cinfo_host);
+    if (dc.slots) s.g = nullptr, s.cinfo = nullptr;  // slot buffers, freed below
+  }
+  for (auto p : dc.slot_g) cudaFree(p);
+  for (auto p : dc.slot_cinfo) cudaFree(p);
+  for (auto e : dc.loaded) cudaEventDestroy(e);
+  for (auto e : dc.freed) cudaEventDestroy(e);
+  if (dc.copy_stream) cudaStreamDestroy(dc.copy_stream);
   if (dc.stream) cudaStreamDestroy(dc.stream);
 }
 
@@ -412,10 +459,14 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
   s.chirp = chirp_of(h, h.bonds[i + 1]);
   s.np = round_up(static_cast<int>(h.d) * s.chirp, 2 * kBN);  // whole N-tile pairs (CTA pairs)
   s.nt = s.np / kBN;
-  if (!s.g) {
+  if (!s.cs) CUDA_OK(cudaMalloc(&s.cs, std::max<size_t>(1, 1ull * s.width * h.d) * sizeof(double)));
+  if (dc.slots) {  // compress into slot 0, then keep the result in pinned host memory
+    CUDA_OK(cudaStreamSynchronize(dc.copy_stream));
+    s.g = dc.slot_g[0];
+    s.cinfo = dc.slot_cinfo[0];
+  } else if (!s.g) {
     CUDA_OK(cudaMalloc(&s.g, 2ull * s.np * s.kp * sizeof(__half)));
     CUDA_OK(cudaMalloc(&s.cinfo, 1ull * s.np * sizeof(float2)));
-    CUDA_OK(cudaMalloc(&s.cs, std::max<size_t>(1, 1ull * s.width * h.d) * sizeof(double)));
   }
   std::vector<double> wl(s.chir);
   for (int r = 0; r < s.chir; ++r) {
@@ -450,8 +501,40 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
     throw Error(MPSG_ERR_NUMERIC, "contract_site: non-finite input (site " + std::to_string(i) +
                                       ") or dynamic range beyond the compressed format");
   }
-  s.tma_g = make_tma_2d(s.g, s.kp, 2ull * s.np);
   s.tma_env = make_tma_env(dc.env, s.kshard, 4ull * dc.cap, h.tp);
+  if (dc.slots) {
+    if (!s.g_host) {
+      CUDA_OK(cudaMallocHost(&s.g_host, 2ull * s.np * s.kp * sizeof(__half)));
+      CUDA_OK(cudaMallocHost(&s.cinfo_host, 1ull * s.np * sizeof(float2)));
+    }
+    CUDA_OK(cudaMemcpyAsync(s.g_host, s.g, 2ull * s.np * s.kp * sizeof(__half), cudaMemcpyDeviceToHost, dc.stream));
+    CUDA_OK(cudaMemcpyAsync(s.cinfo_host, s.cinfo, 1ull * s.np * sizeof(float2), cudaMemcpyDeviceToHost, dc.stream));
+    CUDA_OK(cudaStreamSynchronize(dc.stream));
+    s.tma_slot.resize(dc.slots);
+    for (int q = 0; q < dc.slots; ++q) s.tma_slot[q] = make_tma_2d(dc.slot_g[q], s.kp, 2ull * s.np);
+    s.g = nullptr;
+    s.cinfo = nullptr;
+    dc.issued = dc.consumed = 0;  // slot 0 was overwritten: restart the load sequence
+  } else {
+    s.tma_g = make_tma_2d(s.g, s.kp, 2ull * s.np);
+  }
+}
+
+// Host-streamed mode: issue site loads until `upto` loads are in flight or done.
+static void issue_loads(mpsg_handle_s& h, DevCtx& dc, uint64_t upto) {
+  while (dc.issued < upto) {
+    const uint64_t q = dc.issued;
+    const int slot = static_cast<int>(q % dc.slots);
+    const SiteDev& s = dc.sites[q % h.M];
+    CUDA_OK(cudaStreamWaitEvent(dc.copy_stream, dc.freed[slot], 0));  // consume q - slots done
+    const size_t gb = 2ull * s.np * s.kp * sizeof(__half);
+    CUDA_OK(cudaMemcpyAsync(dc.slot_g[slot], s.g_host, gb, cudaMemcpyHostToDevice, dc.copy_stream));
+    CUDA_OK(cudaMemcpyAsync(dc.slot_cinfo[slot], s.cinfo_host, 1ull * s.np * sizeof(float2),
+                            cudaMemcpyHostToDevice, dc.copy_stream));
+    CUDA_OK(cudaEventRecord(dc.loaded[slot], dc.copy_stream));
+    dc.h2d_bytes += gb + 1ull * s.np * sizeof(float2);
+    ++dc.issued;
+  }
 }
 
 static void ensure_src(DevCtx& dc, size_t bytes) {
@@ -508,8 +591,19 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
   const int rows = round_up(count, kBM);
   launch_init_env(dc.env, dc.cap, dc.sites[0].kshard, h.tp, rows, count, dc.alive, dc.stream);
   po.launches += 1;
+  if (dc.slots) issue_loads(h, dc, dc.consumed + dc.slots);
   for (uint64_t i = 0; i < h.M; ++i) {
     const SiteDev& s = dc.sites[i];
+    const CUtensorMap* tma_g = &s.tma_g;
+    const float2* cinfo = s.cinfo;
+    int slot = -1;
+    if (dc.slots) {
+      if (dc.consumed % h.M != i) throw Error(MPSG_ERR_INTERNAL, "site stream out of sequence");
+      slot = static_cast<int>(dc.consumed % dc.slots);
+      CUDA_OK(cudaStreamWaitEvent(dc.stream, dc.loaded[slot], 0));
+      tma_g = &s.tma_slot[slot];
+      cinfo = dc.slot_cinfo[slot];
+    }
     SiteGemmArgs ga;
     ga.m_tiles = rows / kBM;
     ga.n_tiles = s.nt;
@@ -520,13 +614,18 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
     ga.chirp = s.chirp;
     ga.d = static_cast<int>(h.d);
     ga.group_n = std::min(s.nt / 2, kGroupPairs);
-    ga.cinfo = s.cinfo;
+    ga.cinfo = cinfo;
     ga.temp = dc.temp;
     ga.pstat = dc.pstat;
     const int tiles = ga.m_tiles * ga.n_tiles;  // = 2 x (tile-pair units)
     if (timing >= 2) CUDA_OK(cudaEventRecord(dc.gev[2 * i], dc.stream));
-    launch_site_gemm(h.split, s.tma_env, s.tma_g, ga, std::min(tiles, dc.num_sms), dc.stream);
+    launch_site_gemm(h.split, s.tma_env, *tma_g, ga, std::min(tiles, dc.num_sms), dc.stream);
     if (timing >= 2) CUDA_OK(cudaEventRecord(dc.gev[2 * i + 1], dc.stream));
+    if (dc.slots) {  // K1 is the only reader of the slot: hand it back to the copy stream
+      CUDA_OK(cudaEventRecord(dc.freed[slot], dc.stream));
+      ++dc.consumed;
+      issue_loads(h, dc, dc.consumed + dc.slots);
+    }
 
     SelectArgs sa;
     sa.site = static_cast<int>(i);
@@ -687,6 +786,8 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
       for (uint64_t n = 0; n < count; ++n) st->dead_samples += rows_host[n * h.M + h.M - 1] == kDead;
     st->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     st->h2d_bytes = forced ? count * h.M : 0;
+    for (auto& dc : h.devs) st->h2d_bytes += dc.h2d_bytes;
+    for (auto& dc : h.devs) dc.h2d_bytes = 0;
     st->d2h_bytes = rows_host ? count * h.M : 0;
     if (st->site_seconds) {
       for (uint64_t i = 0; i < h.M; ++i) {
@@ -846,7 +947,7 @@ uint64_t mpsg_state_bytes(mpsg_handle h) {
   if (!h || h->devs.empty()) return 0;
   uint64_t b = 0;
   for (const auto& s : h->devs[0].sites) b += 2ull * s.np * s.kp * sizeof(__half);
-  return b;
+  return b;  // host-streamed: these bytes live in pinned host memory
 }
 
 int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
@@ -858,7 +959,10 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
     const SiteDev& s = dc.sites[site];
     std::vector<__half> g(2ull * s.np * s.kp);
     std::vector<double> cs(std::max<size_t>(1, 1ull * s.width * h->d));
-    CUDA_OK(cudaMemcpy(g.data(), s.g, g.size() * sizeof(__half), cudaMemcpyDeviceToHost));
+    if (dc.slots)
+      std::memcpy(g.data(), s.g_host, g.size() * sizeof(__half));
+    else
+      CUDA_OK(cudaMemcpy(g.data(), s.g, g.size() * sizeof(__half), cudaMemcpyDeviceToHost));
     CUDA_OK(cudaMemcpy(cs.data(), s.cs, cs.size() * sizeof(double), cudaMemcpyDeviceToHost));
     const size_t d = h->d;
     std::vector<int> lpos(s.chil);
@@ -969,6 +1073,7 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
     config_check(h != nullptr && env != nullptr && temp != nullptr, "null argument");
     config_check(site < h->M && h->finished, "bad site / unfinished state");
     config_check(h->tp == 1, "mpsg_contract_site: not available on a tensor-parallel handle");
+    config_check(h->devs[0].slots == 0, "mpsg_contract_site: not available in host-streamed mode");
     DevCtx& dc = h->devs[0];
     config_check(count >= 1 && count <= static_cast<uint64_t>(dc.cap), "count exceeds pass capacity");
     CUDA_OK(cudaSetDevice(dc.device));

@@ -371,22 +371,39 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
     a.alive[n] = live_out ? 1 : 0;
   }
   if (a.kp_next > 0) {
-    // next env row: E[n, r] = temp[n, k, r] * 2^-e, split hi/lo fp16 (zeros for dead / pad)
+    // next env row: E[n, r] = temp[n, k, r] * 2^-e, split hi/lo fp16 (zeros for dead / pad).
+    // Each lane handles 4 consecutive columns: two 16 B loads, one 8 B store per plane.
     const size_t plane = static_cast<size_t>(a.env_cap) * a.kp_next;
     __half* e0 = a.env_next + static_cast<size_t>(n) * a.kp_next;
     const float2* src = a.temp + (static_cast<size_t>(n) * a.d + (live_out ? outcome : 0)) * a.chirp;
-    for (int r = lane; r < a.kp_next; r += 32) {
-      float2 v = make_float2(0.f, 0.f);
-      if (live_out && r < a.chir_loc) {
-        v = src[r];
-        v.x *= scale;
-        v.y *= scale;
+    const int live_cols = live_out ? a.chir_loc : 0;
+    for (int r = lane * 4; r < a.kp_next; r += 128) {  // kp_next is a multiple of 32
+      float4 v01 = make_float4(0.f, 0.f, 0.f, 0.f), v23 = v01;
+      if (r + 3 < live_cols) {  // chirp is a multiple of 128: these loads stay inside the row
+        v01 = *reinterpret_cast<const float4*>(src + r);
+        v23 = *reinterpret_cast<const float4*>(src + r + 2);
+      } else if (r < live_cols) {
+        const float2 z = make_float2(0.f, 0.f);
+        const float2 c0 = src[r];
+        const float2 c1 = r + 1 < live_cols ? src[r + 1] : z;
+        const float2 c2 = r + 2 < live_cols ? src[r + 2] : z;
+        v01 = make_float4(c0.x, c0.y, c1.x, c1.y);
+        v23 = make_float4(c2.x, c2.y, 0.f, 0.f);
       }
-      const __half hr = __float2half_rn(v.x), hi = __float2half_rn(v.y);
-      e0[r] = hr;
-      e0[plane + r] = hi;
-      e0[2 * plane + r] = __float2half_rn(v.x - __half2float(hr));
-      e0[3 * plane + r] = __float2half_rn(v.y - __half2float(hi));
+      const float re[4] = {v01.x * scale, v01.z * scale, v23.x * scale, v23.z * scale};
+      const float im[4] = {v01.y * scale, v01.w * scale, v23.y * scale, v23.w * scale};
+      __align__(8) __half hr[4], hi[4], lr[4], li[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        hr[j] = __float2half_rn(re[j]);
+        hi[j] = __float2half_rn(im[j]);
+        lr[j] = __float2half_rn(re[j] - __half2float(hr[j]));
+        li[j] = __float2half_rn(im[j] - __half2float(hi[j]));
+      }
+      *reinterpret_cast<uint2*>(e0 + r) = *reinterpret_cast<const uint2*>(hr);
+      *reinterpret_cast<uint2*>(e0 + plane + r) = *reinterpret_cast<const uint2*>(hi);
+      *reinterpret_cast<uint2*>(e0 + 2 * plane + r) = *reinterpret_cast<const uint2*>(lr);
+      *reinterpret_cast<uint2*>(e0 + 3 * plane + r) = *reinterpret_cast<const uint2*>(li);
     }
   }
 }

@@ -235,7 +235,8 @@ class GpuSampler:
 
     def __init__(self, mps: MpsState, policy: Optional[PrecisionPolicy] = None, mode: Mode = Mode.AUTO,
                  devices: Optional[Sequence[int]] = None, pass_samples: int = 0,
-                 record_site_times: bool = False, tp_size: int = 1, tp_rank: int = 0):
+                 record_site_times: bool = False, tp_size: int = 1, tp_rank: int = 0,
+                 host_stream_slots: int = 0):
         L = _lib.lib()
         mps.validate()
         self.policy = policy or PrecisionPolicy()
@@ -250,7 +251,8 @@ class GpuSampler:
                             (_lib._pd * len(g))(*[x.ctypes.data_as(_lib._pd) for x in g]),
                             (_lib._pd * len(lam))(*[x.ctypes.data_as(_lib._pd) for x in lam]))
         pol = _lib.Policy(int(self.policy.compute), int(self.policy.storage), int(self.policy.scaling))
-        opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), int(tp_size), int(tp_rank))
+        opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), int(tp_size), int(tp_rank),
+                           int(host_stream_slots))
         self.tp_size, self.tp_rank = tp_size, tp_rank
         devs, nd = self._devices(devices)
         _check(L.mpsg_create(C.byref(view), C.byref(pol), C.byref(opt), devs, nd, C.byref(self._h)))

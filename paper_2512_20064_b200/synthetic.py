@@ -46,7 +46,8 @@ def build_synthetic(num_sites: int, chi: int, d: int, seed: int = 42, level_damp
                     lambda_decay: Optional[float] = None, policy: Optional[PrecisionPolicy] = None,
                     mode: Mode = Mode.AUTO, devices: Optional[Sequence[int]] = None,
                     pass_samples: int = 0, n_base: int = 4, record_site_times: bool = False,
-                    keep_host: bool = False):
+                    keep_host: bool = False, tp_size: int = 1, tp_rank: int = 0,
+                    host_stream_slots: int = 0):
     """Build a GpuSampler holding a synthetic chain; returns (sampler, lambdas[, host gammas]).
 
     The MPS is generated and compressed site by site on the first device, never materialised in
@@ -68,7 +69,8 @@ def build_synthetic(num_sites: int, chi: int, d: int, seed: int = 42, level_damp
     h = C.c_void_p()
     bd = (C.c_uint64 * (num_sites + 1))(*bonds)
     pol = _lib.Policy(int(policy.compute), int(policy.storage), int(policy.scaling))
-    opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times))
+    opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), int(tp_size), int(tp_rank),
+                       int(host_stream_slots))
     devs, nd = GpuSampler._devices(devices)
     _check(L.mpsg_builder_begin(num_sites, d, bd, C.byref(pol), C.byref(opt), devs, nd, C.byref(h)))
     host = [] if keep_host else None
@@ -100,4 +102,5 @@ def build_synthetic(num_sites: int, chi: int, d: int, seed: int = 42, level_damp
         L.mpsg_destroy(h)
         raise
     smp = GpuSampler.from_builder(h, num_sites, d, bonds, policy)
+    smp.tp_size, smp.tp_rank = tp_size, tp_rank
     return (smp, lambdas, host) if keep_host else (smp, lambdas)

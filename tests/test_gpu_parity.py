@@ -170,3 +170,22 @@ def test_tensor_parallel_local(pkg, gold, p2):
     big = ref_marg >= 1e-3
     assert (np.abs(marg[big] - ref_marg[big]) / ref_marg[big]).max() < MARG_RTOL
     tp.close()
+
+
+@pytest.mark.parametrize("slots", [2, 3])
+def test_host_streamed_gamma(pkg, gold, slots):
+    """Gamma kept in pinned host memory and streamed through `slots` device buffers: identical rows
+    to the HBM-resident sweep, across several passes (the load sequence wraps around the chain)."""
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    st = to_state(pkg, mps)
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    res = pkg.GpuSampler(st, pol, pass_samples=256)
+    stm = pkg.GpuSampler(st, pol, pass_samples=256, host_stream_slots=slots)
+    for i in (0, 7, 15):
+        assert np.array_equal(stm.decoded_gamma(i), res.decoded_gamma(i))
+    a = res.sample(0, 1000, 7)
+    stats = pkg.RunStats()
+    b = stm.sample(0, 1000, 7, stats=stats)
+    assert np.array_equal(a, b)
+    assert np.array_equal(stm.sample(123, 77, 7), a[123:200])
