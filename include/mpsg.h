@@ -147,6 +147,17 @@ uint64_t mpsg_state_bytes(mpsg_handle h);
  * handle writes only its own column shard (other entries are left untouched). */
 int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out);
 
+/* ---- MPSB files (the reference's on-disk format, mps_io.hpp:17-24) ----------------------- */
+/* Read an MPSB file (any storage precision, checksums verified -> MPSG_ERR_IO) and build the
+ * device state, streaming sites through a one-slot prefetch thread (SiteStream,
+ * mps_io.cpp:294-350).  The file-based executors run_serial / run_data_parallel
+ * (parallel.hpp:24-52) become mpsg_create_from_file + mpsg_sample. */
+int mpsg_create_from_file(const char* path, const mpsg_policy* policy, const mpsg_options* opts,
+                          const int* devices, int ndev, mpsg_handle* out);
+/* Write the state as an MPSB file (save_mps, mps_io.cpp:167-210): the decoded Gamma values at
+ * `storage` precision (MPSG_F64 / F32 / F16) and the Lambda vectors. */
+int mpsg_save_file(mpsg_handle h, const char* path, int storage);
+
 /* ---- tensor parallelism ------------------------------------------------------------------ */
 /* Per site every rank contracts its Gamma column shard with the full environment, the per-
  * (sample, outcome) (weight, max) partials are all-gathered and summed in rank order (so every

@@ -97,16 +97,27 @@ inline void sample_micro_serial(const DeviceState& st, uint64_t first, size_t co
 }
 
 // mpsamp::sample_batch (sampler.cpp:164-205) on the B200.
-inline mpsamp::SampleBatch sample_batch(const mpsamp::MpsState& mps, const mpsamp::BatchPlan& plan_in,
-                                        const mpsamp::SamplerOptions& opts,
+inline mpsamp::SampleBatch sample_batch(const mpsamp::MpsState& mps_in, const mpsamp::BatchPlan& plan_in,
+                                        const mpsamp::SamplerOptions& opts_in,
                                         mpsamp::RunStats* stats_out = nullptr,
                                         const std::vector<int>& devices = {}) {
-  mps.validate();
-  opts.policy.validate();
+  mps_in.validate();
+  opts_in.policy.validate();
   mpsamp::BatchPlan plan = plan_in;
   plan.normalize();
-  if (opts.schedule || opts.site_transform)
-    throw mpsamp::ConfigError("mpsg: bond schedules / site transforms are not on the GPU path");
+  if (opts_in.site_transform)
+    throw mpsamp::ConfigError("mpsg: site transforms are not on the GPU path");
+  // a BondSchedule truncates the chain first, with the reference's own apply_schedule
+  // (sampler.cpp:173-176)
+  mpsamp::MpsState truncated;
+  const mpsamp::MpsState* state = &mps_in;
+  if (opts_in.schedule) {
+    truncated = mpsamp::apply_schedule(mps_in, *opts_in.schedule);
+    state = &truncated;
+  }
+  const mpsamp::MpsState& mps = *state;
+  mpsamp::SamplerOptions opts = opts_in;
+  opts.schedule.reset();
   mpsg_options o{};
   o.record_site_times = stats_out ? 1 : 0;
   DeviceState st(mps, opts.policy, devices, &o);
@@ -119,6 +130,47 @@ inline mpsamp::SampleBatch sample_batch(const mpsamp::MpsState& mps, const mpsam
   mpsamp::RunStats stats;
   sample_micro_serial(st, 0, plan.total_samples, opts, b.outcomes.data(), stats);
   if (stats_out) *stats_out = std::move(stats);
+  return b;
+}
+
+// run_serial / run_data_parallel (parallel.hpp:24-52) on an MPSB file: the file is streamed into
+// the compressed device state (mpsg_create_from_file) and sampled on `p1` B200s (devices 0..p1-1
+// unless given).  Returns the batch and merged RunStats like ParallelResult (no CommStats: the
+// data path has no collective).
+inline mpsamp::SampleBatch run_data_parallel_file(const std::string& mps_path,
+                                                  const mpsamp::BatchPlan& plan_in, size_t p1,
+                                                  const mpsamp::SamplerOptions& opts,
+                                                  mpsamp::RunStats* stats_out = nullptr,
+                                                  std::vector<int> devices = {}) {
+  if (p1 < 1) throw mpsamp::ConfigError("data parallel needs p1 >= 1");
+  opts.policy.validate();
+  if (opts.site_transform || opts.schedule)
+    throw mpsamp::ConfigError("mpsg: schedules / site transforms are not on the file path");
+  mpsamp::BatchPlan plan = plan_in;
+  plan.normalize();
+  if (devices.empty())
+    for (size_t i = 0; i < p1; ++i) devices.push_back(static_cast<int>(i));
+  const mpsg_policy pol{static_cast<int>(opts.policy.compute), static_cast<int>(opts.policy.storage),
+                        static_cast<int>(opts.policy.scaling)};
+  mpsg_options o{};
+  o.record_site_times = stats_out ? 1 : 0;
+  mpsg_handle h = nullptr;
+  check(mpsg_create_from_file(mps_path.c_str(), &pol, &o, devices.data(),
+                              static_cast<int>(devices.size()), &h));
+  std::unique_ptr<mpsg_handle_s, void (*)(mpsg_handle)> guard(h, mpsg_destroy);
+  // chain shape from the file header (read_mps_info, mps_io.cpp:212-254)
+  mpsamp::MpsFileInfo info = mpsamp::read_mps_info(mps_path);
+  mpsamp::SampleBatch b;
+  b.num_samples = plan.total_samples;
+  b.num_sites = info.num_sites;
+  b.phys_dim = info.phys_dim;
+  b.seed = opts.seed;
+  b.outcomes.assign(plan.total_samples * info.num_sites, mpsamp::kDeadOutcome);
+  std::vector<double> site(info.num_sites, 0.0);
+  mpsg_stats s{};
+  s.site_seconds = site.data();
+  check(mpsg_sample(h, opts.seed, 0, plan.total_samples, b.outcomes.data(), &s));
+  if (stats_out) merge_stats(s, site, *stats_out);
   return b;
 }
 

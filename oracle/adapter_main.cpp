@@ -8,6 +8,7 @@
 
 #include "mpsamp/errors.hpp"
 #include "mpsamp/mps.hpp"
+#include "mpsamp/mps_io.hpp"
 #include "mpsamp/sampler.hpp"
 #include "mpsg_mpsamp.hpp"
 
@@ -47,6 +48,29 @@ int main(int argc, char** argv) {
   size_t diff = 0;
   for (size_t n = 0; n < 1000; ++n)
     diff += std::memcmp(&got.outcomes[n * 16], &want.outcomes[n * 16], 16) != 0;
+  // schedule through the adapter == the reference's truncation sampled directly
+  {
+    mpsamp::SamplerOptions so = opts;
+    so.schedule = mpsamp::BondSchedule::full(mps.bond_dims, 32);
+    so.schedule->per_site_chi[5] = 20;
+    mpsamp::SampleBatch a = mpsg_mpsamp::sample_batch(mps, mpsamp::BatchPlan::simple(300), so);
+    mpsamp::SampleBatch c = mpsg_mpsamp::sample_batch(mpsamp::apply_schedule(mps, *so.schedule),
+                                                      mpsamp::BatchPlan::simple(300), opts);
+    if (a.outcomes != c.outcomes) {
+      std::printf("FAIL: scheduled sampling differs\n");
+      return 1;
+    }
+  }
+  // file executor: save with the reference, run through the adapter
+  {
+    mpsamp::save_mps(mps, "/tmp/mpsg_adapter_c1.mpsb", mpsamp::Precision::F64);
+    mpsamp::SampleBatch f = mpsg_mpsamp::run_data_parallel_file("/tmp/mpsg_adapter_c1.mpsb",
+                                                                mpsamp::BatchPlan::simple(1000), 1, opts);
+    if (f.outcomes != got.outcomes) {
+      std::printf("FAIL: file executor differs from in-memory\n");
+      return 1;
+    }
+  }
   std::printf("adapter gpu: %zu/1000 strings differ from the reference on the original (uncompressed) "
               "Gamma; contraction_macs %llu (reference %llu)\n",
               diff, static_cast<unsigned long long>(st.flops.contraction_macs), 45600000ull);

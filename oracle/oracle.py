@@ -122,6 +122,12 @@ def ref():
         L.ref_time_site_step.argtypes = [C.c_void_p, _sz, _u64, _int, _int, C.POINTER(_u64)]
         L.ref_save_mps.restype = _int
         L.ref_save_mps.argtypes = [C.c_void_p, C.c_char_p, _int]
+        L.ref_mps_load.restype = C.c_void_p
+        L.ref_mps_load.argtypes = [C.c_char_p]
+        L.ref_mps_apply_schedule.restype = C.c_void_p
+        L.ref_mps_apply_schedule.argtypes = [C.c_void_p, C.POINTER(_sz), _sz, _sz]
+        L.ref_sample_batch_scheduled.restype = _int
+        L.ref_sample_batch_scheduled.argtypes = [C.c_void_p, _u64, _u64, _int, C.POINTER(_sz), _sz, _sz, _pu8]
         L.ref_run_scheme.restype = _int
         L.ref_run_scheme.argtypes = [C.c_char_p, _int, _u64, _u64, _u64, _sz, _sz, _u64, _int,
                                      _int, _pu8]
@@ -288,3 +294,30 @@ def orc_time_site_step(gamma: np.ndarray, lam: np.ndarray, count: int):
     t0 = _t.perf_counter()
     macs = orc().orc_site_step(g.ctypes.data_as(_pd), cl, cr, d, lam.ctypes.data_as(_pd), count, 7)
     return _t.perf_counter() - t0, macs
+
+
+def ref_load_mps(path: str) -> Mps:
+    h = ref().ref_mps_load(path.encode())
+    if not h:
+        raise OracleError(4, ref().ref_last_error().decode())
+    try:
+        return _mps_from_handle(h)
+    finally:
+        ref().ref_mps_free(h)
+
+
+def ref_save_mps(mps: Mps, path: str, storage: int = F64) -> None:
+    rs = RefState(mps)
+    _check_ref(ref().ref_save_mps(rs.h, path.encode(), storage))
+
+
+def ref_apply_schedule(mps: Mps, chi: list, chi_max: int) -> Mps:
+    rs = RefState(mps)
+    arr = (_sz * len(chi))(*chi)
+    h = ref().ref_mps_apply_schedule(rs.h, arr, len(chi), chi_max)
+    if not h:
+        raise OracleError(2, ref().ref_last_error().decode())
+    try:
+        return _mps_from_handle(h)
+    finally:
+        ref().ref_mps_free(h)

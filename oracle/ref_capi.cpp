@@ -353,3 +353,43 @@ int ref_contract_site(const double* env, size_t count, size_t chil, const double
     }
 }
 }
+
+extern "C" {
+// load_mps (mps_io.cpp:277-292) -> MpsState handle
+void* ref_mps_load(const char* path) {
+    try {
+        return new MpsState(load_mps(path));
+    } catch (...) {
+        map_exception();
+        return nullptr;
+    }
+}
+// apply_schedule (sampler.cpp:218-246) -> new MpsState handle
+void* ref_mps_apply_schedule(void* h, const size_t* per_site_chi, size_t n, size_t chi_max) {
+    try {
+        BondSchedule s;
+        s.per_site_chi.assign(per_site_chi, per_site_chi + n);
+        s.chi_max = chi_max;
+        return new MpsState(apply_schedule(*static_cast<MpsState*>(h), s));
+    } catch (...) {
+        map_exception();
+        return nullptr;
+    }
+}
+// sample_batch with a BondSchedule in SamplerOptions (sampler.cpp:173-176)
+int ref_sample_batch_scheduled(void* h, uint64_t n, uint64_t seed, int scaling, const size_t* chi,
+                               size_t nchi, size_t chi_max, uint8_t* out) {
+    try {
+        SamplerOptions o = make_opts(seed, 0, scaling);
+        BondSchedule s;
+        s.per_site_chi.assign(chi, chi + nchi);
+        s.chi_max = chi_max;
+        o.schedule = s;
+        SampleBatch b = sample_batch(*static_cast<MpsState*>(h), BatchPlan::simple(n), o);
+        std::memcpy(out, b.outcomes.data(), b.outcomes.size());
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+}

@@ -7,6 +7,11 @@ include/mpsg.h.  This package is the host-side mirror of the reference's ``mpsam
 from .sampler import (  # noqa: F401
     DEAD_OUTCOME,
     BatchPlan,
+    BondSchedule,
+    ParallelResult,
+    apply_schedule,
+    run_data_parallel,
+    run_serial,
     ConfigError,
     DeviceError,
     DimensionError,

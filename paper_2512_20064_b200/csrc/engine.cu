@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "../../include/mpsg.h"
+#include "internal.hpp"
 #include "sweep.cuh"
 
 namespace mpsg {
@@ -40,6 +41,7 @@ struct Error : std::runtime_error {
   Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 #define CUDA_OK(expr)                                                                     \
   do {                                                                                    \
@@ -294,6 +296,7 @@ struct mpsg_handle_s {
   mpsg_options opts{};
   bool split = true;
   std::vector<std::vector<double>> gl, gr;  // per site: left / right bond scales
+  std::vector<std::vector<double>> lambda;  // Lambda_i as given (MPSB save, reporting)
   std::vector<mpsg::DevCtx> devs;
   std::vector<char> site_set;
   bool finished = false;
@@ -556,6 +559,7 @@ static void set_site(mpsg_handle_s& h, uint64_t i, const void* gamma, bool is_de
   const size_t chir = h.bonds[i + 1];
   validate_lambda(lambda, chir);
   h.gr[i] = bond_scales(lambda, chir);
+  h.lambda[i].assign(lambda, lambda + chir);
   if (i + 1 < h.M) h.gl[i + 1] = h.gr[i];
   const size_t elems = 2ull * h.bonds[i] * chir * h.d;
   const size_t bytes = elems * (dtype == MPSG_F64 ? 8 : 4);
@@ -800,6 +804,16 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
   }
 }
 
+void handle_chain(mpsg_handle h, uint64_t& m, uint64_t& d, std::vector<uint64_t>& bonds,
+                  std::vector<const double*>& lambdas) {
+  config_check(h->finished, "state not finished");
+  m = h->M;
+  d = h->d;
+  bonds = h->bonds;
+  lambdas.clear();
+  for (auto& l : h->lambda) lambdas.push_back(l.data());
+}
+
 }  // namespace mpsg
 
 // =============================================================================================
@@ -876,6 +890,7 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
       h->gr[i].assign(h->bonds[i + 1], 1.0);
     }
     h->site_set.assign(num_sites, 0);
+    h->lambda.resize(num_sites);
     if (ndev <= 0 || devices == nullptr) {
       h->devs.resize(1);
       h->devs[0].device = 0;

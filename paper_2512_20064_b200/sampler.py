@@ -257,6 +257,27 @@ class GpuSampler:
         devs, nd = self._devices(devices)
         _check(L.mpsg_create(C.byref(view), C.byref(pol), C.byref(opt), devs, nd, C.byref(self._h)))
 
+    @classmethod
+    def from_file(cls, path: str, policy: Optional[PrecisionPolicy] = None, mode: Mode = Mode.AUTO,
+                  devices: Optional[Sequence[int]] = None, pass_samples: int = 0,
+                  record_site_times: bool = False, host_stream_slots: int = 0) -> "GpuSampler":
+        """Build the device state from an MPSB file (the reference's format, mps_io.hpp:17-24)."""
+        L = _lib.lib()
+        policy = policy or PrecisionPolicy()
+        policy.validate()
+        pol = _lib.Policy(int(policy.compute), int(policy.storage), int(policy.scaling))
+        opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), 1, 0, int(host_stream_slots))
+        devs, nd = cls._devices(devices)
+        h = C.c_void_p()
+        _check(L.mpsg_create_from_file(path.encode(), C.byref(pol), C.byref(opt), devs, nd, C.byref(h)))
+        m, d, bonds = _read_mpsb_shape(path)
+        self = cls.from_builder(h, m, d, bonds, policy)
+        return self
+
+    def save(self, path: str, storage: Precision = Precision.F64) -> None:
+        """save_mps (mps_io.cpp:167-210) of the decoded state."""
+        _check(_lib.lib().mpsg_save_file(self._h, path.encode(), int(storage)))
+
     @staticmethod
     def _devices(devices):
         if not devices:
@@ -340,6 +361,57 @@ class GpuSampler:
         return out
 
 
+def _read_mpsb_shape(path: str):
+    import struct
+    with open(path, "rb") as f:
+        head = f.read(24)
+        if head[:4] != b"MPSB":
+            raise IoError("not an mps file: " + path)
+        m, d = struct.unpack("<QQ", head[8:24])
+        bonds = list(struct.unpack(f"<{m + 1}Q", f.read(8 * (m + 1))))
+    return m, d, bonds
+
+
+# ---- BondSchedule (mps.hpp:27-36, mps.cpp:40-76) and apply_schedule (sampler.cpp:218-246) ------
+@dataclass
+class BondSchedule:
+    per_site_chi: list = field(default_factory=list)  # length M + 1
+    chi_max: int = 0
+
+    def compute_ratio(self) -> float:
+        sites = len(self.per_site_chi) - 1
+        work = sum(float(self.per_site_chi[i]) * self.per_site_chi[i + 1] for i in range(sites))
+        return work / (sites * float(self.chi_max) * self.chi_max)
+
+    def step_ratio(self) -> float:
+        inner = self.per_site_chi[1:-1]
+        return 0.0 if not inner else sum(1 for c in inner if c == self.chi_max) / len(inner)
+
+    def equivalent_chi(self) -> float:
+        inner = self.per_site_chi[1:-1]
+        return 1.0 if not inner else float(np.sqrt(np.mean(np.square(np.array(inner, dtype=float)))))
+
+    @staticmethod
+    def full(bond_dims, chi_max: int) -> "BondSchedule":
+        return BondSchedule(list(bond_dims), chi_max)
+
+
+def apply_schedule(mps: MpsState, schedule: BondSchedule) -> MpsState:
+    """Truncate gammas / lambdas to the schedule's per-site bonds (sampler.cpp:218-246)."""
+    if len(schedule.per_site_chi) != len(mps.bond_dims):
+        raise DimensionError("bond schedule length does not match state")
+    bonds = [min(int(a), int(b)) for a, b in zip(schedule.per_site_chi, mps.bond_dims)]
+    if any(b == 0 for b in bonds):
+        raise DimensionError("bond schedule has a zero bond")
+    bonds[0] = bonds[-1] = 1
+    out = MpsState(mps.num_sites, mps.phys_dim, bonds)
+    for i in range(mps.num_sites):
+        cl, cr = bonds[i], bonds[i + 1]
+        out.gammas.append(np.ascontiguousarray(mps.gammas[i][:cl, :cr, :]))
+        out.lambdas.append(np.ascontiguousarray(np.asarray(mps.lambdas[i])[:cr]))
+    return out
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(_lib.lib().mpsg_nccl_unique_id(buf))
@@ -376,8 +448,8 @@ def sample_batch(mps: MpsState, plan: BatchPlan, opts: SamplerOptions,
     opts.policy.validate()
     plan = BatchPlan(plan.total_samples, plan.macro_batch, plan.micro_batch)
     plan.normalize()
-    if opts.schedule is not None:
-        raise ConfigError("bond schedules are not supported by the GPU sweep (out of scope)")
+    if opts.schedule is not None:  # sampler.cpp:173-176
+        mps = apply_schedule(mps, opts.schedule)
     if opts.site_transform is not None:
         raise ConfigError("site transforms are not supported by the GPU sweep (out of scope)")
     t0 = time.perf_counter()
@@ -391,3 +463,36 @@ def sample_batch(mps: MpsState, plan: BatchPlan, opts: SamplerOptions,
     if stats is not None:
         stats.total_seconds = time.perf_counter() - t0
     return SampleBatch(plan.total_samples, mps.num_sites, mps.phys_dim, opts.seed, rows)
+
+
+# ---- file-backed executors (parallel.hpp:24-52) ------------------------------------------------
+@dataclass
+class ParallelResult:
+    batch: SampleBatch = None
+    stats: RunStats = None
+
+
+def run_serial(mps_path: str, plan: BatchPlan, opts: SamplerOptions) -> ParallelResult:
+    """run_serial (parallel.cpp:232-238): load the MPSB file and sample on one B200."""
+    return run_data_parallel(mps_path, plan, 1, opts)
+
+
+def run_data_parallel(mps_path: str, plan: BatchPlan, p1: int, opts: SamplerOptions,
+                      devices: Optional[Sequence[int]] = None) -> ParallelResult:
+    """run_data_parallel (parallel.cpp:240-330) on p1 B200s of this process: the file is read once
+    (streamed site by site), every device keeps the compressed chain, each sweeps a contiguous
+    share of the samples.  Outcomes equal the serial ones (keyed RNG)."""
+    if p1 < 1:
+        raise ConfigError("data parallel needs p1 >= 1")
+    opts.policy.validate()
+    plan = BatchPlan(plan.total_samples, plan.macro_batch, plan.micro_batch)
+    plan.normalize()
+    devs = list(devices) if devices else list(range(p1))
+    smp = GpuSampler.from_file(mps_path, opts.policy, opts.mode, devs, opts.pass_samples)
+    try:
+        st = RunStats()
+        rows = smp.sample(0, plan.total_samples, opts.seed, stats=st)
+    finally:
+        smp.close()
+    st.dead_samples = int((rows[:, -1] == DEAD_OUTCOME).sum())
+    return ParallelResult(SampleBatch(plan.total_samples, smp.num_sites, smp.phys_dim, opts.seed, rows), st)

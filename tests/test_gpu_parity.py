@@ -189,3 +189,61 @@ def test_host_streamed_gamma(pkg, gold, slots):
     b = stm.sample(0, 1000, 7, stats=stats)
     assert np.array_equal(a, b)
     assert np.array_equal(stm.sample(123, 77, 7), a[123:200])
+
+
+def test_mpsb_files_roundtrip(pkg, gold, tmp_path):
+    """MPSB files written by the reference load into the GPU state (F64 and F16 storage), a GPU state
+    saves to a file the reference loads back bit-exactly, and corrupt payloads raise IoError."""
+    z = np.load(f"{gold}/c1.npz")
+    mps = O.load_npz_mps(z)
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    base = pkg.GpuSampler(to_state(pkg, mps), pol)
+    want = base.sample(0, 500, 7)
+    f64 = str(tmp_path / "c1_f64.mpsb")
+    O.ref_save_mps(mps, f64, O.F64)
+    assert np.array_equal(pkg.GpuSampler.from_file(f64, pol).sample(0, 500, 7), want)
+    f16 = str(tmp_path / "c1_f16.mpsb")
+    O.ref_save_mps(mps, f16, O.F16)
+    # c1's Gamma spans 1e-14..1e10: F16 storage overflows to inf, and like the reference at F64
+    # (contract.cpp:117-119) the GPU path refuses the non-finite tensor
+    with pytest.raises(pkg.NumericError):
+        pkg.GpuSampler.from_file(f16, pol)
+    mb = O.load_npz_mps(np.load(f"{gold}/c1b.npz"))
+    O.ref_save_mps(mb, f16, O.F16)
+    m16 = O.ref_load_mps(f16)  # the F16-rounded values the file holds
+    a = pkg.GpuSampler.from_file(f16, pol)
+    b = pkg.GpuSampler(to_state(pkg, m16), pol)
+    for i in range(mps.num_sites):
+        assert np.array_equal(a.decoded_gamma(i), b.decoded_gamma(i))
+    assert np.array_equal(a.sample(0, 500, 7), b.sample(0, 500, 7))
+    out = str(tmp_path / "ours.mpsb")
+    base.save(out, pkg.Precision.F64)
+    back = O.ref_load_mps(out)
+    for i in range(mps.num_sites):
+        assert np.array_equal(back.gammas[i], base.decoded_gamma(i))
+        assert np.array_equal(back.lambdas[i], mps.lambdas[i])
+    res = pkg.run_data_parallel(f64, pkg.BatchPlan(500), 1, pkg.SamplerOptions(policy=pol, seed=7))
+    assert np.array_equal(res.batch.outcomes, want)
+    raw = bytearray(open(f64, "rb").read())
+    raw[-100] ^= 0x40  # flip a bit in the last site's payload
+    bad = str(tmp_path / "bad.mpsb")
+    open(bad, "wb").write(bytes(raw))
+    with pytest.raises(pkg.IoError, match="checksum"):
+        pkg.GpuSampler.from_file(bad, pol)
+
+
+def test_bond_schedule(pkg, gold):
+    """sample_batch with a BondSchedule (sampler.cpp:173-176): the truncated chain, sampled on the GPU,
+    matches the oracle on the same truncated (decoded) chain."""
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    chi = [1, 4, 16, 24, 32, 20, 32, 32, 12, 32, 32, 32, 32, 28, 16, 4, 1]
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    opts = pkg.SamplerOptions(policy=pol, seed=7, schedule=pkg.BondSchedule(chi, 32))
+    got = pkg.sample_batch(to_state(pkg, mps), pkg.BatchPlan(1000), opts).outcomes
+    trunc = O.ref_apply_schedule(mps, chi, 32)
+    smp = pkg.GpuSampler(to_state(pkg, trunc), pol)
+    assert np.array_equal(smp.sample(0, 1000, 7), got)
+    ref_rows, ref_marg, _ = O.orc_sample_range(decoded_mps(smp, trunc), 0, 1000, 7, want_marginals=True)
+    ndiff, explained = compare_strings(got, ref_rows, ref_marg, 7)
+    assert ndiff == explained, (ndiff, explained)

@@ -113,7 +113,35 @@ def test_sample_batch_rejects_out_of_scope_options(gold):
     mps = O.load_npz_mps(z)
     st = P.MpsState(mps.num_sites, mps.phys_dim, list(mps.bond_dims), list(mps.gammas), list(mps.lambdas))
     with pytest.raises(P.ConfigError):
-        P.sample_batch(st, P.BatchPlan(10), P.SamplerOptions(schedule=object()))
+        P.sample_batch(st, P.BatchPlan(10), P.SamplerOptions(site_transform=lambda *a: None))
+
+
+@pytest.mark.skipif(not O.have_ref(), reason="oracle/_ref not built")
+def test_apply_schedule_matches_reference(gold):
+    """BondSchedule truncation (sampler.cpp:218-246) restated on the host == the reference's."""
+    z = np.load(os.path.join(gold, "c1.npz"))
+    mps = O.load_npz_mps(z)
+    st = P.MpsState(mps.num_sites, mps.phys_dim, list(mps.bond_dims), list(mps.gammas), list(mps.lambdas))
+    chi = [1, 4, 9, 20, 32, 17, 32, 32, 5, 32, 32, 32, 32, 32, 16, 4, 1]
+    got = P.apply_schedule(st, P.BondSchedule(chi, 32))
+    want = O.ref_apply_schedule(mps, chi, 32)
+    assert got.bond_dims == want.bond_dims
+    for a, b in zip(got.gammas, want.gammas):
+        assert np.array_equal(a, b)
+    for a, b in zip(got.lambdas, want.lambdas):
+        assert np.array_equal(a, b)
+    sched = P.BondSchedule(chi, 32)
+    assert abs(sched.compute_ratio() - sum(chi[i] * chi[i + 1] for i in range(16)) / (16 * 32 * 32)) < 1e-15
+
+
+def test_mpsb_header_errors_are_io_errors(tmp_path):
+    """read_mps_info (mps_io.cpp:212-254) failures surface as IoError before any device work."""
+    bad = tmp_path / "bad.mpsb"
+    bad.write_bytes(b"NOPE" + bytes(40))
+    with pytest.raises(P.IoError):
+        P.GpuSampler.from_file(str(bad))
+    with pytest.raises(P.IoError):
+        P.GpuSampler.from_file(str(tmp_path / "missing.mpsb"))
 
 
 # ---- data-parallel driver ----------------------------------------------------------------------
