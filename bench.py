@@ -95,13 +95,15 @@ class ClockSampler:
         if not rows:
             return None
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        pw = sorted(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())
         mx = max(float(r[2]) for r in rows)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[j] for r in rows for j in range(4)
                           if len(r) > 5 + j and r[5 + j].strip() == "Active"})
         load = sorted(sm)[len(sm) // 2:] if sm else []
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows),
+                "power_w_median": statistics.median(pw[len(pw) // 2:]) if pw else None}
 
 
 # ---------------------------------------------------------------------------------------------

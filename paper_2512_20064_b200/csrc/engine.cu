@@ -19,6 +19,7 @@
 #include <memory>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -77,12 +78,13 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// fp16 matrix [rows][cols] (cols contiguous), box 32 cols x 128 rows, 64 B swizzle.
-static CUtensorMap make_tma_2d(const void* base, uint64_t cols, uint64_t rows) {
+// fp16 matrix [rows][cols] (cols contiguous), box 32 cols x box_rows rows, 64 B swizzle.
+static CUtensorMap make_tma_2d(const void* base, uint64_t cols, uint64_t rows,
+                               uint32_t box_rows = kBM) {
   CUtensorMap m;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(kBM)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -249,11 +251,11 @@ struct SiteDev {
   __half* g = nullptr;       // [2][np][kp]
   float2* cinfo = nullptr;   // [np]
   double* cs = nullptr;      // [chir * d]
-  CUtensorMap tma_g{}, tma_env{};
+  CUtensorMap tma_g{}, tma_env{}, tma_g64{};
   // host-streamed mode: the compressed site lives in pinned host memory
   __half* g_host = nullptr;
   float2* cinfo_host = nullptr;
-  std::vector<CUtensorMap> tma_slot;  // G map per device slot
+  std::vector<CUtensorMap> tma_slot, tma_slot64;  // G maps per device slot
 };
 
 struct DevCtx {
@@ -301,6 +303,7 @@ struct mpsg_handle_s {
   std::vector<char> site_set;
   bool finished = false;
   int tp = 1, tp_rank = 0;                 // tensor-parallel group (column-sharded Gamma)
+  bool pair = true;                        // K1 variant: CTA-pair UMMA (M=256) vs A-multicast pairs
   std::unique_ptr<mpsg::Comm> comm;
   std::mutex mu;
 };
@@ -375,7 +378,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     const double budget = 6.0e9;  // bytes of per-pass working set
     want = std::min<uint64_t>(65536, static_cast<uint64_t>(budget / row_bytes));
   }
-  dc.cap = std::max(kBM, round_up(static_cast<int>(std::min<uint64_t>(want, 1u << 22)), kBM));
+  dc.cap = std::max(2 * kBM, round_up(static_cast<int>(std::min<uint64_t>(want, 1u << 22)), 2 * kBM));
   dc.sites.resize(h.M);
   CUDA_OK(cudaMalloc(&dc.env, 4ull * dc.cap * kmax * sizeof(__half)));
   CUDA_OK(cudaMalloc(&dc.temp, 1ull * dc.cap * h.d * chirpm * sizeof(float2)));
@@ -394,7 +397,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     for (uint64_t i = 0; i < h.M; ++i) {
       const size_t kp = static_cast<size_t>(h.tp) * kshard_of(h, h.bonds[i]);
       const size_t np = round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN);
-      gmax = std::max(gmax, 2 * np * kp);
+      gmax = std::max(gmax, static_cast<size_t>(kGPlanes) * np * kp);
       nmax = std::max(nmax, np);
     }
     CUDA_OK(cudaStreamCreateWithFlags(&dc.copy_stream, cudaStreamNonBlocking));
@@ -468,7 +471,7 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
     s.g = dc.slot_g[0];
     s.cinfo = dc.slot_cinfo[0];
   } else if (!s.g) {
-    CUDA_OK(cudaMalloc(&s.g, 2ull * s.np * s.kp * sizeof(__half)));
+    CUDA_OK(cudaMalloc(&s.g, static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half)));
     CUDA_OK(cudaMalloc(&s.cinfo, 1ull * s.np * sizeof(float2)));
   }
   std::vector<double> wl(s.chir);
@@ -491,7 +494,7 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
   CUDA_OK(cudaMemcpyAsync(d_gr, h.gr[i].data(), sizeof(double) * s.chir, cudaMemcpyHostToDevice, dc.stream));
   CUDA_OK(cudaMemcpyAsync(d_wl, wl.data(), sizeof(double) * s.chir, cudaMemcpyHostToDevice, dc.stream));
   CUDA_OK(cudaMemcpyAsync(d_lpos, lpos.data(), sizeof(int) * s.chil, cudaMemcpyHostToDevice, dc.stream));
-  CUDA_OK(cudaMemsetAsync(s.g, 0, 2ull * s.np * s.kp * sizeof(__half), dc.stream));
+  CUDA_OK(cudaMemsetAsync(s.g, 0, static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half), dc.stream));
   CUDA_OK(cudaMemsetAsync(s.cinfo, 0, 1ull * s.np * sizeof(float2), dc.stream));
   launch_compress_site(src_dev, f64, s.chil, s.chir, static_cast<int>(h.d), s.b0, s.width, s.kp,
                        s.chirp, d_lpos, d_gl, d_gr, d_wl, s.g, s.cinfo, s.cs, dc.err, dc.stream);
@@ -507,19 +510,24 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
   s.tma_env = make_tma_env(dc.env, s.kshard, 4ull * dc.cap, h.tp);
   if (dc.slots) {
     if (!s.g_host) {
-      CUDA_OK(cudaMallocHost(&s.g_host, 2ull * s.np * s.kp * sizeof(__half)));
+      CUDA_OK(cudaMallocHost(&s.g_host, static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half)));
       CUDA_OK(cudaMallocHost(&s.cinfo_host, 1ull * s.np * sizeof(float2)));
     }
-    CUDA_OK(cudaMemcpyAsync(s.g_host, s.g, 2ull * s.np * s.kp * sizeof(__half), cudaMemcpyDeviceToHost, dc.stream));
+    CUDA_OK(cudaMemcpyAsync(s.g_host, s.g, static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half), cudaMemcpyDeviceToHost, dc.stream));
     CUDA_OK(cudaMemcpyAsync(s.cinfo_host, s.cinfo, 1ull * s.np * sizeof(float2), cudaMemcpyDeviceToHost, dc.stream));
     CUDA_OK(cudaStreamSynchronize(dc.stream));
     s.tma_slot.resize(dc.slots);
-    for (int q = 0; q < dc.slots; ++q) s.tma_slot[q] = make_tma_2d(dc.slot_g[q], s.kp, 2ull * s.np);
+    s.tma_slot64.resize(dc.slots);
+    for (int q = 0; q < dc.slots; ++q) {
+      s.tma_slot[q] = make_tma_2d(dc.slot_g[q], s.kp, static_cast<uint64_t>(kGPlanes) * s.np);
+      s.tma_slot64[q] = make_tma_2d(dc.slot_g[q], s.kp, static_cast<uint64_t>(kGPlanes) * s.np, kBN / 2);
+    }
     s.g = nullptr;
     s.cinfo = nullptr;
     dc.issued = dc.consumed = 0;  // slot 0 was overwritten: restart the load sequence
   } else {
-    s.tma_g = make_tma_2d(s.g, s.kp, 2ull * s.np);
+    s.tma_g = make_tma_2d(s.g, s.kp, static_cast<uint64_t>(kGPlanes) * s.np);
+    s.tma_g64 = make_tma_2d(s.g, s.kp, static_cast<uint64_t>(kGPlanes) * s.np, kBN / 2);
   }
 }
 
@@ -530,7 +538,7 @@ static void issue_loads(mpsg_handle_s& h, DevCtx& dc, uint64_t upto) {
     const int slot = static_cast<int>(q % dc.slots);
     const SiteDev& s = dc.sites[q % h.M];
     CUDA_OK(cudaStreamWaitEvent(dc.copy_stream, dc.freed[slot], 0));  // consume q - slots done
-    const size_t gb = 2ull * s.np * s.kp * sizeof(__half);
+    const size_t gb = static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half);
     CUDA_OK(cudaMemcpyAsync(dc.slot_g[slot], s.g_host, gb, cudaMemcpyHostToDevice, dc.copy_stream));
     CUDA_OK(cudaMemcpyAsync(dc.slot_cinfo[slot], s.cinfo_host, 1ull * s.np * sizeof(float2),
                             cudaMemcpyHostToDevice, dc.copy_stream));
@@ -592,24 +600,24 @@ struct PassOut {
 // Runs one pass of `count` (<= cap) samples starting at global index `first` on dc.
 static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first, int count,
                      const uint8_t* forced_dev, double* marg_dev, PassOut& po, int timing) {
-  const int rows = round_up(count, kBM);
+  const int rows = round_up(count, h.pair ? 2 * kBM : kBM);
   launch_init_env(dc.env, dc.cap, dc.sites[0].kshard, h.tp, rows, count, dc.alive, dc.stream);
   po.launches += 1;
   if (dc.slots) issue_loads(h, dc, dc.consumed + dc.slots);
   for (uint64_t i = 0; i < h.M; ++i) {
     const SiteDev& s = dc.sites[i];
-    const CUtensorMap* tma_g = &s.tma_g;
+    const CUtensorMap* tma_g = h.pair ? &s.tma_g64 : &s.tma_g;
     const float2* cinfo = s.cinfo;
     int slot = -1;
     if (dc.slots) {
       if (dc.consumed % h.M != i) throw Error(MPSG_ERR_INTERNAL, "site stream out of sequence");
       slot = static_cast<int>(dc.consumed % dc.slots);
       CUDA_OK(cudaStreamWaitEvent(dc.stream, dc.loaded[slot], 0));
-      tma_g = &s.tma_slot[slot];
+      tma_g = h.pair ? &s.tma_slot64[slot] : &s.tma_slot[slot];
       cinfo = dc.slot_cinfo[slot];
     }
     SiteGemmArgs ga;
-    ga.m_tiles = rows / kBM;
+    ga.m_tiles = rows / (h.pair ? 2 * kBM : kBM);
     ga.n_tiles = s.nt;
     ga.k_blocks = s.kp / kBK;
     ga.kshard_blocks = s.kshard / kBK;
@@ -617,13 +625,16 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
     ga.np = s.np;
     ga.chirp = s.chirp;
     ga.d = static_cast<int>(h.d);
-    ga.group_n = std::min(s.nt / 2, kGroupPairs);
+    ga.group_n = h.pair ? std::min(s.nt, 2 * kGroupPairs) : std::min(s.nt / 2, kGroupPairs);
     ga.cinfo = cinfo;
     ga.temp = dc.temp;
     ga.pstat = dc.pstat;
-    const int tiles = ga.m_tiles * ga.n_tiles;  // = 2 x (tile-pair units)
+    const int ctas = h.pair ? 2 * ga.m_tiles * ga.n_tiles : ga.m_tiles * ga.n_tiles;
     if (timing >= 2) CUDA_OK(cudaEventRecord(dc.gev[2 * i], dc.stream));
-    launch_site_gemm(h.split, s.tma_env, *tma_g, ga, std::min(tiles, dc.num_sms), dc.stream);
+    if (h.pair)
+      launch_site_gemm_pair(h.split, s.tma_env, *tma_g, ga, std::min(ctas, dc.num_sms), dc.stream);
+    else
+      launch_site_gemm(h.split, s.tma_env, *tma_g, ga, std::min(ctas, dc.num_sms), dc.stream);
     if (timing >= 2) CUDA_OK(cudaEventRecord(dc.gev[2 * i + 1], dc.stream));
     if (dc.slots) {  // K1 is the only reader of the slot: hand it back to the copy stream
       CUDA_OK(cudaEventRecord(dc.freed[slot], dc.stream));
@@ -877,6 +888,10 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
     h->policy = pol;
     if (opts) h->opts = *opts;
     config_check(h->opts.mode >= MPSG_MODE_AUTO && h->opts.mode <= MPSG_MODE_SINGLE, "unknown mode");
+    {
+      const char* v = std::getenv("MPSG_GEMM");  // A/B switch for the contraction kernel
+      h->pair = !(v && std::string(v) == "cluster");
+    }
     h->tp = std::max(1, h->opts.tp_size);
     h->tp_rank = h->opts.tp_rank;
     config_check(h->tp_rank >= 0 && h->tp_rank < h->tp, "tp_rank out of range");
@@ -961,7 +976,7 @@ void mpsg_destroy(mpsg_handle h) {
 uint64_t mpsg_state_bytes(mpsg_handle h) {
   if (!h || h->devs.empty()) return 0;
   uint64_t b = 0;
-  for (const auto& s : h->devs[0].sites) b += 2ull * s.np * s.kp * sizeof(__half);
+  for (const auto& s : h->devs[0].sites) b += static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half);
   return b;  // host-streamed: these bytes live in pinned host memory
 }
 
@@ -972,7 +987,7 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
     DevCtx& dc = h->devs[0];
     CUDA_OK(cudaSetDevice(dc.device));
     const SiteDev& s = dc.sites[site];
-    std::vector<__half> g(2ull * s.np * s.kp);
+    std::vector<__half> g(static_cast<size_t>(kGPlanes) * s.np * s.kp);
     std::vector<double> cs(std::max<size_t>(1, 1ull * s.width * h->d));
     if (dc.slots)
       std::memcpy(g.data(), s.g_host, g.size() * sizeof(__half));
@@ -994,8 +1009,8 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
           const double f = static_cast<double>(static_cast<float>(cs[rl * d + k])) * h->gl[site][l] /
                            h->gr[site][r];
           const size_t o = 2 * ((static_cast<size_t>(l) * s.chir + r) * d + k);
-          out[o] = static_cast<double>(__half2float(g[row * s.kp + lpos[l]])) * f;
-          out[o + 1] = static_cast<double>(__half2float(g[(s.np + row) * s.kp + lpos[l]])) * f;
+          out[o] = static_cast<double>(__half2float(g[(static_cast<size_t>(kPlaneRe) * s.np + row) * s.kp + lpos[l]])) * f;
+          out[o + 1] = static_cast<double>(__half2float(g[(static_cast<size_t>(kPlaneIm) * s.np + row) * s.kp + lpos[l]])) * f;
         }
   });
 }
@@ -1095,7 +1110,7 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
     std::lock_guard<std::mutex> lk(h->mu);
     const SiteDev& s = dc.sites[site];
     const int n = static_cast<int>(count);
-    const int rows = round_up(n, kBM);
+    const int rows = round_up(n, h->pair ? 2 * kBM : kBM);
     // host: internal env E = env * gl * sigma_n (sigma_n power of two), hi/lo fp16 planes
     const size_t plane = 1ull * dc.cap * s.kp;
     std::vector<__half> e(4 * plane, __float2half_rn(0.f));
@@ -1123,7 +1138,7 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
     }
     CUDA_OK(cudaMemcpy(dc.env, e.data(), e.size() * sizeof(__half), cudaMemcpyHostToDevice));
     SiteGemmArgs ga;
-    ga.m_tiles = rows / kBM;
+    ga.m_tiles = rows / (h->pair ? 2 * kBM : kBM);
     ga.n_tiles = s.nt;
     ga.k_blocks = s.kp / kBK;
     ga.kshard_blocks = s.kshard / kBK;
@@ -1131,12 +1146,15 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
     ga.np = s.np;
     ga.chirp = s.chirp;
     ga.d = static_cast<int>(h->d);
-    ga.group_n = std::min(s.nt / 2, kGroupPairs);
+    ga.group_n = h->pair ? std::min(s.nt, 2 * kGroupPairs) : std::min(s.nt / 2, kGroupPairs);
     ga.cinfo = s.cinfo;
     ga.temp = dc.temp;
     ga.pstat = dc.pstat;
-    launch_site_gemm(h->split, s.tma_env, s.tma_g, ga, std::min(ga.m_tiles * ga.n_tiles, dc.num_sms),
-                     dc.stream);
+    const int ctas = h->pair ? 2 * ga.m_tiles * ga.n_tiles : ga.m_tiles * ga.n_tiles;
+    if (h->pair)
+      launch_site_gemm_pair(h->split, s.tma_env, s.tma_g64, ga, std::min(ctas, dc.num_sms), dc.stream);
+    else
+      launch_site_gemm(h->split, s.tma_env, s.tma_g, ga, std::min(ctas, dc.num_sms), dc.stream);
     CUDA_OK(cudaGetLastError());
     std::vector<float2> t(1ull * n * h->d * s.chirp);
     CUDA_OK(cudaMemcpyAsync(t.data(), dc.temp, t.size() * sizeof(float2), cudaMemcpyDeviceToHost,

@@ -80,6 +80,69 @@ __device__ __forceinline__ void tma_load_3d_mc(const CUtensorMap* m, uint64_t* b
       "l"(policy)
       : "memory");
 }
+// ---- CTA-pair (cta_group::2) variants ---------------------------------------------------
+// Peer-bit-cleared barrier address: transaction bytes of both CTAs land on the leader's barrier.
+__device__ __forceinline__ uint32_t leader_bar(const uint64_t* bar) {
+  return smem_u32(bar) & 0xFEFFFFFFu;
+}
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* m, uint32_t leader_bar_addr,
+                                                 void* dst, int32_t c0, int32_t c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar_addr), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap* m, uint32_t leader_bar_addr,
+                                                 void* dst, int32_t c0, int32_t c1, int32_t c2,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar_addr), "r"(c0), "r"(c1), "r"(c2),
+      "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_relinquish_pair() {
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+#define MPSG_UMMA_PAIR(NAME, QUAL)                                                              \
+  __device__ __forceinline__ void NAME(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,      \
+                                       uint32_t idesc, uint32_t accumulate) {                  \
+    asm volatile(                                                                               \
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                                     \
+        "tcgen05.mma.cta_group::2.kind::f16" QUAL " [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),    \
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)                                   \
+        : "memory");                                                                            \
+  }
+MPSG_UMMA_PAIR(umma_pair, "")
+MPSG_UMMA_PAIR(umma_pair_afill, ".collector::a::fill")
+MPSG_UMMA_PAIR(umma_pair_alast, ".collector::a::lastuse")
+#undef MPSG_UMMA_PAIR
+// Arrive on the barrier at `bar`'s offset in both CTAs of the pair once the pair's MMAs retire.
+__device__ __forceinline__ void umma_commit_pair_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// Arrive on the barrier at `bar`'s offset in cluster CTA `rank` (release at cluster scope).
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));

@@ -1,7 +1,7 @@
 // Kernel interface of the per-site sweep step (host engine <-> device kernels).
 //
 // Device data layout:
-//   G    fp16  [2 planes (re, im)][Np][Kp]   compressed site tensor, K-major (l contiguous);
+//   G    fp16  [kGPlanes][Np][Kp]   compressed site tensor ([-Gi, Gr, Gi]), K-major (l contiguous);
 //              output column j = k * chirp + r  (k-major so a 128-column tile is one outcome k)
 //   cinfo float2 [Np]  (column scale cs_j, weight factor wl_r = (Lambda_r / gamma_r)^2)
 //   env  fp16  [4 planes (hi.re, hi.im, lo.re, lo.im)][cap rows][Kp]   internal environment
@@ -19,6 +19,14 @@ constexpr int kBM = 128;  // samples per tile (UMMA M)
 constexpr int kBN = 128;  // complex output columns per tile (UMMA N per real plane)
 constexpr int kBK = 32;   // K elements per pipeline stage (64 B rows, SWIZZLE_64B)
 constexpr int kGemmThreads = 256;
+// Compressed Gamma planes: 3 = [-Gi | Gr | Gi] (two N=256 UMMAs per K-step and env pair:
+// Er x [Gr;Gi] and Ei x [-Gi;Gr]); 2 = [Gr | Gi] (four N=128 UMMAs).
+#ifndef MPSG_GPLANES
+#define MPSG_GPLANES 2
+#endif
+constexpr int kGPlanes = MPSG_GPLANES;
+constexpr int kPlaneRe = kGPlanes == 3 ? 1 : 0;
+constexpr int kPlaneIm = kGPlanes == 3 ? 2 : 1;
 constexpr uint64_t kMeasureStream = 0x6d656173ull;  // rng.hpp:19
 constexpr uint8_t kDead = 0xFF;                      // sampler.hpp:17
 
@@ -64,6 +72,11 @@ struct SelectArgs {
 // host launchers (sweep_kernels.cu)
 void launch_site_gemm(bool split, const CUtensorMap& tma_env, const CUtensorMap& tma_g,
                       const SiteGemmArgs& a, int grid, cudaStream_t s);
+// CTA-pair variant (cta_group::2, M = 256 per unit; a.m_tiles counts 256-row tiles; the Gamma map
+// has a 64-row box).
+void launch_site_gemm_pair(bool split, const CUtensorMap& tma_env, const CUtensorMap& tma_g64,
+                           const SiteGemmArgs& a, int grid, cudaStream_t s);
+int gemm_pair_smem_bytes(bool split);
 void launch_select(const SelectArgs& a, cudaStream_t s);
 // pstat [rows][nt] -> out [rows][d]: (sum of weights, max) over the tiles of each outcome
 void launch_reduce_tiles(const float2* pstat, int nt, int tiles_per_k, int d, int rows,

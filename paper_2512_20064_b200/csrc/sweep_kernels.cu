@@ -48,8 +48,8 @@ template <bool kSplit>
 struct GemmCfg {
   static constexpr int kAPlanes = kSplit ? 4 : 2;  // env planes: hi.re hi.im [lo.re lo.im]
   static constexpr int kTile = kBM * kBK * 2;      // 8 KiB: 128 rows x 64 B (A and B alike)
-  static constexpr int kStageBytes = (kAPlanes + 2) * kTile;
-  static constexpr int kStages = kSplit ? 4 : 6;
+  static constexpr int kStageBytes = (kAPlanes + kGPlanes) * kTile;
+  static constexpr int kStages = kGPlanes == 3 ? (kSplit ? 4 : 5) : (kSplit ? 4 : 6);
   static constexpr int kBarrierBytes = 256;
   static constexpr int kSmem = kStages * kStageBytes + 1024 + kBarrierBytes;
   static_assert(kBM == 128 && kBN == 128 && kBK == 32, "tile shape baked into descriptors");
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             ptx::tma_load_3d_mc(&tma_env, &full[stage], st + q * C::kTile, kin * kBK,
                                 q * a.plane_rows_a + m * kBM, shard, 0x3, pol_env);
 #pragma unroll
-          for (int p = 0; p < 2; ++p)
+          for (int p = 0; p < kGPlanes; ++p)
             ptx::tma_load_2d(&tma_g, &full[stage], st + (C::kAPlanes + p) * C::kTile, kb * kBK,
                              p * a.np + n * kBN, pol_g);
           if (++stage == C::kStages) {
@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       constexpr uint32_t kId = ptx::idesc_f16_f32(kBM, kBN, false);
       constexpr uint32_t kIdNeg = ptx::idesc_f16_f32(kBM, kBN, true);
+      constexpr uint32_t kId256 = ptx::idesc_f16_f32(kBM, 2 * kBN, false);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -173,21 +174,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int ks = 0; ks < kBK / 16; ++ks) {
             const uint32_t off = ks * 32;  // 16 fp16 along K
-            const uint64_t br = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 0) * C::kTile + off);
-            const uint64_t bi = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 1) * C::kTile + off);
             const uint32_t accum = (kb | ks) ? 1u : 0u;
-            // Re += Er.Gr - Ei.Gi ; Im += Er.Gi + Ei.Gr.  The Er tile feeds two consecutive MMAs
-            // through the A collector (read from shared memory once).  The collector is not used
-            // for the Ei pair: reuse combined with an operand negation gives wrong results.
+            if constexpr (kGPlanes == 3) {
+              // B tiles [-Gi | Gr | Gi]: [Gr;Gi] and [-Gi;Gr] are contiguous 256-row operands, so
+              // D[:, 0:256] = [Re | Im] += Er x [Gr;Gi] + Ei x [-Gi;Gr] in two N=256 UMMAs.
+              const uint64_t b_rg = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 1) * C::kTile + off);
+              const uint64_t b_nr = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 0) * C::kTile + off);
 #pragma unroll
-            for (int h = 0; h < (kSplit ? 2 : 1); ++h) {
-              const uint32_t acc0 = h ? 1u : accum;
-              const uint64_t ar = ptx::sdesc_kmajor_sw64(st + (2 * h + 0) * C::kTile + off);
-              const uint64_t ai = ptx::sdesc_kmajor_sw64(st + (2 * h + 1) * C::kTile + off);
-              ptx::umma_f16_ss_afill(d_re, ar, br, kId, acc0);
-              ptx::umma_f16_ss_alast(d_im, ar, bi, kId, acc0);
-              ptx::umma_f16_ss(d_re, ai, bi, kIdNeg, 1u);
-              ptx::umma_f16_ss(d_im, ai, br, kId, 1u);
+              for (int h = 0; h < (kSplit ? 2 : 1); ++h) {
+                const uint64_t ar = ptx::sdesc_kmajor_sw64(st + (2 * h + 0) * C::kTile + off);
+                const uint64_t ai = ptx::sdesc_kmajor_sw64(st + (2 * h + 1) * C::kTile + off);
+                ptx::umma_f16_ss(d_re, ar, b_rg, kId256, h ? 1u : accum);
+                ptx::umma_f16_ss(d_re, ai, b_nr, kId256, 1u);
+              }
+            } else {
+              const uint64_t br = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 0) * C::kTile + off);
+              const uint64_t bi = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 1) * C::kTile + off);
+              // Re += Er.Gr - Ei.Gi ; Im += Er.Gi + Ei.Gr.  The Er tile feeds two consecutive MMAs
+              // through the A collector; no collector for the Ei pair (reuse combined with an operand
+              // negation gives wrong results).
+#pragma unroll
+              for (int h = 0; h < (kSplit ? 2 : 1); ++h) {
+                const uint32_t acc0 = h ? 1u : accum;
+                const uint64_t ar = ptx::sdesc_kmajor_sw64(st + (2 * h + 0) * C::kTile + off);
+                const uint64_t ai = ptx::sdesc_kmajor_sw64(st + (2 * h + 1) * C::kTile + off);
+                ptx::umma_f16_ss_afill(d_re, ar, br, kId, acc0);
+                ptx::umma_f16_ss_alast(d_im, ar, bi, kId, acc0);
+                ptx::umma_f16_ss(d_re, ai, bi, kIdNeg, 1u);
+                ptx::umma_f16_ss(d_im, ai, br, kId, 1u);
+              }
             }
           }
           ptx::umma_commit_mc(&empty[stage], 0x3);  // slot free in both CTAs once MMAs retire
@@ -287,6 +302,250 @@ void launch_site_gemm(bool split, const CUtensorMap& tma_env, const CUtensorMap&
     launch_gemm_t<true>(tma_env, tma_g, a, grid, s);
   else
     launch_gemm_t<false>(tma_env, tma_g, a, grid, s);
+}
+
+// --------------------------------------------------------------------------------------------
+// K1 (pair): the CTA pair issues one M=256 UMMA (cta_group::2): each SM stores and reads its own
+// 128 env rows and half (64 rows) of the Gamma tile, halving the per-SM shared-memory traffic of
+// the B operand.  Unit = (256-row M tile, 128-column N tile).
+// --------------------------------------------------------------------------------------------
+template <bool kSplit>
+struct PairCfg {
+  static constexpr int kAPlanes = kSplit ? 4 : 2;
+  static constexpr int kATile = kBM * kBK * 2;         // 8 KiB: 128 rows x 64 B
+  static constexpr int kBTile = (kBN / 2) * kBK * 2;   // 4 KiB: this CTA's 64 of the 128 B rows
+  static constexpr int kStageBytes = kAPlanes * kATile + 2 * kBTile;
+  static constexpr int kStages = kSplit ? 5 : 8;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+};
+
+int gemm_pair_smem_bytes(bool split) { return split ? PairCfg<true>::kSmem : PairCfg<false>::kSmem; }
+
+__device__ __forceinline__ void unit_coords_pair(int u, const SiteGemmArgs& a, int& m, int& n) {
+  const int per_group = a.group_n * a.m_tiles;
+  const int g = u / per_group;
+  const int n0 = g * a.group_n;
+  const int gw = min(a.group_n, a.n_tiles - n0);
+  const int r = u - g * per_group;
+  m = r / gw;
+  n = n0 + (r - m * gw);
+}
+
+// a.m_tiles counts 256-row tiles here.
+template <bool kSplit>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    site_gemm_pair_kernel(const __grid_constant__ CUtensorMap tma_env,
+                          const __grid_constant__ CUtensorMap tma_g64, const SiteGemmArgs a) {
+  using C = PairCfg<kSplit>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int rank = static_cast<int>(ptx::cluster_ctarank());
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int num_clusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);   // leader: own expect_tx, bytes from both CTAs
+      ptx::mbar_init(&empty[s], 1);  // the leader's multicast commit
+    }
+    for (int j = 0; j < 2; ++j) {
+      ptx::mbar_init(&tfull[j], 1);
+      ptx::mbar_init(&tempty[j], 8);  // leader: one arrival per epilogue warp of both CTAs
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tma_env);
+    ptx::tma_prefetch_desc(&tma_g64);
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc_pair(tmem_slot, 512);
+    ptx::tmem_relinquish_pair();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int units = a.m_tiles * a.n_tiles;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs; bytes counted on the leader's barrier) ----------
+    if (lane == 0) {
+      const uint64_t pol_env = ptx::l2_policy_evict_normal();
+      const uint64_t pol_g = ptx::l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cluster; u < units; u += num_clusters) {
+        int m, n;
+        unit_coords_pair(u, a, m, n);
+        int shard = 0, kin = 0;
+        for (int kb = 0; kb < a.k_blocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * C::kStageBytes;
+          const uint32_t lbar = ptx::leader_bar(&full[stage]);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
+#pragma unroll
+          for (int q = 0; q < C::kAPlanes; ++q)
+            ptx::tma_load_3d_pair(&tma_env, lbar, st + q * C::kATile, kin * kBK,
+                                  q * a.plane_rows_a + m * 2 * kBM + rank * kBM, shard, pol_env);
+#pragma unroll
+          for (int p = 0; p < 2; ++p)
+            ptx::tma_load_2d_pair(&tma_g64, lbar, st + C::kAPlanes * C::kATile + p * C::kBTile,
+                                  kb * kBK, p * a.np + n * kBN + rank * (kBN / 2), pol_g);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+          if (++kin == a.kshard_blocks) {
+            kin = 0;
+            ++shard;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: one thread of the leader CTA drives both SMs ----------------
+    if (lane == 0 && leader) {
+      constexpr uint32_t kId = ptx::idesc_f16_f32(2 * kBM, kBN, false);
+      constexpr uint32_t kIdNeg = ptx::idesc_f16_f32(2 * kBM, kBN, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = cluster; u < units; u += num_clusters) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_re = tmem_base + acc * 256;
+        const uint32_t d_im = d_re + 128;
+        for (int kb = 0; kb < a.k_blocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t st = ptx::smem_u32(smem + stage * C::kStageBytes);
+#pragma unroll
+          for (int ks = 0; ks < kBK / 16; ++ks) {
+            const uint32_t off = ks * 32;
+            const uint64_t br = ptx::sdesc_kmajor_sw64(st + C::kAPlanes * C::kATile + off);
+            const uint64_t bi = ptx::sdesc_kmajor_sw64(st + C::kAPlanes * C::kATile + C::kBTile + off);
+            const uint32_t accum = (kb | ks) ? 1u : 0u;
+#pragma unroll
+            for (int h = 0; h < (kSplit ? 2 : 1); ++h) {
+              const uint32_t acc0 = h ? 1u : accum;
+              const uint64_t ar = ptx::sdesc_kmajor_sw64(st + (2 * h + 0) * C::kATile + off);
+              const uint64_t ai = ptx::sdesc_kmajor_sw64(st + (2 * h + 1) * C::kATile + off);
+              ptx::umma_pair_afill(d_re, ar, br, kId, acc0);
+              ptx::umma_pair_alast(d_im, ar, bi, kId, acc0);
+              ptx::umma_pair(d_re, ai, bi, kIdNeg, 1u);
+              ptx::umma_pair(d_im, ai, br, kId, 1u);
+            }
+          }
+          ptx::umma_commit_pair_mc(&empty[stage], 0x3);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit_pair_mc(&tfull[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs, each on its own 128 rows) ----------------
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = cluster; u < units; u += num_clusters) {
+      int m, n;
+      unit_coords_pair(u, a, m, n);
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row = m * 2 * kBM + rank * kBM + q * 32 + lane;
+      const int col0 = n * kBN;
+      const int k = col0 / a.chirp;
+      if (k < a.d) {
+        const int r0 = col0 - k * a.chirp;
+        float2* dst = a.temp + (static_cast<size_t>(row) * a.d + k) * a.chirp + r0;
+        const float2* ci = a.cinfo + col0;
+        const uint32_t tb = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
+        float w = 0.f, mx = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < kBN / 32; ++c) {
+          float re[32], im[32];
+          ptx::tmem_ld_32x32b_x32(tb + c * 32, re);
+          ptx::tmem_ld_32x32b_x32(tb + 128 + c * 32, im);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float4 cc = *reinterpret_cast<const float4*>(ci + c * 32 + j);
+            const float tr0 = re[j] * cc.x, ti0 = im[j] * cc.x;
+            const float tr1 = re[j + 1] * cc.z, ti1 = im[j + 1] * cc.z;
+            w = fmaf(cc.y, fmaf(tr0, tr0, ti0 * ti0), w);
+            w = fmaf(cc.w, fmaf(tr1, tr1, ti1 * ti1), w);
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(tr0), fabsf(ti0)), fmaxf(fabsf(tr1), fabsf(ti1))));
+            *reinterpret_cast<float4*>(dst + c * 32 + j) = make_float4(tr0, ti0, tr1, ti1);
+          }
+        }
+        a.pstat[static_cast<size_t>(row) * a.n_tiles + n] = make_float2(w, mx);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_remote(&tempty[acc], 0);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_pair(tmem_base, 512);
+  }
+}
+
+template <bool kSplit>
+static void launch_gemm_pair_t(const CUtensorMap& tma_env, const CUtensorMap& tma_g64,
+                               const SiteGemmArgs& a, int grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(site_gemm_pair_kernel<kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         PairCfg<kSplit>::kSmem);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = PairCfg<kSplit>::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, site_gemm_pair_kernel<kSplit>, tma_env, tma_g64, a);
+}
+
+void launch_site_gemm_pair(bool split, const CUtensorMap& tma_env, const CUtensorMap& tma_g64,
+                           const SiteGemmArgs& a, int grid, cudaStream_t s) {
+  grid = (grid + 1) & ~1;
+  if (split)
+    launch_gemm_pair_t<true>(tma_env, tma_g64, a, grid, s);
+  else
+    launch_gemm_pair_t<false>(tma_env, tma_g64, a, grid, s);
 }
 
 // ============================================================================================
@@ -552,8 +811,9 @@ __global__ void pack_kernel(const void* src, int chil, int chir, int d, int b0, 
       const int rl = jl / d, k = jl - rl * d;
       const size_t row = static_cast<size_t>(k) * chirp + rl;
       const size_t col = static_cast<size_t>(lpos[l]);
-      g_out[row * kp + col] = tre[tx][yy];
-      g_out[(static_cast<size_t>(np) + row) * kp + col] = tim[tx][yy];
+      g_out[(static_cast<size_t>(kPlaneRe) * np + row) * kp + col] = tre[tx][yy];
+      g_out[(static_cast<size_t>(kPlaneIm) * np + row) * kp + col] = tim[tx][yy];
+      if (kGPlanes == 3) g_out[row * kp + col] = __hneg(tim[tx][yy]);
     }
   }
 }
