@@ -247,3 +247,56 @@ def test_bond_schedule(pkg, gold):
     ref_rows, ref_marg, _ = O.orc_sample_range(decoded_mps(smp, trunc), 0, 1000, 7, want_marginals=True)
     ndiff, explained = compare_strings(got, ref_rows, ref_marg, 7)
     assert ndiff == explained, (ndiff, explained)
+
+
+def _synthetic(pkg, m, chi, d, **kw):
+    from paper_2512_20064_b200.synthetic import build_synthetic
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    smp, lams = build_synthetic(m, chi, d, seed=11, policy=pol, **kw)
+    return smp, lams, pol
+
+
+@pytest.mark.parametrize("m,chi,d,n", [(10, 512, 6, 48), (10, 2048, 6, 12)])
+def test_parity_at_benchmark_bond_dims(pkg, m, chi, d, n):
+    """Device-generated chains at the c2 / c3 bond dimensions (short M so the f64 oracle is quick):
+    teacher-forced marginals within 1e-4 and identical strings (boundary draws excepted)."""
+    smp, lams, _ = _synthetic(pkg, m, chi, d)
+    dec = O.Mps(d, list(smp.bond_dims), [smp.decoded_gamma(i) for i in range(m)], list(lams))
+    ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, n, 7, want_marginals=True)
+    gpu_rows = smp.sample(0, n, 7)
+    gm = smp.marginals(0, ref_rows)
+    big = ref_marg >= 1e-3
+    rel = np.abs(gm[big] - ref_marg[big]) / ref_marg[big]
+    assert rel.max() < MARG_RTOL, rel.max()
+    ndiff, explained = compare_strings(gpu_rows, ref_rows, ref_marg, 7)
+    assert ndiff == explained, (ndiff, explained)
+
+
+def test_invariants_at_chi2048(pkg):
+    """Size-independent properties on a chi=2048, d=6 chain (c3 bond dimension): outcomes do not depend
+    on the pass size, on host streaming, or on tensor-parallel sharding; site-0 frequencies follow the
+    exact site-0 distribution (chi-square)."""
+    from paper_2512_20064_b200.parallel import TensorParallelLocal
+    m, chi, d = 16, 2048, 6
+    a, lams, pol = _synthetic(pkg, m, chi, d, pass_samples=512)
+    rows = a.sample(0, 4096, 3)
+    b, _, _ = _synthetic(pkg, m, chi, d, pass_samples=4096, host_stream_slots=2)
+    assert np.array_equal(b.sample(0, 4096, 3), rows)
+    assert np.array_equal(a.sample(1000, 300, 3), rows[1000:1300])
+    # exact site-0 distribution from the decoded tensor (sampler.cpp:83-90 with env = 1)
+    g0 = a.decoded_gamma(0)[0]
+    w = (lams[0][:, None] ** 2 * np.abs(g0) ** 2).sum(axis=0)
+    p = w / w.sum()
+    cnt = np.bincount(rows[:, 0], minlength=d)
+    live = p * len(rows) > 5
+    chi2 = (((cnt - p * len(rows)) ** 2) / (p * len(rows)))[live].sum()
+    assert chi2 < 40.0, (chi2, cnt, p)
+    # tensor-parallel (p2 = 2 ranks on this device) on a state built from the decoded tensors
+    st = pkg.MpsState(m, d, list(a.bond_dims), [a.decoded_gamma(i) for i in range(m)], list(lams))
+    tp = TensorParallelLocal(st, 2, policy=pol)
+    one = pkg.GpuSampler(st, pol)
+    t = tp.sample(0, 512, 3)
+    assert np.array_equal(t[0], t[1])
+    ref = one.sample(0, 512, 3)
+    assert (t[0] != ref).any(axis=1).sum() <= 2  # only draws at a CDF boundary may flip
+    tp.close()
