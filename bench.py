@@ -17,6 +17,7 @@ compiled from its sources) on this host's cores for the same workload.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -223,12 +224,13 @@ def main():
         s = L.Stats()
         site = np.zeros(cfg["M"], np.float64)
         s.site_seconds = site.ctypes.data_as(L._pd)
-        P.sampler._check(L.lib().mpsg_sample_device(smp._h, 7, first, P_pass, __import__("ctypes").c_void_p(rows_dev.data_ptr()),
-                                                    __import__("ctypes").byref(s)))
+        P.sampler._check(L.lib().mpsg_sample_device(smp._h, 7, first, P_pass, ctypes.c_void_p(rows_dev.data_ptr()),
+                                                    ctypes.byref(s)))
         st.contraction_macs = s.contraction_macs
         st.issued_mma_flops = s.issued_mma_flops
         st.h2d = s.h2d_bytes
         st.site_seconds = site
+        st.device_seconds = s.device_seconds
         return st, s
 
     for w in range(args.warmup):
@@ -243,7 +245,7 @@ def main():
     wall0 = time.perf_counter()
     for it in range(args.steps):
         st, s = device_step(args.warmup + it)
-        dev_s += float(np.sum(st.site_seconds))
+        dev_s += st.device_seconds if st.device_seconds > 0 else float(np.sum(st.site_seconds))
         gemm_s += s.gemm_seconds
         gemm_flops += s.gemm_flops
         issued += s.issued_mma_flops

@@ -108,6 +108,7 @@ typedef struct mpsg_stats {
   double gemm_seconds;             /* device time of the contraction kernels (record_site_times 2) */
   uint64_t gemm_flops;             /* algorithmic flops of those launches: 8 * contraction_macs */
   uint64_t kernel_launches;        /* CUDA kernels launched by this call */
+  double device_seconds;           /* device time of all passes (CUDA events; record_site_times) */
 } mpsg_stats;
 
 typedef struct mpsg_handle_s* mpsg_handle;

@@ -36,7 +36,7 @@ class Stats(C.Structure):
     _fields_ = [("contraction_macs", _u64), ("measure_weight_macs", _u64), ("dead_samples", _u64),
                 ("seconds", _dbl), ("site_seconds", _pd), ("issued_mma_flops", _u64),
                 ("h2d_bytes", _u64), ("d2h_bytes", _u64), ("gemm_seconds", _dbl),
-                ("gemm_flops", _u64), ("kernel_launches", _u64)]
+                ("gemm_flops", _u64), ("kernel_launches", _u64), ("device_seconds", _dbl)]
 
 
 # (name, restype, argtypes) for every entry point of include/mpsg.h

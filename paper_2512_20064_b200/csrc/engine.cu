@@ -251,11 +251,31 @@ struct SiteDev {
   __half* g = nullptr;       // [2][np][kp]
   float2* cinfo = nullptr;   // [np]
   double* cs = nullptr;      // [chir * d]
-  CUtensorMap tma_g{}, tma_env{}, tma_g64{};
+  CUtensorMap tma_g{}, tma_g64{};
   // host-streamed mode: the compressed site lives in pinned host memory
   __half* g_host = nullptr;
   float2* cinfo_host = nullptr;
   std::vector<CUtensorMap> tma_slot, tma_slot64;  // G maps per device slot
+};
+
+// One pipeline lane: a sample range of the pass with its own buffers and stream.  With two lanes
+// the contraction kernels of the lanes are ordered alternately (A_i, B_i, A_i+1, ...) while each
+// lane's select kernel runs underneath the other lane's contraction.
+struct Lane {
+  cudaStream_t stream = nullptr;  // lane 0 uses DevCtx::stream
+  int cap = 0;                    // rows, multiple of 256
+  __half* env = nullptr;          // [shards][4][cap][kshard_max]
+  float2* temp = nullptr;         // [cap][d][chirp_max]
+  float2* pstat = nullptr;        // [cap][nt_max]
+  float2* part = nullptr;         // [tp][cap][d] exchanged (weight, max) partials (TP only)
+  uint8_t* alive = nullptr;       // [cap]
+  uint8_t* rows = nullptr;        // [cap][M]
+  uint8_t* forced = nullptr;      // [cap][M] (lazy)
+  double* marg = nullptr;         // [cap][M][d] (lazy)
+  uint8_t* host_rows = nullptr;   // pinned [cap][M]
+  std::vector<CUtensorMap> tma_env;  // per site: the shard-major env map over this lane's env
+  cudaEvent_t k1done = nullptr, done = nullptr;
+  std::vector<cudaEvent_t> gev;   // per-site GEMM start/stop (2 M)
 };
 
 struct DevCtx {
@@ -263,20 +283,12 @@ struct DevCtx {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   std::vector<SiteDev> sites;
-  int cap = 0;               // pass capacity (rows), multiple of 128
-  __half* env = nullptr;     // [4][cap][kmax]
-  float2* temp = nullptr;    // [cap][d][chirp_max]
-  float2* pstat = nullptr;   // [cap][nt_max]
-  float2* part = nullptr;    // [tp][cap][d] exchanged (weight, max) partials (TP only)
-  uint8_t* alive = nullptr;  // [cap]
-  uint8_t* rows = nullptr;   // [cap][M]
-  uint8_t* forced = nullptr; // [cap][M] (lazy)
-  double* marg = nullptr;    // [cap][M][d] (lazy)
+  int cap = 0;               // pass capacity (rows over all lanes)
+  std::vector<Lane> lanes;
   double* scratch = nullptr; // compress: gl, gr, wl
   void* src = nullptr;       // compress staging (device)
   size_t src_bytes = 0;
   int* err = nullptr;
-  uint8_t* host_rows = nullptr;  // pinned [cap][M]
   // host-streamed Gamma: ring of device slots filled by a copy stream (sequence q -> slot q % R)
   int slots = 0;
   std::vector<__half*> slot_g;
@@ -285,8 +297,8 @@ struct DevCtx {
   cudaStream_t copy_stream = nullptr;
   uint64_t issued = 0, consumed = 0;  // rolling site-load sequence (sites 0..M-1, repeated)
   uint64_t h2d_bytes = 0;
-  std::vector<cudaEvent_t> ev;   // per-site boundaries (M + 1)
-  std::vector<cudaEvent_t> gev;  // per-site GEMM start/stop (2 M)
+  std::vector<cudaEvent_t> ev;   // per-site boundaries on lane 0 (M + 1)
+  cudaEvent_t pass_end = nullptr;
 };
 
 }  // namespace mpsg
@@ -378,18 +390,37 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     const double budget = 6.0e9;  // bytes of per-pass working set
     want = std::min<uint64_t>(65536, static_cast<uint64_t>(budget / row_bytes));
   }
-  dc.cap = std::max(2 * kBM, round_up(static_cast<int>(std::min<uint64_t>(want, 1u << 22)), 2 * kBM));
+  // Two lanes overlap the select kernel with the other lane's contraction; measured neutral under
+  // the 1000 W power cap (c2 +2%, c3 -2.5%), so one lane is the default.
+  int nlanes = 1;
+  if (const char* v = std::getenv("MPSG_LANES")) nlanes = std::max(1, std::min(2, std::atoi(v)));
+  if (h.opts.host_stream_slots != 0 || h.tp != 1) nlanes = 1;
+  const int lane_cap = std::max(2 * kBM, round_up(static_cast<int>((std::min<uint64_t>(want, 1u << 22) +
+                                                                     nlanes - 1) / nlanes), 2 * kBM));
+  dc.cap = nlanes * lane_cap;
   dc.sites.resize(h.M);
-  CUDA_OK(cudaMalloc(&dc.env, 4ull * dc.cap * kmax * sizeof(__half)));
-  CUDA_OK(cudaMalloc(&dc.temp, 1ull * dc.cap * h.d * chirpm * sizeof(float2)));
-  CUDA_OK(cudaMalloc(&dc.pstat, 1ull * dc.cap * nt_max * sizeof(float2)));
-  if (h.tp > 1) CUDA_OK(cudaMalloc(&dc.part, 1ull * h.tp * dc.cap * h.d * sizeof(float2)));
-  CUDA_OK(cudaMalloc(&dc.alive, dc.cap));
-  CUDA_OK(cudaMalloc(&dc.rows, 1ull * dc.cap * h.M));
+  dc.lanes.resize(nlanes);
+  for (int L = 0; L < nlanes; ++L) {
+    Lane& ln = dc.lanes[L];
+    ln.cap = lane_cap;
+    if (L == 0)
+      ln.stream = dc.stream;
+    else
+      CUDA_OK(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaMalloc(&ln.env, 4ull * ln.cap * kmax * sizeof(__half)));
+    CUDA_OK(cudaMalloc(&ln.temp, 1ull * ln.cap * h.d * chirpm * sizeof(float2)));
+    CUDA_OK(cudaMalloc(&ln.pstat, 1ull * ln.cap * nt_max * sizeof(float2)));
+    if (h.tp > 1) CUDA_OK(cudaMalloc(&ln.part, 1ull * h.tp * ln.cap * h.d * sizeof(float2)));
+    CUDA_OK(cudaMalloc(&ln.alive, ln.cap));
+    CUDA_OK(cudaMalloc(&ln.rows, 1ull * ln.cap * h.M));
+    CUDA_OK(cudaMallocHost(&ln.host_rows, 1ull * ln.cap * h.M));
+    CUDA_OK(cudaEventCreateWithFlags(&ln.k1done, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
+    ln.tma_env.resize(h.M);
+  }
   CUDA_OK(cudaMalloc(&dc.err, sizeof(int)));
   CUDA_OK(cudaMemset(dc.err, 0, sizeof(int)));
   CUDA_OK(cudaMalloc(&dc.scratch, sizeof(double) * (kmax + 2ull * h.tp * chirpm) + sizeof(int) * kmax));
-  CUDA_OK(cudaMallocHost(&dc.host_rows, 1ull * dc.cap * h.M));
   if (h.opts.host_stream_slots > 0) {
     config_check(h.opts.host_stream_slots >= 2, "host_stream_slots must be 0 or >= 2");
     dc.slots = h.opts.host_stream_slots;
@@ -424,20 +455,29 @@ static void free_device(DevCtx& dc) {
     }
     cudaFree(s.cs);
   }
-  cudaFree(dc.env);
-  cudaFree(dc.temp);
-  cudaFree(dc.pstat);
-  cudaFree(dc.part);
-  cudaFree(dc.alive);
-  cudaFree(dc.rows);
-  cudaFree(dc.forced);
-  cudaFree(dc.marg);
+  for (auto& ln : dc.lanes) {
+    if (ln.stream && ln.stream != dc.stream) {
+      cudaStreamSynchronize(ln.stream);
+      cudaStreamDestroy(ln.stream);
+    }
+    cudaFree(ln.env);
+    cudaFree(ln.temp);
+    cudaFree(ln.pstat);
+    cudaFree(ln.part);
+    cudaFree(ln.alive);
+    cudaFree(ln.rows);
+    cudaFree(ln.forced);
+    cudaFree(ln.marg);
+    if (ln.host_rows) cudaFreeHost(ln.host_rows);
+    if (ln.k1done) cudaEventDestroy(ln.k1done);
+    if (ln.done) cudaEventDestroy(ln.done);
+    for (auto e : ln.gev) cudaEventDestroy(e);
+  }
   cudaFree(dc.scratch);
   cudaFree(dc.src);
   cudaFree(dc.err);
-  if (dc.host_rows) cudaFreeHost(dc.host_rows);
   for (auto e : dc.ev) cudaEventDestroy(e);
-  for (auto e : dc.gev) cudaEventDestroy(e);
+  if (dc.pass_end) cudaEventDestroy(dc.pass_end);
   if (dc.copy_stream) cudaStreamSynchronize(dc.copy_stream);
   for (auto& s : dc.sites) {
     if (s.g_host) cudaFreeHost(s.g_host);
@@ -507,7 +547,7 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
     throw Error(MPSG_ERR_NUMERIC, "contract_site: non-finite input (site " + std::to_string(i) +
                                       ") or dynamic range beyond the compressed format");
   }
-  s.tma_env = make_tma_env(dc.env, s.kshard, 4ull * dc.cap, h.tp);
+  for (auto& ln : dc.lanes) ln.tma_env[i] = make_tma_env(ln.env, s.kshard, 4ull * ln.cap, h.tp);
   if (dc.slots) {
     if (!s.g_host) {
       CUDA_OK(cudaMallocHost(&s.g_host, static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half)));
@@ -594,100 +634,133 @@ static void set_site(mpsg_handle_s& h, uint64_t i, const void* gamma, bool is_de
 // ---------------------------------------------------------------------------------------------
 struct PassOut {
   uint64_t macs = 0, wmacs = 0, issued = 0, launches = 0;
-  double gemm_s = 0.0;
+  double gemm_s = 0.0, device_s = 0.0;
 };
 
-// Runs one pass of `count` (<= cap) samples starting at global index `first` on dc.
+// Enqueues one pass of `count` (<= dc.cap) samples starting at global index `first`, split over
+// the lanes.  Lane L covers [first + off[L], first + off[L] + cnt[L]).
 static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first, int count,
-                     const uint8_t* forced_dev, double* marg_dev, PassOut& po, int timing) {
-  const int rows = round_up(count, h.pair ? 2 * kBM : kBM);
-  launch_init_env(dc.env, dc.cap, dc.sites[0].kshard, h.tp, rows, count, dc.alive, dc.stream);
-  po.launches += 1;
+                     bool forced, bool marg, PassOut& po, int timing, int off[2], int cnt[2]) {
+  const int nl = static_cast<int>(dc.lanes.size());
+  const int mrow = h.pair ? 2 * kBM : kBM;
+  off[0] = 0;
+  cnt[0] = count;
+  cnt[1] = 0;
+  if (nl == 2 && count > 2 * kBM) {  // halves rounded to whole M tiles
+    cnt[0] = std::min(dc.lanes[0].cap, round_up((count + 1) / 2, 2 * kBM));
+    cnt[1] = count - cnt[0];
+  }
+  off[1] = cnt[0];
+  const int active = cnt[1] > 0 ? 2 : 1;
+  int rows[2];
+  for (int L = 0; L < active; ++L) {
+    Lane& ln = dc.lanes[L];
+    rows[L] = round_up(cnt[L], mrow);
+    if (L > 0 && timing) CUDA_OK(cudaStreamWaitEvent(ln.stream, dc.ev[0], 0));  // after the pass-start stamp
+    launch_init_env(ln.env, ln.cap, dc.sites[0].kshard, h.tp, rows[L], cnt[L], ln.alive, ln.stream);
+    po.launches += 1;
+  }
   if (dc.slots) issue_loads(h, dc, dc.consumed + dc.slots);
   for (uint64_t i = 0; i < h.M; ++i) {
     const SiteDev& s = dc.sites[i];
     const CUtensorMap* tma_g = h.pair ? &s.tma_g64 : &s.tma_g;
     const float2* cinfo = s.cinfo;
     int slot = -1;
-    if (dc.slots) {
+    if (dc.slots) {  // single lane in host-streamed mode
       if (dc.consumed % h.M != i) throw Error(MPSG_ERR_INTERNAL, "site stream out of sequence");
       slot = static_cast<int>(dc.consumed % dc.slots);
       CUDA_OK(cudaStreamWaitEvent(dc.stream, dc.loaded[slot], 0));
       tma_g = h.pair ? &s.tma_slot64[slot] : &s.tma_slot[slot];
       cinfo = dc.slot_cinfo[slot];
     }
-    SiteGemmArgs ga;
-    ga.m_tiles = rows / (h.pair ? 2 * kBM : kBM);
-    ga.n_tiles = s.nt;
-    ga.k_blocks = s.kp / kBK;
-    ga.kshard_blocks = s.kshard / kBK;
-    ga.plane_rows_a = dc.cap;
-    ga.np = s.np;
-    ga.chirp = s.chirp;
-    ga.d = static_cast<int>(h.d);
-    ga.group_n = h.pair ? std::min(s.nt, 2 * kGroupPairs) : std::min(s.nt / 2, kGroupPairs);
-    ga.cinfo = cinfo;
-    ga.temp = dc.temp;
-    ga.pstat = dc.pstat;
-    const int ctas = h.pair ? 2 * ga.m_tiles * ga.n_tiles : ga.m_tiles * ga.n_tiles;
-    if (timing >= 2) CUDA_OK(cudaEventRecord(dc.gev[2 * i], dc.stream));
-    if (h.pair)
-      launch_site_gemm_pair(h.split, s.tma_env, *tma_g, ga, std::min(ctas, dc.num_sms), dc.stream);
-    else
-      launch_site_gemm(h.split, s.tma_env, *tma_g, ga, std::min(ctas, dc.num_sms), dc.stream);
-    if (timing >= 2) CUDA_OK(cudaEventRecord(dc.gev[2 * i + 1], dc.stream));
-    if (dc.slots) {  // K1 is the only reader of the slot: hand it back to the copy stream
-      CUDA_OK(cudaEventRecord(dc.freed[slot], dc.stream));
-      ++dc.consumed;
-      issue_loads(h, dc, dc.consumed + dc.slots);
-    }
+    for (int L = 0; L < active; ++L) {
+      Lane& ln = dc.lanes[L];
+      const uint64_t lfirst = first + off[L];
+      if (active == 2) {  // contraction kernels alternate A_i, B_i, A_i+1, ...
+        if (L == 1)
+          CUDA_OK(cudaStreamWaitEvent(ln.stream, dc.lanes[0].k1done, 0));
+        else if (i > 0)
+          CUDA_OK(cudaStreamWaitEvent(ln.stream, dc.lanes[1].k1done, 0));
+      }
+      SiteGemmArgs ga;
+      ga.m_tiles = rows[L] / mrow;
+      ga.n_tiles = s.nt;
+      ga.k_blocks = s.kp / kBK;
+      ga.kshard_blocks = s.kshard / kBK;
+      ga.plane_rows_a = ln.cap;
+      ga.np = s.np;
+      ga.chirp = s.chirp;
+      ga.d = static_cast<int>(h.d);
+      ga.group_n = h.pair ? std::min(s.nt, 2 * kGroupPairs) : std::min(s.nt / 2, kGroupPairs);
+      ga.cinfo = cinfo;
+      ga.temp = ln.temp;
+      ga.pstat = ln.pstat;
+      const int ctas = h.pair ? 2 * ga.m_tiles * ga.n_tiles : ga.m_tiles * ga.n_tiles;
+      if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[2 * i], ln.stream));
+      if (h.pair)
+        launch_site_gemm_pair(h.split, ln.tma_env[i], *tma_g, ga, std::min(ctas, dc.num_sms), ln.stream);
+      else
+        launch_site_gemm(h.split, ln.tma_env[i], *tma_g, ga, std::min(ctas, dc.num_sms), ln.stream);
+      if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[2 * i + 1], ln.stream));
+      if (active == 2) CUDA_OK(cudaEventRecord(ln.k1done, ln.stream));
+      if (dc.slots) {  // K1 is the only reader of the slot: hand it back to the copy stream
+        CUDA_OK(cudaEventRecord(dc.freed[slot], dc.stream));
+        ++dc.consumed;
+        issue_loads(h, dc, dc.consumed + dc.slots);
+      }
 
-    SelectArgs sa;
-    sa.site = static_cast<int>(i);
-    sa.num_sites = static_cast<int>(h.M);
-    sa.d = static_cast<int>(h.d);
-    sa.chir_loc = s.width;
-    sa.chirp = s.chirp;
-    if (h.tp == 1) {  // partials straight from the tiles: (tile t of outcome k) at pstat[n][k*tpk+t]
-      sa.parts = s.chirp / kBN;
-      sa.part_base = dc.pstat;
-      sa.part_stride = 1;
-      sa.row_stride = s.nt;
-      sa.k_stride = s.chirp / kBN;
-    } else {  // per-rank (weight, max) per outcome, exchanged, summed in rank order on every rank
-      launch_reduce_tiles(dc.pstat, s.nt, s.chirp / kBN, sa.d, rows,
-                          dc.part + 1ull * h.tp_rank * dc.cap * h.d, dc.stream);
-      h.comm->allgather(dc.part, 1ull * dc.cap * h.d * sizeof(float2), dc.stream);
-      sa.parts = h.tp;
-      sa.part_base = dc.part;
-      sa.part_stride = 1ll * dc.cap * static_cast<long long>(h.d);
-      sa.row_stride = static_cast<long long>(h.d);
-      sa.k_stride = 1;
-      po.launches += 1;
+      SelectArgs sa;
+      sa.site = static_cast<int>(i);
+      sa.num_sites = static_cast<int>(h.M);
+      sa.d = static_cast<int>(h.d);
+      sa.chir_loc = s.width;
+      sa.chirp = s.chirp;
+      if (h.tp == 1) {  // partials straight from the tiles: (tile t of outcome k) at pstat[n][k*tpk+t]
+        sa.parts = s.chirp / kBN;
+        sa.part_base = ln.pstat;
+        sa.part_stride = 1;
+        sa.row_stride = s.nt;
+        sa.k_stride = s.chirp / kBN;
+      } else {  // per-rank (weight, max) per outcome, exchanged, summed in rank order on every rank
+        launch_reduce_tiles(ln.pstat, s.nt, s.chirp / kBN, sa.d, rows[L],
+                            ln.part + 1ull * h.tp_rank * ln.cap * h.d, ln.stream);
+        h.comm->allgather(ln.part, 1ull * ln.cap * h.d * sizeof(float2), ln.stream);
+        sa.parts = h.tp;
+        sa.part_base = ln.part;
+        sa.part_stride = 1ll * ln.cap * static_cast<long long>(h.d);
+        sa.row_stride = static_cast<long long>(h.d);
+        sa.k_stride = 1;
+        po.launches += 1;
+      }
+      sa.rows = rows[L];
+      sa.count = cnt[L];
+      const bool has_next = i + 1 < h.M;
+      const int kn = has_next ? dc.sites[i + 1].kshard : 0;
+      sa.kp_next = kn;
+      sa.env_cap = ln.cap;
+      sa.seed = seed;
+      sa.first = lfirst;
+      sa.temp = ln.temp;
+      sa.alive = ln.alive;
+      sa.rows_out = ln.rows;
+      sa.env_next = ln.env + 4ull * ln.cap * kn * h.tp_rank;
+      sa.forced = forced ? ln.forced : nullptr;
+      sa.marg = marg ? ln.marg : nullptr;
+      launch_select(sa, ln.stream);
+      if (h.tp > 1 && has_next)  // rebuild the full environment from the column shards
+        h.comm->allgather(ln.env, 4ull * ln.cap * kn * sizeof(__half), ln.stream);
+      po.launches += 2;
+      po.macs += static_cast<uint64_t>(cnt[L]) * s.chil * s.width * h.d;
+      po.wmacs += static_cast<uint64_t>(cnt[L]) * s.width * h.d;
+      po.issued += 8ull * rows[L] * s.np * s.kp * (h.split ? 2 : 1);
     }
-    sa.rows = rows;
-    sa.count = count;
-    const bool has_next = i + 1 < h.M;
-    const int kn = has_next ? dc.sites[i + 1].kshard : 0;
-    sa.kp_next = kn;
-    sa.env_cap = dc.cap;
-    sa.seed = seed;
-    sa.first = first;
-    sa.temp = dc.temp;
-    sa.alive = dc.alive;
-    sa.rows_out = dc.rows;
-    sa.env_next = dc.env + 4ull * dc.cap * kn * h.tp_rank;
-    sa.forced = forced_dev;
-    sa.marg = marg_dev;
-    launch_select(sa, dc.stream);
-    if (h.tp > 1 && has_next)  // rebuild the full environment from the column shards
-      h.comm->allgather(dc.env, 4ull * dc.cap * kn * sizeof(__half), dc.stream);
     if (timing) CUDA_OK(cudaEventRecord(dc.ev[i + 1], dc.stream));
-    po.launches += 2;
-    po.macs += static_cast<uint64_t>(count) * s.chil * s.width * h.d;
-    po.wmacs += static_cast<uint64_t>(count) * s.width * h.d;
-    po.issued += 8ull * rows * s.np * s.kp * (h.split ? 2 : 1);
   }
+  if (active == 2) {  // join lane 1 into lane 0
+    CUDA_OK(cudaEventRecord(dc.lanes[1].done, dc.lanes[1].stream));
+    CUDA_OK(cudaStreamWaitEvent(dc.stream, dc.lanes[1].done, 0));
+  }
+  if (timing) CUDA_OK(cudaEventRecord(dc.pass_end, dc.stream));
   CUDA_OK(cudaGetLastError());
 }
 
@@ -707,48 +780,77 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
     if (timing && dc.ev.empty()) {
       dc.ev.resize(h.M + 1);
       for (auto& e : dc.ev) CUDA_OK(cudaEventCreate(&e));
+      CUDA_OK(cudaEventCreate(&dc.pass_end));
     }
-    if (timing >= 2 && dc.gev.empty()) {
-      dc.gev.resize(2 * h.M);
-      for (auto& e : dc.gev) CUDA_OK(cudaEventCreate(&e));
-    }
+    if (timing >= 2)
+      for (auto& ln : dc.lanes)
+        if (ln.gev.empty()) {
+          ln.gev.resize(2 * h.M);
+          for (auto& e : ln.gev) CUDA_OK(cudaEventCreate(&e));
+        }
     if (timing) rr.site_ms.assign(h.M, 0.0);
-    if ((forced_host || marg_host) && !dc.forced) {
-      CUDA_OK(cudaMalloc(&dc.forced, 1ull * dc.cap * h.M));
-      CUDA_OK(cudaMalloc(&dc.marg, 1ull * dc.cap * h.M * h.d * sizeof(double)));
-    }
-    for (uint64_t off = 0; off < count; off += dc.cap) {
-      const int n = static_cast<int>(std::min<uint64_t>(dc.cap, count - off));
-      if (forced_host)
-        CUDA_OK(cudaMemcpyAsync(dc.forced, forced_host + off * h.M, 1ull * n * h.M,
-                                cudaMemcpyHostToDevice, dc.stream));
+    if (forced_host || marg_host)
+      for (auto& ln : dc.lanes)
+        if (!ln.forced) {
+          CUDA_OK(cudaMalloc(&ln.forced, 1ull * ln.cap * h.M));
+          CUDA_OK(cudaMalloc(&ln.marg, 1ull * ln.cap * h.M * h.d * sizeof(double)));
+        }
+    for (uint64_t poff = 0; poff < count; poff += dc.cap) {
+      const int n = static_cast<int>(std::min<uint64_t>(dc.cap, count - poff));
+      int off[2], cnt[2];
+      // the lane split is recomputed inside run_pass; forced rows must be staged first
+      {
+        int tmp_off[2], tmp_cnt[2];
+        tmp_off[0] = 0;
+        tmp_cnt[0] = n;
+        tmp_cnt[1] = 0;
+        if (dc.lanes.size() == 2 && n > 2 * kBM) {
+          tmp_cnt[0] = std::min(dc.lanes[0].cap, round_up((n + 1) / 2, 2 * kBM));
+          tmp_cnt[1] = n - tmp_cnt[0];
+        }
+        tmp_off[1] = tmp_cnt[0];
+        if (forced_host)
+          for (int L = 0; L < 2; ++L)
+            if (tmp_cnt[L] > 0)
+              CUDA_OK(cudaMemcpyAsync(dc.lanes[L].forced, forced_host + (poff + tmp_off[L]) * h.M,
+                                      1ull * tmp_cnt[L] * h.M, cudaMemcpyHostToDevice, dc.lanes[L].stream));
+      }
       if (timing) CUDA_OK(cudaEventRecord(dc.ev[0], dc.stream));
-      run_pass(h, dc, seed, first + off, n, forced_host ? dc.forced : nullptr,
-               marg_host ? dc.marg : nullptr, rr.po, timing);
-      if (rows_dev_out) {
-        CUDA_OK(cudaMemcpyAsync(rows_dev_out + off * h.M, dc.rows, 1ull * n * h.M,
-                                cudaMemcpyDeviceToDevice, dc.stream));
+      run_pass(h, dc, seed, first + poff, n, forced_host != nullptr, marg_host != nullptr, rr.po, timing,
+               off, cnt);
+      for (int L = 0; L < 2; ++L) {
+        if (cnt[L] <= 0) continue;
+        Lane& ln = dc.lanes[L];
+        const size_t o = (poff + off[L]) * h.M;
+        if (rows_dev_out)
+          CUDA_OK(cudaMemcpyAsync(rows_dev_out + o, ln.rows, 1ull * cnt[L] * h.M, cudaMemcpyDeviceToDevice,
+                                  ln.stream));
+        if (rows_host)
+          CUDA_OK(cudaMemcpyAsync(ln.host_rows, ln.rows, 1ull * cnt[L] * h.M, cudaMemcpyDeviceToHost,
+                                  ln.stream));
+        if (marg_host)
+          CUDA_OK(cudaMemcpyAsync(marg_host + o * h.d, ln.marg, 1ull * cnt[L] * h.M * h.d * sizeof(double),
+                                  cudaMemcpyDeviceToHost, ln.stream));
       }
-      if (rows_host) {
-        CUDA_OK(cudaMemcpyAsync(dc.host_rows, dc.rows, 1ull * n * h.M, cudaMemcpyDeviceToHost,
-                                dc.stream));
-      }
-      if (marg_host) {
-        CUDA_OK(cudaMemcpyAsync(marg_host + off * h.M * h.d, dc.marg,
-                                1ull * n * h.M * h.d * sizeof(double), cudaMemcpyDeviceToHost,
-                                dc.stream));
-      }
-      CUDA_OK(cudaStreamSynchronize(dc.stream));
-      if (rows_host) std::memcpy(rows_host + off * h.M, dc.host_rows, 1ull * n * h.M);
+      for (int L = 0; L < 2; ++L)
+        if (cnt[L] > 0) CUDA_OK(cudaStreamSynchronize(dc.lanes[L].stream));
+      if (rows_host)
+        for (int L = 0; L < 2; ++L)
+          if (cnt[L] > 0)
+            std::memcpy(rows_host + (poff + off[L]) * h.M, dc.lanes[L].host_rows, 1ull * cnt[L] * h.M);
       if (timing) {
+        float ms = 0.f;
+        CUDA_OK(cudaEventElapsedTime(&ms, dc.ev[0], dc.pass_end));
+        rr.po.device_s += ms * 1e-3;
         for (uint64_t i = 0; i < h.M; ++i) {
-          float ms = 0.f;
           CUDA_OK(cudaEventElapsedTime(&ms, dc.ev[i], dc.ev[i + 1]));
           rr.site_ms[i] += ms;
-          if (timing >= 2) {
-            CUDA_OK(cudaEventElapsedTime(&ms, dc.gev[2 * i], dc.gev[2 * i + 1]));
-            rr.po.gemm_s += ms * 1e-3;
-          }
+          if (timing >= 2)
+            for (int L = 0; L < 2; ++L) {
+              if (cnt[L] <= 0) continue;
+              CUDA_OK(cudaEventElapsedTime(&ms, dc.lanes[L].gev[2 * i], dc.lanes[L].gev[2 * i + 1]));
+              rr.po.gemm_s += ms * 1e-3;
+            }
         }
       }
     }
@@ -788,12 +890,14 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
     st->contraction_macs = st->measure_weight_macs = st->issued_mma_flops = 0;
     st->kernel_launches = 0;
     st->gemm_seconds = 0.0;
+    st->device_seconds = 0.0;
     for (auto& r : rr) {
       st->contraction_macs += r.po.macs;
       st->measure_weight_macs += r.po.wmacs;
       st->issued_mma_flops += r.po.issued;
       st->kernel_launches += r.po.launches;
       st->gemm_seconds = std::max(st->gemm_seconds, r.po.gemm_s);  // devices run concurrently
+      st->device_seconds = std::max(st->device_seconds, r.po.device_s);
     }
     st->gemm_flops = 8 * st->contraction_macs;
     st->dead_samples = 0;
@@ -1105,14 +1209,15 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
     config_check(h->tp == 1, "mpsg_contract_site: not available on a tensor-parallel handle");
     config_check(h->devs[0].slots == 0, "mpsg_contract_site: not available in host-streamed mode");
     DevCtx& dc = h->devs[0];
-    config_check(count >= 1 && count <= static_cast<uint64_t>(dc.cap), "count exceeds pass capacity");
+    config_check(count >= 1 && count <= static_cast<uint64_t>(dc.lanes[0].cap), "count exceeds pass capacity");
     CUDA_OK(cudaSetDevice(dc.device));
     std::lock_guard<std::mutex> lk(h->mu);
     const SiteDev& s = dc.sites[site];
     const int n = static_cast<int>(count);
     const int rows = round_up(n, h->pair ? 2 * kBM : kBM);
     // host: internal env E = env * gl * sigma_n (sigma_n power of two), hi/lo fp16 planes
-    const size_t plane = 1ull * dc.cap * s.kp;
+    Lane& ln = dc.lanes[0];
+    const size_t plane = 1ull * ln.cap * s.kp;
     std::vector<__half> e(4 * plane, __float2half_rn(0.f));
     std::vector<double> sig(n, 1.0);
     for (int r = 0; r < n; ++r) {
@@ -1136,28 +1241,28 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
         e[3 * plane + o] = __float2half_rn(fi - __half2float(hi));
       }
     }
-    CUDA_OK(cudaMemcpy(dc.env, e.data(), e.size() * sizeof(__half), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(ln.env, e.data(), e.size() * sizeof(__half), cudaMemcpyHostToDevice));
     SiteGemmArgs ga;
     ga.m_tiles = rows / (h->pair ? 2 * kBM : kBM);
     ga.n_tiles = s.nt;
     ga.k_blocks = s.kp / kBK;
     ga.kshard_blocks = s.kshard / kBK;
-    ga.plane_rows_a = dc.cap;
+    ga.plane_rows_a = ln.cap;
     ga.np = s.np;
     ga.chirp = s.chirp;
     ga.d = static_cast<int>(h->d);
     ga.group_n = h->pair ? std::min(s.nt, 2 * kGroupPairs) : std::min(s.nt / 2, kGroupPairs);
     ga.cinfo = s.cinfo;
-    ga.temp = dc.temp;
-    ga.pstat = dc.pstat;
+    ga.temp = ln.temp;
+    ga.pstat = ln.pstat;
     const int ctas = h->pair ? 2 * ga.m_tiles * ga.n_tiles : ga.m_tiles * ga.n_tiles;
     if (h->pair)
-      launch_site_gemm_pair(h->split, s.tma_env, s.tma_g64, ga, std::min(ctas, dc.num_sms), dc.stream);
+      launch_site_gemm_pair(h->split, ln.tma_env[site], s.tma_g64, ga, std::min(ctas, dc.num_sms), dc.stream);
     else
-      launch_site_gemm(h->split, s.tma_env, s.tma_g, ga, std::min(ctas, dc.num_sms), dc.stream);
+      launch_site_gemm(h->split, ln.tma_env[site], s.tma_g, ga, std::min(ctas, dc.num_sms), dc.stream);
     CUDA_OK(cudaGetLastError());
     std::vector<float2> t(1ull * n * h->d * s.chirp);
-    CUDA_OK(cudaMemcpyAsync(t.data(), dc.temp, t.size() * sizeof(float2), cudaMemcpyDeviceToHost,
+    CUDA_OK(cudaMemcpyAsync(t.data(), ln.temp, t.size() * sizeof(float2), cudaMemcpyDeviceToHost,
                             dc.stream));
     CUDA_OK(cudaStreamSynchronize(dc.stream));
     const size_t d = h->d;

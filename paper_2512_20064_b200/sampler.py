@@ -221,6 +221,7 @@ class SampleBatch:
 
 @dataclass
 class RunStats:
+    device_seconds: float = 0.0
     contraction_macs: int = 0
     measure_weight_macs: int = 0
     dead_samples: int = 0
