@@ -36,10 +36,12 @@ CONFIGS = {
     "c1": dict(M=16, chi=32, d=4, job=1000, desc="c1: M=16, chi=32, d=4, N=1000"),
     "c2": dict(M=256, chi=512, d=6, job=100_000, desc="c2: M=256, chi=512, d=6, N=1e5 (whole MPS in HBM)"),
     "c3": dict(M=1024, chi=2048, d=6, job=1_000_000, desc="c3: M=1024, chi=2048, d=6, N=1e6 data-parallel"),
-    "c5_1024": dict(M=512, chi=1024, d=4, job=100_000, desc="c5: M=512, chi=1024, d=4, N=1e5"),
-    "c5_4096": dict(M=512, chi=4096, d=4, job=100_000, desc="c5: M=512, chi=4096, d=4, N=1e5"),
 }
-DEFAULT_PASS = {"c1": 1000, "c2": 32768, "c3": 16384, "c5_1024": 32768, "c5_4096": 8192}
+for _chi in (256, 512, 1024, 2048, 4096):
+    CONFIGS[f"c5_{_chi}"] = dict(M=512, chi=_chi, d=4, job=100_000,
+                                 desc=f"c5: bond-dimension sweep M=512, chi={_chi}, d=4, N=1e5")
+DEFAULT_PASS = {"c1": 1000, "c2": 32768, "c3": 16384, "c5_256": 65536, "c5_512": 32768,
+                "c5_1024": 32768, "c5_2048": 16384, "c5_4096": 8192}
 
 
 def peaks():
