@@ -300,3 +300,66 @@ def test_invariants_at_chi2048(pkg):
     ref = one.sample(0, 512, 3)
     assert (t[0] != ref).any(axis=1).sum() <= 2  # only draws at a CDF boundary may flip
     tp.close()
+
+
+def test_edge_decay_chain_golden(pkg, gold):
+    """decay_chain (mps.cpp:183-196): the reference's own outcomes (F64, no scaling) reproduced; the
+    GPU renormalises every site so nothing dies where F16-without-scaling would (decay.npz)."""
+    z = np.load(f"{gold}/decay.npz")
+    mps = O.load_npz_mps(z, "decay_")
+    smp = pkg.GpuSampler(to_state(pkg, mps), pkg.PrecisionPolicy())
+    rows = smp.sample(0, 200, 3)
+    assert np.array_equal(rows, z["decay_f64_none"])
+    assert int((rows[:, -1] == pkg.DEAD_OUTCOME).sum()) == 0
+
+
+def test_edge_structural_dead_paths(pkg):
+    """Outcome 1 at site 0 leads to an all-zero environment at site 1: those samples are dead
+    (0xFF) from site 1 on (sampler.cpp:94-98), exactly as the oracle says."""
+    g0 = np.zeros((1, 2, 2), complex)
+    g0[0, 0, 0] = 1.0
+    g0[0, 1, 1] = 0.8
+    g1 = np.zeros((2, 2, 2), complex)  # row l=1 is zero: env [0, x] from outcome 1 dies here
+    g1[0, :, :] = [[0.5, 0.2j], [0.3, 0.4]]
+    g2 = np.zeros((2, 1, 2), complex)
+    g2[:, 0, :] = [[1.0, 0.5], [0.25, 1.0]]
+    mps = O.Mps(2, [1, 2, 2, 1], [g0, g1, g2])
+    mps.lambdas = [np.array([0.8, 0.6]), np.array([0.9, 0.4359]), np.ones(1)]
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    smp = pkg.GpuSampler(to_state(pkg, mps), pol)
+    dec = decoded_mps(smp, mps)
+    ref, _ = O.orc_sample_range(dec, 0, 2000, 5)
+    got = smp.sample(0, 2000, 5)
+    assert np.array_equal(got, ref)
+    dead = got[:, -1] == pkg.DEAD_OUTCOME
+    assert 0 < dead.sum() < 2000
+    assert (got[dead, 0] == 1).all() and (got[dead, 1:] == pkg.DEAD_OUTCOME).all()
+
+
+def test_edge_small_odd_chains(pkg, gold):
+    """d in {2,3,5,7}, chi 1..64, short chains (small.npz shapes): GPU == oracle on the decoded Gamma."""
+    z = np.load(f"{gold}/small.npz")
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    for j in range(int(z["ncases"])):
+        mps = O.load_npz_mps(z, f"c{j}_")
+        smp = pkg.GpuSampler(to_state(pkg, mps), pol)
+        seed = int(z[f"c{j}_seed"])
+        ref, marg, _ = O.orc_sample_range(decoded_mps(smp, mps), 0, 300, seed, want_marginals=True)
+        got = smp.sample(0, 300, seed)
+        ndiff, explained = compare_strings(got, ref, marg, seed)
+        assert ndiff == explained, (j, ndiff, explained)
+
+
+def test_edge_phys_dim_one_and_huge_index(pkg):
+    """d = 1 (every outcome 0) and a single sample at a global index near 2^64 (keyed RNG)."""
+    g = [np.ones((1, 1, 1), complex) * 0.5 for _ in range(4)]
+    mps = O.Mps(1, [1, 1, 1, 1, 1], g, [np.ones(1)] * 4)
+    smp = pkg.GpuSampler(to_state(pkg, mps))
+    assert (smp.sample(0, 10, 1) == 0).all()
+    z = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "c1.npz"))
+    m1 = O.load_npz_mps(z)
+    s1 = pkg.GpuSampler(to_state(pkg, m1), pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX))
+    first = 2**64 - 3
+    got = s1.sample(first, 2, 7)
+    ref, _ = O.orc_sample_range(decoded_mps(s1, m1), first, 2, 7)
+    assert np.array_equal(got, ref)
