@@ -93,7 +93,10 @@ typedef struct mpsg_options {
                                       pinned host memory and streamed per site through this many
                                       device slots by a copy stream overlapping the compute
                                       (the reference's SiteStream prefetch, mps_io.cpp:294-350) */
-  int reserved[2];
+  int record_decay_trace;          /* fill mpsg_stats.decay_trace: mean |env| per site before
+                                      scaling, in the reference's own scaling (sampler.cpp:149-153,
+                                      decay_probe :207-216); GlobalMax is traced as None */
+  int reserved;
 } mpsg_options;
 
 /* Mirrors mpsamp::RunStats + FlopCounters (sampler.hpp:46-54, contract.hpp:12-25). */
@@ -109,6 +112,7 @@ typedef struct mpsg_stats {
   uint64_t gemm_flops;             /* algorithmic flops of those launches: 8 * contraction_macs */
   uint64_t kernel_launches;        /* CUDA kernels launched by this call */
   double device_seconds;           /* device time of all passes (CUDA events; record_site_times) */
+  double* decay_trace;             /* optional caller array of length M (record_decay_trace) */
 } mpsg_stats;
 
 typedef struct mpsg_handle_s* mpsg_handle;

@@ -128,6 +128,8 @@ def ref():
         L.ref_mps_apply_schedule.argtypes = [C.c_void_p, C.POINTER(_sz), _sz, _sz]
         L.ref_sample_batch_scheduled.restype = _int
         L.ref_sample_batch_scheduled.argtypes = [C.c_void_p, _u64, _u64, _int, C.POINTER(_sz), _sz, _sz, _pu8]
+        L.ref_decay_probe.restype = _int
+        L.ref_decay_probe.argtypes = [C.c_void_p, _int, _int, _u64, _u64, _pd]
         L.ref_run_scheme.restype = _int
         L.ref_run_scheme.argtypes = [C.c_char_p, _int, _u64, _u64, _u64, _sz, _sz, _u64, _int,
                                      _int, _pu8]
@@ -236,6 +238,11 @@ class RefState:
         _check_ref(ref().ref_marginals_forced(self.h, n, compute, scaling,
                                               forced.ctypes.data_as(_pu8), marg.ctypes.data_as(_pd)))
         return marg
+
+    def decay_probe(self, count, seed=1, compute=F64, scaling=SCALE_NONE):
+        out = np.empty(self.mps.num_sites, np.float64)
+        _check_ref(ref().ref_decay_probe(self.h, compute, scaling, count, seed, out.ctypes.data_as(_pd)))
+        return out
 
     def time_site_step(self, site, count, threads, reps=1):
         macs = _u64()

@@ -393,3 +393,19 @@ int ref_sample_batch_scheduled(void* h, uint64_t n, uint64_t seed, int scaling, 
     }
 }
 }
+
+extern "C" {
+// decay_probe (sampler.cpp:207-216): per-site mean |env| before scaling. out: M doubles.
+int ref_decay_probe(void* h, int compute, int scaling, uint64_t count, uint64_t seed, double* out) {
+    try {
+        PrecisionPolicy pol;
+        pol.compute = static_cast<Precision>(compute);
+        pol.scaling = static_cast<ScalingMode>(scaling);
+        std::vector<double> t = decay_probe(*static_cast<MpsState*>(h), pol, count, seed);
+        std::memcpy(out, t.data(), t.size() * sizeof(double));
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+}

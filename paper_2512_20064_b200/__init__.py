@@ -28,6 +28,7 @@ from .sampler import (  # noqa: F401
     SamplerOptions,
     ScalingMode,
     capped_bond_dims,
+    decay_probe,
     device_draws,
     sample_batch,
     sample_micro_serial,

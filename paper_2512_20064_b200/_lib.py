@@ -29,14 +29,15 @@ class Policy(C.Structure):
 class Options(C.Structure):
     _fields_ = [("mode", _int), ("pass_samples", _u64), ("record_site_times", _int),
                 ("tp_size", _int), ("tp_rank", _int), ("host_stream_slots", _int),
-                ("reserved", _int * 2)]
+                ("record_decay_trace", _int), ("reserved", _int)]
 
 
 class Stats(C.Structure):
     _fields_ = [("contraction_macs", _u64), ("measure_weight_macs", _u64), ("dead_samples", _u64),
                 ("seconds", _dbl), ("site_seconds", _pd), ("issued_mma_flops", _u64),
                 ("h2d_bytes", _u64), ("d2h_bytes", _u64), ("gemm_seconds", _dbl),
-                ("gemm_flops", _u64), ("kernel_launches", _u64), ("device_seconds", _dbl)]
+                ("gemm_flops", _u64), ("kernel_launches", _u64), ("device_seconds", _dbl),
+                ("decay_trace", _pd)]
 
 
 # (name, restype, argtypes) for every entry point of include/mpsg.h

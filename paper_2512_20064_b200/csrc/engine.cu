@@ -251,6 +251,7 @@ struct SiteDev {
   __half* g = nullptr;       // [2][np][kp]
   float2* cinfo = nullptr;   // [np]
   double* cs = nullptr;      // [chir * d]
+  double* inv_gamma = nullptr;  // [width] 1 / gamma_i[r] of the local columns (decay trace)
   CUtensorMap tma_g{}, tma_g64{};
   // host-streamed mode: the compressed site lives in pinned host memory
   __half* g_host = nullptr;
@@ -272,6 +273,7 @@ struct Lane {
   uint8_t* rows = nullptr;        // [cap][M]
   uint8_t* forced = nullptr;      // [cap][M] (lazy)
   double* marg = nullptr;         // [cap][M][d] (lazy)
+  double* logscale = nullptr;     // [cap] (lazy, decay trace)
   uint8_t* host_rows = nullptr;   // pinned [cap][M]
   std::vector<CUtensorMap> tma_env;  // per site: the shard-major env map over this lane's env
   cudaEvent_t k1done = nullptr, done = nullptr;
@@ -299,6 +301,7 @@ struct DevCtx {
   uint64_t h2d_bytes = 0;
   std::vector<cudaEvent_t> ev;   // per-site boundaries on lane 0 (M + 1)
   cudaEvent_t pass_end = nullptr;
+  double* trace = nullptr;       // [M] sum |env_ref| per site (decay trace, lazy)
 };
 
 }  // namespace mpsg
@@ -468,6 +471,7 @@ static void free_device(DevCtx& dc) {
     cudaFree(ln.rows);
     cudaFree(ln.forced);
     cudaFree(ln.marg);
+    cudaFree(ln.logscale);
     if (ln.host_rows) cudaFreeHost(ln.host_rows);
     if (ln.k1done) cudaEventDestroy(ln.k1done);
     if (ln.done) cudaEventDestroy(ln.done);
@@ -476,6 +480,8 @@ static void free_device(DevCtx& dc) {
   cudaFree(dc.scratch);
   cudaFree(dc.src);
   cudaFree(dc.err);
+  cudaFree(dc.trace);
+  for (auto& s : dc.sites) cudaFree(s.inv_gamma);
   for (auto e : dc.ev) cudaEventDestroy(e);
   if (dc.pass_end) cudaEventDestroy(dc.pass_end);
   if (dc.copy_stream) cudaStreamSynchronize(dc.copy_stream);
@@ -536,6 +542,12 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
   CUDA_OK(cudaMemcpyAsync(d_lpos, lpos.data(), sizeof(int) * s.chil, cudaMemcpyHostToDevice, dc.stream));
   CUDA_OK(cudaMemsetAsync(s.g, 0, static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half), dc.stream));
   CUDA_OK(cudaMemsetAsync(s.cinfo, 0, 1ull * s.np * sizeof(float2), dc.stream));
+  if (!s.inv_gamma) CUDA_OK(cudaMalloc(&s.inv_gamma, std::max<size_t>(1, s.width) * sizeof(double)));
+  {
+    std::vector<double> ig(std::max(1, s.width));
+    for (int r = 0; r < s.width; ++r) ig[r] = 1.0 / h.gr[i][s.b0 + r];
+    CUDA_OK(cudaMemcpyAsync(s.inv_gamma, ig.data(), sizeof(double) * ig.size(), cudaMemcpyHostToDevice, dc.stream));
+  }
   launch_compress_site(src_dev, f64, s.chil, s.chir, static_cast<int>(h.d), s.b0, s.width, s.kp,
                        s.chirp, d_lpos, d_gl, d_gr, d_wl, s.g, s.cinfo, s.cs, dc.err, dc.stream);
   CUDA_OK(cudaGetLastError());
@@ -657,7 +669,8 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
     Lane& ln = dc.lanes[L];
     rows[L] = round_up(cnt[L], mrow);
     if (L > 0 && timing) CUDA_OK(cudaStreamWaitEvent(ln.stream, dc.ev[0], 0));  // after the pass-start stamp
-    launch_init_env(ln.env, ln.cap, dc.sites[0].kshard, h.tp, rows[L], cnt[L], ln.alive, ln.stream);
+    launch_init_env(ln.env, ln.cap, dc.sites[0].kshard, h.tp, rows[L], cnt[L], ln.alive, ln.stream,
+                    dc.trace ? ln.logscale : nullptr);
     po.launches += 1;
   }
   if (dc.slots) issue_loads(h, dc, dc.consumed + dc.slots);
@@ -746,6 +759,10 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       sa.env_next = ln.env + 4ull * ln.cap * kn * h.tp_rank;
       sa.forced = forced ? ln.forced : nullptr;
       sa.marg = marg ? ln.marg : nullptr;
+      sa.logscale = dc.trace ? ln.logscale : nullptr;
+      sa.inv_gamma = s.inv_gamma;
+      sa.trace = dc.trace ? dc.trace + i : nullptr;
+      sa.scaling = h.policy.scaling;
       launch_select(sa, ln.stream);
       if (h.tp > 1 && has_next)  // rebuild the full environment from the column shards
         h.comm->allgather(ln.env, 4ull * ln.cap * kn * sizeof(__half), ln.stream);
@@ -789,6 +806,14 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
           for (auto& e : ln.gev) CUDA_OK(cudaEventCreate(&e));
         }
     if (timing) rr.site_ms.assign(h.M, 0.0);
+    if (h.opts.record_decay_trace) {  // record_decay_trace
+      if (!dc.trace) {
+        CUDA_OK(cudaMalloc(&dc.trace, h.M * sizeof(double)));
+        for (auto& ln : dc.lanes) CUDA_OK(cudaMalloc(&ln.logscale, ln.cap * sizeof(double)));
+      }
+      CUDA_OK(cudaMemsetAsync(dc.trace, 0, h.M * sizeof(double), dc.stream));
+      CUDA_OK(cudaStreamSynchronize(dc.stream));
+    }
     if (forced_host || marg_host)
       for (auto& ln : dc.lanes)
         if (!ln.forced) {
@@ -908,6 +933,17 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
     for (auto& dc : h.devs) st->h2d_bytes += dc.h2d_bytes;
     for (auto& dc : h.devs) dc.h2d_bytes = 0;
     st->d2h_bytes = rows_host ? count * h.M : 0;
+    if (st->decay_trace && h.opts.record_decay_trace) {  // sampler.cpp:196-201 normalisation
+      std::vector<double> sum(h.M, 0.0), part(h.M);
+      for (auto& dc : h.devs) {
+        if (!dc.trace) continue;
+        CUDA_OK(cudaSetDevice(dc.device));
+        CUDA_OK(cudaMemcpy(part.data(), dc.trace, h.M * sizeof(double), cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < h.M; ++i) sum[i] += part[i];
+      }
+      for (uint64_t i = 0; i < h.M; ++i)
+        st->decay_trace[i] = sum[i] / (static_cast<double>(count) * static_cast<double>(h.bonds[i + 1]));
+    }
     if (st->site_seconds) {
       for (uint64_t i = 0; i < h.M; ++i) {
         double mx = 0.0;  // devices run concurrently: report the slowest
@@ -997,6 +1033,7 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
       h->pair = !(v && std::string(v) == "cluster");
     }
     h->tp = std::max(1, h->opts.tp_size);
+    config_check(!(h->opts.record_decay_trace && h->opts.tp_size > 1), "decay trace is not available with tensor parallelism");
     h->tp_rank = h->opts.tp_rank;
     config_check(h->tp_rank >= 0 && h->tp_rank < h->tp, "tp_rank out of range");
     config_check(h->tp == 1 || ndev <= 1, "a tensor-parallel rank drives exactly one device");

@@ -67,6 +67,12 @@ struct SelectArgs {
   __half* env_next;         // this rank's shard of the next env: [4][env_cap][kp_next]
   const uint8_t* forced;    // optional [count][num_sites] teacher forcing
   double* marg;             // optional [count][num_sites][d]
+  // decay trace (sampler.cpp:149-153): optional.  logscale[n] = ln(E_int / (env_ref * gamma)) per
+  // sample; inv_gamma[r] = 1 / gamma_i[r] (local columns); trace accumulates sum |env_ref|.
+  double* logscale;
+  const double* inv_gamma;
+  double* trace;
+  int scaling;              // reference ScalingMode for the logscale update (precision.cpp:135-165)
 };
 
 // host launchers (sweep_kernels.cu)
@@ -83,7 +89,7 @@ void launch_reduce_tiles(const float2* pstat, int nt, int tiles_per_k, int d, in
                          float2* out, cudaStream_t s);
 // Site-0 env in the shard-major layout [shards][4][cap][kshard]: E[n][0] = 1 (shard 0).
 void launch_init_env(__half* env, int env_cap, int kshard0, int shards, int rows, int count,
-                     uint8_t* alive, cudaStream_t s);
+                     uint8_t* alive, cudaStream_t s, double* logscale = nullptr);
 void launch_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, double* out,
                   cudaStream_t s);
 // Compression of one site's column shard [b0, b0 + width) of chiR: src complex (chiL, chiR, d)

@@ -629,6 +629,29 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
     a.rows_out[static_cast<size_t>(n) * a.num_sites + a.site] = static_cast<uint8_t>(outcome);
     a.alive[n] = live_out ? 1 : 0;
   }
+  if (a.trace != nullptr && outcome != kDead) {
+    // reference-scale |env| of the gathered slice: |temp_int| / gamma_r * exp(-logscale)
+    const float2* src = a.temp + (static_cast<size_t>(n) * a.d + outcome) * a.chirp;
+    double acc = 0.0, mref = 0.0;
+    for (int r = lane; r < a.chir_loc; r += 32) {
+      const float2 v = src[r];
+      const double ig = a.inv_gamma[r];
+      acc += hypot(static_cast<double>(v.x), static_cast<double>(v.y)) * ig;
+      mref = fmax(mref, fmax(fabs(static_cast<double>(v.x)), fabs(static_cast<double>(v.y))) * ig);
+    }
+    acc = warp_sum(acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mref = fmax(mref, __shfl_xor_sync(0xffffffffu, mref, o));
+    if (lane == 0) {
+      const double ls = a.logscale[n];
+      atomicAdd(a.trace, acc * exp(-ls));
+      // next site: E_next = temp_int * scale  ->  logscale' = logscale + ln(scale) (+ ln m for
+      // PerSampleMax, whose reference env is divided by its max component m = mref * exp(-ls))
+      double nl = ls + log(static_cast<double>(scale));
+      if (a.scaling == 2 && mref > 0.0) nl += log(mref) - ls;
+      a.logscale[n] = live_out ? nl : 0.0;
+    }
+  }
   if (a.kp_next > 0) {
     // next env row: E[n, r] = temp[n, k, r] * 2^-e, split hi/lo fp16 (zeros for dead / pad).
     // Each lane handles 4 consecutive columns: two 16 B loads, one 8 B store per plane.
@@ -705,7 +728,7 @@ void launch_select(const SelectArgs& a, cudaStream_t s) {
 // site-0 environment (sampler.cpp:136-138: env = ones(count, 1), all alive)
 // ============================================================================================
 __global__ void init_env_kernel(__half* env, int env_cap, int kshard0, int shards, int rows,
-                                int count, uint8_t* alive) {
+                                int count, uint8_t* alive, double* logscale) {
   const size_t plane = static_cast<size_t>(env_cap) * kshard0;
   const size_t total = static_cast<size_t>(shards) * 4 * plane;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
@@ -714,13 +737,15 @@ __global__ void init_env_kernel(__half* env, int env_cap, int kshard0, int shard
     const size_t n = rem / kshard0, c = rem - n * kshard0;
     env[i] = __float2half_rn((p == 0 && c == 0 && n < static_cast<size_t>(count)) ? 1.0f : 0.0f);
   }
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < rows; n += gridDim.x * blockDim.x)
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < rows; n += gridDim.x * blockDim.x) {
     alive[n] = n < count ? 1 : 0;
+    if (logscale) logscale[n] = 0.0;
+  }
 }
 
 void launch_init_env(__half* env, int env_cap, int kshard0, int shards, int rows, int count,
-                     uint8_t* alive, cudaStream_t s) {
-  init_env_kernel<<<296, 256, 0, s>>>(env, env_cap, kshard0, shards, rows, count, alive);
+                     uint8_t* alive, cudaStream_t s, double* logscale) {
+  init_env_kernel<<<296, 256, 0, s>>>(env, env_cap, kshard0, shards, rows, count, alive, logscale);
 }
 
 __global__ void draws_kernel(uint64_t seed, uint64_t first, uint64_t count, uint64_t site,

@@ -222,6 +222,7 @@ class SampleBatch:
 @dataclass
 class RunStats:
     device_seconds: float = 0.0
+    decay_trace: list = field(default_factory=list)
     contraction_macs: int = 0
     measure_weight_macs: int = 0
     dead_samples: int = 0
@@ -237,7 +238,7 @@ class GpuSampler:
     def __init__(self, mps: MpsState, policy: Optional[PrecisionPolicy] = None, mode: Mode = Mode.AUTO,
                  devices: Optional[Sequence[int]] = None, pass_samples: int = 0,
                  record_site_times: bool = False, tp_size: int = 1, tp_rank: int = 0,
-                 host_stream_slots: int = 0):
+                 host_stream_slots: int = 0, record_decay_trace: bool = False):
         L = _lib.lib()
         mps.validate()
         self.policy = policy or PrecisionPolicy()
@@ -253,7 +254,7 @@ class GpuSampler:
                             (_lib._pd * len(lam))(*[x.ctypes.data_as(_lib._pd) for x in lam]))
         pol = _lib.Policy(int(self.policy.compute), int(self.policy.storage), int(self.policy.scaling))
         opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), int(tp_size), int(tp_rank),
-                           int(host_stream_slots))
+                           int(host_stream_slots), int(record_decay_trace))
         self.tp_size, self.tp_rank = tp_size, tp_rank
         devs, nd = self._devices(devices)
         _check(L.mpsg_create(C.byref(view), C.byref(pol), C.byref(opt), devs, nd, C.byref(self._h)))
@@ -322,6 +323,8 @@ class GpuSampler:
         rows = out if out is not None else np.empty((count, self.num_sites), np.uint8)
         st = _lib.Stats()
         site_s = None
+        trace = np.zeros(self.num_sites, np.float64)
+        st.decay_trace = trace.ctypes.data_as(_lib._pd)
         if stats is not None:
             site_s = np.zeros(self.num_sites, np.float64)
             st.site_seconds = site_s.ctypes.data_as(_lib._pd)
@@ -334,6 +337,7 @@ class GpuSampler:
             stats.total_seconds += st.seconds
             stats.issued_mma_flops += st.issued_mma_flops
             stats.site_seconds = list(np.asarray(stats.site_seconds or np.zeros(self.num_sites)) + site_s)
+            stats.decay_trace = list(trace)
         return rows
 
     def sample_device(self, first: int, count: int, seed: int, rows_dev_ptr: int) -> None:
@@ -413,6 +417,14 @@ def apply_schedule(mps: MpsState, schedule: BondSchedule) -> MpsState:
     return out
 
 
+def decay_probe(mps: MpsState, policy: PrecisionPolicy, sample_count: int, seed: int = 1) -> list:
+    """decay_probe (sampler.cpp:207-216): per-site mean |env| before scaling, on the B200."""
+    stats = RunStats()
+    sample_batch(mps, BatchPlan.simple(sample_count),
+                 SamplerOptions(policy=policy, seed=seed, record_decay_trace=True), stats)
+    return stats.decay_trace
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(_lib.lib().mpsg_nccl_unique_id(buf))
@@ -455,7 +467,7 @@ def sample_batch(mps: MpsState, plan: BatchPlan, opts: SamplerOptions,
         raise ConfigError("site transforms are not supported by the GPU sweep (out of scope)")
     t0 = time.perf_counter()
     smp = GpuSampler(mps, opts.policy, opts.mode, devices, opts.pass_samples,
-                     record_site_times=stats is not None)
+                     record_site_times=stats is not None, record_decay_trace=opts.record_decay_trace)
     try:
         st = stats if stats is not None else RunStats()
         rows = smp.sample(0, plan.total_samples, opts.seed, stats=st)

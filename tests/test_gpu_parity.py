@@ -363,3 +363,19 @@ def test_edge_phys_dim_one_and_huge_index(pkg):
     got = s1.sample(first, 2, 7)
     ref, _ = O.orc_sample_range(decoded_mps(s1, m1), first, 2, 7)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("scaling", [0, 2])
+def test_decay_trace_matches_reference(pkg, gold, scaling):
+    """RunStats.decay_trace / decay_probe (sampler.cpp:149-153, 207-216): mean |env| per site before
+    scaling, in the reference's own scaling, vs the compiled reference on the same (decoded) chains."""
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not available")
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode(scaling))
+    for name, prefix in (("c1b", ""), ("decay", "decay_")):
+        mps = O.load_npz_mps(np.load(f"{gold}/{name}.npz"), prefix)
+        smp = pkg.GpuSampler(to_state(pkg, mps), pol)
+        dec = decoded_mps(smp, mps)
+        want = O.RefState(dec).decay_probe(500, seed=1, scaling=scaling)
+        got = np.array(pkg.decay_probe(to_state(pkg, dec), pol, 500, seed=1))
+        np.testing.assert_allclose(got, want, rtol=2e-5, atol=0)
