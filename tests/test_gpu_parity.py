@@ -379,3 +379,16 @@ def test_decay_trace_matches_reference(pkg, gold, scaling):
         want = O.RefState(dec).decay_probe(500, seed=1, scaling=scaling)
         got = np.array(pkg.decay_probe(to_state(pkg, dec), pol, 500, seed=1))
         np.testing.assert_allclose(got, want, rtol=2e-5, atol=0)
+
+
+def test_multi_device_handle_threads(pkg, gold):
+    """mpsg_create with several devices (one host thread + stream + replica each) splits the range
+    contiguously; listing device 0 twice exercises that path on a single-GPU box."""
+    z = np.load(f"{gold}/c1b.npz")
+    st = to_state(pkg, O.load_npz_mps(z))
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    one = pkg.GpuSampler(st, pol).sample(0, 1000, 7)
+    two = pkg.GpuSampler(st, pol, devices=[0, 0], pass_samples=256).sample(0, 1000, 7)
+    assert np.array_equal(one, two)
+    res = pkg.sample_batch(st, pkg.BatchPlan(1000), pkg.SamplerOptions(policy=pol, seed=7), devices=[0, 0])
+    assert np.array_equal(res.outcomes, one)
