@@ -316,7 +316,8 @@ struct PairCfg {
   static constexpr int kBTile = (kBN / 2) * kBK * 2;   // 4 KiB: this CTA's 64 of the 128 B rows
   static constexpr int kStageBytes = kAPlanes * kATile + 2 * kBTile;
   static constexpr int kStages = kSplit ? 5 : 8;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kCinfoBytes = 2 * kBN * 8;  // double-buffered column info of the tile
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256 + kCinfoBytes;
 };
 
 int gemm_pair_smem_bytes(bool split) { return split ? PairCfg<true>::kSmem : PairCfg<false>::kSmem; }
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float2* s_cinfo = reinterpret_cast<float2*>(smem + C::kStages * C::kStageBytes + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -465,18 +467,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
+    const int et = threadIdx.x - 128;  // epilogue thread 0..127
     for (int u = cluster; u < units; u += num_clusters) {
       int m, n;
       unit_coords_pair(u, a, m, n);
+      const int col0 = n * kBN;
+      // stage this tile's (cs, wl) column info in shared memory before the accumulator is ready
+      float2* ci = s_cinfo + acc * kBN;
+      ci[et] = a.cinfo[col0 + et];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       const int row = m * 2 * kBM + rank * kBM + q * 32 + lane;
-      const int col0 = n * kBN;
       const int k = col0 / a.chirp;
       if (k < a.d) {
         const int r0 = col0 - k * a.chirp;
         float2* dst = a.temp + (static_cast<size_t>(row) * a.d + k) * a.chirp + r0;
-        const float2* ci = a.cinfo + col0;
         const uint32_t tb = tmem_base + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
         float w = 0.f, mx = 0.f;
 #pragma unroll 1
