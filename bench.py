@@ -176,6 +176,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--pass", dest="pass_samples", type=int, default=0)
     ap.add_argument("--mode", default="split", choices=["split", "single"])
+    ap.add_argument("--scheme", default="auto", choices=["auto", "3m", "4m"],
+                    help="complex decomposition of the contraction (auto = 3M when the state fits)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -208,7 +210,9 @@ def main():
     t0 = time.perf_counter()
     smp, _ = build_synthetic(cfg["M"], cfg["chi"], cfg["d"], seed=42, mode=mode, devices=[local],
                              pass_samples=P_pass, record_site_times=2, host_stream_slots=args.stream_slots,
-                             policy=P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX))
+                             policy=P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX),
+                             scheme={"auto": 0, "3m": 3, "4m": 4}[args.scheme])
+    scheme = "3M" if smp.scheme == P.Scheme.M3 else "4M"
     build_s = time.perf_counter() - t0
     macs_per_sample, bonds = chain_macs(cfg["M"], cfg["chi"], cfg["d"])
     rows_dev = torch.empty((P_pass, cfg["M"]), dtype=torch.uint8, device="cuda")
@@ -299,7 +303,7 @@ def main():
             "config": {"workload": cfg["desc"] + f"; step = one sweep of {P_pass} samples/GPU over all M sites",
                        "M": cfg["M"], "chi": cfg["chi"], "d": cfg["d"], "pass_samples_per_gpu": P_pass,
                        "job_samples": cfg["job"], "job_seconds_at_value": cfg["job"] / value,
-                       "mode": args.mode, "parallelism": f"dp{world}",
+                       "mode": args.mode, "scheme": scheme, "parallelism": f"dp{world}",
                        "l2": f"inputs larger than L2 (compressed MPS {smp.state_bytes / 1e9:.1f} GB)",
                        "gamma_residency": (f"pinned host memory, streamed per site through {args.stream_slots} "
                                            f"device slots ({h2d / args.steps / 1e9:.1f} GB H2D per step, "
@@ -308,8 +312,10 @@ def main():
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
                          "frac": achieved / sustained if achieved else None, "traffic": traffic,
                          "peak_kind": f"bf16 dense sustained ({src})",
-                         "kernel": "site_gemm_kernel (tcgen05, all sites of the sweep)",
-                         "flops_per_unit": "8*chiL*chiR*d per sample per site (4M, = 8 x contraction_macs)",
+                         "kernel": ("site_gemm_3m_kernel" if scheme == "3M" else "site_gemm_pair_kernel")
+                                   + " (tcgen05, all sites of the sweep)",
+                         "flops_per_unit": "8*chiL*chiR*d per sample per site (the 4M count, = 8 x "
+                                           "contraction_macs; 3M issues 6/8 of it per precision pass)",
                          "issued_tflops": issued / gemm_s / 1e12 if gemm_s > 0 else None,
                          "issued_frac": issued / gemm_s / 1e12 / sustained if gemm_s > 0 else None,
                          "frac_of_burst": achieved / burst if achieved else None,

@@ -59,6 +59,11 @@ enum { MPSG_SCALE_NONE = 0, MPSG_SCALE_GLOBAL_MAX = 1, MPSG_SCALE_PER_SAMPLE_MAX
  *                     Used for compute = TF32 / F16.
  *   MPSG_MODE_AUTO    pick from policy.compute. */
 enum { MPSG_MODE_AUTO = 0, MPSG_MODE_SPLIT = 1, MPSG_MODE_SINGLE = 2 };
+/* Complex decomposition of the contraction:
+ *   MPSG_SCHEME_3M  Gauss: 3 real products (Gamma planes Gr, Gi, Gr+Gi: 6 bytes per complex entry)
+ *   MPSG_SCHEME_4M  4 real products (Gamma planes Gr, Gi: 4 bytes per complex entry)
+ *   MPSG_SCHEME_AUTO  3M when Gamma is resident and the 3-plane state fits in device memory. */
+enum { MPSG_SCHEME_AUTO = 0, MPSG_SCHEME_3M = 3, MPSG_SCHEME_4M = 4 };
 
 #define MPSG_DEAD 0xFF
 
@@ -96,7 +101,9 @@ typedef struct mpsg_options {
   int record_decay_trace;          /* fill mpsg_stats.decay_trace: mean |env| per site before
                                       scaling, in the reference's own scaling (sampler.cpp:149-153,
                                       decay_probe :207-216); GlobalMax is traced as None */
-  int reserved;
+  int scheme;                      /* complex decomposition of the contraction: MPSG_SCHEME_AUTO (3M
+                                      when the 3-plane state fits in HBM and Gamma is resident,
+                                      else 4M), MPSG_SCHEME_3M or MPSG_SCHEME_4M */
 } mpsg_options;
 
 /* Mirrors mpsamp::RunStats + FlopCounters (sampler.hpp:46-54, contract.hpp:12-25). */
@@ -146,6 +153,8 @@ void mpsg_destroy(mpsg_handle h);
 
 /* Device bytes held for the compressed state on one device (algorithmic Gamma bytes). */
 uint64_t mpsg_state_bytes(mpsg_handle h);
+/* The contraction scheme the handle runs: MPSG_SCHEME_3M or MPSG_SCHEME_4M (0 for a null handle). */
+int mpsg_scheme(mpsg_handle h);
 
 /* The Gamma values the GPU actually samples (decoded compressed format), reference layout:
  * complex128 interleaved (chiL, chiR, d).  The CPU oracle consumes these.  A tensor-parallel

@@ -27,6 +27,7 @@ from .sampler import (  # noqa: F401
     SampleBatch,
     SamplerOptions,
     ScalingMode,
+    Scheme,
     capped_bond_dims,
     decay_probe,
     device_draws,

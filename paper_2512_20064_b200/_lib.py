@@ -29,7 +29,7 @@ class Policy(C.Structure):
 class Options(C.Structure):
     _fields_ = [("mode", _int), ("pass_samples", _u64), ("record_site_times", _int),
                 ("tp_size", _int), ("tp_rank", _int), ("host_stream_slots", _int),
-                ("record_decay_trace", _int), ("reserved", _int)]
+                ("record_decay_trace", _int), ("scheme", _int)]
 
 
 class Stats(C.Structure):
@@ -53,6 +53,7 @@ SIGNATURES = [
     ("mpsg_builder_finish", _int, [C.c_void_p]),
     ("mpsg_destroy", None, [C.c_void_p]),
     ("mpsg_state_bytes", _u64, [C.c_void_p]),
+    ("mpsg_scheme", _int, [C.c_void_p]),
     ("mpsg_decoded_gamma", _int, [C.c_void_p, _u64, _pd]),
     ("mpsg_sample", _int, [C.c_void_p, _u64, _u64, _u64, _pu8, C.POINTER(Stats)]),
     ("mpsg_sample_device", _int, [C.c_void_p, _u64, _u64, _u64, C.c_void_p, C.POINTER(Stats)]),

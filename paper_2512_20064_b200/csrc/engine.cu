@@ -78,32 +78,36 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// fp16 matrix [rows][cols] (cols contiguous), box 32 cols x box_rows rows, 64 B swizzle.
+// fp16 matrix [rows][cols] (cols contiguous), box box_k cols x box_rows rows; 64-wide boxes use
+// the 128 B swizzle, 32-wide ones the 64 B swizzle.
 static CUtensorMap make_tma_2d(const void* base, uint64_t cols, uint64_t rows,
-                               uint32_t box_rows = kBM) {
+                               uint32_t box_rows = kBM, uint32_t box_k = kBK) {
   CUtensorMap m;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), box_rows};
+  cuuint32_t box[2] = {box_k, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           box_k == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(MPSG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return m;
 }
 
-// Shard-major env [shards][4 planes * cap rows][kshard]: box 32 k x 128 rows x 1 shard.
-static CUtensorMap make_tma_env(const void* base, uint64_t kshard, uint64_t rows, uint64_t shards) {
+// Shard-major env [shards][planes * cap rows][kshard]: box 32 k x box_rows rows x 1 shard.
+static CUtensorMap make_tma_env(const void* base, uint64_t kshard, uint64_t rows, uint64_t shards,
+                                uint32_t box_rows = kBM, uint32_t box_k = kBK) {
   CUtensorMap m;
   cuuint64_t dims[3] = {kshard, rows, shards};
   cuuint64_t strides[2] = {kshard * 2, rows * kshard * 2};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(kBM), 1};
+  cuuint32_t box[3] = {box_k, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           box_k == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(MPSG_ERR_CUDA, "cuTensorMapEncodeTiled (3d) failed");
   return m;
@@ -248,7 +252,7 @@ struct SiteDev {
   int chil = 0, chir = 0, kp = 0, chirp = 0, np = 0, nt = 0;
   int b0 = 0, width = 0;     // this rank's column shard [b0, b0 + width) of chiR
   int kshard = 0;            // env K extent per shard (kp = shards * kshard)
-  __half* g = nullptr;       // [2][np][kp]
+  __half* g = nullptr;       // [gplanes][np][kp]
   float2* cinfo = nullptr;   // [np]
   double* cs = nullptr;      // [chir * d]
   double* inv_gamma = nullptr;  // [width] 1 / gamma_i[r] of the local columns (decay trace)
@@ -265,7 +269,7 @@ struct SiteDev {
 struct Lane {
   cudaStream_t stream = nullptr;  // lane 0 uses DevCtx::stream
   int cap = 0;                    // rows, multiple of 256
-  __half* env = nullptr;          // [shards][4][cap][kshard_max]
+  __half* env = nullptr;          // [shards][2 * env_comp][cap][kshard_max]
   float2* temp = nullptr;         // [cap][d][chirp_max]
   float2* pstat = nullptr;        // [cap][nt_max]
   float2* part = nullptr;         // [tp][cap][d] exchanged (weight, max) partials (TP only)
@@ -275,7 +279,8 @@ struct Lane {
   double* marg = nullptr;         // [cap][M][d] (lazy)
   double* logscale = nullptr;     // [cap] (lazy, decay trace)
   uint8_t* host_rows = nullptr;   // pinned [cap][M]
-  std::vector<CUtensorMap> tma_env;  // per site: the shard-major env map over this lane's env
+  std::vector<CUtensorMap> tma_env;    // per site: the shard-major env map over this lane's env
+  std::vector<CUtensorMap> tma_env64;  // same with a 64-row box (3M kernel: env is the B operand)
   cudaEvent_t k1done = nullptr, done = nullptr;
   std::vector<cudaEvent_t> gev;   // per-site GEMM start/stop (2 M)
 };
@@ -319,6 +324,8 @@ struct mpsg_handle_s {
   bool finished = false;
   int tp = 1, tp_rank = 0;                 // tensor-parallel group (column-sharded Gamma)
   bool pair = true;                        // K1 variant: CTA-pair UMMA (M=256) vs A-multicast pairs
+  bool m3 = false;                         // 3M contraction (Gamma planes Gr, Gi, Gs; env re, im, s)
+  int gplanes = 2, env_comp = 2;
   std::unique_ptr<mpsg::Comm> comm;
   std::mutex mu;
 };
@@ -330,7 +337,7 @@ namespace mpsg {
 constexpr int kGroupPairs = 16;
 
 static int kshard_of(const mpsg_handle_s& h, uint64_t bond) {
-  return round_up((static_cast<int>(bond) + h.tp - 1) / h.tp, kBK);
+  return round_up((static_cast<int>(bond) + h.tp - 1) / h.tp, h.m3 ? kBK3 : kBK);
 }
 static int kshard_max_of(const mpsg_handle_s& h) {
   int k = kBK;
@@ -344,6 +351,30 @@ static int chirp_max_of(const mpsg_handle_s& h) {
   int c = kBN;
   for (uint64_t i = 1; i <= h.M; ++i) c = std::max(c, chirp_of(h, h.bonds[i]));
   return c;
+}
+
+// 3M unless asked otherwise, Gamma is host-streamed (the stream would carry 1.5x the bytes), the
+// A-multicast 4M variant was selected, or the 3-plane state does not fit next to the pass buffers.
+static void choose_scheme(mpsg_handle_s& h) {
+  bool m3 = h.opts.scheme != MPSG_SCHEME_4M;
+  if (h.opts.scheme == MPSG_SCHEME_AUTO) {
+    if (h.opts.host_stream_slots != 0 || !h.pair) m3 = false;
+    double state3 = 0.0;
+    for (uint64_t i = 0; i < h.M; ++i) {
+      const double kp = static_cast<double>(h.tp) * kshard_of(h, h.bonds[i]);
+      const double np = round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN);
+      state3 += 3.0 * 2.0 * np * kp;
+    }
+    for (auto& dc : h.devs) {
+      size_t free_b = 0, total_b = 0;
+      CUDA_OK(cudaSetDevice(dc.device));
+      CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+      if (state3 + 10.0e9 > static_cast<double>(free_b)) m3 = false;  // pass buffers + headroom
+    }
+  }
+  h.m3 = m3;
+  h.gplanes = m3 ? 3 : 2;
+  h.env_comp = m3 ? 3 : 2;
 }
 
 static void validate_shape(uint64_t m, uint64_t d, const uint64_t* bonds) {
@@ -386,7 +417,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
   CUDA_OK(cudaStreamCreateWithFlags(&dc.stream, cudaStreamNonBlocking));
   const int kmax = h.tp * kshard_max_of(h), chirpm = chirp_max_of(h);
   const size_t nt_max = h.d * (chirpm / kBN) + 1;  // + the pair-padding tile
-  const size_t row_bytes = 8ull * kmax + 8ull * h.d * chirpm + 8ull * nt_max + 1 + h.M +
+  const size_t row_bytes = 4ull * h.env_comp * kmax + 8ull * h.d * chirpm + 8ull * nt_max + 1 + h.M +
                            (h.tp > 1 ? 8ull * h.tp * h.d : 0);
   uint64_t want = h.opts.pass_samples;
   if (want == 0) {
@@ -410,7 +441,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
       ln.stream = dc.stream;
     else
       CUDA_OK(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking));
-    CUDA_OK(cudaMalloc(&ln.env, 4ull * ln.cap * kmax * sizeof(__half)));
+    CUDA_OK(cudaMalloc(&ln.env, 2ull * h.env_comp * ln.cap * kmax * sizeof(__half)));
     CUDA_OK(cudaMalloc(&ln.temp, 1ull * ln.cap * h.d * chirpm * sizeof(float2)));
     CUDA_OK(cudaMalloc(&ln.pstat, 1ull * ln.cap * nt_max * sizeof(float2)));
     if (h.tp > 1) CUDA_OK(cudaMalloc(&ln.part, 1ull * h.tp * ln.cap * h.d * sizeof(float2)));
@@ -420,6 +451,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     CUDA_OK(cudaEventCreateWithFlags(&ln.k1done, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
     ln.tma_env.resize(h.M);
+    ln.tma_env64.resize(h.M);
   }
   CUDA_OK(cudaMalloc(&dc.err, sizeof(int)));
   CUDA_OK(cudaMemset(dc.err, 0, sizeof(int)));
@@ -431,7 +463,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     for (uint64_t i = 0; i < h.M; ++i) {
       const size_t kp = static_cast<size_t>(h.tp) * kshard_of(h, h.bonds[i]);
       const size_t np = round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN);
-      gmax = std::max(gmax, static_cast<size_t>(kGPlanes) * np * kp);
+      gmax = std::max(gmax, static_cast<size_t>(h.gplanes) * np * kp);
       nmax = std::max(nmax, np);
     }
     CUDA_OK(cudaStreamCreateWithFlags(&dc.copy_stream, cudaStreamNonBlocking));
@@ -517,7 +549,7 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
     s.g = dc.slot_g[0];
     s.cinfo = dc.slot_cinfo[0];
   } else if (!s.g) {
-    CUDA_OK(cudaMalloc(&s.g, static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half)));
+    CUDA_OK(cudaMalloc(&s.g, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half)));
     CUDA_OK(cudaMalloc(&s.cinfo, 1ull * s.np * sizeof(float2)));
   }
   std::vector<double> wl(s.chir);
@@ -540,7 +572,7 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
   CUDA_OK(cudaMemcpyAsync(d_gr, h.gr[i].data(), sizeof(double) * s.chir, cudaMemcpyHostToDevice, dc.stream));
   CUDA_OK(cudaMemcpyAsync(d_wl, wl.data(), sizeof(double) * s.chir, cudaMemcpyHostToDevice, dc.stream));
   CUDA_OK(cudaMemcpyAsync(d_lpos, lpos.data(), sizeof(int) * s.chil, cudaMemcpyHostToDevice, dc.stream));
-  CUDA_OK(cudaMemsetAsync(s.g, 0, static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half), dc.stream));
+  CUDA_OK(cudaMemsetAsync(s.g, 0, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half), dc.stream));
   CUDA_OK(cudaMemsetAsync(s.cinfo, 0, 1ull * s.np * sizeof(float2), dc.stream));
   if (!s.inv_gamma) CUDA_OK(cudaMalloc(&s.inv_gamma, std::max<size_t>(1, s.width) * sizeof(double)));
   {
@@ -549,7 +581,7 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
     CUDA_OK(cudaMemcpyAsync(s.inv_gamma, ig.data(), sizeof(double) * ig.size(), cudaMemcpyHostToDevice, dc.stream));
   }
   launch_compress_site(src_dev, f64, s.chil, s.chir, static_cast<int>(h.d), s.b0, s.width, s.kp,
-                       s.chirp, d_lpos, d_gl, d_gr, d_wl, s.g, s.cinfo, s.cs, dc.err, dc.stream);
+                       s.chirp, d_lpos, d_gl, d_gr, d_wl, h.gplanes, s.g, s.cinfo, s.cs, dc.err, dc.stream);
   CUDA_OK(cudaGetLastError());
   int err = 0;
   CUDA_OK(cudaMemcpyAsync(&err, dc.err, sizeof(int), cudaMemcpyDeviceToHost, dc.stream));
@@ -559,27 +591,32 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
     throw Error(MPSG_ERR_NUMERIC, "contract_site: non-finite input (site " + std::to_string(i) +
                                       ") or dynamic range beyond the compressed format");
   }
-  for (auto& ln : dc.lanes) ln.tma_env[i] = make_tma_env(ln.env, s.kshard, 4ull * ln.cap, h.tp);
+  for (auto& ln : dc.lanes) {
+    const uint64_t env_rows = 2ull * h.env_comp * ln.cap;
+    ln.tma_env[i] = make_tma_env(ln.env, s.kshard, env_rows, h.tp);
+    if (h.m3) ln.tma_env64[i] = make_tma_env(ln.env, s.kshard, env_rows, h.tp, kBM / 2, kBK3);
+  }
   if (dc.slots) {
     if (!s.g_host) {
-      CUDA_OK(cudaMallocHost(&s.g_host, static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half)));
+      CUDA_OK(cudaMallocHost(&s.g_host, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half)));
       CUDA_OK(cudaMallocHost(&s.cinfo_host, 1ull * s.np * sizeof(float2)));
     }
-    CUDA_OK(cudaMemcpyAsync(s.g_host, s.g, static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half), cudaMemcpyDeviceToHost, dc.stream));
+    CUDA_OK(cudaMemcpyAsync(s.g_host, s.g, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half), cudaMemcpyDeviceToHost, dc.stream));
     CUDA_OK(cudaMemcpyAsync(s.cinfo_host, s.cinfo, 1ull * s.np * sizeof(float2), cudaMemcpyDeviceToHost, dc.stream));
     CUDA_OK(cudaStreamSynchronize(dc.stream));
     s.tma_slot.resize(dc.slots);
     s.tma_slot64.resize(dc.slots);
     for (int q = 0; q < dc.slots; ++q) {
-      s.tma_slot[q] = make_tma_2d(dc.slot_g[q], s.kp, static_cast<uint64_t>(kGPlanes) * s.np);
-      s.tma_slot64[q] = make_tma_2d(dc.slot_g[q], s.kp, static_cast<uint64_t>(kGPlanes) * s.np, kBN / 2);
+      s.tma_slot[q] = make_tma_2d(dc.slot_g[q], s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBM,
+                                  h.m3 ? kBK3 : kBK);
+      s.tma_slot64[q] = make_tma_2d(dc.slot_g[q], s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBN / 2);
     }
     s.g = nullptr;
     s.cinfo = nullptr;
     dc.issued = dc.consumed = 0;  // slot 0 was overwritten: restart the load sequence
   } else {
-    s.tma_g = make_tma_2d(s.g, s.kp, static_cast<uint64_t>(kGPlanes) * s.np);
-    s.tma_g64 = make_tma_2d(s.g, s.kp, static_cast<uint64_t>(kGPlanes) * s.np, kBN / 2);
+    s.tma_g = make_tma_2d(s.g, s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBM, h.m3 ? kBK3 : kBK);
+    s.tma_g64 = make_tma_2d(s.g, s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBN / 2);
   }
 }
 
@@ -590,7 +627,7 @@ static void issue_loads(mpsg_handle_s& h, DevCtx& dc, uint64_t upto) {
     const int slot = static_cast<int>(q % dc.slots);
     const SiteDev& s = dc.sites[q % h.M];
     CUDA_OK(cudaStreamWaitEvent(dc.copy_stream, dc.freed[slot], 0));  // consume q - slots done
-    const size_t gb = static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half);
+    const size_t gb = static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half);
     CUDA_OK(cudaMemcpyAsync(dc.slot_g[slot], s.g_host, gb, cudaMemcpyHostToDevice, dc.copy_stream));
     CUDA_OK(cudaMemcpyAsync(dc.slot_cinfo[slot], s.cinfo_host, 1ull * s.np * sizeof(float2),
                             cudaMemcpyHostToDevice, dc.copy_stream));
@@ -649,12 +686,66 @@ struct PassOut {
   double gemm_s = 0.0, device_s = 0.0;
 };
 
+// K1 for `rows` samples of lane `ln` at site i.  tma_g128 / tma_g64: Gamma maps with 128 / 64-row
+// boxes (the 3M kernel loads Gamma as its A operand; the 4M pair kernel as its half-B operand).
+static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const SiteDev& s, const Lane& ln,
+                               uint64_t i, int rows, const CUtensorMap* tma_g128,
+                               const CUtensorMap& tma_g64, const float2* cinfo, cudaStream_t stream) {
+  if (h.m3) {
+    Gemm3MArgs ga;
+    ga.g_tiles = s.np / (2 * kBN);
+    ga.s_tiles = rows / kBM;
+    ga.k_blocks = s.kp / kBK3;
+    ga.kshard_blocks = s.kshard / kBK3;
+    ga.env_cap = ln.cap;
+    ga.np = s.np;
+    ga.chirp = s.chirp;
+    ga.d = static_cast<int>(h.d);
+    ga.nt = s.nt;
+    static const int env_group = [] {
+      const char* v = std::getenv("MPSG_3M_GROUP");
+      return v ? std::max(1, std::atoi(v)) : kGroupPairs;
+    }();
+    static const int env_flags = [] {
+      const char* v = std::getenv("MPSG_3M_FLAGS");
+      return v ? std::atoi(v) : 0;
+    }();
+    ga.group = std::min(ga.g_tiles, env_group);
+    ga.flags = env_flags;
+    ga.cinfo = cinfo;
+    ga.temp = ln.temp;
+    ga.pstat = ln.pstat;
+    const int ctas = 2 * ga.g_tiles * ga.s_tiles;
+    launch_site_gemm_3m(h.split, ln.tma_env64[i], *tma_g128, ga, std::min(ctas, dc.num_sms), stream);
+    return;
+  }
+  const int mrow = h.pair ? 2 * kBM : kBM;
+  SiteGemmArgs ga;
+  ga.m_tiles = rows / mrow;
+  ga.n_tiles = s.nt;
+  ga.k_blocks = s.kp / kBK;
+  ga.kshard_blocks = s.kshard / kBK;
+  ga.plane_rows_a = ln.cap;
+  ga.np = s.np;
+  ga.chirp = s.chirp;
+  ga.d = static_cast<int>(h.d);
+  ga.group_n = h.pair ? std::min(s.nt, 2 * kGroupPairs) : std::min(s.nt / 2, kGroupPairs);
+  ga.cinfo = cinfo;
+  ga.temp = ln.temp;
+  ga.pstat = ln.pstat;
+  const int ctas = h.pair ? 2 * ga.m_tiles * ga.n_tiles : ga.m_tiles * ga.n_tiles;
+  if (h.pair)
+    launch_site_gemm_pair(h.split, ln.tma_env[i], tma_g64, ga, std::min(ctas, dc.num_sms), stream);
+  else
+    launch_site_gemm(h.split, ln.tma_env[i], *tma_g128, ga, std::min(ctas, dc.num_sms), stream);
+}
+
 // Enqueues one pass of `count` (<= dc.cap) samples starting at global index `first`, split over
 // the lanes.  Lane L covers [first + off[L], first + off[L] + cnt[L]).
 static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first, int count,
                      bool forced, bool marg, PassOut& po, int timing, int off[2], int cnt[2]) {
   const int nl = static_cast<int>(dc.lanes.size());
-  const int mrow = h.pair ? 2 * kBM : kBM;
+  const int mrow = (h.pair && !h.m3) ? 2 * kBM : kBM;
   off[0] = 0;
   cnt[0] = count;
   cnt[1] = 0;
@@ -669,21 +760,23 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
     Lane& ln = dc.lanes[L];
     rows[L] = round_up(cnt[L], mrow);
     if (L > 0 && timing) CUDA_OK(cudaStreamWaitEvent(ln.stream, dc.ev[0], 0));  // after the pass-start stamp
-    launch_init_env(ln.env, ln.cap, dc.sites[0].kshard, h.tp, rows[L], cnt[L], ln.alive, ln.stream,
-                    dc.trace ? ln.logscale : nullptr);
+    launch_init_env(ln.env, h.env_comp, ln.cap, dc.sites[0].kshard, h.tp, rows[L], cnt[L], ln.alive,
+                    ln.stream, dc.trace ? ln.logscale : nullptr);
     po.launches += 1;
   }
   if (dc.slots) issue_loads(h, dc, dc.consumed + dc.slots);
   for (uint64_t i = 0; i < h.M; ++i) {
     const SiteDev& s = dc.sites[i];
-    const CUtensorMap* tma_g = h.pair ? &s.tma_g64 : &s.tma_g;
+    const CUtensorMap* tma_g128 = &s.tma_g;
+    const CUtensorMap* tma_g64 = &s.tma_g64;
     const float2* cinfo = s.cinfo;
     int slot = -1;
     if (dc.slots) {  // single lane in host-streamed mode
       if (dc.consumed % h.M != i) throw Error(MPSG_ERR_INTERNAL, "site stream out of sequence");
       slot = static_cast<int>(dc.consumed % dc.slots);
       CUDA_OK(cudaStreamWaitEvent(dc.stream, dc.loaded[slot], 0));
-      tma_g = h.pair ? &s.tma_slot64[slot] : &s.tma_slot[slot];
+      tma_g128 = &s.tma_slot[slot];
+      tma_g64 = &s.tma_slot64[slot];
       cinfo = dc.slot_cinfo[slot];
     }
     for (int L = 0; L < active; ++L) {
@@ -695,25 +788,8 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
         else if (i > 0)
           CUDA_OK(cudaStreamWaitEvent(ln.stream, dc.lanes[1].k1done, 0));
       }
-      SiteGemmArgs ga;
-      ga.m_tiles = rows[L] / mrow;
-      ga.n_tiles = s.nt;
-      ga.k_blocks = s.kp / kBK;
-      ga.kshard_blocks = s.kshard / kBK;
-      ga.plane_rows_a = ln.cap;
-      ga.np = s.np;
-      ga.chirp = s.chirp;
-      ga.d = static_cast<int>(h.d);
-      ga.group_n = h.pair ? std::min(s.nt, 2 * kGroupPairs) : std::min(s.nt / 2, kGroupPairs);
-      ga.cinfo = cinfo;
-      ga.temp = ln.temp;
-      ga.pstat = ln.pstat;
-      const int ctas = h.pair ? 2 * ga.m_tiles * ga.n_tiles : ga.m_tiles * ga.n_tiles;
       if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[2 * i], ln.stream));
-      if (h.pair)
-        launch_site_gemm_pair(h.split, ln.tma_env[i], *tma_g, ga, std::min(ctas, dc.num_sms), ln.stream);
-      else
-        launch_site_gemm(h.split, ln.tma_env[i], *tma_g, ga, std::min(ctas, dc.num_sms), ln.stream);
+      launch_contraction(h, dc, s, ln, i, rows[L], tma_g128, *tma_g64, cinfo, ln.stream);
       if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[2 * i + 1], ln.stream));
       if (active == 2) CUDA_OK(cudaEventRecord(ln.k1done, ln.stream));
       if (dc.slots) {  // K1 is the only reader of the slot: hand it back to the copy stream
@@ -751,12 +827,13 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       const int kn = has_next ? dc.sites[i + 1].kshard : 0;
       sa.kp_next = kn;
       sa.env_cap = ln.cap;
+      sa.env_comp = h.env_comp;
       sa.seed = seed;
       sa.first = lfirst;
       sa.temp = ln.temp;
       sa.alive = ln.alive;
       sa.rows_out = ln.rows;
-      sa.env_next = ln.env + 4ull * ln.cap * kn * h.tp_rank;
+      sa.env_next = ln.env + 2ull * h.env_comp * ln.cap * kn * h.tp_rank;
       sa.forced = forced ? ln.forced : nullptr;
       sa.marg = marg ? ln.marg : nullptr;
       sa.logscale = dc.trace ? ln.logscale : nullptr;
@@ -765,11 +842,11 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       sa.scaling = h.policy.scaling;
       launch_select(sa, ln.stream);
       if (h.tp > 1 && has_next)  // rebuild the full environment from the column shards
-        h.comm->allgather(ln.env, 4ull * ln.cap * kn * sizeof(__half), ln.stream);
+        h.comm->allgather(ln.env, 2ull * h.env_comp * ln.cap * kn * sizeof(__half), ln.stream);
       po.launches += 2;
       po.macs += static_cast<uint64_t>(cnt[L]) * s.chil * s.width * h.d;
       po.wmacs += static_cast<uint64_t>(cnt[L]) * s.width * h.d;
-      po.issued += 8ull * rows[L] * s.np * s.kp * (h.split ? 2 : 1);
+      po.issued += (h.m3 ? 6ull : 8ull) * rows[L] * s.np * s.kp * (h.split ? 2 : 1);
     }
     if (timing) CUDA_OK(cudaEventRecord(dc.ev[i + 1], dc.stream));
   }
@@ -1039,6 +1116,8 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
     config_check(h->tp == 1 || ndev <= 1, "a tensor-parallel rank drives exactly one device");
     h->split = h->opts.mode == MPSG_MODE_SPLIT ||
                (h->opts.mode == MPSG_MODE_AUTO && (pol.compute == MPSG_F64 || pol.compute == MPSG_F32));
+    config_check(h->opts.scheme == MPSG_SCHEME_AUTO || h->opts.scheme == MPSG_SCHEME_3M ||
+                     h->opts.scheme == MPSG_SCHEME_4M, "unknown contraction scheme");
     h->gl.resize(num_sites);
     h->gr.resize(num_sites);
     for (uint64_t i = 0; i < num_sites; ++i) {
@@ -1055,6 +1134,7 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
       for (int k = 0; k < ndev; ++k) h->devs[k].device = devices[k];
     }
     if (mpsg_device_count() == 0) throw Error(MPSG_ERR_CUDA, "no sm_100 CUDA device visible");
+    choose_scheme(*h);
     try {
       for (auto& dc : h->devs) alloc_device(*h, dc);
     } catch (...) {
@@ -1117,9 +1197,11 @@ void mpsg_destroy(mpsg_handle h) {
 uint64_t mpsg_state_bytes(mpsg_handle h) {
   if (!h || h->devs.empty()) return 0;
   uint64_t b = 0;
-  for (const auto& s : h->devs[0].sites) b += static_cast<size_t>(kGPlanes) * s.np * s.kp * sizeof(__half);
+  for (const auto& s : h->devs[0].sites) b += static_cast<size_t>(h->gplanes) * s.np * s.kp * sizeof(__half);
   return b;  // host-streamed: these bytes live in pinned host memory
 }
+
+int mpsg_scheme(mpsg_handle h) { return h ? (h->m3 ? MPSG_SCHEME_3M : MPSG_SCHEME_4M) : 0; }
 
 int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
   return guarded([&] {
@@ -1128,7 +1210,7 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
     DevCtx& dc = h->devs[0];
     CUDA_OK(cudaSetDevice(dc.device));
     const SiteDev& s = dc.sites[site];
-    std::vector<__half> g(static_cast<size_t>(kGPlanes) * s.np * s.kp);
+    std::vector<__half> g(static_cast<size_t>(h->gplanes) * s.np * s.kp);
     std::vector<double> cs(std::max<size_t>(1, 1ull * s.width * h->d));
     if (dc.slots)
       std::memcpy(g.data(), s.g_host, g.size() * sizeof(__half));
@@ -1251,11 +1333,13 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
     std::lock_guard<std::mutex> lk(h->mu);
     const SiteDev& s = dc.sites[site];
     const int n = static_cast<int>(count);
-    const int rows = round_up(n, h->pair ? 2 * kBM : kBM);
-    // host: internal env E = env * gl * sigma_n (sigma_n power of two), hi/lo fp16 planes
+    const int rows = round_up(n, (h->pair && !h->m3) ? 2 * kBM : kBM);
+    // host: internal env E = env * gl * sigma_n (sigma_n power of two), hi/lo fp16 planes per
+    // component (re, im and, for 3M, re + im rounded once in fp32)
     Lane& ln = dc.lanes[0];
     const size_t plane = 1ull * ln.cap * s.kp;
-    std::vector<__half> e(4 * plane, __float2half_rn(0.f));
+    const int C = h->env_comp;
+    std::vector<__half> e(2ull * C * plane, __float2half_rn(0.f));
     std::vector<double> sig(n, 1.0);
     for (int r = 0; r < n; ++r) {
       double mx = 0.0;
@@ -1268,35 +1352,20 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
       sig[r] = std::ldexp(1.0, -ex);
       for (int l = 0; l < s.chil; ++l) {
         const double* v = env + 2 * (static_cast<size_t>(r) * s.chil + l);
-        const float fr = static_cast<float>(v[0] * h->gl[site][l] * sig[r]);
-        const float fi = static_cast<float>(v[1] * h->gl[site][l] * sig[r]);
-        const __half hr = __float2half_rn(fr), hi = __float2half_rn(fi);
+        float comp[3];
+        comp[0] = static_cast<float>(v[0] * h->gl[site][l] * sig[r]);
+        comp[1] = static_cast<float>(v[1] * h->gl[site][l] * sig[r]);
+        comp[2] = comp[0] + comp[1];
         const size_t o = static_cast<size_t>(r) * s.kp + l;
-        e[o] = hr;
-        e[plane + o] = hi;
-        e[2 * plane + o] = __float2half_rn(fr - __half2float(hr));
-        e[3 * plane + o] = __float2half_rn(fi - __half2float(hi));
+        for (int c = 0; c < C; ++c) {
+          const __half hv = __float2half_rn(comp[c]);
+          e[c * plane + o] = hv;
+          e[(C + c) * plane + o] = __float2half_rn(comp[c] - __half2float(hv));
+        }
       }
     }
     CUDA_OK(cudaMemcpy(ln.env, e.data(), e.size() * sizeof(__half), cudaMemcpyHostToDevice));
-    SiteGemmArgs ga;
-    ga.m_tiles = rows / (h->pair ? 2 * kBM : kBM);
-    ga.n_tiles = s.nt;
-    ga.k_blocks = s.kp / kBK;
-    ga.kshard_blocks = s.kshard / kBK;
-    ga.plane_rows_a = ln.cap;
-    ga.np = s.np;
-    ga.chirp = s.chirp;
-    ga.d = static_cast<int>(h->d);
-    ga.group_n = h->pair ? std::min(s.nt, 2 * kGroupPairs) : std::min(s.nt / 2, kGroupPairs);
-    ga.cinfo = s.cinfo;
-    ga.temp = ln.temp;
-    ga.pstat = ln.pstat;
-    const int ctas = h->pair ? 2 * ga.m_tiles * ga.n_tiles : ga.m_tiles * ga.n_tiles;
-    if (h->pair)
-      launch_site_gemm_pair(h->split, ln.tma_env[site], s.tma_g64, ga, std::min(ctas, dc.num_sms), dc.stream);
-    else
-      launch_site_gemm(h->split, ln.tma_env[site], s.tma_g, ga, std::min(ctas, dc.num_sms), dc.stream);
+    launch_contraction(*h, dc, s, ln, site, rows, &s.tma_g, s.tma_g64, s.cinfo, dc.stream);
     CUDA_OK(cudaGetLastError());
     std::vector<float2> t(1ull * n * h->d * s.chirp);
     CUDA_OK(cudaMemcpyAsync(t.data(), ln.temp, t.size() * sizeof(float2), cudaMemcpyDeviceToHost,

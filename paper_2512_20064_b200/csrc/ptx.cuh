@@ -129,6 +129,39 @@ MPSG_UMMA_PAIR(umma_pair, "")
 MPSG_UMMA_PAIR(umma_pair_afill, ".collector::a::fill")
 MPSG_UMMA_PAIR(umma_pair_alast, ".collector::a::lastuse")
 #undef MPSG_UMMA_PAIR
+// Warp-collective forms: the whole (converged) warp executes them with warp-uniform operands and
+// one elected lane issues, so the operands stay in uniform registers (no per-MMA R2UR waterfall).
+__device__ __forceinline__ void umma_pair_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                uint32_t idesc, uint32_t accumulate, bool afill,
+                                                bool alast) {
+  if (afill) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else if (alast) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void umma_commit_pair_mc_elect(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 // Arrive on the barrier at `bar`'s offset in both CTAs of the pair once the pair's MMAs retire.
 __device__ __forceinline__ void umma_commit_pair_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
@@ -142,6 +175,14 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// Same with relaxed semantics: no ordering of prior global / shared memory operations (the caller
+// orders its TMEM reads with tcgen05.wait::ld + tcgen05.fence::before_thread_sync), so no
+// GPU-scope memory barrier is emitted in front of the arrive.
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -216,6 +257,18 @@ __device__ __forceinline__ uint64_t sdesc_kmajor_sw64(uint32_t saddr) {
   d |= static_cast<uint64_t>(512u >> 4) << 32;         // [32,46) SBO = 512 B
   d |= static_cast<uint64_t>(1u) << 46;                // [46,48) descriptor version (sm100)
   d |= static_cast<uint64_t>(4u) << 61;                // [61,64) layout: SWIZZLE_64B
+  return d;
+}
+
+// Same for the SWIZZLE_128B canonical layout: rows of 128 bytes (64 fp16 along K), 8-row core
+// groups 1024 bytes apart; a K16 step inside the swizzle atom advances the start address by 32 B.
+__device__ __forceinline__ uint64_t sdesc_kmajor_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;
+  d |= static_cast<uint64_t>(1024u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(2u) << 61;                // SWIZZLE_128B
   return d;
 }
 

@@ -1,0 +1,359 @@
+// K1 (3M): the site contraction temp = env x Gamma_i as three real products on tcgen05.
+//
+//   P_re = E_re . G_re,   P_im = E_im . G_im,   P_s = E_s . G_s     (E_s = E_re + E_im, G_s = G_re + G_im)
+//   Re = P_re - P_im,     Im = P_s - P_re - P_im
+//
+// Gauss's 3-multiplication complex product: 6 instead of 8 issued UMMAs per K-step in SPLIT mode
+// (hi + lo environment), 3 instead of 4 in SINGLE mode.  G_s is exact in fp16 by construction
+// (quantize_pair in sweep_kernels.cu), E_s is rounded once in fp32 by the select kernel before
+// its hi/lo split, so the contraction keeps the F32-class accuracy of the 4M kernel.
+//
+// Orientation: Gamma is the A operand (M = 256 output columns per CTA pair, 128 per SM) and the
+// environment is B (N = 128 samples per unit, each SM stores 64 of them), so one Gamma tile in the
+// A collector feeds both the hi and the lo environment MMA.  The three products of a unit run as
+// three sequential K loops, each into its own 128-column TMEM slot of a 4-slot ring: while the
+// epilogue drains unit t (slots s, s+1, s+2) the MMAs of unit t+1 already fill slot s+3.
+//
+// Epilogue (4 warps per SM, thread = output column j): Re/Im for 32 samples per TMEM load,
+// column scale cs_j, Born weight wl_j |t|^2 and max component per (sample, column); the per-sample
+// sums over the warp's 32 columns come from a register transpose-reduction (31 shuffles per 32
+// values), then over the 4 warps through shared memory in a fixed order -> pstat[n][tile];
+// temp[n][k][r] stores are 256 B contiguous per sample.
+//
+// Reference: contract_site (contract.cpp:18-41,109-121) + the weight loop of measure
+// (sampler.cpp:83-90) + partial_measure_stats (parallel.cpp:90-114).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ptx.cuh"
+#include "sweep.cuh"
+
+namespace mpsg {
+
+template <bool kSplit>
+struct Cfg3M {
+  static constexpr int kHalves = kSplit ? 2 : 1;
+  static constexpr int kATile = kBM * kBK3 * 2;        // 16 KiB: 128 Gamma rows x 128 B
+  static constexpr int kBTile = (kBM / 2) * kBK3 * 2;  // 8 KiB: this SM's 64 sample rows
+  static constexpr int kStageBytes = kATile + kHalves * kBTile;
+  static constexpr int kStages = kSplit ? 6 : 8;
+  static constexpr int kRedBytes = 4 * kBM * 8;        // [4 warps][128 samples] float2
+  static constexpr int kBarBytes = 512;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + kBarBytes + kRedBytes;
+};
+
+int gemm_3m_smem_bytes(bool split) { return split ? Cfg3M<true>::kSmem : Cfg3M<false>::kSmem; }
+
+// Unit u -> (Gamma tile m, sample tile t).  Groups of `group` Gamma tiles are swept over all sample
+// tiles (Gamma index fastest), so the group's Gamma planes stay in L2 while each environment tile
+// is fetched from DRAM once per group.
+__device__ __forceinline__ void unit_coords_3m(int u, const Gemm3MArgs& a, int& m, int& t) {
+  const int per_group = a.group * a.s_tiles;
+  const int g = u / per_group;
+  const int m0 = g * a.group;
+  const int gw = min(a.group, a.g_tiles - m0);
+  const int r = u - g * per_group;
+  t = r / gw;
+  m = m0 + (r - t * gw);
+}
+
+// v[i] (i = 0..31, one value per sample) summed / maxed over the 32 lanes: afterwards lane L holds
+// the reduction for sample L.  Each round halves the vector, exchanging the half the partner keeps.
+template <bool kMax>
+__device__ __forceinline__ float transpose_reduce(float (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = up ? v[i] : v[i + o];
+      const float keep = up ? v[i + o] : v[i];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, o);
+      v[i] = kMax ? fmaxf(keep, recv) : keep + recv;
+    }
+  }
+  return v[0];
+}
+
+// Timing probes (flags & 32): [0] epilogue cycles waiting for the accumulators, [1] epilogue busy
+// cycles, [2] MMA cycles waiting for a free TMEM slot, [3] MMA cycles waiting for operands,
+// [4] units, [5] epilogue cycles from accumulator-ready to slot release.
+__device__ unsigned long long g_prof3m[8];
+
+template <bool kSplit>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    site_gemm_3m_kernel(const __grid_constant__ CUtensorMap tma_env64,
+                        const __grid_constant__ CUtensorMap tma_g, const Gemm3MArgs a) {
+  using C = Cfg3M<kSplit>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;  // [2] per unit parity
+  uint64_t* tempty = tfull + 2;          // [4] per TMEM slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
+  float2* red = reinterpret_cast<float2*>(smem + C::kStages * C::kStageBytes + C::kBarBytes);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int rank = static_cast<int>(ptx::cluster_ctarank());
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int num_clusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);   // leader: own expect_tx, bytes from both CTAs
+      ptx::mbar_init(&empty[s], 1);  // the leader's multicast commit
+    }
+    for (int j = 0; j < 2; ++j) ptx::mbar_init(&tfull[j], 1);
+    for (int j = 0; j < 4; ++j) ptx::mbar_init(&tempty[j], 8);  // 4 epilogue warps x 2 CTAs
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tma_env64);
+    ptx::tma_prefetch_desc(&tma_g);
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc_pair(tmem_slot, 512);  // 4 slots x 128 fp32 columns
+    ptx::tmem_relinquish_pair();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int units = a.g_tiles * a.s_tiles;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs; bytes counted on the leader's barrier) ----------
+    if (lane == 0) {
+      const uint64_t pol_env = ptx::l2_policy_evict_normal();
+      const uint64_t pol_g = ptx::l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cluster; u < units; u += num_clusters) {
+        int m, t;
+        unit_coords_3m(u, a, m, t);
+        const int grow = ((a.flags & 8) ? 0 : m * 2 * kBM) + rank * kBM;     // this SM's Gamma rows
+        const int erow = ((a.flags & 8) ? 0 : t * kBM) + rank * (kBM / 2);   // this SM's sample rows
+#pragma unroll 1
+        for (int c = 0; c < 3; ++c) {
+          int shard = 0, kin = 0;
+          for (int kb = 0; kb < a.k_blocks; ++kb) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* st = smem + stage * C::kStageBytes;
+            const uint32_t lbar = ptx::leader_bar(&full[stage]);
+            if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
+            ptx::tma_load_2d_pair(&tma_g, lbar, st, kb * kBK3, c * a.np + grow, pol_g);
+#pragma unroll
+            for (int h = 0; h < C::kHalves; ++h)
+              ptx::tma_load_3d_pair(&tma_env64, lbar, st + C::kATile + h * C::kBTile, kin * kBK3,
+                                    (3 * h + c) * a.env_cap + erow, shard, pol_env);
+            if (++stage == C::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            if (++kin == a.kshard_blocks) {
+              kin = 0;
+              ++shard;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: the leader CTA's warp 1 drives both SMs ----------------
+    // The whole warp runs the loop (uniform control flow and operands); one elected lane issues.
+    if (leader) {
+      constexpr uint32_t kId = ptx::idesc_f16_f32(2 * kBM, kBM, false);
+      const uint64_t desc0 = ptx::sdesc_kmajor_sw128(ptx::smem_u32(smem));
+      long long w_slot = 0, w_full = 0;
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t gp = 0;  // running product index: TMEM slot gp % 4
+      int unit = 0;
+      for (int u = cluster; u < units; u += num_clusters, ++unit) {
+#pragma unroll 1
+        for (int c = 0; c < 3; ++c, ++gp) {
+          const uint32_t slot = gp & 3;
+          long long t0 = (a.flags & 32) ? clock64() : 0;
+          ptx::mbar_wait(&tempty[slot], ((gp >> 2) & 1) ^ 1);
+          if (a.flags & 32) w_slot += clock64() - t0;
+          ptx::tc_fence_after();
+          const uint32_t d = tmem_base + slot * 128;
+          for (int kb = 0; kb < a.k_blocks; ++kb) {
+            if (a.flags & 32) t0 = clock64();
+            ptx::mbar_wait(&full[stage], phase);
+            if (a.flags & 32) w_full += clock64() - t0;
+            ptx::tc_fence_after();
+            // descriptor start addresses are in 16 B units: +32 B per K16 step inside the atom
+            const uint64_t ad = desc0 + ((stage * C::kStageBytes) >> 4);
+            const uint64_t bd = ad + (C::kATile >> 4);
+#pragma unroll
+            for (int ks = 0; ks < kBK3 / 16; ++ks) {
+              const uint32_t accum = (kb | ks) ? 1u : 0u;
+              if constexpr (kSplit) {
+                ptx::umma_pair_elect(d, ad + 2 * ks, bd + 2 * ks, kId, accum, true, false);
+                ptx::umma_pair_elect(d, ad + 2 * ks, bd + (C::kBTile >> 4) + 2 * ks, kId, 1u, false, true);
+              } else {
+                ptx::umma_pair_elect(d, ad + 2 * ks, bd + 2 * ks, kId, accum, false, false);
+              }
+            }
+            ptx::umma_commit_pair_mc_elect(&empty[stage], 0x3);
+            if (++stage == C::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+        ptx::umma_commit_pair_mc_elect(&tfull[unit & 1], 0x3);  // all three products of the unit done
+      }
+      if ((a.flags & 32) && lane == 0) {
+        atomicAdd(&g_prof3m[2], static_cast<unsigned long long>(w_slot));
+        atomicAdd(&g_prof3m[3], static_cast<unsigned long long>(w_full));
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs, thread = one of this SM's 128 output columns) --------
+    const int q = warp & 3;
+    const int et = threadIdx.x - 128;
+    uint32_t gp = 0;
+    int unit = 0;
+    for (int u = cluster; u < units; u += num_clusters, ++unit, gp += 3) {
+      int m, t;
+      unit_coords_3m(u, a, m, t);
+      const int col0 = m * 2 * kBM + rank * kBM;  // first of this SM's 128 columns (one outcome)
+      const int k = col0 / a.chirp;
+      const bool valid = k < a.d;                  // the pair-padding tile has nothing to store
+      const int r = col0 - k * a.chirp + et;
+      const float2 ci = valid ? a.cinfo[col0 + et] : make_float2(0.f, 0.f);
+      const long long e0 = (a.flags & 32) ? clock64() : 0;
+      ptx::mbar_wait(&tfull[unit & 1], (unit >> 1) & 1);
+      const long long e1 = (a.flags & 32) ? clock64() : 0;
+      long long e2 = 0;
+      ptx::tc_fence_after();
+      const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
+      const uint32_t t_re = tmem_base + lanes + ((gp + 0) & 3) * 128;
+      const uint32_t t_im = tmem_base + lanes + ((gp + 1) & 3) * 128;
+      const uint32_t t_s = tmem_base + lanes + ((gp + 2) & 3) * 128;
+      float2* dst = a.temp + (static_cast<size_t>(t) * kBM * a.d + k) * a.chirp + r;
+      const size_t row_stride = static_cast<size_t>(a.d) * a.chirp;
+#pragma unroll 1
+      for (int ch = 0; ch < kBM / 32; ++ch) {
+        float pr[32], pi[32], ps[32];
+        ptx::tmem_ld_32x32b_x32(t_re + ch * 32, pr);
+        ptx::tmem_ld_32x32b_x32(t_im + ch * 32, pi);
+        ptx::tmem_ld_32x32b_x32(t_s + ch * 32, ps);
+        ptx::tmem_wait_ld();
+        if (ch == kBM / 32 - 1) {  // the unit's three slots are free for the MMAs of unit + 2
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (a.flags & 32) e2 = clock64();
+          if (lane == 0) {
+            ptx::mbar_arrive_remote_relaxed(&tempty[(gp + 0) & 3], 0);
+            ptx::mbar_arrive_remote_relaxed(&tempty[(gp + 1) & 3], 0);
+            ptx::mbar_arrive_remote_relaxed(&tempty[(gp + 2) & 3], 0);
+          }
+        }
+        if (valid && !(a.flags & 1)) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float re = (pr[i] - pi[i]) * ci.x;
+            const float im = (ps[i] - pr[i] - pi[i]) * ci.x;
+            if (!(a.flags & 2)) {
+              if (a.flags & 16)
+                dst[(ch * 32 + i) * row_stride] = make_float2(re, im);
+              else  // streaming store: temp (1.6 GB per c3 site) must not evict the Gamma group from L2
+                __stcs(dst + (ch * 32 + i) * row_stride, make_float2(re, im));
+            }
+            pr[i] = ci.y * fmaf(re, re, im * im);
+            pi[i] = fmaxf(fabsf(re), fabsf(im));
+          }
+          if (!(a.flags & 4)) {
+            const float w = transpose_reduce<false>(pr, lane);
+            const float mx = transpose_reduce<true>(pi, lane);
+            red[q * kBM + ch * 32 + lane] = make_float2(w, mx);
+          } else {
+            red[q * kBM + ch * 32 + lane] = make_float2(pr[0], pi[0]);
+          }
+        }
+      }
+      if (valid && !(a.flags & 1)) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        float2 v = red[et];
+#pragma unroll
+        for (int w = 1; w < 4; ++w) {
+          const float2 o = red[w * kBM + et];
+          v.x += o.x;
+          v.y = fmaxf(v.y, o.y);
+        }
+        a.pstat[(static_cast<size_t>(t) * kBM + et) * a.nt + col0 / kBM] = v;
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // red is rewritten by the next unit
+      }
+      if ((a.flags & 32) && threadIdx.x == 128) {
+        const long long e3 = clock64();
+        atomicAdd(&g_prof3m[0], static_cast<unsigned long long>(e1 - e0));
+        atomicAdd(&g_prof3m[1], static_cast<unsigned long long>(e3 - e1));
+        atomicAdd(&g_prof3m[5], static_cast<unsigned long long>(e2 - e1));
+        atomicAdd(&g_prof3m[4], 1ull);
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_pair(tmem_base, 512);
+  }
+}
+
+template <bool kSplit>
+static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
+                        int grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(site_gemm_3m_kernel<kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg3M<kSplit>::kSmem);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = Cfg3M<kSplit>::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, site_gemm_3m_kernel<kSplit>, tma_env64, tma_g, a);
+}
+
+void launch_site_gemm_3m(bool split, const CUtensorMap& tma_env64, const CUtensorMap& tma_g,
+                         const Gemm3MArgs& a, int grid, cudaStream_t s) {
+  grid = (grid + 1) & ~1;  // whole CTA pairs
+  if (split)
+    launch_3m_t<true>(tma_env64, tma_g, a, grid, s);
+  else
+    launch_3m_t<false>(tma_env64, tma_g, a, grid, s);
+}
+
+}  // namespace mpsg
+
+// diagnostics (not part of include/mpsg.h): read and reset the 3M kernel's timing probes
+extern "C" __attribute__((visibility("default"))) int mpsg_debug_prof3m(unsigned long long* out, int n) {
+  unsigned long long h[8] = {0};
+  if (cudaMemcpyFromSymbol(h, mpsg::g_prof3m, sizeof(h)) != cudaSuccess) return 5;
+  const unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(mpsg::g_prof3m, z, sizeof(z));
+  for (int i = 0; i < n && i < 8; ++i) out[i] = h[i];
+  return 0;
+}

@@ -1,10 +1,12 @@
 // Kernel interface of the per-site sweep step (host engine <-> device kernels).
 //
 // Device data layout:
-//   G    fp16  [kGPlanes][Np][Kp]   compressed site tensor ([-Gi, Gr, Gi]), K-major (l contiguous);
+//   G    fp16  [gplanes][Np][Kp]   compressed site tensor, planes [Gr, Gi] (4M) or
+//              [Gr, Gi, Gs = Gr + Gi] (3M, Gs exact by construction), K-major (l contiguous);
 //              output column j = k * chirp + r  (k-major so a 128-column tile is one outcome k)
 //   cinfo float2 [Np]  (column scale cs_j, weight factor wl_r = (Lambda_r / gamma_r)^2)
-//   env  fp16  [4 planes (hi.re, hi.im, lo.re, lo.im)][cap rows][Kp]   internal environment
+//   env  fp16  [2 * C planes][cap rows][Kp]   internal environment, C = 2 components (re, im) for
+//              4M or 3 (re, im, re + im) for 3M; planes [hi.c0 .. hi.cC-1, lo.c0 .. lo.cC-1]
 //   temp float2 [rows][d][chirp]  contracted site, internal scaling, complex fp32
 //   pstat float2 [rows][ntiles]   per (sample, 128-column tile): (sum wl*|t|^2, max |t| comp.)
 #pragma once
@@ -18,15 +20,10 @@ namespace mpsg {
 constexpr int kBM = 128;  // samples per tile (UMMA M)
 constexpr int kBN = 128;  // complex output columns per tile (UMMA N per real plane)
 constexpr int kBK = 32;   // K elements per pipeline stage (64 B rows, SWIZZLE_64B)
+constexpr int kBK3 = 64;  // 3M kernel: K elements per stage (128 B rows, SWIZZLE_128B)
 constexpr int kGemmThreads = 256;
-// Compressed Gamma planes: 3 = [-Gi | Gr | Gi] (two N=256 UMMAs per K-step and env pair:
-// Er x [Gr;Gi] and Ei x [-Gi;Gr]); 2 = [Gr | Gi] (four N=128 UMMAs).
-#ifndef MPSG_GPLANES
-#define MPSG_GPLANES 2
-#endif
-constexpr int kGPlanes = MPSG_GPLANES;
-constexpr int kPlaneRe = kGPlanes == 3 ? 1 : 0;
-constexpr int kPlaneIm = kGPlanes == 3 ? 2 : 1;
+constexpr int kPlaneRe = 0;  // Gamma planes: Gr, Gi (, Gs)
+constexpr int kPlaneIm = 1;
 constexpr uint64_t kMeasureStream = 0x6d656173ull;  // rng.hpp:19
 constexpr uint8_t kDead = 0xFF;                      // sampler.hpp:17
 
@@ -47,6 +44,25 @@ struct SiteGemmArgs {
   float2* pstat;
 };
 
+// 3M kernel (site_gemm_3m_kernel): D[j, n] = sum_l Gamma[j, l] E[n, l] with Gamma as the A
+// operand (a CTA pair covers 256 output columns, 128 per SM) and the environment as B
+// (128 samples per unit, 64 rows per SM).  Products P_c = E_c x G_c for c = re, im, s; then
+// Re = P_re - P_im and Im = P_s - P_re - P_im.
+struct Gemm3MArgs {
+  int g_tiles;       // Np / 256 (Gamma column tiles of the pair)
+  int s_tiles;       // rows / 128 (sample tiles)
+  int k_blocks, kshard_blocks;
+  int env_cap;       // row offset between env planes
+  int np;            // row offset between Gamma planes
+  int chirp, d;
+  int nt;            // Np / 128: pstat row stride
+  int group;         // Gamma tiles per raster group
+  int flags;         // experiment switches (0 in production): 1 = skip the epilogue math / stores
+  const float2* cinfo;
+  float2* temp;
+  float2* pstat;
+};
+
 // Per-(sample, outcome) partials read by the select kernel: element (part, n, k) lives at
 // part_base[part * part_stride + n * row_stride + k * k_stride]; parts are summed in order.
 struct SelectArgs {
@@ -59,6 +75,7 @@ struct SelectArgs {
   int count;                // live samples this pass
   int kp_next;              // width of this rank's next-env shard (0 on the last site)
   int env_cap;              // env plane stride in rows
+  int env_comp;             // env components per precision half: 2 (re, im) or 3 (re, im, re+im)
   uint64_t seed, first;
   const float2* temp;
   const float2* part_base;
@@ -83,21 +100,27 @@ void launch_site_gemm(bool split, const CUtensorMap& tma_env, const CUtensorMap&
 void launch_site_gemm_pair(bool split, const CUtensorMap& tma_env, const CUtensorMap& tma_g64,
                            const SiteGemmArgs& a, int grid, cudaStream_t s);
 int gemm_pair_smem_bytes(bool split);
+// 3M kernel: tma_g has a 64 x 128-row box over [3][Np][Kp], tma_env a 64 x 64-row box over the
+// 6-plane env, both SWIZZLE_128B; Kp and the env shard width are multiples of 64.
+void launch_site_gemm_3m(bool split, const CUtensorMap& tma_env64, const CUtensorMap& tma_g,
+                         const Gemm3MArgs& a, int grid, cudaStream_t s);
+int gemm_3m_smem_bytes(bool split);
 void launch_select(const SelectArgs& a, cudaStream_t s);
 // pstat [rows][nt] -> out [rows][d]: (sum of weights, max) over the tiles of each outcome
 void launch_reduce_tiles(const float2* pstat, int nt, int tiles_per_k, int d, int rows,
                          float2* out, cudaStream_t s);
-// Site-0 env in the shard-major layout [shards][4][cap][kshard]: E[n][0] = 1 (shard 0).
-void launch_init_env(__half* env, int env_cap, int kshard0, int shards, int rows, int count,
-                     uint8_t* alive, cudaStream_t s, double* logscale = nullptr);
+// Site-0 env in the shard-major layout [shards][2C][cap][kshard]: E[n][0] = 1 (shard 0) in the
+// hi.re plane and, for C = 3, the hi.s plane.
+void launch_init_env(__half* env, int env_comp, int env_cap, int kshard0, int shards, int rows,
+                     int count, uint8_t* alive, cudaStream_t s, double* logscale = nullptr);
 void launch_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, double* out,
                   cudaStream_t s);
 // Compression of one site's column shard [b0, b0 + width) of chiR: src complex (chiL, chiR, d)
 // f64 or f32 interleaved on device; row l goes to padded K position lpos[l].
 void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
                           int width, int kp, int chirp, const int* lpos, const double* gl,
-                          const double* gr, const double* wl, __half* g_out, float2* cinfo_out,
-                          double* cs_out, int* err, cudaStream_t s);
+                          const double* gr, const double* wl, int gplanes, __half* g_out,
+                          float2* cinfo_out, double* cs_out, int* err, cudaStream_t s);
 int gemm_smem_bytes(bool split);
 
 }  // namespace mpsg

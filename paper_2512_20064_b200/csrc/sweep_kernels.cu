@@ -48,8 +48,8 @@ template <bool kSplit>
 struct GemmCfg {
   static constexpr int kAPlanes = kSplit ? 4 : 2;  // env planes: hi.re hi.im [lo.re lo.im]
   static constexpr int kTile = kBM * kBK * 2;      // 8 KiB: 128 rows x 64 B (A and B alike)
-  static constexpr int kStageBytes = (kAPlanes + kGPlanes) * kTile;
-  static constexpr int kStages = kGPlanes == 3 ? (kSplit ? 4 : 5) : (kSplit ? 4 : 6);
+  static constexpr int kStageBytes = (kAPlanes + 2) * kTile;
+  static constexpr int kStages = kSplit ? 4 : 6;
   static constexpr int kBarrierBytes = 256;
   static constexpr int kSmem = kStages * kStageBytes + 1024 + kBarrierBytes;
   static_assert(kBM == 128 && kBN == 128 && kBK == 32, "tile shape baked into descriptors");
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             ptx::tma_load_3d_mc(&tma_env, &full[stage], st + q * C::kTile, kin * kBK,
                                 q * a.plane_rows_a + m * kBM, shard, 0x3, pol_env);
 #pragma unroll
-          for (int p = 0; p < kGPlanes; ++p)
+          for (int p = 0; p < 2; ++p)
             ptx::tma_load_2d(&tma_g, &full[stage], st + (C::kAPlanes + p) * C::kTile, kb * kBK,
                              p * a.np + n * kBN, pol_g);
           if (++stage == C::kStages) {
@@ -157,7 +157,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       constexpr uint32_t kId = ptx::idesc_f16_f32(kBM, kBN, false);
       constexpr uint32_t kIdNeg = ptx::idesc_f16_f32(kBM, kBN, true);
-      constexpr uint32_t kId256 = ptx::idesc_f16_f32(kBM, 2 * kBN, false);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -175,34 +174,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int ks = 0; ks < kBK / 16; ++ks) {
             const uint32_t off = ks * 32;  // 16 fp16 along K
             const uint32_t accum = (kb | ks) ? 1u : 0u;
-            if constexpr (kGPlanes == 3) {
-              // B tiles [-Gi | Gr | Gi]: [Gr;Gi] and [-Gi;Gr] are contiguous 256-row operands, so
-              // D[:, 0:256] = [Re | Im] += Er x [Gr;Gi] + Ei x [-Gi;Gr] in two N=256 UMMAs.
-              const uint64_t b_rg = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 1) * C::kTile + off);
-              const uint64_t b_nr = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 0) * C::kTile + off);
+            const uint64_t br = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 0) * C::kTile + off);
+            const uint64_t bi = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 1) * C::kTile + off);
+            // Re += Er.Gr - Ei.Gi ; Im += Er.Gi + Ei.Gr.  The Er tile feeds two consecutive MMAs
+            // through the A collector; no collector for the Ei pair (reuse combined with an operand
+            // negation gives wrong results).
 #pragma unroll
-              for (int h = 0; h < (kSplit ? 2 : 1); ++h) {
-                const uint64_t ar = ptx::sdesc_kmajor_sw64(st + (2 * h + 0) * C::kTile + off);
-                const uint64_t ai = ptx::sdesc_kmajor_sw64(st + (2 * h + 1) * C::kTile + off);
-                ptx::umma_f16_ss(d_re, ar, b_rg, kId256, h ? 1u : accum);
-                ptx::umma_f16_ss(d_re, ai, b_nr, kId256, 1u);
-              }
-            } else {
-              const uint64_t br = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 0) * C::kTile + off);
-              const uint64_t bi = ptx::sdesc_kmajor_sw64(st + (C::kAPlanes + 1) * C::kTile + off);
-              // Re += Er.Gr - Ei.Gi ; Im += Er.Gi + Ei.Gr.  The Er tile feeds two consecutive MMAs
-              // through the A collector; no collector for the Ei pair (reuse combined with an operand
-              // negation gives wrong results).
-#pragma unroll
-              for (int h = 0; h < (kSplit ? 2 : 1); ++h) {
-                const uint32_t acc0 = h ? 1u : accum;
-                const uint64_t ar = ptx::sdesc_kmajor_sw64(st + (2 * h + 0) * C::kTile + off);
-                const uint64_t ai = ptx::sdesc_kmajor_sw64(st + (2 * h + 1) * C::kTile + off);
-                ptx::umma_f16_ss_afill(d_re, ar, br, kId, acc0);
-                ptx::umma_f16_ss_alast(d_im, ar, bi, kId, acc0);
-                ptx::umma_f16_ss(d_re, ai, bi, kIdNeg, 1u);
-                ptx::umma_f16_ss(d_im, ai, br, kId, 1u);
-              }
+            for (int h = 0; h < (kSplit ? 2 : 1); ++h) {
+              const uint32_t acc0 = h ? 1u : accum;
+              const uint64_t ar = ptx::sdesc_kmajor_sw64(st + (2 * h + 0) * C::kTile + off);
+              const uint64_t ai = ptx::sdesc_kmajor_sw64(st + (2 * h + 1) * C::kTile + off);
+              ptx::umma_f16_ss_afill(d_re, ar, br, kId, acc0);
+              ptx::umma_f16_ss_alast(d_im, ar, bi, kId, acc0);
+              ptx::umma_f16_ss(d_re, ai, bi, kIdNeg, 1u);
+              ptx::umma_f16_ss(d_im, ai, br, kId, 1u);
             }
           }
           ptx::umma_commit_mc(&empty[stage], 0x3);  // slot free in both CTAs once MMAs retire
@@ -506,7 +491,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_remote(&tempty[acc], 0);
+      if (lane == 0) ptx::mbar_arrive_remote_relaxed(&tempty[acc], 0);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -659,12 +644,14 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
     }
   }
   if (a.kp_next > 0) {
-    // next env row: E[n, r] = temp[n, k, r] * 2^-e, split hi/lo fp16 (zeros for dead / pad).
+    // next env row: E[n, r] = temp[n, k, r] * 2^-e, split hi/lo fp16 (zeros for dead / pad), per
+    // component re, im (and re + im for the 3M contraction, rounded once in fp32 then split).
     // Each lane handles 4 consecutive columns: two 16 B loads, one 8 B store per plane.
     const size_t plane = static_cast<size_t>(a.env_cap) * a.kp_next;
     __half* e0 = a.env_next + static_cast<size_t>(n) * a.kp_next;
     const float2* src = a.temp + (static_cast<size_t>(n) * a.d + (live_out ? outcome : 0)) * a.chirp;
     const int live_cols = live_out ? a.chir_loc : 0;
+    const int C = a.env_comp;
     for (int r = lane * 4; r < a.kp_next; r += 128) {  // kp_next is a multiple of 32
       float4 v01 = make_float4(0.f, 0.f, 0.f, 0.f), v23 = v01;
       if (r + 3 < live_cols) {  // chirp is a multiple of 128: these loads stay inside the row
@@ -678,20 +665,23 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
         v01 = make_float4(c0.x, c0.y, c1.x, c1.y);
         v23 = make_float4(c2.x, c2.y, 0.f, 0.f);
       }
-      const float re[4] = {v01.x * scale, v01.z * scale, v23.x * scale, v23.z * scale};
-      const float im[4] = {v01.y * scale, v01.w * scale, v23.y * scale, v23.w * scale};
-      __align__(8) __half hr[4], hi[4], lr[4], li[4];
+      float comp[3][4];
+      comp[0][0] = v01.x * scale, comp[0][1] = v01.z * scale, comp[0][2] = v23.x * scale, comp[0][3] = v23.z * scale;
+      comp[1][0] = v01.y * scale, comp[1][1] = v01.w * scale, comp[1][2] = v23.y * scale, comp[1][3] = v23.w * scale;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        hr[j] = __float2half_rn(re[j]);
-        hi[j] = __float2half_rn(im[j]);
-        lr[j] = __float2half_rn(re[j] - __half2float(hr[j]));
-        li[j] = __float2half_rn(im[j] - __half2float(hi[j]));
+      for (int j = 0; j < 4; ++j) comp[2][j] = comp[0][j] + comp[1][j];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (c >= C) break;
+        __align__(8) __half hv[4], lv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          hv[j] = __float2half_rn(comp[c][j]);
+          lv[j] = __float2half_rn(comp[c][j] - __half2float(hv[j]));
+        }
+        *reinterpret_cast<uint2*>(e0 + c * plane + r) = *reinterpret_cast<const uint2*>(hv);
+        *reinterpret_cast<uint2*>(e0 + (C + c) * plane + r) = *reinterpret_cast<const uint2*>(lv);
       }
-      *reinterpret_cast<uint2*>(e0 + r) = *reinterpret_cast<const uint2*>(hr);
-      *reinterpret_cast<uint2*>(e0 + plane + r) = *reinterpret_cast<const uint2*>(hi);
-      *reinterpret_cast<uint2*>(e0 + 2 * plane + r) = *reinterpret_cast<const uint2*>(lr);
-      *reinterpret_cast<uint2*>(e0 + 3 * plane + r) = *reinterpret_cast<const uint2*>(li);
     }
   }
 }
@@ -733,15 +723,18 @@ void launch_select(const SelectArgs& a, cudaStream_t s) {
 // ============================================================================================
 // site-0 environment (sampler.cpp:136-138: env = ones(count, 1), all alive)
 // ============================================================================================
-__global__ void init_env_kernel(__half* env, int env_cap, int kshard0, int shards, int rows,
-                                int count, uint8_t* alive, double* logscale) {
+__global__ void init_env_kernel(__half* env, int env_comp, int env_cap, int kshard0, int shards,
+                                int rows, int count, uint8_t* alive, double* logscale) {
+  const int planes = 2 * env_comp;
   const size_t plane = static_cast<size_t>(env_cap) * kshard0;
-  const size_t total = static_cast<size_t>(shards) * 4 * plane;
+  const size_t total = static_cast<size_t>(shards) * planes * plane;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t p = i / plane, rem = i - p * plane;  // p = shard * 4 + plane
+    const size_t p = i / plane, rem = i - p * plane;  // p = shard * planes + plane
     const size_t n = rem / kshard0, c = rem - n * kshard0;
-    env[i] = __float2half_rn((p == 0 && c == 0 && n < static_cast<size_t>(count)) ? 1.0f : 0.0f);
+    // E = 1 + 0i: hi.re = 1 and, for the 3M layout, hi.(re + im) = 1
+    const bool one = (p == 0 || (env_comp == 3 && p == 2)) && c == 0 && n < static_cast<size_t>(count);
+    env[i] = __float2half_rn(one ? 1.0f : 0.0f);
   }
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < rows; n += gridDim.x * blockDim.x) {
     alive[n] = n < count ? 1 : 0;
@@ -749,9 +742,10 @@ __global__ void init_env_kernel(__half* env, int env_cap, int kshard0, int shard
   }
 }
 
-void launch_init_env(__half* env, int env_cap, int kshard0, int shards, int rows, int count,
-                     uint8_t* alive, cudaStream_t s, double* logscale) {
-  init_env_kernel<<<296, 256, 0, s>>>(env, env_cap, kshard0, shards, rows, count, alive, logscale);
+void launch_init_env(__half* env, int env_comp, int env_cap, int kshard0, int shards, int rows,
+                     int count, uint8_t* alive, cudaStream_t s, double* logscale) {
+  init_env_kernel<<<296, 256, 0, s>>>(env, env_comp, env_cap, kshard0, shards, rows, count, alive,
+                                      logscale);
 }
 
 __global__ void draws_kernel(uint64_t seed, uint64_t first, uint64_t count, uint64_t site,
@@ -812,28 +806,46 @@ __global__ void colscale_kernel(const void* src, int chil, int chir, int d, int 
   cinfo[k * chirp + rl] = make_float2(static_cast<float>(cs), static_cast<float>(wl[r]));
 }
 
+// Rounds (a, b) onto the fp16 grid of the binade of max(|a|, |b|, |a + b|), so that a, b and
+// a + b are all exactly representable in fp16 (the 3M contraction stores Gs = Gr + Gi and must
+// sample exactly the decoded Gamma).  |a|, |b| < 1 after column scaling.
+__device__ __forceinline__ void quantize_pair(double a, double b, __half& ha, __half& hb, __half& hs) {
+  const double m = fmax(fmax(fabs(a), fabs(b)), fabs(a + b));
+  if (m == 0.0) {
+    ha = hb = hs = __float2half_rn(0.f);
+    return;
+  }
+  int e;
+  frexp(m, &e);  // m in [2^(e-1), 2^e): fp16 spacing there is 2^(e-11)
+  const double u = ldexp(1.0, max(e - 11, -24));
+  const double qa = rint(a / u) * u, qb = rint(b / u) * u;  // RNE; |qa + qb| <= 2^e
+  ha = __double2half(qa);
+  hb = __double2half(qb);
+  hs = __double2half(qa + qb);
+}
+
 template <typename T>
 __global__ void pack_kernel(const void* src, int chil, int chir, int d, int b0, int width, int kp,
                             int chirp, const int* lpos, const double* gl, const double* gr,
-                            const double* cs, __half* g_out, int np) {
-  __shared__ __half tre[32][33], tim[32][33];
+                            const double* cs, int gplanes, __half* g_out, int np) {
+  __shared__ __half tre[32][33], tim[32][33], tsm[32][33];
   const int wcols = width * d;
   const size_t stride = static_cast<size_t>(chir) * d;
   const int j0 = blockIdx.x * 32, l0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
   for (int yy = ty; yy < 32; yy += 8) {
     const int l = l0 + yy, jl = j0 + tx;
-    __half hr = __float2half_rn(0.f), hi = hr;
+    __half hr = __float2half_rn(0.f), hi = hr, hs = hr;
     if (l < chil && jl < wcols) {
       const int rl = jl / d, k = jl - rl * d;
       double re, im;
       load_c<T>(src, static_cast<size_t>(l) * stride + static_cast<size_t>(b0 + rl) * d + k, re, im);
       const double f = gr[b0 + rl] / gl[l] / cs[jl];
-      hr = __double2half(re * f);
-      hi = __double2half(im * f);
+      quantize_pair(re * f, im * f, hr, hi, hs);
     }
     tre[yy][tx] = hr;
     tim[yy][tx] = hi;
+    tsm[yy][tx] = hs;
   }
   __syncthreads();
   for (int yy = ty; yy < 32; yy += 8) {
@@ -844,15 +856,15 @@ __global__ void pack_kernel(const void* src, int chil, int chir, int d, int b0, 
       const size_t col = static_cast<size_t>(lpos[l]);
       g_out[(static_cast<size_t>(kPlaneRe) * np + row) * kp + col] = tre[tx][yy];
       g_out[(static_cast<size_t>(kPlaneIm) * np + row) * kp + col] = tim[tx][yy];
-      if (kGPlanes == 3) g_out[row * kp + col] = __hneg(tim[tx][yy]);
+      if (gplanes == 3) g_out[(2ull * np + row) * kp + col] = tsm[tx][yy];
     }
   }
 }
 
 void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
                           int width, int kp, int chirp, const int* lpos, const double* gl,
-                          const double* gr, const double* wl, __half* g_out, float2* cinfo_out,
-                          double* cs_out, int* err, cudaStream_t s) {
+                          const double* gr, const double* wl, int gplanes, __half* g_out,
+                          float2* cinfo_out, double* cs_out, int* err, cudaStream_t s) {
   if (width <= 0) return;
   const int wcols = width * d;
   const int np = round_up(d * chirp, 2 * kBN);
@@ -862,12 +874,12 @@ void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int
     colscale_kernel<double><<<cb, 128, 0, s>>>(src, chil, chir, d, b0, width, chirp, gl, gr, wl,
                                                cinfo_out, cs_out, err);
     pack_kernel<double><<<pb, dim3(32, 8), 0, s>>>(src, chil, chir, d, b0, width, kp, chirp, lpos,
-                                                   gl, gr, cs_out, g_out, np);
+                                                   gl, gr, cs_out, gplanes, g_out, np);
   } else {
     colscale_kernel<float><<<cb, 128, 0, s>>>(src, chil, chir, d, b0, width, chirp, gl, gr, wl,
                                               cinfo_out, cs_out, err);
     pack_kernel<float><<<pb, dim3(32, 8), 0, s>>>(src, chil, chir, d, b0, width, kp, chirp, lpos, gl,
-                                                  gr, cs_out, g_out, np);
+                                                  gr, cs_out, gplanes, g_out, np);
   }
 }
 

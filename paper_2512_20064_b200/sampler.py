@@ -114,10 +114,18 @@ class PrecisionPolicy:
 
 
 class Mode(enum.IntEnum):
-    """GPU contraction scheme; AUTO picks SPLIT for F64/F32 compute."""
+    """GPU contraction precision; AUTO picks SPLIT for F64/F32 compute."""
     AUTO = 0
     SPLIT = 1
     SINGLE = 2
+
+
+class Scheme(enum.IntEnum):
+    """Complex decomposition of the contraction: Gauss 3M (Gamma planes
+    Gr, Gi, Gr+Gi) or 4M (Gr, Gi); AUTO = 3M when Gamma is resident and the state fits."""
+    AUTO = 0
+    M3 = 3
+    M4 = 4
 
 
 # ---- mps.hpp ---------------------------------------------------------------------------------
@@ -202,6 +210,7 @@ class SamplerOptions:
     record_decay_trace: bool = False
     mode: Mode = Mode.AUTO
     pass_samples: int = 0
+    scheme: Scheme = Scheme.AUTO
 
 
 @dataclass
@@ -238,7 +247,8 @@ class GpuSampler:
     def __init__(self, mps: MpsState, policy: Optional[PrecisionPolicy] = None, mode: Mode = Mode.AUTO,
                  devices: Optional[Sequence[int]] = None, pass_samples: int = 0,
                  record_site_times: bool = False, tp_size: int = 1, tp_rank: int = 0,
-                 host_stream_slots: int = 0, record_decay_trace: bool = False):
+                 host_stream_slots: int = 0, record_decay_trace: bool = False,
+                 scheme: Scheme = Scheme.AUTO):
         L = _lib.lib()
         mps.validate()
         self.policy = policy or PrecisionPolicy()
@@ -254,7 +264,7 @@ class GpuSampler:
                             (_lib._pd * len(lam))(*[x.ctypes.data_as(_lib._pd) for x in lam]))
         pol = _lib.Policy(int(self.policy.compute), int(self.policy.storage), int(self.policy.scaling))
         opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), int(tp_size), int(tp_rank),
-                           int(host_stream_slots), int(record_decay_trace))
+                           int(host_stream_slots), int(record_decay_trace), int(scheme))
         self.tp_size, self.tp_rank = tp_size, tp_rank
         devs, nd = self._devices(devices)
         _check(L.mpsg_create(C.byref(view), C.byref(pol), C.byref(opt), devs, nd, C.byref(self._h)))
@@ -262,13 +272,15 @@ class GpuSampler:
     @classmethod
     def from_file(cls, path: str, policy: Optional[PrecisionPolicy] = None, mode: Mode = Mode.AUTO,
                   devices: Optional[Sequence[int]] = None, pass_samples: int = 0,
-                  record_site_times: bool = False, host_stream_slots: int = 0) -> "GpuSampler":
+                  record_site_times: bool = False, host_stream_slots: int = 0,
+                  scheme: Scheme = Scheme.AUTO) -> "GpuSampler":
         """Build the device state from an MPSB file (the reference's format, mps_io.hpp:17-24)."""
         L = _lib.lib()
         policy = policy or PrecisionPolicy()
         policy.validate()
         pol = _lib.Policy(int(policy.compute), int(policy.storage), int(policy.scaling))
-        opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), 1, 0, int(host_stream_slots))
+        opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), 1, 0, int(host_stream_slots), 0,
+                           int(scheme))
         devs, nd = cls._devices(devices)
         h = C.c_void_p()
         _check(L.mpsg_create_from_file(path.encode(), C.byref(pol), C.byref(opt), devs, nd, C.byref(h)))
@@ -350,6 +362,11 @@ class GpuSampler:
         _check(_lib.lib().mpsg_marginals(self._h, first, n, forced.ctypes.data_as(_lib._pu8),
                                          marg.ctypes.data_as(_lib._pd)))
         return marg
+
+    @property
+    def scheme(self) -> Scheme:
+        """The contraction scheme this handle runs (3M or 4M)."""
+        return Scheme(_lib.lib().mpsg_scheme(self._h))
 
     def decoded_gamma(self, site: int) -> np.ndarray:
         b = self.bond_dims
@@ -467,7 +484,8 @@ def sample_batch(mps: MpsState, plan: BatchPlan, opts: SamplerOptions,
         raise ConfigError("site transforms are not supported by the GPU sweep (out of scope)")
     t0 = time.perf_counter()
     smp = GpuSampler(mps, opts.policy, opts.mode, devices, opts.pass_samples,
-                     record_site_times=stats is not None, record_decay_trace=opts.record_decay_trace)
+                     record_site_times=stats is not None, record_decay_trace=opts.record_decay_trace,
+                     scheme=opts.scheme)
     try:
         st = stats if stats is not None else RunStats()
         rows = smp.sample(0, plan.total_samples, opts.seed, stats=st)
@@ -501,7 +519,7 @@ def run_data_parallel(mps_path: str, plan: BatchPlan, p1: int, opts: SamplerOpti
     plan = BatchPlan(plan.total_samples, plan.macro_batch, plan.micro_batch)
     plan.normalize()
     devs = list(devices) if devices else list(range(p1))
-    smp = GpuSampler.from_file(mps_path, opts.policy, opts.mode, devs, opts.pass_samples)
+    smp = GpuSampler.from_file(mps_path, opts.policy, opts.mode, devs, opts.pass_samples, scheme=opts.scheme)
     try:
         st = RunStats()
         rows = smp.sample(0, plan.total_samples, opts.seed, stats=st)

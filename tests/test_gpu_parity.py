@@ -78,11 +78,13 @@ def test_decode_close_to_input(pkg, gold):
         assert (err <= colmax * 2.0 ** -10 + 1e-300).all(), i
 
 
+@pytest.mark.parametrize("scheme", [3, 4])
 @pytest.mark.parametrize("mode", ["split", "single"])
-def test_contract_site_numerics(pkg, gold, mode):
+def test_contract_site_numerics(pkg, gold, mode, scheme):
     z = np.load(f"{gold}/c1b.npz")
     mps = O.load_npz_mps(z)
-    smp = pkg.GpuSampler(to_state(pkg, mps), mode=pkg.Mode.SPLIT if mode == "split" else pkg.Mode.SINGLE)
+    smp = pkg.GpuSampler(to_state(pkg, mps), mode=pkg.Mode.SPLIT if mode == "split" else pkg.Mode.SINGLE,
+                         scheme=pkg.Scheme(scheme))
     rng = np.random.default_rng(3)
     tol = 2e-6 if mode == "split" else 2e-3
     for i in [0, 1, 2, 5, 13, 14, 15]:
@@ -96,12 +98,14 @@ def test_contract_site_numerics(pkg, gold, mode):
         assert rel < tol, (i, rel)
 
 
+@pytest.mark.parametrize("scheme", [3, 4])
 @pytest.mark.parametrize("name", ["c1", "c1b"])
-def test_c1_strings_and_marginals(pkg, gold, name):
+def test_c1_strings_and_marginals(pkg, gold, name, scheme):
     z = np.load(f"{gold}/{name}.npz")
     mps = O.load_npz_mps(z)
     n, seed = int(z["n"]), int(z["seed"])
-    smp = pkg.GpuSampler(to_state(pkg, mps), pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX))
+    smp = pkg.GpuSampler(to_state(pkg, mps), pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX),
+                         scheme=pkg.Scheme(scheme))
     dec = decoded_mps(smp, mps)
     ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, n, seed, want_marginals=True)
     gpu_rows = smp.sample(0, n, seed)
@@ -172,16 +176,16 @@ def test_tensor_parallel_local(pkg, gold, p2):
     tp.close()
 
 
-@pytest.mark.parametrize("slots", [2, 3])
-def test_host_streamed_gamma(pkg, gold, slots):
+@pytest.mark.parametrize("slots,scheme", [(2, 4), (3, 4), (2, 3)])
+def test_host_streamed_gamma(pkg, gold, slots, scheme):
     """Gamma kept in pinned host memory and streamed through `slots` device buffers: identical rows
     to the HBM-resident sweep, across several passes (the load sequence wraps around the chain)."""
     z = np.load(f"{gold}/c1b.npz")
     mps = O.load_npz_mps(z)
     st = to_state(pkg, mps)
     pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
-    res = pkg.GpuSampler(st, pol, pass_samples=256)
-    stm = pkg.GpuSampler(st, pol, pass_samples=256, host_stream_slots=slots)
+    res = pkg.GpuSampler(st, pol, pass_samples=256, scheme=pkg.Scheme(scheme))
+    stm = pkg.GpuSampler(st, pol, pass_samples=256, host_stream_slots=slots, scheme=pkg.Scheme(scheme))
     for i in (0, 7, 15):
         assert np.array_equal(stm.decoded_gamma(i), res.decoded_gamma(i))
     a = res.sample(0, 1000, 7)
@@ -256,11 +260,12 @@ def _synthetic(pkg, m, chi, d, **kw):
     return smp, lams, pol
 
 
-@pytest.mark.parametrize("m,chi,d,n", [(10, 512, 6, 48), (10, 2048, 6, 12)])
-def test_parity_at_benchmark_bond_dims(pkg, m, chi, d, n):
+@pytest.mark.parametrize("m,chi,d,n,scheme", [(10, 512, 6, 48, 3), (10, 512, 6, 48, 4), (10, 2048, 6, 12, 3),
+                                              (10, 2048, 6, 12, 4)])
+def test_parity_at_benchmark_bond_dims(pkg, m, chi, d, n, scheme):
     """Device-generated chains at the c2 / c3 bond dimensions (short M so the f64 oracle is quick):
     teacher-forced marginals within 1e-4 and identical strings (boundary draws excepted)."""
-    smp, lams, _ = _synthetic(pkg, m, chi, d)
+    smp, lams, _ = _synthetic(pkg, m, chi, d, scheme=scheme)
     dec = O.Mps(d, list(smp.bond_dims), [smp.decoded_gamma(i) for i in range(m)], list(lams))
     ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, n, 7, want_marginals=True)
     gpu_rows = smp.sample(0, n, 7)
@@ -278,10 +283,13 @@ def test_invariants_at_chi2048(pkg):
     exact site-0 distribution (chi-square)."""
     from paper_2512_20064_b200.parallel import TensorParallelLocal
     m, chi, d = 16, 2048, 6
-    a, lams, pol = _synthetic(pkg, m, chi, d, pass_samples=512)
+    a, lams, pol = _synthetic(pkg, m, chi, d, pass_samples=512)  # 3M (auto)
     rows = a.sample(0, 4096, 3)
-    b, _, _ = _synthetic(pkg, m, chi, d, pass_samples=4096, host_stream_slots=2)
+    b, _, _ = _synthetic(pkg, m, chi, d, pass_samples=4096, host_stream_slots=2, scheme=3)
     assert np.array_equal(b.sample(0, 4096, 3), rows)
+    # the 4M kernel on the same decoded tensor: only CDF-boundary draws may differ
+    c, _, _ = _synthetic(pkg, m, chi, d, pass_samples=4096, scheme=4)
+    assert (c.sample(0, 4096, 3) != rows).any(axis=1).sum() <= 4
     assert np.array_equal(a.sample(1000, 300, 3), rows[1000:1300])
     # exact site-0 distribution from the decoded tensor (sampler.cpp:83-90 with env = 1)
     g0 = a.decoded_gamma(0)[0]

@@ -1,6 +1,6 @@
 """Perf probe: per-site device times and algorithmic TFLOP/s for a synthetic chain.
 
-usage: python tools/perf_probe.py M CHI D N [mode] [pass]
+usage: python tools/perf_probe.py M CHI D N [mode] [pass] [scheme 0|3|4]
 """
 import os
 import sys
@@ -17,9 +17,10 @@ from paper_2512_20064_b200.synthetic import build_synthetic  # noqa: E402
 M, chi, d, N = (int(x) for x in sys.argv[1:5])
 mode = P.Mode.SINGLE if len(sys.argv) > 5 and sys.argv[5] == "single" else P.Mode.SPLIT
 ps = int(sys.argv[6]) if len(sys.argv) > 6 else 0
+scheme = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 t = time.time()
-smp, lams = build_synthetic(M, chi, d, mode=mode, pass_samples=ps or N, record_site_times=True)
-print(f"build {time.time()-t:.1f}s state {smp.state_bytes/1e9:.2f} GB", flush=True)
+smp, lams = build_synthetic(M, chi, d, mode=mode, pass_samples=ps or N, record_site_times=True, scheme=scheme)
+print(f"build {time.time()-t:.1f}s state {smp.state_bytes/1e9:.2f} GB scheme {int(smp.scheme)}", flush=True)
 bonds = smp.bond_dims
 rows = torch.empty((N, M), dtype=torch.uint8, device="cuda")
 for rep in range(3):
@@ -32,6 +33,13 @@ for rep in range(3):
     ss = np.array(st.site_seconds)
     print(f"rep {rep}: {el:.3f}s  {N/el:.0f} samples/s  alg {flops/el/1e12:.1f} TF/s  issued {st.issued_mma_flops/el/1e12:.1f} TF/s"
           f"  sum(site) {ss.sum():.3f}s  dead {st.dead_samples}", flush=True)
+if int(os.environ.get("MPSG_3M_FLAGS", "0")) & 32:
+    import ctypes
+    buf = (ctypes.c_ulonglong * 8)()
+    P.sampler._lib.lib().mpsg_debug_prof3m(buf, 8)
+    u = max(buf[4], 1)
+    print(f"prof3m per unit (cycles): epi wait {buf[0]/u:.0f} epi busy {buf[1]/u:.0f} epi to-release {buf[5]/u:.0f}"
+          f" | per CTA-pair unit: mma slot-wait {2*buf[2]/u:.0f} mma full-wait {2*buf[3]/u:.0f}  units {buf[4]}", flush=True)
 full = [i for i in range(M) if bonds[i] == chi and bonds[i + 1] == chi]
 if full:
     i = full[len(full) // 2]
