@@ -62,7 +62,8 @@ enum { MPSG_MODE_AUTO = 0, MPSG_MODE_SPLIT = 1, MPSG_MODE_SINGLE = 2 };
 /* Complex decomposition of the contraction:
  *   MPSG_SCHEME_3M  Gauss: 3 real products (Gamma planes Gr, Gi, Gr+Gi: 6 bytes per complex entry)
  *   MPSG_SCHEME_4M  4 real products (Gamma planes Gr, Gi: 4 bytes per complex entry)
- *   MPSG_SCHEME_AUTO  3M when Gamma is resident and the 3-plane state fits in device memory. */
+ *   MPSG_SCHEME_AUTO  3M when the 3-plane state fits (device memory when resident, host memory
+ *                     when host-streamed), else 4M. */
 enum { MPSG_SCHEME_AUTO = 0, MPSG_SCHEME_3M = 3, MPSG_SCHEME_4M = 4 };
 
 #define MPSG_DEAD 0xFF
@@ -101,9 +102,8 @@ typedef struct mpsg_options {
   int record_decay_trace;          /* fill mpsg_stats.decay_trace: mean |env| per site before
                                       scaling, in the reference's own scaling (sampler.cpp:149-153,
                                       decay_probe :207-216); GlobalMax is traced as None */
-  int scheme;                      /* complex decomposition of the contraction: MPSG_SCHEME_AUTO (3M
-                                      when the 3-plane state fits in HBM and Gamma is resident,
-                                      else 4M), MPSG_SCHEME_3M or MPSG_SCHEME_4M */
+  int scheme;                      /* complex decomposition of the contraction: MPSG_SCHEME_AUTO,
+                                      MPSG_SCHEME_3M or MPSG_SCHEME_4M (see above) */
 } mpsg_options;
 
 /* Mirrors mpsamp::RunStats + FlopCounters (sampler.hpp:46-54, contract.hpp:12-25). */

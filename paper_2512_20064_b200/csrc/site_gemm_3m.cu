@@ -131,8 +131,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs; bytes counted on the leader's barrier) ----------
     if (lane == 0) {
-      const uint64_t pol_env = ptx::l2_policy_evict_normal();
-      const uint64_t pol_g = ptx::l2_policy_evict_last();
+      const uint64_t pol_env = (a.flags & 128) ? ptx::l2_policy_evict_first()
+                               : (a.flags & 256) ? ptx::l2_policy_evict_last() : ptx::l2_policy_evict_normal();
+      const uint64_t pol_g = (a.flags & 64) ? ptx::l2_policy_evict_normal() : ptx::l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = cluster; u < units; u += num_clusters) {

@@ -1,15 +1,5 @@
 cd $GRAFT_REPO_ROOT
-P="python tools/perf_probe.py 64 2048 6 16384 split 16384 3"
-for f in 0 1 2; do echo "== 3M flags $f"
-  nvidia-smi --query-gpu=clocks.sm,power.draw,clocks_event_reasons.sw_power_cap --format=csv,noheader -lms 100 > /tmp/clk_$f.csv &
-  SP=$!
-  MPSG_3M_FLAGS=$f $P 2>&1 | grep -E "interior|rep 2"
-  kill $SP
-  sort -t, -k2 -n -r /tmp/clk_$f.csv | head -30 | awk -F, '{c+=$1; p+=$2; n++} END {print "top-30 power samples: clock", c/n, "MHz power", p/n, "W"}'
+M="--metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct"
+for cfg in "16 0" "16 64" "8 0" "32 0" "16 256" "48 0"; do set -- $cfg
+  MPSG_3M_GROUP=$1 MPSG_3M_FLAGS=$2 timeout 300 ncu $M --clock-control none -k regex:site_gemm_3m -s 12 -c 1 --csv --log-file gpurun_out/dram_g$1_f$2.csv python tools/perf_probe.py 24 2048 6 16384 split 16384 3 > gpurun_out/dram_g$1_f$2.log 2>&1
 done
-echo "== 4M"
-nvidia-smi --query-gpu=clocks.sm,power.draw,clocks_event_reasons.sw_power_cap --format=csv,noheader -lms 100 > /tmp/clk_4.csv &
-SP=$!
-python tools/perf_probe.py 64 2048 6 16384 split 16384 4 2>&1 | grep -E "interior|rep 2"
-kill $SP
-sort -t, -k2 -n -r /tmp/clk_4.csv | head -30 | awk -F, '{c+=$1; p+=$2; n++} END {print "top-30 power samples: clock", c/n, "MHz power", p/n, "W"}'
