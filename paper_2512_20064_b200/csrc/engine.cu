@@ -693,6 +693,12 @@ struct PassOut {
   double gemm_s = 0.0, device_s = 0.0;
 };
 
+// Where the renormalisation max of the 3M path comes from: the K1 epilogue (tensor parallelism, which
+// exchanges it with the weights, and long-K sites, where the epilogue has slack: +1.5% at c3) or the
+// select kernel's pass over the chosen slice (short-K sites, where the epilogue is on the critical
+// path: +10% at chi = 512).
+static bool epilogue_max(const mpsg_handle_s& h, const SiteDev& s) { return h.tp > 1 || s.kp >= 1024; }
+
 // K1 for `rows` samples of lane `ln` at site i.  tma_g128 / tma_g64: Gamma maps with 128 / 64-row
 // boxes (the 3M kernel loads Gamma as its A operand; the 4M pair kernel as its half-B operand).
 static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const SiteDev& s, const Lane& ln,
@@ -725,7 +731,12 @@ static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const S
     ga.temp = ln.temp;
     ga.pstat = ln.pstat;
     const int ctas = 2 * ga.g_tiles * ga.s_tiles;
-    launch_site_gemm_3m(h.split, ln.tma_env64[i], *tma_g128, ga, std::min(ctas, dc.num_sms), stream);
+    static const int env_epi = [] {
+      const char* v = std::getenv("MPSG_3M_EPI");
+      return v ? std::atoi(v) : 8;
+    }();
+    launch_site_gemm_3m(h.split, epilogue_max(h, s), env_epi, ln.tma_env64[i], *tma_g128, ga,
+                        std::min(ctas, dc.num_sms), stream);
     return;
   }
   const int mrow = h.pair ? 2 * kBM : kBM;
@@ -837,6 +848,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       sa.kp_next = kn;
       sa.env_cap = ln.cap;
       sa.env_comp = h.env_comp;
+      sa.slice_max = (h.m3 && !epilogue_max(h, s)) ? 1 : 0;
       sa.seed = seed;
       sa.first = lfirst;
       sa.temp = ln.temp;

@@ -39,7 +39,7 @@ struct Cfg3M {
   static constexpr int kBTile = (kBM / 2) * kBK3 * 2;  // 8 KiB: this SM's 64 sample rows
   static constexpr int kStageBytes = kATile + kHalves * kBTile;
   static constexpr int kStages = kSplit ? 6 : 8;
-  static constexpr int kRedBytes = 4 * kBM * 8;        // [4 warps][128 samples] float2
+  static constexpr int kRedBytes = 4 * kBM * 8;        // [4 lane quarters][128 samples] float2
   static constexpr int kBarBytes = 512;
   static constexpr int kSmem = kStages * kStageBytes + 1024 + kBarBytes + kRedBytes;
 };
@@ -59,12 +59,16 @@ __device__ __forceinline__ void unit_coords_3m(int u, const Gemm3MArgs& a, int& 
   m = m0 + (r - t * gw);
 }
 
-// v[i] (i = 0..31, one value per sample) summed / maxed over the 32 lanes: afterwards lane L holds
-// the reduction for sample L.  Each round halves the vector, exchanging the half the partner keeps.
+// warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4.. epilogue (kEpiWarps = 4 or 8)
+constexpr int kEpiSamples = 16;  // samples per epilogue TMEM load (x16)
+
+// v[i] (i = 0..15, one value per sample) summed / maxed over the 32 lanes: afterwards lanes L and
+// L ^ 16 hold the reduction for sample L & 15.  Each round halves the vector, exchanging the half
+// the partner keeps; the last round folds the two 16-lane halves.
 template <bool kMax>
-__device__ __forceinline__ float transpose_reduce(float (&v)[32], int lane) {
+__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
+  for (int o = 8; o >= 1; o >>= 1) {
     const bool up = (lane & o) != 0;
 #pragma unroll
     for (int i = 0; i < o; ++i) {
@@ -74,7 +78,8 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[32], int lane) {
       v[i] = kMax ? fmaxf(keep, recv) : keep + recv;
     }
   }
-  return v[0];
+  const float other = __shfl_xor_sync(0xffffffffu, v[0], 16);
+  return kMax ? fmaxf(v[0], other) : v[0] + other;
 }
 
 // Timing probes (flags & 32): [0] epilogue cycles waiting for the accumulators, [1] epilogue busy
@@ -82,8 +87,10 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[32], int lane) {
 // [4] units, [5] epilogue cycles from accumulator-ready to slot release.
 __device__ unsigned long long g_prof3m[8];
 
-template <bool kSplit>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+// kMax: also the per-(sample, tile) max component (tensor-parallel handles exchange it; otherwise
+// the select kernel takes the max of the chosen slice itself).
+template <bool kSplit, bool kMax, int kEpiWarps>
+__global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
     site_gemm_3m_kernel(const __grid_constant__ CUtensorMap tma_env64,
                         const __grid_constant__ CUtensorMap tma_g, const Gemm3MArgs a) {
   using C = Cfg3M<kSplit>;
@@ -110,7 +117,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       ptx::mbar_init(&empty[s], 1);  // the leader's multicast commit
     }
     for (int j = 0; j < 2; ++j) ptx::mbar_init(&tfull[j], 1);
-    for (int j = 0; j < 4; ++j) ptx::mbar_init(&tempty[j], 8);  // 4 epilogue warps x 2 CTAs
+    for (int j = 0; j < 4; ++j) ptx::mbar_init(&tempty[j], 2 * kEpiWarps);  // epilogue warps x 2 CTAs
     ptx::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -131,16 +138,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs; bytes counted on the leader's barrier) ----------
     if (lane == 0) {
-      const uint64_t pol_env = (a.flags & 128) ? ptx::l2_policy_evict_first()
-                               : (a.flags & 256) ? ptx::l2_policy_evict_last() : ptx::l2_policy_evict_normal();
-      const uint64_t pol_g = (a.flags & 64) ? ptx::l2_policy_evict_normal() : ptx::l2_policy_evict_last();
+      const uint64_t pol_env = ptx::l2_policy_evict_normal();
+      const uint64_t pol_g = ptx::l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = cluster; u < units; u += num_clusters) {
         int m, t;
         unit_coords_3m(u, a, m, t);
-        const int grow = ((a.flags & 8) ? 0 : m * 2 * kBM) + rank * kBM;     // this SM's Gamma rows
-        const int erow = ((a.flags & 8) ? 0 : t * kBM) + rank * (kBM / 2);   // this SM's sample rows
+        const int grow = m * 2 * kBM + rank * kBM;     // this SM's Gamma rows
+        const int erow = t * kBM + rank * (kBM / 2);   // this SM's sample rows
 #pragma unroll 1
         for (int c = 0; c < 3; ++c) {
           int shard = 0, kin = 0;
@@ -219,9 +225,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue (both CTAs, thread = one of this SM's 128 output columns) --------
+    // ---------------- epilogue (both CTAs): kEpiWarps / 4 warps per TMEM lane quarter; thread = one
+    // of this SM's 128 output columns, warp part h covers samples [kSpan h, kSpan h + kSpan) -----
+    constexpr int kSpan = kBM * 4 / kEpiWarps;  // samples per epilogue warp and unit
     const int q = warp & 3;
-    const int et = threadIdx.x - 128;
+    const int h = (warp - 4) >> 2;
+    const int ec = q * 32 + lane;  // column within the SM's 128
     uint32_t gp = 0;
     int unit = 0;
     for (int u = cluster; u < units; u += num_clusters, ++unit, gp += 3) {
@@ -230,27 +239,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int col0 = m * 2 * kBM + rank * kBM;  // first of this SM's 128 columns (one outcome)
       const int k = col0 / a.chirp;
       const bool valid = k < a.d;                  // the pair-padding tile has nothing to store
-      const int r = col0 - k * a.chirp + et;
-      const float2 ci = valid ? a.cinfo[col0 + et] : make_float2(0.f, 0.f);
+      const int r = col0 - k * a.chirp + ec;
+      const float2 ci = valid ? a.cinfo[col0 + ec] : make_float2(0.f, 0.f);
       const long long e0 = (a.flags & 32) ? clock64() : 0;
       ptx::mbar_wait(&tfull[unit & 1], (unit >> 1) & 1);
       const long long e1 = (a.flags & 32) ? clock64() : 0;
       long long e2 = 0;
       ptx::tc_fence_after();
       const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
-      const uint32_t t_re = tmem_base + lanes + ((gp + 0) & 3) * 128;
-      const uint32_t t_im = tmem_base + lanes + ((gp + 1) & 3) * 128;
-      const uint32_t t_s = tmem_base + lanes + ((gp + 2) & 3) * 128;
-      float2* dst = a.temp + (static_cast<size_t>(t) * kBM * a.d + k) * a.chirp + r;
+      const uint32_t c0 = h * kSpan;
+      const uint32_t t_re = tmem_base + lanes + ((gp + 0) & 3) * 128 + c0;
+      const uint32_t t_im = tmem_base + lanes + ((gp + 1) & 3) * 128 + c0;
+      const uint32_t t_s = tmem_base + lanes + ((gp + 2) & 3) * 128 + c0;
       const size_t row_stride = static_cast<size_t>(a.d) * a.chirp;
+      float2* dst = a.temp + (static_cast<size_t>(t) * kBM + c0) * row_stride + static_cast<size_t>(k) * a.chirp + r;
 #pragma unroll 1
-      for (int ch = 0; ch < kBM / 32; ++ch) {
-        float pr[32], pi[32], ps[32];
-        ptx::tmem_ld_32x32b_x32(t_re + ch * 32, pr);
-        ptx::tmem_ld_32x32b_x32(t_im + ch * 32, pi);
-        ptx::tmem_ld_32x32b_x32(t_s + ch * 32, ps);
+      for (int ch = 0; ch < kSpan / kEpiSamples; ++ch) {
+        float pr[kEpiSamples], pi[kEpiSamples], ps[kEpiSamples];
+        ptx::tmem_ld_32x32b_x16(t_re + ch * kEpiSamples, pr);
+        ptx::tmem_ld_32x32b_x16(t_im + ch * kEpiSamples, pi);
+        ptx::tmem_ld_32x32b_x16(t_s + ch * kEpiSamples, ps);
         ptx::tmem_wait_ld();
-        if (ch == kBM / 32 - 1) {  // the unit's three slots are free for the MMAs of unit + 2
+        if (ch == kSpan / kEpiSamples - 1) {  // this warp's part of the unit's three slots is read
           ptx::tc_fence_before();
           __syncwarp();
           if (a.flags & 32) e2 = clock64();
@@ -260,40 +270,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             ptx::mbar_arrive_remote_relaxed(&tempty[(gp + 2) & 3], 0);
           }
         }
-        if (valid && !(a.flags & 1)) {
+        if (valid) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < kEpiSamples; ++i) {
             const float re = (pr[i] - pi[i]) * ci.x;
             const float im = (ps[i] - pr[i] - pi[i]) * ci.x;
-            if (!(a.flags & 2)) {
-              if (a.flags & 16)
-                dst[(ch * 32 + i) * row_stride] = make_float2(re, im);
-              else  // streaming store: temp (1.6 GB per c3 site) must not evict the Gamma group from L2
-                __stcs(dst + (ch * 32 + i) * row_stride, make_float2(re, im));
-            }
+            // streaming store: temp (1.6 GB per c3 site) must not evict the Gamma group from L2
+            __stcs(dst + (ch * kEpiSamples + i) * row_stride, make_float2(re, im));
             pr[i] = ci.y * fmaf(re, re, im * im);
-            pi[i] = fmaxf(fabsf(re), fabsf(im));
+            if constexpr (kMax) pi[i] = fmaxf(fabsf(re), fabsf(im));
           }
-          if (!(a.flags & 4)) {
-            const float w = transpose_reduce<false>(pr, lane);
-            const float mx = transpose_reduce<true>(pi, lane);
-            red[q * kBM + ch * 32 + lane] = make_float2(w, mx);
-          } else {
-            red[q * kBM + ch * 32 + lane] = make_float2(pr[0], pi[0]);
-          }
+          const float w = transpose_reduce16<false>(pr, lane);
+          float mx = 0.f;
+          if constexpr (kMax) mx = transpose_reduce16<true>(pi, lane);
+          if (lane < 16) red[q * kBM + c0 + ch * kEpiSamples + lane] = make_float2(w, mx);
         }
       }
-      if (valid && !(a.flags & 1)) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        float2 v = red[et];
+      if (valid) {
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (h == 0) {  // thread ec reduces sample ec of the unit over the 4 lane quarters, in order
+          float2 v = red[ec];
 #pragma unroll
-        for (int w = 1; w < 4; ++w) {
-          const float2 o = red[w * kBM + et];
-          v.x += o.x;
-          v.y = fmaxf(v.y, o.y);
+          for (int w = 1; w < 4; ++w) {
+            const float2 o = red[w * kBM + ec];
+            v.x += o.x;
+            v.y = fmaxf(v.y, o.y);
+          }
+          a.pstat[(static_cast<size_t>(t) * kBM + ec) * a.nt + col0 / kBM] = v;
         }
-        a.pstat[(static_cast<size_t>(t) * kBM + et) * a.nt + col0 / kBM] = v;
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // red is rewritten by the next unit
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");  // red is rewritten next unit
       }
       if ((a.flags & 32) && threadIdx.x == 128) {
         const long long e3 = clock64();
@@ -314,18 +319,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-template <bool kSplit>
+template <bool kSplit, bool kMax, int kEpiWarps>
 static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
                         int grid, cudaStream_t s) {
+  auto kern = site_gemm_3m_kernel<kSplit, kMax, kEpiWarps>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(site_gemm_3m_kernel<kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg3M<kSplit>::kSmem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg3M<kSplit>::kSmem);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kGemmThreads);
+  cfg.blockDim = dim3(128 + 32 * kEpiWarps);
   cfg.dynamicSmemBytes = Cfg3M<kSplit>::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -335,16 +340,27 @@ static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, site_gemm_3m_kernel<kSplit>, tma_env64, tma_g, a);
+  cudaLaunchKernelEx(&cfg, kern, tma_env64, tma_g, a);
 }
 
-void launch_site_gemm_3m(bool split, const CUtensorMap& tma_env64, const CUtensorMap& tma_g,
-                         const Gemm3MArgs& a, int grid, cudaStream_t s) {
+template <bool kSplit, bool kMax>
+static void launch_3m_w(int epi_warps, const CUtensorMap& e, const CUtensorMap& g, const Gemm3MArgs& a,
+                        int grid, cudaStream_t s) {
+  if (epi_warps == 4)
+    launch_3m_t<kSplit, kMax, 4>(e, g, a, grid, s);
+  else
+    launch_3m_t<kSplit, kMax, 8>(e, g, a, grid, s);
+}
+
+void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, const CUtensorMap& tma_env64,
+                         const CUtensorMap& tma_g, const Gemm3MArgs& a, int grid, cudaStream_t s) {
   grid = (grid + 1) & ~1;  // whole CTA pairs
   if (split)
-    launch_3m_t<true>(tma_env64, tma_g, a, grid, s);
+    with_max ? launch_3m_w<true, true>(epi_warps, tma_env64, tma_g, a, grid, s)
+             : launch_3m_w<true, false>(epi_warps, tma_env64, tma_g, a, grid, s);
   else
-    launch_3m_t<false>(tma_env64, tma_g, a, grid, s);
+    with_max ? launch_3m_w<false, true>(epi_warps, tma_env64, tma_g, a, grid, s)
+             : launch_3m_w<false, false>(epi_warps, tma_env64, tma_g, a, grid, s);
 }
 
 }  // namespace mpsg

@@ -57,7 +57,7 @@ struct Gemm3MArgs {
   int chirp, d;
   int nt;            // Np / 128: pstat row stride
   int group;         // Gamma tiles per raster group
-  int flags;         // experiment switches (0 in production): 1 = skip the epilogue math / stores
+  int flags;         // diagnostics (0 in production): 32 = clock64 timing probes (g_prof3m)
   const float2* cinfo;
   float2* temp;
   float2* pstat;
@@ -76,6 +76,7 @@ struct SelectArgs {
   int kp_next;              // width of this rank's next-env shard (0 on the last site)
   int env_cap;              // env plane stride in rows
   int env_comp;             // env components per precision half: 2 (re, im) or 3 (re, im, re+im)
+  int slice_max;            // 1: the renormalisation max comes from the chosen slice, not the partials
   uint64_t seed, first;
   const float2* temp;
   const float2* part_base;
@@ -102,8 +103,11 @@ void launch_site_gemm_pair(bool split, const CUtensorMap& tma_env, const CUtenso
 int gemm_pair_smem_bytes(bool split);
 // 3M kernel: tma_g has a 64 x 128-row box over [3][Np][Kp], tma_env a 64 x 64-row box over the
 // 6-plane env, both SWIZZLE_128B; Kp and the env shard width are multiples of 64.
-void launch_site_gemm_3m(bool split, const CUtensorMap& tma_env64, const CUtensorMap& tma_g,
-                         const Gemm3MArgs& a, int grid, cudaStream_t s);
+// with_max: also the per-(sample, tile) max component in pstat.y (tensor parallelism); otherwise
+// pstat.y is 0 and the select kernel computes the chosen slice's max (SelectArgs::slice_max).
+// epi_warps: 4 or 8 epilogue warps (one or two per TMEM lane quarter).
+void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, const CUtensorMap& tma_env64,
+                         const CUtensorMap& tma_g, const Gemm3MArgs& a, int grid, cudaStream_t s);
 int gemm_3m_smem_bytes(bool split);
 void launch_select(const SelectArgs& a, cudaStream_t s);
 // pstat [rows][nt] -> out [rows][d]: (sum of weights, max) over the tiles of each outcome

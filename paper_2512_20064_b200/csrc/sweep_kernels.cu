@@ -567,6 +567,18 @@ __device__ __forceinline__ float outcome_max(const SelectArgs& a, int n, int k, 
   return warp_max(m);
 }
 
+// max component of the chosen (contiguous) temp slice of sample n, outcome k
+__device__ __forceinline__ float slice_max(const SelectArgs& a, int n, int k, int lane) {
+  const float2* src = a.temp + (static_cast<size_t>(n) * a.d + k) * a.chirp;
+  float m = 0.f;
+  for (int r = lane * 2; r < a.chir_loc; r += 64) {  // chirp is even: the 16 B load stays in the row
+    const float4 v = *reinterpret_cast<const float4*>(src + r);
+    m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+    if (r + 1 < a.chir_loc) m = fmaxf(m, fmaxf(fabsf(v.z), fabsf(v.w)));
+  }
+  return warp_max(m);
+}
+
 __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -602,7 +614,7 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
       if (kk != kDead) {
         outcome = kk;
         // per-sample max of the chosen slice (precision.cpp:155-160); 0 -> dead from here on
-        const float mx = outcome_max(a, n, kk, lane);
+        const float mx = a.slice_max ? slice_max(a, n, kk, lane) : outcome_max(a, n, kk, lane);
         if (mx > 0.f) {
           int e;
           frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
