@@ -37,11 +37,16 @@ CONFIGS = {
     "c2": dict(M=256, chi=512, d=6, job=100_000, desc="c2: M=256, chi=512, d=6, N=1e5 (whole MPS in HBM)"),
     "c3": dict(M=1024, chi=2048, d=6, job=1_000_000, desc="c3: M=1024, chi=2048, d=6, N=1e6 data-parallel"),
 }
+# c4 slice: the first 64 sites of the c4 chain shape (chi = 1e4, d = 4: 2.4 GB of 3M planes per
+# interior site) on one GPU with Gamma streamed from pinned host memory -- the per-site work of the
+# M = 8176 chain, which needs TP over 8 GPUs and 19.6 TB of host / disk storage
+CONFIGS["c4s"] = dict(M=64, chi=10000, d=4, job=1_000_000, stream=3,
+                      desc="c4 slice: M=64 sites of the c4 shape (chi=1e4, d=4), N=1e6, Gamma host-streamed")
 for _chi in (256, 512, 1024, 2048, 4096):
     CONFIGS[f"c5_{_chi}"] = dict(M=512, chi=_chi, d=4, job=100_000,
                                  desc=f"c5: bond-dimension sweep M=512, chi={_chi}, d=4, N=1e5")
 DEFAULT_PASS = {"c1": 1000, "c2": 32768, "c3": 16384, "c5_256": 65536, "c5_512": 32768,
-                "c5_1024": 32768, "c5_2048": 16384, "c5_4096": 8192}
+                "c5_1024": 32768, "c5_2048": 16384, "c5_4096": 8192, "c4s": 8192}
 
 
 def peaks():
@@ -112,6 +117,23 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------------
 # CPU reference timing (oracle/_ref = the reference compiled from its own sources)
 # ---------------------------------------------------------------------------------------------
+def measure_link_gbs(device: int, nbytes: int = 1 << 30, reps: int = 4) -> float:
+    """Pinned host -> device copy bandwidth (best of `reps`, CUDA events): the host-link roofline."""
+    import torch
+    src = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+    best = 0.0
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = max(best, nbytes / (a.elapsed_time(b) * 1e-3) / 1e9)
+    del src, dst
+    return best
+
+
 def host_mem_available() -> int:
     try:
         with open("/proc/meminfo") as f:
@@ -162,7 +184,7 @@ def run_reference_arm(args, cfg):
     macs_per_sample, _ = chain_macs(cfg["M"], cfg["chi"], cfg["d"])
     vals = []
     for step in range(args.warmup + args.steps):
-        rate, threads, kind, sample, secs = cpu_reference_rate(cfg["chi"], cfg["d"], target_s=args.ref_seconds)
+        rate, threads, kind, sample, secs = cpu_reference_rate(min(cfg["chi"], 4096), cfg["d"], target_s=args.ref_seconds)
         if step >= args.warmup:
             vals.append(rate / macs_per_sample)
     v = statistics.median(vals)
@@ -201,6 +223,8 @@ def main():
                          "through this many device slots (0 = resident in HBM)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if not args.stream_slots and cfg.get("stream"):
+        args.stream_slots = cfg["stream"]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
         return
@@ -317,6 +341,16 @@ def main():
     value = P_pass * world * args.steps / t_max
     burst, sustained, hbm, src = peaks()
     achieved = gemm_flops / gemm_s / 1e12 if gemm_s > 0 else None
+    # north-star roofline: the slower of the GEMM at tensor peak and the Gamma bytes over the link
+    # (host-streamed) -- per step, on this rank
+    link = None
+    if args.stream_slots and rank == 0:
+        link_gbs = measure_link_gbs(local)
+        t_tensor = gemm_flops / args.steps / (sustained * 1e12)
+        t_link = h2d / args.steps / (link_gbs * 1e9)
+        link = {"h2d_gb_per_step": h2d / args.steps / 1e9, "link_peak_gbs": link_gbs,
+                "achieved_gbs": h2d / t_max / 1e9, "t_link_s": t_link, "t_tensor_s": t_tensor,
+                "bound": "link" if t_link > t_tensor else "tensor"}
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.mode}_p{P_pass}.json")
     if os.path.exists(prof):
@@ -326,7 +360,10 @@ def main():
             traffic = tj.get("bytes_per_launch")
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, threads, kind, sample, secs = cpu_reference_rate(cfg["chi"], cfg["d"], target_s=args.ref_seconds)
+        # the reference's per-MAC rate is flat in chi at this size; a chi <= 4096 site keeps host memory
+        # free for a host-streamed state (c4s)
+        rate, threads, kind, sample, secs = cpu_reference_rate(min(cfg["chi"], 4096), cfg["d"],
+                                                               target_s=args.ref_seconds)
         cpu = {"value": rate / macs_per_sample, "unit": "samples/s", "cores": threads, "kind": kind,
                "sample": sample, "seconds": round(secs, 2)}
     if rank == 0:
@@ -358,6 +395,7 @@ def main():
                          "frac_of_burst": achieved / burst if achieved else None,
                          "gemm_share_of_step": gemm_s / dev_s if dev_s > 0 else None},
             "cpu_baseline": cpu,
+            "host_link": link,
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": e2e_h2d // max(args.e2e_steps, 1),
                     "d2h_bytes_per_step": P_pass * cfg["M"], "mode": e2e_mode,
                     "note": ("mpsg_sample (C ABI) with host output rows; the compressed MPS lives in pinned host "

@@ -1,7 +1,5 @@
 cd $GRAFT_REPO_ROOT
-b() { timeout 600 env "$@" python bench.py --no-cpu-baseline --e2e resident --e2e-steps 1 --steps 4 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['roofline']['issued_frac'], d['roofline']['gemm_share_of_step'], d['clocks']['sm_mhz'], d['clocks']['power_w_median'])"; }
-echo "epi8"; b MPSG_3M_EPI=8
-echo "epi4"; b MPSG_3M_EPI=4
-echo "epi4 max"; b MPSG_3M_EPI=4 MPSG_3M_MAX=1
-echo "epi8 max"; b MPSG_3M_EPI=8 MPSG_3M_MAX=1
-echo "epi8"; b MPSG_3M_EPI=8
+for sc in 4m 3m; do
+timeout 1500 python bench.py --config c4s --scheme $sc --steps 3 --warmup 2 --e2e-steps 1 --no-cpu-baseline > gpurun_out/bench_c4s_$sc.json 2> gpurun_out/bench_c4s_$sc.err
+python -c "import json; d=json.load(open('gpurun_out/bench_c4s_$sc.json')); print('$sc', d['value'], d['roofline']['issued_frac'], d['clocks']['sm_mhz'], d['host_link'], d['e2e']['value'])"
+done
