@@ -68,6 +68,39 @@ def test_abi_config_validation_precedes_device():
     assert _begin([1, 4, 1], d=300) == _lib.MPSG_ERR_CONFIG   # u8 outcomes
 
 
+def test_abi_scheme_option_validated_before_device():
+    """mpsg_options.scheme: only AUTO / 3M / 4M are accepted (ConfigError before any device work)."""
+    L = _lib.lib()
+    bd = (C.c_uint64 * 3)(1, 4, 1)
+    pol = _lib.Policy(0, 0, 0)
+    for bad in (1, 2, 5, -1):
+        h = C.c_void_p()
+        opt = _lib.Options(scheme=bad)
+        assert L.mpsg_builder_begin(2, 2, bd, C.byref(pol), C.byref(opt), None, 0, C.byref(h)) == _lib.MPSG_ERR_CONFIG
+    assert L.mpsg_scheme(None) == 0
+    assert [int(x) for x in P.Scheme] == [0, 3, 4]
+
+
+def test_options_struct_layout_matches_header(tmp_path):
+    """The ctypes mirrors of mpsg_options / mpsg_stats have the header's layout (gcc offsetof)."""
+    import subprocess
+    fields = [f for f, _ in _lib.Options._fields_]
+    sfields = [f for f, _ in _lib.Stats._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "mpsg.h"\nint main(void){\n'
+                   + "".join(f'printf("%zu ", offsetof(mpsg_options, {f}));' for f in fields)
+                   + 'printf("%zu\\n", sizeof(mpsg_options));'
+                   + "".join(f'printf("%zu ", offsetof(mpsg_stats, {f}));' for f in sfields)
+                   + 'printf("%zu\\n", sizeof(mpsg_stats)); return 0;}\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    lines = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    want_o = [getattr(_lib.Options, f).offset for f in fields] + [C.sizeof(_lib.Options)]
+    want_s = [getattr(_lib.Stats, f).offset for f in sfields] + [C.sizeof(_lib.Stats)]
+    assert [int(x) for x in lines[0].split()] == want_o
+    assert [int(x) for x in lines[1].split()] == want_s
+
+
 # ---- host mirror of the reference interface ----------------------------------------------------
 def test_batch_plan_normalize_matches_reference():
     p = P.BatchPlan(1000, 0, 5000)
