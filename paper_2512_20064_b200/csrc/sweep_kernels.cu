@@ -588,13 +588,34 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
   bool live_out = false; // carries into the next site
   float scale = 0.f;
   if (live_in) {
+    // Born weights of the outcomes (sampler.cpp:83-90): for d <= 32 lane k owns outcome k and sums
+    // its tile partials sequentially in f64 (fixed order); the totals and the CDF walk broadcast the
+    // per-lane weights in ascending k, exactly the reference's accumulation order over k.
+    const bool by_lane = a.d <= 32;
+    double wk = 0.0;
+    float mk = 0.f;
+    if (by_lane && lane < a.d) {
+      const float2* base = a.part_base + n * a.row_stride + lane * a.k_stride;
+      for (int t = 0; t < a.parts; ++t) {
+        const float2 v = base[t * a.part_stride];
+        wk += static_cast<double>(v.x);
+        mk = fmaxf(mk, v.y);
+      }
+    }
+    auto weight = [&](int k) -> double {
+      return by_lane ? __shfl_sync(0xffffffffu, wk, k) : outcome_weight(a, n, k, lane);
+    };
     double total = 0.0;  // sampler.cpp:92-93, ascending k
-    for (int k = 0; k < a.d; ++k) total += outcome_weight(a, n, k, lane);
+    for (int k = 0; k < a.d; ++k) total += weight(k);
     if (a.marg != nullptr) {
       double* mrow = a.marg + (static_cast<size_t>(n) * a.num_sites + a.site) * a.d;
-      for (int k = 0; k < a.d; ++k) {
-        const double wk = outcome_weight(a, n, k, lane);
-        if (lane == 0) mrow[k] = total == 0.0 ? -1.0 : wk / total;
+      if (by_lane) {
+        if (lane < a.d) mrow[lane] = total == 0.0 ? -1.0 : wk / total;
+      } else {
+        for (int k = 0; k < a.d; ++k) {
+          const double w = outcome_weight(a, n, k, lane);
+          if (lane == 0) mrow[k] = total == 0.0 ? -1.0 : w / total;
+        }
       }
     }
     if (total != 0.0) {  // total == 0 -> dead (sampler.cpp:94-98)
@@ -606,7 +627,7 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
         double cum = 0.0;
         kk = 0;
         for (int k = 0; k < a.d; ++k) {  // sampler.cpp:100-106: strict '>', no early break
-          cum += outcome_weight(a, n, k, lane) / total;
+          cum += weight(k) / total;
           if (draw > cum) ++kk;
         }
         if (kk >= a.d) kk = a.d - 1;  // :107
@@ -614,7 +635,11 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
       if (kk != kDead) {
         outcome = kk;
         // per-sample max of the chosen slice (precision.cpp:155-160); 0 -> dead from here on
-        const float mx = a.slice_max ? slice_max(a, n, kk, lane) : outcome_max(a, n, kk, lane);
+        float mx;
+        if (a.slice_max)
+          mx = slice_max(a, n, kk, lane);
+        else
+          mx = by_lane ? __shfl_sync(0xffffffffu, mk, kk) : outcome_max(a, n, kk, lane);
         if (mx > 0.f) {
           int e;
           frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
