@@ -204,6 +204,20 @@ int mpsg_sample_device(mpsg_handle h, uint64_t seed, uint64_t first, uint64_t co
 int mpsg_marginals(mpsg_handle h, uint64_t first, uint64_t count, const uint8_t* forced,
                    double* marg);
 
+/* ---- GBS displacement: the SiteTransform hook (sampler.hpp:71-79, applied at sampler.cpp:143)
+ * specialised to the paper's displacement operators (SPEC.md gbs-ops, §3.4).  mu is
+ * complex128 (count, M) row-major: sample n of the range is displaced by D(mu[n][i]) at site i,
+ * temp[n, b, :] <- D temp[n, b, :] between the contraction and the measurement; D(mu) =
+ * exp(-|mu|^2/2) exp(mu a^dag) exp(-conj(mu) a) in closed form (exact Fock-basis elements).
+ * phys_dim <= 16.  The reference's src/gbs.cpp is absent; parity is against the oracle's
+ * restatement of SPEC.md:366-381 (oracle/mpsamp_oracle.c orc_displacement). */
+int mpsg_sample_displaced(mpsg_handle h, uint64_t seed, uint64_t first, uint64_t count,
+                          const double* mu, uint8_t* rows, mpsg_stats* stats);
+int mpsg_marginals_displaced(mpsg_handle h, uint64_t first, uint64_t count, const uint8_t* forced,
+                             const double* mu, double* marg);
+/* expm_displacement on the device: D(mu), n x n complex128 row-major (n <= 64). */
+int mpsg_displacement_matrix(double mu_re, double mu_im, uint64_t n, double* out);
+
 /* The device RNG: draws[j] = uniform(seed, 0x6d656173, first + j, site) computed by the GPU
  * (detail::measurement_draws, sampler.cpp:120-127). */
 int mpsg_device_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, double* out);

@@ -272,12 +272,82 @@ void orc_scale_rows(double* env, size_t count, size_t row, int mode, uint8_t* al
     }
 }
 
+/* ---- GBS displacement (SPEC.md gbs-ops, §3.4 Eq. 6) ------------------------------
+ * expm_displacement: D(mu) = exp(-|mu|^2/2) L U with L = exp(mu a^dag) lower triangular,
+ * L[a][b] = mu^(a-b) sqrt(a!/b!) / (a-b)!, and U = exp(-conj(mu) a) upper triangular,
+ * U[b][c] = (-conj(mu))^(c-b) sqrt(c!/b!) / (c-b)! (closed form, no iterative
+ * expm; factorial ratios through lgamma).  out: n x n complex, row-major D[a][c] interleaved. */
+static void cpow_int(double re, double im, int k, double* ore, double* oim) {
+    double r = 1.0, i = 0.0;
+    for (int j = 0; j < k; ++j) {
+        const double t = r * re - i * im;
+        i = r * im + i * re;
+        r = t;
+    }
+    *ore = r;
+    *oim = i;
+}
+
+void orc_displacement(double mu_re, double mu_im, size_t n, double* out) {
+    const double pre = exp(-0.5 * (mu_re * mu_re + mu_im * mu_im));
+    for (size_t a = 0; a < n; ++a)
+        for (size_t c = 0; c < n; ++c) {
+            double sr = 0.0, si = 0.0;
+            const size_t bmax = a < c ? a : c;
+            for (size_t b = 0; b <= bmax; ++b) {
+                double lr, li, ur, ui;
+                cpow_int(mu_re, mu_im, (int)(a - b), &lr, &li);
+                cpow_int(-mu_re, mu_im, (int)(c - b), &ur, &ui); /* -conj(mu) */
+                const double fl = exp(0.5 * (lgamma((double)a + 1) - lgamma((double)b + 1)) - lgamma((double)(a - b) + 1));
+                const double fu = exp(0.5 * (lgamma((double)c + 1) - lgamma((double)b + 1)) - lgamma((double)(c - b) + 1));
+                lr *= fl, li *= fl, ur *= fu, ui *= fu;
+                sr += lr * ur - li * ui;
+                si += lr * ui + li * ur;
+            }
+            out[2 * (a * n + c)] = pre * sr;
+            out[2 * (a * n + c) + 1] = pre * si;
+        }
+}
+
+/* apply_displacement as the reference's SiteTransform hook: temp (count, chi, d)
+ * row-major, temp[n, b, :] <- D(mu[n]) temp[n, b, :] */
+static void apply_displacement(double* temp, size_t count, size_t chi, size_t d, const double* mu,
+                               size_t mu_stride, double* dbuf, double* v) {
+    for (size_t n = 0; n < count; ++n) {
+        orc_displacement(mu[2 * n * mu_stride], mu[2 * n * mu_stride + 1], d, dbuf);
+        for (size_t b = 0; b < chi; ++b) {
+            double* t = temp + 2 * (n * chi + b) * d;
+            memcpy(v, t, sizeof(double) * 2 * d);
+            for (size_t k = 0; k < d; ++k) {
+                double sr = 0.0, si = 0.0;
+                for (size_t q = 0; q < d; ++q) {
+                    const double dr = dbuf[2 * (k * d + q)], di = dbuf[2 * (k * d + q) + 1];
+                    sr += dr * v[2 * q] - di * v[2 * q + 1];
+                    si += dr * v[2 * q + 1] + di * v[2 * q];
+                }
+                t[2 * k] = sr;
+                t[2 * k + 1] = si;
+            }
+        }
+    }
+}
+
 /* ---- the site loop: detail::sample_micro_serial sampler.cpp:129-162 ----------------------- */
 
 int orc_sample_range(size_t m, size_t d, const size_t* bonds, const double* const* gamma,
                      const double* const* lambda, uint64_t first, size_t count, uint64_t seed,
                      int compute, int scaling, const uint8_t* forced, uint8_t* rows,
                      double* marg, uint64_t* contraction_macs) {
+    return orc_sample_range_displaced(m, d, bonds, gamma, lambda, first, count, seed, compute, scaling,
+                                      forced, NULL, rows, marg, contraction_macs);
+}
+
+/* Same with the GBS displacement hook (sampler.cpp:143: site_transform between contract_site and
+ * the draws): mu = NULL or complex128 (count, m), mu[n][i] the displacement of sample n at site i. */
+int orc_sample_range_displaced(size_t m, size_t d, const size_t* bonds, const double* const* gamma,
+                               const double* const* lambda, uint64_t first, size_t count, uint64_t seed,
+                               int compute, int scaling, const uint8_t* forced, const double* mu,
+                               uint8_t* rows, double* marg, uint64_t* contraction_macs) {
     size_t maxchi = 1;
     for (size_t i = 0; i <= m; ++i) maxchi = bonds[i] > maxchi ? bonds[i] : maxchi;
     double* env = (double*)malloc(sizeof(double) * 2 * count * maxchi);
@@ -288,6 +358,8 @@ int orc_sample_range(size_t m, size_t d, const size_t* bonds, const double* cons
     uint8_t* oc = (uint8_t*)malloc(count);
     double* w = marg ? (double*)malloc(sizeof(double) * count * d) : NULL;
     int rc = 0;
+    double* dbuf = (double*)malloc(sizeof(double) * 2 * d * d);
+    double* dvec = (double*)malloc(sizeof(double) * 2 * d);
     for (size_t n = 0; n < count; ++n) { /* :136-138 */
         env[2 * n] = 1.0;
         env[2 * n + 1] = 0.0;
@@ -299,6 +371,7 @@ int orc_sample_range(size_t m, size_t d, const size_t* bonds, const double* cons
         rc = orc_contract_site(env, count, cl, gamma[i], cr, d, compute, temp);
         if (rc) break;
         if (contraction_macs) *contraction_macs += (uint64_t)count * cl * cr * d; /* contract.cpp:97-100 */
+        if (mu) apply_displacement(temp, count, cr, d, mu + 2 * i, m, dbuf, dvec); /* sampler.cpp:143 */
         for (size_t j = 0; j < count; ++j) draws[j] = orc_uniform(seed, ORC_MEASURE_STREAM, first + j, i);
         orc_measure(temp, count, cr, d, lambda[i], draws, alive, oc, next, w);
         if (forced) { /* teacher forcing: continue along the given outcome string */
@@ -331,6 +404,8 @@ int orc_sample_range(size_t m, size_t d, const size_t* bonds, const double* cons
     free(alive);
     free(oc);
     free(w);
+    free(dbuf);
+    free(dvec);
     return rc;
 }
 

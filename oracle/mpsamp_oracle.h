@@ -31,6 +31,11 @@ int orc_sample_range(size_t m, size_t d, const size_t* bonds, const double* cons
                      const double* const* lambda, uint64_t first, size_t count, uint64_t seed,
                      int compute, int scaling, const uint8_t* forced, uint8_t* rows,
                      double* marg, uint64_t* contraction_macs);
+int orc_sample_range_displaced(size_t m, size_t d, const size_t* bonds, const double* const* gamma,
+                               const double* const* lambda, uint64_t first, size_t count, uint64_t seed,
+                               int compute, int scaling, const uint8_t* forced, const double* mu,
+                               uint8_t* rows, double* marg, uint64_t* contraction_macs);
+void orc_displacement(double mu_re, double mu_im, size_t n, double* out);
 void orc_capped_bond_dims(size_t m, size_t d, size_t chi_max, size_t* out);
 uint64_t orc_fnv1a(const uint8_t* p, size_t n);
 uint64_t orc_site_step(const double* gamma, size_t chil, size_t chir, size_t d, const double* lambda,

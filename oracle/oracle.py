@@ -63,6 +63,11 @@ def orc():
         L.orc_sample_range.argtypes = [_sz, _sz, C.POINTER(_sz), C.POINTER(_pd), C.POINTER(_pd),
                                        _u64, _sz, _u64, _int, _int, _pu8, _pu8, _pd,
                                        C.POINTER(_u64)]
+        L.orc_sample_range_displaced.restype = _int
+        L.orc_sample_range_displaced.argtypes = [_sz, _sz, C.POINTER(_sz), C.POINTER(_pd), C.POINTER(_pd),
+                                                 _u64, _sz, _u64, _int, _int, _pu8, _pd, _pu8, _pd,
+                                                 C.POINTER(_u64)]
+        L.orc_displacement.argtypes = [_dbl, _dbl, _sz, _pd]
         L.orc_capped_bond_dims.argtypes = [_sz, _sz, _sz, C.POINTER(_sz)]
         L.orc_fnv1a.restype = _u64
         L.orc_fnv1a.argtypes = [_pu8, _sz]
@@ -250,9 +255,17 @@ class RefState:
         return s, macs.value
 
 
+def orc_displacement(mu: complex, n: int) -> np.ndarray:
+    """expm_displacement closed form: D(mu) = exp(-|mu|^2/2) L U, n x n."""
+    out = np.empty((n, n), np.complex128)
+    orc().orc_displacement(float(np.real(mu)), float(np.imag(mu)), n, out.ctypes.data_as(_pd))
+    return out
+
+
 def orc_sample_range(mps: Mps, first, count, seed, compute=F64, scaling=SCALE_PER_SAMPLE,
-                     forced=None, want_marginals=False):
-    """Plain-C restatement of detail::sample_micro_serial (sampler.cpp:129-162)."""
+                     forced=None, want_marginals=False, mu=None):
+    """Plain-C restatement of detail::sample_micro_serial (sampler.cpp:129-162); mu (count, M)
+    complex applies the GBS displacement D(mu[n, i]) as the site transform (sampler.cpp:143)."""
     keep, bd, gp, lp = mps.arrays()
     m, d = mps.num_sites, mps.phys_dim
     rows = np.empty((count, m), np.uint8)
@@ -262,10 +275,15 @@ def orc_sample_range(mps: Mps, first, count, seed, compute=F64, scaling=SCALE_PE
         forced = np.ascontiguousarray(forced, np.uint8)
         f = forced.ctypes.data_as(_pu8)
     macs = _u64()
-    rc = orc().orc_sample_range(m, d, bd, gp, lp, first, count, seed, compute, scaling, f,
-                                rows.ctypes.data_as(_pu8),
-                                marg.ctypes.data_as(_pd) if marg is not None else None,
-                                C.byref(macs))
+    mu_p = None
+    if mu is not None:
+        mu = np.ascontiguousarray(mu, np.complex128)
+        assert mu.shape == (count, m)
+        mu_p = mu.ctypes.data_as(_pd)
+    rc = orc().orc_sample_range_displaced(m, d, bd, gp, lp, first, count, seed, compute, scaling, f, mu_p,
+                                          rows.ctypes.data_as(_pu8),
+                                          marg.ctypes.data_as(_pd) if marg is not None else None,
+                                          C.byref(macs))
     if rc != 0:
         raise OracleError(rc, "oracle numeric error (non-finite input)")
     return (rows, marg, macs.value) if want_marginals else (rows, macs.value)

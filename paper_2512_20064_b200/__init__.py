@@ -15,6 +15,7 @@ from .sampler import (  # noqa: F401
     ConfigError,
     DeviceError,
     DimensionError,
+    Displacement,
     Error,
     GpuSampler,
     IoError,
@@ -31,6 +32,7 @@ from .sampler import (  # noqa: F401
     capped_bond_dims,
     decay_probe,
     device_draws,
+    displacement_matrix,
     sample_batch,
     sample_micro_serial,
 )

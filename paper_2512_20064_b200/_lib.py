@@ -58,6 +58,9 @@ SIGNATURES = [
     ("mpsg_sample", _int, [C.c_void_p, _u64, _u64, _u64, _pu8, C.POINTER(Stats)]),
     ("mpsg_sample_device", _int, [C.c_void_p, _u64, _u64, _u64, C.c_void_p, C.POINTER(Stats)]),
     ("mpsg_marginals", _int, [C.c_void_p, _u64, _u64, _pu8, _pd]),
+    ("mpsg_sample_displaced", _int, [C.c_void_p, _u64, _u64, _u64, _pd, _pu8, C.POINTER(Stats)]),
+    ("mpsg_marginals_displaced", _int, [C.c_void_p, _u64, _u64, _pu8, _pd, _pd]),
+    ("mpsg_displacement_matrix", _int, [_dbl, _dbl, _u64, _pd]),
     ("mpsg_device_draws", _int, [_u64, _u64, _u64, _u64, _pd]),
     ("mpsg_contract_site", _int, [C.c_void_p, _u64, _pd, _u64, _pd]),
     ("mpsg_create_from_file", _int, [C.c_char_p, C.POINTER(Policy), C.POINTER(Options),

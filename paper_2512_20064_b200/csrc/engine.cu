@@ -279,6 +279,7 @@ struct Lane {
   uint8_t* forced = nullptr;      // [cap][M] (lazy)
   double* marg = nullptr;         // [cap][M][d] (lazy)
   double* logscale = nullptr;     // [cap] (lazy, decay trace)
+  double2* mu = nullptr;          // [cap][M] displacement amplitudes of the pass (lazy)
   uint8_t* host_rows = nullptr;   // pinned [cap][M]
   std::vector<CUtensorMap> tma_env;    // per site: the shard-major env map over this lane's env
   std::vector<CUtensorMap> tma_env64;  // same with a 64-row box (3M kernel: env is the B operand)
@@ -511,6 +512,7 @@ static void free_device(DevCtx& dc) {
     cudaFree(ln.forced);
     cudaFree(ln.marg);
     cudaFree(ln.logscale);
+    cudaFree(ln.mu);
     if (ln.host_rows) cudaFreeHost(ln.host_rows);
     if (ln.k1done) cudaEventDestroy(ln.k1done);
     if (ln.done) cudaEventDestroy(ln.done);
@@ -763,7 +765,8 @@ static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const S
 // Enqueues one pass of `count` (<= dc.cap) samples starting at global index `first`, split over
 // the lanes.  Lane L covers [first + off[L], first + off[L] + cnt[L]).
 static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first, int count,
-                     bool forced, bool marg, PassOut& po, int timing, int off[2], int cnt[2]) {
+                     bool forced, bool marg, bool displaced, PassOut& po, int timing, int off[2],
+                     int cnt[2]) {
   const int nl = static_cast<int>(dc.lanes.size());
   const int mrow = (h.pair && !h.m3) ? 2 * kBM : kBM;
   off[0] = 0;
@@ -811,6 +814,25 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[2 * i], ln.stream));
       launch_contraction(h, dc, s, ln, i, rows[L], tma_g128, *tma_g64, cinfo, ln.stream);
       if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[2 * i + 1], ln.stream));
+      if (displaced) {  // the SiteTransform hook position (sampler.cpp:143): after contract_site
+        DisplaceArgs da;
+        da.d = static_cast<int>(h.d);
+        da.chirp = s.chirp;
+        da.chir_loc = s.width;
+        da.nt = s.nt;
+        da.tpk = s.chirp / kBN;
+        da.rows = rows[L];
+        da.count = cnt[L];
+        da.site = static_cast<int>(i);
+        da.num_sites = static_cast<int>(h.M);
+        da.mu = ln.mu;
+        da.alive = ln.alive;
+        da.cinfo = cinfo;
+        da.temp = ln.temp;
+        da.pstat = ln.pstat;
+        launch_displace(da, ln.stream);
+        po.launches += 1;
+      }
       if (active == 2) CUDA_OK(cudaEventRecord(ln.k1done, ln.stream));
       if (dc.slots) {  // K1 is the only reader of the slot: hand it back to the copy stream
         CUDA_OK(cudaEventRecord(dc.freed[slot], dc.stream));
@@ -888,7 +910,8 @@ struct RangeResult {
 // Samples [first, first+count) on one device; rows_host may be null when rows_dev_out is set.
 static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first,
                       uint64_t count, uint8_t* rows_host, uint8_t* rows_dev_out,
-                      const uint8_t* forced_host, double* marg_host, RangeResult& rr) {
+                      const uint8_t* forced_host, double* marg_host, const double* mu_host,
+                      RangeResult& rr) {
   try {
     CUDA_OK(cudaSetDevice(dc.device));
     const int timing = h.opts.record_site_times;
@@ -912,6 +935,9 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
       CUDA_OK(cudaMemsetAsync(dc.trace, 0, h.M * sizeof(double), dc.stream));
       CUDA_OK(cudaStreamSynchronize(dc.stream));
     }
+    if (mu_host)
+      for (auto& ln : dc.lanes)
+        if (!ln.mu) CUDA_OK(cudaMalloc(&ln.mu, sizeof(double2) * ln.cap * h.M));
     if (forced_host || marg_host)
       for (auto& ln : dc.lanes)
         if (!ln.forced) {
@@ -937,9 +963,16 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
             if (tmp_cnt[L] > 0)
               CUDA_OK(cudaMemcpyAsync(dc.lanes[L].forced, forced_host + (poff + tmp_off[L]) * h.M,
                                       1ull * tmp_cnt[L] * h.M, cudaMemcpyHostToDevice, dc.lanes[L].stream));
+        if (mu_host)
+          for (int L = 0; L < 2; ++L)
+            if (tmp_cnt[L] > 0)
+              CUDA_OK(cudaMemcpyAsync(dc.lanes[L].mu, mu_host + 2 * (poff + tmp_off[L]) * h.M,
+                                      sizeof(double2) * tmp_cnt[L] * h.M, cudaMemcpyHostToDevice,
+                                      dc.lanes[L].stream));
       }
       if (timing) CUDA_OK(cudaEventRecord(dc.ev[0], dc.stream));
-      run_pass(h, dc, seed, first + poff, n, forced_host != nullptr, marg_host != nullptr, rr.po, timing,
+      run_pass(h, dc, seed, first + poff, n, forced_host != nullptr, marg_host != nullptr, mu_host != nullptr,
+               rr.po, timing,
                off, cnt);
       for (int L = 0; L < 2; ++L) {
         if (cnt[L] <= 0) continue;
@@ -984,7 +1017,9 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
 
 static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_t count,
                         uint8_t* rows_host, uint8_t* rows_dev, const uint8_t* forced,
-                        double* marg, mpsg_stats* st) {
+                        double* marg, mpsg_stats* st, const double* mu = nullptr) {
+  config_check(mu == nullptr || h.d <= static_cast<uint64_t>(kMaxDisplacedDim),
+               "displacement: phys_dim must be <= 16");
   config_check(h.finished, "state not finished (mpsg_builder_finish)");
   config_check(h.tp == 1 || h.comm != nullptr, "tensor-parallel handle not connected (mpsg_tp_connect_*)");
   config_check(h.tp == 1 || h.devs.size() == 1, "a tensor-parallel rank drives exactly one device");
@@ -999,7 +1034,7 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
     auto body = [&, k, a, b] {
       run_range(h, h.devs[k], seed, first + a, b - a, rows_host ? rows_host + a * h.M : nullptr,
                 rows_dev ? rows_dev + a * h.M : nullptr, forced ? forced + a * h.M : nullptr,
-                marg ? marg + a * h.M * h.d : nullptr, rr[k]);
+                marg ? marg + a * h.M * h.d : nullptr, mu ? mu + 2 * a * h.M : nullptr, rr[k]);
     };
     if (nd == 1)
       body();
@@ -1325,6 +1360,38 @@ int mpsg_marginals(mpsg_handle h, uint64_t first, uint64_t count, const uint8_t*
     config_check(count >= 1, "count must be >= 1");
     std::vector<uint8_t> rows(count * h->M);
     sample_impl(*h, 0, first, count, rows.data(), nullptr, forced, marg, nullptr);
+  });
+}
+
+int mpsg_sample_displaced(mpsg_handle h, uint64_t seed, uint64_t first, uint64_t count,
+                          const double* mu, uint8_t* rows, mpsg_stats* stats) {
+  return guarded([&] {
+    config_check(h != nullptr && rows != nullptr && mu != nullptr, "null argument");
+    config_check(count >= 1, "batch plan: total samples must be >= 1");
+    sample_impl(*h, seed, first, count, rows, nullptr, nullptr, nullptr, stats, mu);
+  });
+}
+
+int mpsg_marginals_displaced(mpsg_handle h, uint64_t first, uint64_t count, const uint8_t* forced,
+                             const double* mu, double* marg) {
+  return guarded([&] {
+    config_check(h != nullptr && forced != nullptr && marg != nullptr && mu != nullptr, "null argument");
+    config_check(count >= 1, "count must be >= 1");
+    std::vector<uint8_t> rows(count * h->M);
+    sample_impl(*h, 0, first, count, rows.data(), nullptr, forced, marg, nullptr, mu);
+  });
+}
+
+int mpsg_displacement_matrix(double mu_re, double mu_im, uint64_t n, double* out) {
+  return guarded([&] {
+    config_check(out != nullptr && n >= 1 && n <= 64, "displacement matrix: 1 <= n <= 64");
+    if (mpsg_device_count() == 0) throw Error(MPSG_ERR_CUDA, "no sm_100 CUDA device visible");
+    double2* d = nullptr;
+    CUDA_OK(cudaMalloc(&d, sizeof(double2) * n * n));
+    launch_displacement_matrix(mu_re, mu_im, static_cast<int>(n), d, nullptr);
+    cudaError_t e = cudaMemcpy(out, d, sizeof(double2) * n * n, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    CUDA_OK(e);
   });
 }
 

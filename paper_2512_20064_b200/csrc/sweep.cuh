@@ -93,7 +93,25 @@ struct SelectArgs {
   int scaling;              // reference ScalingMode for the logscale update (precision.cpp:135-165)
 };
 
+// GBS displacement site transform (SPEC.md gbs-ops; the hook of sampler.cpp:143): for every live
+// sample n and local column r, temp[n, :, r] <- D(mu[n]) temp[n, :, r], then the per-(sample, tile)
+// Born-weight partials and max are recomputed into pstat.
+constexpr int kMaxDisplacedDim = 16;
+struct DisplaceArgs {
+  int d, chirp, chir_loc, nt, tpk;  // tpk = chirp / 128 tiles per outcome
+  int rows, count;
+  int site, num_sites;
+  const double2* mu;                // [rows][num_sites] displacement amplitudes of this pass
+  const uint8_t* alive;
+  const float2* cinfo;              // site column info: wl_r = cinfo[r].y
+  float2* temp;
+  float2* pstat;
+};
+
 // host launchers (sweep_kernels.cu)
+void launch_displace(const DisplaceArgs& a, cudaStream_t s);
+// D(mu) (n x n, f64, row-major complex) computed by the device generator.
+void launch_displacement_matrix(double mu_re, double mu_im, int n, double2* out, cudaStream_t s);
 void launch_site_gemm(bool split, const CUtensorMap& tma_env, const CUtensorMap& tma_g,
                       const SiteGemmArgs& a, int grid, cudaStream_t s);
 // CTA-pair variant (cta_group::2, M = 256 per unit; a.m_tiles counts 256-row tiles; the Gamma map

@@ -758,6 +758,110 @@ void launch_select(const SelectArgs& a, cudaStream_t s) {
 }
 
 // ============================================================================================
+// GBS displacement (§3.4 Eq. 6): D(mu) = exp(-|mu|^2/2) L U with the
+// closed-form triangular factors L = exp(mu a^dag), U = exp(-conj(mu) a); applied per sample to the
+// d outcome components of every column of temp (the reference's SiteTransform hook position,
+// sampler.cpp:143).  The closed form gives the exact Fock-basis elements of D(mu) (no truncation
+// of the generator).
+// ============================================================================================
+__device__ __forceinline__ double2 displacement_element(double mr, double mi, int a, int c) {
+  // D[a][c] = exp(-|mu|^2/2) sum_{b <= min(a, c)} L[a][b] U[b][c]
+  const double pre = exp(-0.5 * (mr * mr + mi * mi));
+  double sr = 0.0, si = 0.0;
+  const int bmax = min(a, c);
+  for (int b = 0; b <= bmax; ++b) {
+    double lr = 1.0, li = 0.0, ur = 1.0, ui = 0.0;
+    for (int j = 0; j < a - b; ++j) {  // mu^(a-b)
+      const double t = lr * mr - li * mi;
+      li = lr * mi + li * mr;
+      lr = t;
+    }
+    for (int j = 0; j < c - b; ++j) {  // (-conj(mu))^(c-b) = (-mr + i mi)^(c-b)
+      const double t = -ur * mr - ui * mi;
+      ui = ur * mi - ui * mr;
+      ur = t;
+    }
+    const double fl = exp(0.5 * (lgamma(a + 1.0) - lgamma(b + 1.0)) - lgamma(a - b + 1.0));
+    const double fu = exp(0.5 * (lgamma(c + 1.0) - lgamma(b + 1.0)) - lgamma(c - b + 1.0));
+    lr *= fl, li *= fl, ur *= fu, ui *= fu;
+    sr += lr * ur - li * ui;
+    si += lr * ui + li * ur;
+  }
+  return make_double2(pre * sr, pre * si);
+}
+
+__global__ void displacement_matrix_kernel(double mr, double mi, int n, double2* out) {
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) out[e] = displacement_element(mr, mi, e / n, e % n);
+}
+
+void launch_displacement_matrix(double mu_re, double mu_im, int n, double2* out, cudaStream_t s) {
+  displacement_matrix_kernel<<<1, 256, 0, s>>>(mu_re, mu_im, n, out);
+}
+
+// One warp per sample: D(mu_n) into shared memory (f64 generation, fp32 apply), then per 128-column
+// tile the transformed components, their Born-weight partials and max (fixed-order warp trees).
+__global__ void __launch_bounds__(256) displace_kernel(const DisplaceArgs a) {
+  __shared__ float2 sD[8][kMaxDisplacedDim * kMaxDisplacedDim];
+  const int wib = threadIdx.x >> 5;
+  const int n = blockIdx.x * 8 + wib;
+  const int lane = threadIdx.x & 31;
+  if (n >= a.count || !a.alive[n]) return;  // warp-uniform
+  const int d = a.d;
+  const double2 mu = a.mu[static_cast<size_t>(n) * a.num_sites + a.site];
+  for (int e = lane; e < d * d; e += 32) {
+    const double2 v = displacement_element(mu.x, mu.y, e / d, e % d);
+    sD[wib][e] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+  }
+  __syncwarp();
+  const float2* D = sD[wib];
+  float2* row = a.temp + static_cast<size_t>(n) * d * a.chirp;  // [d][chirp]
+  for (int t = 0; t < a.tpk; ++t) {
+    float w[kMaxDisplacedDim], mx[kMaxDisplacedDim];
+#pragma unroll
+    for (int k = 0; k < kMaxDisplacedDim; ++k) w[k] = 0.f, mx[k] = 0.f;
+    for (int j = 0; j < 4; ++j) {
+      const int r = t * 128 + j * 32 + lane;
+      if (r >= a.chir_loc) continue;
+      float2 v[kMaxDisplacedDim];
+#pragma unroll
+      for (int k = 0; k < kMaxDisplacedDim; ++k)
+        if (k < d) v[k] = row[static_cast<size_t>(k) * a.chirp + r];
+      const float wl = a.cinfo[r].y;
+#pragma unroll
+      for (int k = 0; k < kMaxDisplacedDim; ++k) {
+        if (k >= d) break;
+        float orr = 0.f, oi = 0.f;
+#pragma unroll
+        for (int q = 0; q < kMaxDisplacedDim; ++q) {
+          if (q >= d) break;
+          const float2 dk = D[k * d + q];
+          orr = fmaf(dk.x, v[q].x, fmaf(-dk.y, v[q].y, orr));
+          oi = fmaf(dk.x, v[q].y, fmaf(dk.y, v[q].x, oi));
+        }
+        row[static_cast<size_t>(k) * a.chirp + r] = make_float2(orr, oi);
+        w[k] = fmaf(wl, fmaf(orr, orr, oi * oi), w[k]);
+        mx[k] = fmaxf(mx[k], fmaxf(fabsf(orr), fabsf(oi)));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxDisplacedDim; ++k) {
+      if (k >= d) break;
+      float ws = w[k], ms = mx[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ws += __shfl_xor_sync(0xffffffffu, ws, o);
+        ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+      }
+      if (lane == 0) a.pstat[static_cast<size_t>(n) * a.nt + k * a.tpk + t] = make_float2(ws, ms);
+    }
+  }
+}
+
+void launch_displace(const DisplaceArgs& a, cudaStream_t s) {
+  displace_kernel<<<(a.count + 7) / 8, 256, 0, s>>>(a);
+}
+
+// ============================================================================================
 // site-0 environment (sampler.cpp:136-138: env = ones(count, 1), all alive)
 // ============================================================================================
 __global__ void init_env_kernel(__half* env, int env_comp, int env_cap, int kshard0, int shards,

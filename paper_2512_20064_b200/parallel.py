@@ -110,12 +110,12 @@ class TensorParallelLocal:
             raise err[0]
         return out
 
-    def sample(self, first: int, count: int, seed: int):
+    def sample(self, first: int, count: int, seed: int, mu=None):
         """Returns every rank's rows (they are identical)."""
-        return self._all(lambda s: s.sample(first, count, seed))
+        return self._all(lambda s: s.sample(first, count, seed, mu=mu))
 
-    def marginals(self, first: int, forced):
-        return self._all(lambda s: s.marginals(first, forced))
+    def marginals(self, first: int, forced, mu=None):
+        return self._all(lambda s: s.marginals(first, forced, mu=mu))
 
     def decoded_gamma(self, site: int):
         """The full decoded Gamma_i assembled from every rank's column shard."""

@@ -206,7 +206,7 @@ class SamplerOptions:
     policy: PrecisionPolicy = field(default_factory=PrecisionPolicy)
     seed: int = 0
     schedule: Optional[object] = None        # BondSchedule: not supported on the GPU path
-    site_transform: Optional[object] = None  # SiteTransform hook: not supported on the GPU path
+    site_transform: Optional[object] = None  # SiteTransform hook: a Displacement, else ConfigError
     record_decay_trace: bool = False
     mode: Mode = Mode.AUTO
     pass_samples: int = 0
@@ -332,8 +332,9 @@ class GpuSampler:
         return int(_lib.lib().mpsg_state_bytes(self._h))
 
     def sample(self, first: int, count: int, seed: int, stats: Optional[RunStats] = None,
-               out: Optional[np.ndarray] = None) -> np.ndarray:
-        """detail::sample_micro_serial over global samples [first, first+count)."""
+               out: Optional[np.ndarray] = None, mu: Optional[np.ndarray] = None) -> np.ndarray:
+        """detail::sample_micro_serial over global samples [first, first+count); mu (count, M)
+        complex applies the GBS displacement D(mu[n, i]) as the site transform (sampler.cpp:143)."""
         rows = out if out is not None else np.empty((count, self.num_sites), np.uint8)
         st = _lib.Stats()
         site_s = None
@@ -342,8 +343,13 @@ class GpuSampler:
         if stats is not None:
             site_s = np.zeros(self.num_sites, np.float64)
             st.site_seconds = site_s.ctypes.data_as(_lib._pd)
-        _check(_lib.lib().mpsg_sample(self._h, seed, first, count, rows.ctypes.data_as(_lib._pu8),
-                                      C.byref(st)))
+        if mu is None:
+            _check(_lib.lib().mpsg_sample(self._h, seed, first, count, rows.ctypes.data_as(_lib._pu8),
+                                          C.byref(st)))
+        else:
+            mu = self._mu(mu, count)
+            _check(_lib.lib().mpsg_sample_displaced(self._h, seed, first, count, mu.ctypes.data_as(_lib._pd),
+                                                    rows.ctypes.data_as(_lib._pu8), C.byref(st)))
         if stats is not None:
             stats.contraction_macs += st.contraction_macs
             stats.measure_weight_macs += st.measure_weight_macs
@@ -359,13 +365,24 @@ class GpuSampler:
     def sample_device(self, first: int, count: int, seed: int, rows_dev_ptr: int) -> None:
         _check(_lib.lib().mpsg_sample_device(self._h, seed, first, count, C.c_void_p(rows_dev_ptr), None))
 
-    def marginals(self, first: int, forced: np.ndarray) -> np.ndarray:
+    def marginals(self, first: int, forced: np.ndarray, mu: Optional[np.ndarray] = None) -> np.ndarray:
         forced = np.ascontiguousarray(forced, np.uint8)
         n = forced.shape[0]
         marg = np.empty((n, self.num_sites, self.phys_dim), np.float64)
-        _check(_lib.lib().mpsg_marginals(self._h, first, n, forced.ctypes.data_as(_lib._pu8),
-                                         marg.ctypes.data_as(_lib._pd)))
+        if mu is None:
+            _check(_lib.lib().mpsg_marginals(self._h, first, n, forced.ctypes.data_as(_lib._pu8),
+                                             marg.ctypes.data_as(_lib._pd)))
+        else:
+            mu = self._mu(mu, n)
+            _check(_lib.lib().mpsg_marginals_displaced(self._h, first, n, forced.ctypes.data_as(_lib._pu8),
+                                                       mu.ctypes.data_as(_lib._pd), marg.ctypes.data_as(_lib._pd)))
         return marg
+
+    def _mu(self, mu, count):
+        mu = np.ascontiguousarray(mu, np.complex128)
+        if mu.shape != (count, self.num_sites):
+            raise DimensionError(f"displacement amplitudes must be ({count}, {self.num_sites})")
+        return mu
 
     @property
     def scheme(self) -> Scheme:
@@ -458,6 +475,30 @@ def connect_local(samplers: Sequence["GpuSampler"]) -> None:
     _check(_lib.lib().mpsg_tp_connect_local(arr, len(samplers)))
 
 
+@dataclass
+class Displacement:
+    """The GBS displacement site transform (SPEC.md gbs-ops, §3.4): sample n is displaced by
+    D(mu[n, i]) at site i, applied to the contracted site between contract_site and measure (the
+    reference's SiteTransform hook, sampler.hpp:71-79, sampler.cpp:143).  mu: complex (N, M) over the
+    global sample indices of the batch."""
+
+    mu: np.ndarray
+
+    def amplitudes(self, first: int, count: int, num_sites: int) -> np.ndarray:
+        mu = np.asarray(self.mu)
+        if mu.ndim != 2 or mu.shape[1] != num_sites or mu.shape[0] < first + count:
+            raise DimensionError("Displacement.mu must be (N, M) covering the batch")
+        return np.ascontiguousarray(mu[first:first + count], np.complex128)
+
+
+def displacement_matrix(mu: complex, n: int) -> np.ndarray:
+    """expm_displacement evaluated by the device generator: D(mu), n x n."""
+    out = np.empty((n, n), np.complex128)
+    _check(_lib.lib().mpsg_displacement_matrix(float(np.real(mu)), float(np.imag(mu)), n,
+                                               out.ctypes.data_as(_lib._pd)))
+    return out
+
+
 def device_draws(seed: int, first: int, count: int, site: int) -> np.ndarray:
     """detail::measurement_draws (sampler.cpp:120-127) computed on the GPU."""
     out = np.empty(count, np.float64)
@@ -484,15 +525,18 @@ def sample_batch(mps: MpsState, plan: BatchPlan, opts: SamplerOptions,
     plan.normalize()
     if opts.schedule is not None:  # sampler.cpp:173-176
         mps = apply_schedule(mps, opts.schedule)
+    mu = None
     if opts.site_transform is not None:
-        raise ConfigError("site transforms are not supported by the GPU sweep (out of scope)")
+        if not isinstance(opts.site_transform, Displacement):
+            raise ConfigError("site transforms other than the GBS Displacement are not supported by the GPU sweep")
+        mu = opts.site_transform.amplitudes(0, plan.total_samples, mps.num_sites)
     t0 = time.perf_counter()
     smp = GpuSampler(mps, opts.policy, opts.mode, devices, opts.pass_samples,
                      record_site_times=stats is not None, record_decay_trace=opts.record_decay_trace,
                      scheme=opts.scheme)
     try:
         st = stats if stats is not None else RunStats()
-        rows = smp.sample(0, plan.total_samples, opts.seed, stats=st)
+        rows = smp.sample(0, plan.total_samples, opts.seed, stats=st, mu=mu)
     finally:
         smp.close()
     if stats is not None:

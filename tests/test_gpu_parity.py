@@ -400,3 +400,67 @@ def test_multi_device_handle_threads(pkg, gold):
     assert np.array_equal(one, two)
     res = pkg.sample_batch(st, pkg.BatchPlan(1000), pkg.SamplerOptions(policy=pol, seed=7), devices=[0, 0])
     assert np.array_equal(res.outcomes, one)
+
+
+# ---- GBS displacement site transform (SPEC.md gbs-ops, hook position sampler.cpp:143) ---------
+def test_displacement_matrix_device_matches_oracle(pkg):
+    rng = np.random.default_rng(2)
+    for n in (1, 2, 4, 6, 10, 16):
+        for _ in range(5):
+            mu = complex(*rng.uniform(-1.2, 1.2, 2))
+            # f64 on both sides; device vs host libm (exp, lgamma) differ in the last bits
+            np.testing.assert_allclose(pkg.displacement_matrix(mu, n), O.orc_displacement(mu, n),
+                                       rtol=1e-10, atol=1e-11)
+
+
+@pytest.mark.parametrize("scheme", [3, 4])
+def test_displaced_sampling_parity(pkg, gold, scheme):
+    """Per-sample displacement D(mu[n, i]) between contraction and measurement: strings and
+    teacher-forced marginals vs the oracle with the same mu (c1b, d = 4); mu = 0 reproduces the
+    undisplaced sweep exactly."""
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    smp = pkg.GpuSampler(to_state(pkg, mps), pol, scheme=pkg.Scheme(scheme), pass_samples=256)
+    n, m = 1000, mps.num_sites
+    zero = smp.sample(0, n, 7, mu=np.zeros((n, m), complex))
+    assert np.array_equal(zero, smp.sample(0, n, 7))
+    rng = np.random.default_rng(9)
+    mu = 0.6 * (rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m)))
+    dec = decoded_mps(smp, mps)
+    ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, n, 7, want_marginals=True, mu=mu)
+    gpu_rows = smp.sample(0, n, 7, mu=mu)
+    assert (gpu_rows != zero).any()
+    gm = smp.marginals(0, ref_rows, mu=mu)
+    big = ref_marg >= 1e-3
+    rel = np.abs(gm[big] - ref_marg[big]) / ref_marg[big]
+    assert rel.max() < MARG_RTOL, rel.max()
+    ndiff, explained = compare_strings(gpu_rows, ref_rows, ref_marg, 7)
+    assert ndiff == explained, (ndiff, explained)
+    # the reference-shaped API: SamplerOptions.site_transform = Displacement(mu)
+    opts = pkg.SamplerOptions(policy=pol, seed=7, site_transform=pkg.Displacement(mu), scheme=pkg.Scheme(scheme))
+    assert np.array_equal(pkg.sample_batch(to_state(pkg, mps), pkg.BatchPlan(n), opts).outcomes, gpu_rows)
+
+
+def test_displaced_sampling_bench_dims_and_tp(pkg):
+    """chi = 512, d = 6 device-generated chain with displacement: parity vs the oracle; the
+    tensor-parallel sweep (p2 = 2, one device) agrees with the unsharded one."""
+    from paper_2512_20064_b200.parallel import TensorParallelLocal
+    smp, lams, pol = _synthetic(pkg, 8, 512, 6)
+    m, n, d = 8, 48, 6
+    rng = np.random.default_rng(3)
+    mu = 0.5 * (rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m)))
+    dec = O.Mps(d, list(smp.bond_dims), [smp.decoded_gamma(i) for i in range(m)], list(lams))
+    ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, n, 7, want_marginals=True, mu=mu)
+    gpu_rows = smp.sample(0, n, 7, mu=mu)
+    gm = smp.marginals(0, ref_rows, mu=mu)
+    big = ref_marg >= 1e-3
+    assert (np.abs(gm[big] - ref_marg[big]) / ref_marg[big]).max() < MARG_RTOL
+    ndiff, explained = compare_strings(gpu_rows, ref_rows, ref_marg, 7)
+    assert ndiff == explained, (ndiff, explained)
+    st = pkg.MpsState(m, d, list(dec.bond_dims), list(dec.gammas), list(dec.lambdas))
+    tp = TensorParallelLocal(st, 2, policy=pol)
+    t = tp.sample(0, n, 7, mu=mu)
+    assert np.array_equal(t[0], t[1])
+    assert (t[0] != gpu_rows).any(axis=1).sum() <= 1
+    tp.close()

@@ -125,3 +125,57 @@ def test_live_cross_check_random():
         forced = want
         np.testing.assert_allclose(O.orc_sample_range(mps, 0, 200, 1, forced=forced, want_marginals=True)[1],
                                    rs.marginals_forced(forced), rtol=1e-12, atol=1e-15)
+
+
+# ---- GBS displacement (SPEC.md gbs-ops; the reference's src/gbs.cpp is absent) ---------------
+def test_displacement_closed_form_kats():
+    """expm_displacement: mu = 0 -> identity; n = 2 closed form; the closed form
+    L U e^{-|mu|^2/2} equals the exact Fock-basis matrix elements of D(mu) (expm of the generator at
+    a 60-level cutoff, leading n x n block); vs the exact expm of the generator truncated at n = 10,
+    1000 random |mu| <= 1, the leading 4 x 4 block (the levels a d = 4 site samples) agrees within
+    the paper's 0.2% (§4.1) -- the difference is the generator's truncation, not the
+    closed form."""
+    from scipy.linalg import expm
+    assert np.array_equal(O.orc_displacement(0.0, 6), np.eye(6))
+    mu = 0.3
+    want = np.exp(-mu * mu / 2) * np.array([[1, -mu], [mu, 1 - mu * mu]])
+    np.testing.assert_allclose(O.orc_displacement(mu, 2), want, rtol=1e-15, atol=1e-16)
+    rng = np.random.default_rng(1)
+    n, big_n = 10, 60
+    a10 = np.diag(np.sqrt(np.arange(1, n)), 1)
+    a60 = np.diag(np.sqrt(np.arange(1, big_n)), 1)
+    worst_exact = worst_trunc = 0.0
+    for j in range(1000):
+        m = rng.uniform(0, 1) * np.exp(2j * np.pi * rng.uniform())
+        d = O.orc_displacement(m, n)
+        if j < 50:
+            exact = expm(m * a60.T - np.conj(m) * a60)[:n, :n]
+            worst_exact = max(worst_exact, np.abs(d - exact).max())
+        trunc = expm(m * a10.T - np.conj(m) * a10)[:4, :4]
+        sel = np.abs(trunc) > 1e-3
+        worst_trunc = max(worst_trunc, (np.abs(d[:4, :4] - trunc)[sel] / np.abs(trunc)[sel]).max())
+    assert worst_exact < 1e-12, worst_exact
+    assert worst_trunc < 2e-3, worst_trunc
+    # first-order sanity (SPEC.md:405): D(mu) -> I + mu a^dag - conj(mu) a
+    eps = 1e-6 * (1 + 1j)
+    np.testing.assert_allclose(O.orc_displacement(eps, 5), np.eye(5) + eps * np.diag(np.sqrt(np.arange(1, 5)), -1)
+                               - np.conj(eps) * np.diag(np.sqrt(np.arange(1, 5)), 1), atol=1e-11)
+
+
+def test_displaced_sampler_hook(gold):
+    """The displacement hook sits between contract_site and measure (sampler.cpp:143): mu = 0 gives
+    the undisplaced outcomes; a per-sample loop applying D(mu[n, i]) to temp matches the hook."""
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    n, m = 200, mps.num_sites
+    base, _ = O.orc_sample_range(mps, 0, n, 7)
+    zero, _ = O.orc_sample_range(mps, 0, n, 7, mu=np.zeros((n, m), complex))
+    assert np.array_equal(base, zero)
+    rng = np.random.default_rng(4)
+    mu = 0.5 * (rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m)))
+    rows, marg, _ = O.orc_sample_range(mps, 0, n, 7, want_marginals=True, mu=mu)
+    assert (rows != base).any()
+    # marginals of sample 0 at site 0 by hand: D applied to Gamma_0[0, b, :], weights sum_b L^2 |.|^2
+    t = mps.gammas[0][0] @ O.orc_displacement(mu[0, 0], mps.phys_dim).T
+    w = (mps.lambdas[0][:, None] ** 2 * np.abs(t) ** 2).sum(axis=0)
+    np.testing.assert_allclose(marg[0, 0], w / w.sum(), rtol=1e-12)
