@@ -215,6 +215,9 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--displace", type=float, default=0.0,
+                    help="GBS displacement site transform with mu ~ complex normal of this std per "
+                         "(sample, site) (0 = none)")
     ap.add_argument("--e2e", default="auto", choices=["auto", "stream", "resident"],
                     help="end-to-end arm: 'stream' rebuilds the state in pinned host memory and streams the "
                          "compressed MPS H2D every step (auto: when host memory holds it for every local rank)")
@@ -255,10 +258,17 @@ def main():
     macs_per_sample, bonds = chain_macs(cfg["M"], cfg["chi"], cfg["d"])
     rows_dev = torch.empty((P_pass, cfg["M"]), dtype=torch.uint8, device="cuda")
 
+    mu_host = rows_host = None
+    if args.displace > 0:
+        rng = np.random.default_rng(1)
+        mu_host = (args.displace * (rng.standard_normal((P_pass, cfg["M"]))
+                                    + 1j * rng.standard_normal((P_pass, cfg["M"])))).astype(np.complex128)
+        rows_host = np.empty((P_pass, cfg["M"]), np.uint8)
+
     def step(it):
         st = P.RunStats()
         first = (it * world + rank) * P_pass
-        rows = smp.sample(first, P_pass, 7, stats=st)  # host rows; device time from events
+        rows = smp.sample(first, P_pass, 7, stats=st, mu=mu_host)  # host rows; device time from events
         return st, rows
 
     def device_step(it):
@@ -268,8 +278,12 @@ def main():
         s = L.Stats()
         site = np.zeros(cfg["M"], np.float64)
         s.site_seconds = site.ctypes.data_as(L._pd)
-        P.sampler._check(L.lib().mpsg_sample_device(smp._h, 7, first, P_pass, ctypes.c_void_p(rows_dev.data_ptr()),
-                                                    ctypes.byref(s)))
+        if mu_host is None:
+            P.sampler._check(L.lib().mpsg_sample_device(smp._h, 7, first, P_pass,
+                                                        ctypes.c_void_p(rows_dev.data_ptr()), ctypes.byref(s)))
+        else:  # GBS displacement site transform; device time from the engine's events
+            P.sampler._check(L.lib().mpsg_sample_displaced(smp._h, 7, first, P_pass, mu_host.ctypes.data_as(L._pd),
+                                                           rows_host.ctypes.data_as(L._pu8), ctypes.byref(s)))
         st.contraction_macs = s.contraction_macs
         st.issued_mma_flops = s.issued_mma_flops
         st.h2d = s.h2d_bytes
@@ -378,6 +392,8 @@ def main():
                        "M": cfg["M"], "chi": cfg["chi"], "d": cfg["d"], "pass_samples_per_gpu": P_pass,
                        "job_samples": cfg["job"], "job_seconds_at_value": cfg["job"] / value,
                        "mode": args.mode, "scheme": scheme, "parallelism": f"dp{world}",
+                       "displacement": (f"GBS displacement D(mu) per (sample, site), mu ~ CN(0, {args.displace}^2)"
+                                        if args.displace > 0 else None),
                        "l2": f"inputs larger than L2 (compressed MPS {smp.state_bytes / 1e9:.1f} GB)",
                        "gamma_residency": (f"pinned host memory, streamed per site through {args.stream_slots} "
                                            f"device slots ({h2d / args.steps / 1e9:.1f} GB H2D per step, "

@@ -814,7 +814,11 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[2 * i], ln.stream));
       launch_contraction(h, dc, s, ln, i, rows[L], tma_g128, *tma_g64, cinfo, ln.stream);
       if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[2 * i + 1], ln.stream));
-      if (displaced) {  // the SiteTransform hook position (sampler.cpp:143): after contract_site
+      // Displacement fused into the selection (one read of temp) unless the weights must be exchanged
+      // first (tensor parallelism) or the decay trace reads the transformed slice.
+      static const bool no_fuse = std::getenv("MPSG_DISPLACE_SEPARATE") != nullptr;
+      const bool fuse_displace = displaced && h.tp == 1 && !dc.trace && !no_fuse;
+      if (displaced && !fuse_displace) {  // the SiteTransform hook position (sampler.cpp:143)
         DisplaceArgs da;
         da.d = static_cast<int>(h.d);
         da.chirp = s.chirp;
@@ -883,6 +887,8 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       sa.inv_gamma = s.inv_gamma;
       sa.trace = dc.trace ? dc.trace + i : nullptr;
       sa.scaling = h.policy.scaling;
+      sa.mu = fuse_displace ? ln.mu : nullptr;
+      sa.cinfo = cinfo;
       launch_select(sa, ln.stream);
       if (h.tp > 1 && has_next)  // rebuild the full environment from the column shards
         h.comm->allgather(ln.env, 2ull * h.env_comp * ln.cap * kn * sizeof(__half), ln.stream);

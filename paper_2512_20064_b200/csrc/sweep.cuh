@@ -91,6 +91,10 @@ struct SelectArgs {
   const double* inv_gamma;
   double* trace;
   int scaling;              // reference ScalingMode for the logscale update (precision.cpp:135-165)
+  // GBS displacement fused into the selection (tp == 1, no decay trace): the weights, the draw and
+  // the gathered slice use D(mu[n]) temp[n, :, r] computed on the fly from the d stored outcomes
+  const double2* mu;        // [rows][num_sites] or null
+  const float2* cinfo;      // site column info (wl_r = cinfo[r].y) for the displaced weights
 };
 
 // GBS displacement site transform (SPEC.md gbs-ops; the hook of sampler.cpp:143): for every live

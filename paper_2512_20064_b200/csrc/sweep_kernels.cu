@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
+
 #include "ptx.cuh"
 
 
@@ -540,6 +542,129 @@ void launch_site_gemm_pair(bool split, const CUtensorMap& tma_env, const CUtenso
 }
 
 // ============================================================================================
+// GBS displacement (SPEC.md:366-381, PAPER.md §3.4 Eq. 6): D(mu) = exp(-|mu|^2/2) L U with the
+// closed-form triangular factors L = exp(mu a^dag), U = exp(-conj(mu) a); applied per sample to the
+// d outcome components of every column of temp (the reference's SiteTransform hook position,
+// sampler.cpp:143).  The closed form gives the exact Fock-basis elements of D(mu) (no truncation
+// of the generator).
+// ============================================================================================
+// c_fact[a][b] = sqrt(a! / b!) / (a - b)! for b <= a <= 64 (the closed-form factors of L and U)
+__constant__ double c_fact[65][65];
+static bool g_fact_ready = false;
+static void ensure_fact_table() {
+  if (g_fact_ready) return;
+  static double h[65][65];
+  for (int a = 0; a <= 64; ++a)
+    for (int b = 0; b <= 64; ++b)
+      h[a][b] = b <= a ? std::exp(0.5 * (std::lgamma(a + 1.0) - std::lgamma(b + 1.0)) - std::lgamma(a - b + 1.0)) : 0.0;
+  cudaMemcpyToSymbol(c_fact, h, sizeof(h));
+  g_fact_ready = true;
+}
+
+__device__ __forceinline__ double2 displacement_element(double mr, double mi, int a, int c) {
+  // D[a][c] = exp(-|mu|^2/2) sum_{b <= min(a, c)} L[a][b] U[b][c]
+  const double pre = exp(-0.5 * (mr * mr + mi * mi));
+  double sr = 0.0, si = 0.0;
+  const int bmax = min(a, c);
+  for (int b = 0; b <= bmax; ++b) {
+    double lr = 1.0, li = 0.0, ur = 1.0, ui = 0.0;
+    for (int j = 0; j < a - b; ++j) {  // mu^(a-b)
+      const double t = lr * mr - li * mi;
+      li = lr * mi + li * mr;
+      lr = t;
+    }
+    for (int j = 0; j < c - b; ++j) {  // (-conj(mu))^(c-b) = (-mr + i mi)^(c-b)
+      const double t = -ur * mr - ui * mi;
+      ui = ur * mi - ui * mr;
+      ur = t;
+    }
+    const double fl = c_fact[a][b];
+    const double fu = c_fact[c][b];
+    lr *= fl, li *= fl, ur *= fu, ui *= fu;
+    sr += lr * ur - li * ui;
+    si += lr * ui + li * ur;
+  }
+  return make_double2(pre * sr, pre * si);
+}
+
+__global__ void displacement_matrix_kernel(double mr, double mi, int n, double2* out) {
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) out[e] = displacement_element(mr, mi, e / n, e % n);
+}
+
+void launch_displacement_matrix(double mu_re, double mu_im, int n, double2* out, cudaStream_t s) {
+  ensure_fact_table();
+  displacement_matrix_kernel<<<1, 256, 0, s>>>(mu_re, mu_im, n, out);
+}
+
+// One warp per sample: D(mu_n) into shared memory (f64 generation, fp32 apply), then per 128-column
+// tile the transformed components, their Born-weight partials and max (fixed-order warp trees).
+template <int MAXD>
+__global__ void __launch_bounds__(256) displace_kernel(const DisplaceArgs a) {
+  __shared__ float2 sD[8][MAXD * MAXD];
+  const int wib = threadIdx.x >> 5;
+  const int n = blockIdx.x * 8 + wib;
+  const int lane = threadIdx.x & 31;
+  if (n >= a.count || !a.alive[n]) return;  // warp-uniform
+  const int d = a.d;
+  const double2 mu = a.mu[static_cast<size_t>(n) * a.num_sites + a.site];
+  for (int e = lane; e < d * d; e += 32) {
+    const double2 v = displacement_element(mu.x, mu.y, e / d, e % d);
+    sD[wib][e] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+  }
+  __syncwarp();
+  const float2* D = sD[wib];
+  float2* row = a.temp + static_cast<size_t>(n) * d * a.chirp;  // [d][chirp]
+  for (int t = 0; t < a.tpk; ++t) {
+    float w[MAXD], mx[MAXD];
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) w[k] = 0.f, mx[k] = 0.f;
+    for (int j = 0; j < 4; ++j) {
+      const int r = t * 128 + j * 32 + lane;
+      if (r >= a.chir_loc) continue;
+      float2 v[MAXD];
+#pragma unroll
+      for (int k = 0; k < MAXD; ++k)
+        if (k < d) v[k] = row[static_cast<size_t>(k) * a.chirp + r];
+      const float wl = a.cinfo[r].y;
+#pragma unroll
+      for (int k = 0; k < MAXD; ++k) {
+        if (k >= d) break;
+        float orr = 0.f, oi = 0.f;
+#pragma unroll
+        for (int q = 0; q < MAXD; ++q) {
+          if (q >= d) break;
+          const float2 dk = D[k * d + q];
+          orr = fmaf(dk.x, v[q].x, fmaf(-dk.y, v[q].y, orr));
+          oi = fmaf(dk.x, v[q].y, fmaf(dk.y, v[q].x, oi));
+        }
+        row[static_cast<size_t>(k) * a.chirp + r] = make_float2(orr, oi);
+        w[k] = fmaf(wl, fmaf(orr, orr, oi * oi), w[k]);
+        mx[k] = fmaxf(mx[k], fmaxf(fabsf(orr), fabsf(oi)));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+      if (k >= d) break;
+      float ws = w[k], ms = mx[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ws += __shfl_xor_sync(0xffffffffu, ws, o);
+        ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+      }
+      if (lane == 0) a.pstat[static_cast<size_t>(n) * a.nt + k * a.tpk + t] = make_float2(ws, ms);
+    }
+  }
+}
+
+void launch_displace(const DisplaceArgs& a, cudaStream_t s) {
+  ensure_fact_table();
+  if (a.d <= 8)
+    displace_kernel<8><<<(a.count + 7) / 8, 256, 0, s>>>(a);
+  else
+    displace_kernel<kMaxDisplacedDim><<<(a.count + 7) / 8, 256, 0, s>>>(a);
+}
+
+// ============================================================================================
 // K2: measurement select + gather + renormalise + split (one warp per sample)
 // ============================================================================================
 __device__ __forceinline__ double warp_sum(double v) {
@@ -579,15 +704,113 @@ __device__ __forceinline__ float slice_max(const SelectArgs& a, int n, int k, in
   return warp_max(m);
 }
 
+// Displaced selection (SelectArgs::mu): D(mu_n) in shared memory, then one pass over the d stored
+// outcomes of every column computes the transformed Born weights and maxima (f64 per lane, fixed-
+// order warp trees); returns the chosen outcome (or kDead) exactly like the undisplaced path.
+template <int MAXD>
+__device__ int select_displaced(const SelectArgs& a, int n, int lane, const float2* D, float& mx_out) {
+  const int d = a.d;
+  double ws[MAXD];
+  float ms[MAXD];
+#pragma unroll
+  for (int k = 0; k < MAXD; ++k) ws[k] = 0.0, ms[k] = 0.f;
+  // lane handles 2 consecutive columns per step (one 16 B load per outcome; the padding columns
+  // of temp and cinfo are zero, so the even-rounded tail is harmless)
+  const int lim = (a.chir_loc + 1) & ~1;
+  for (int r = lane * 2; r < lim; r += 64) {
+    float4 v[MAXD];
+#pragma unroll
+    for (int q = 0; q < MAXD; ++q)
+      if (q < d) v[q] = *reinterpret_cast<const float4*>(a.temp + (static_cast<size_t>(n) * d + q) * a.chirp + r);
+    const float4 wl2 = *reinterpret_cast<const float4*>(a.cinfo + r);  // (cs0, wl0, cs1, wl1)
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+      if (k >= d) break;
+      float o0r = 0.f, o0i = 0.f, o1r = 0.f, o1i = 0.f;
+#pragma unroll
+      for (int q = 0; q < MAXD; ++q) {
+        if (q >= d) break;
+        const float2 dk = D[k * d + q];
+        o0r = fmaf(dk.x, v[q].x, fmaf(-dk.y, v[q].y, o0r));
+        o0i = fmaf(dk.x, v[q].y, fmaf(dk.y, v[q].x, o0i));
+        o1r = fmaf(dk.x, v[q].z, fmaf(-dk.y, v[q].w, o1r));
+        o1i = fmaf(dk.x, v[q].w, fmaf(dk.y, v[q].z, o1i));
+      }
+      ws[k] += static_cast<double>(wl2.y) * (static_cast<double>(o0r) * o0r + static_cast<double>(o0i) * o0i) +
+               static_cast<double>(wl2.w) * (static_cast<double>(o1r) * o1r + static_cast<double>(o1i) * o1i);
+      ms[k] = fmaxf(ms[k], fmaxf(fmaxf(fabsf(o0r), fabsf(o0i)), fmaxf(fabsf(o1r), fabsf(o1i))));
+    }
+  }
+  double total = 0.0;  // sampler.cpp:92-93, ascending k
+#pragma unroll
+  for (int k = 0; k < MAXD; ++k) {
+    if (k >= d) break;
+    ws[k] = warp_sum(ws[k]);
+    ms[k] = warp_max(ms[k]);
+    total += ws[k];
+  }
+  if (a.marg != nullptr) {
+    double* mrow = a.marg + (static_cast<size_t>(n) * a.num_sites + a.site) * d;
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k)
+      if (k < d && lane == k) mrow[k] = total == 0.0 ? -1.0 : ws[k] / total;
+  }
+  if (total == 0.0) return kDead;  // sampler.cpp:94-98
+  int kk;
+  if (a.forced != nullptr) {
+    kk = a.forced[static_cast<size_t>(n) * a.num_sites + a.site];
+    if (kk == kDead) return kDead;
+  } else {
+    const double draw = keyed_uniform(a.seed, kMeasureStream, a.first + n, a.site);
+    double cum = 0.0;
+    kk = 0;
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {  // sampler.cpp:100-106
+      if (k >= d) break;
+      cum += ws[k] / total;
+      if (draw > cum) ++kk;
+    }
+    if (kk >= d) kk = d - 1;  // :107
+  }
+  float mx = 0.f;
+#pragma unroll
+  for (int k = 0; k < MAXD; ++k)
+    if (k == kk) mx = ms[k];
+  mx_out = mx;
+  return kk;
+}
+
+template <bool kDisp, int MAXD = 1>
 __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
+  __shared__ float2 sD[kDisp ? 8 : 1][MAXD * MAXD];
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
   if (n >= a.rows) return;
   const bool live_in = n < a.count && a.alive[n];
   int outcome = kDead;   // recorded at this site
   bool live_out = false; // carries into the next site
   float scale = 0.f;
-  if (live_in) {
+  const float2* D = sD[kDisp ? wib : 0];
+  if (kDisp && live_in) {
+    const double2 mu = a.mu[static_cast<size_t>(n) * a.num_sites + a.site];
+    for (int e = lane; e < a.d * a.d; e += 32) {
+      const double2 v = displacement_element(mu.x, mu.y, e / a.d, e % a.d);
+      sD[wib][e] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+    }
+    __syncwarp();
+    float mx = 0.f;
+    const int kk = select_displaced<MAXD>(a, n, lane, D, mx);
+    if (kk != kDead) {
+      outcome = kk;
+      if (mx > 0.f) {
+        int e;
+        frexpf(mx, &e);
+        scale = ldexpf(1.0f, -e);
+        live_out = true;
+      }
+    }
+  } else if (live_in) {
     // Born weights of the outcomes (sampler.cpp:83-90): for d <= 32 lane k owns outcome k and sums
     // its tile partials sequentially in f64 (fixed order); the totals and the CDF walk broadcast the
     // per-lane weights in ascending k, exactly the reference's accumulation order over k.
@@ -691,7 +914,26 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
     const int C = a.env_comp;
     for (int r = lane * 4; r < a.kp_next; r += 128) {  // kp_next is a multiple of 32
       float4 v01 = make_float4(0.f, 0.f, 0.f, 0.f), v23 = v01;
-      if (r + 3 < live_cols) {  // chirp is a multiple of 128: these loads stay inside the row
+      if (kDisp && r < live_cols) {  // displaced: row `outcome` of D applied on the fly
+        float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int q = 0; q < a.d; ++q) {  // chirp is a multiple of 128: the 4 columns stay in the row
+          const float2 dk = D[outcome * a.d + q];
+          const float2* src_q = a.temp + (static_cast<size_t>(n) * a.d + q) * a.chirp + r;
+          const float4 x01 = *reinterpret_cast<const float4*>(src_q);
+          const float4 x23 = *reinterpret_cast<const float4*>(src_q + 2);
+          const float xs[8] = {x01.x, x01.y, x01.z, x01.w, x23.x, x23.y, x23.z, x23.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            o[2 * j] = fmaf(dk.x, xs[2 * j], fmaf(-dk.y, xs[2 * j + 1], o[2 * j]));
+            o[2 * j + 1] = fmaf(dk.x, xs[2 * j + 1], fmaf(dk.y, xs[2 * j], o[2 * j + 1]));
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (r + j >= live_cols) o[2 * j] = o[2 * j + 1] = 0.f;
+        v01 = make_float4(o[0], o[1], o[2], o[3]);
+        v23 = make_float4(o[4], o[5], o[6], o[7]);
+      } else if (r + 3 < live_cols) {  // chirp is a multiple of 128: these loads stay inside the row
         v01 = *reinterpret_cast<const float4*>(src + r);
         v23 = *reinterpret_cast<const float4*>(src + r + 2);
       } else if (r < live_cols) {
@@ -754,111 +996,15 @@ void launch_reduce_tiles(const float2* pstat, int nt, int tiles_per_k, int d, in
 void launch_select(const SelectArgs& a, cudaStream_t s) {
   const int threads = 256;
   const int blocks = (a.rows * 32 + threads - 1) / threads;
-  select_kernel<<<blocks, threads, 0, s>>>(a);
-}
-
-// ============================================================================================
-// GBS displacement (SPEC.md:366-381, PAPER.md §3.4 Eq. 6): D(mu) = exp(-|mu|^2/2) L U with the
-// closed-form triangular factors L = exp(mu a^dag), U = exp(-conj(mu) a); applied per sample to the
-// d outcome components of every column of temp (the reference's SiteTransform hook position,
-// sampler.cpp:143).  The closed form gives the exact Fock-basis elements of D(mu) (no truncation
-// of the generator).
-// ============================================================================================
-__device__ __forceinline__ double2 displacement_element(double mr, double mi, int a, int c) {
-  // D[a][c] = exp(-|mu|^2/2) sum_{b <= min(a, c)} L[a][b] U[b][c]
-  const double pre = exp(-0.5 * (mr * mr + mi * mi));
-  double sr = 0.0, si = 0.0;
-  const int bmax = min(a, c);
-  for (int b = 0; b <= bmax; ++b) {
-    double lr = 1.0, li = 0.0, ur = 1.0, ui = 0.0;
-    for (int j = 0; j < a - b; ++j) {  // mu^(a-b)
-      const double t = lr * mr - li * mi;
-      li = lr * mi + li * mr;
-      lr = t;
-    }
-    for (int j = 0; j < c - b; ++j) {  // (-conj(mu))^(c-b) = (-mr + i mi)^(c-b)
-      const double t = -ur * mr - ui * mi;
-      ui = ur * mi - ui * mr;
-      ur = t;
-    }
-    const double fl = exp(0.5 * (lgamma(a + 1.0) - lgamma(b + 1.0)) - lgamma(a - b + 1.0));
-    const double fu = exp(0.5 * (lgamma(c + 1.0) - lgamma(b + 1.0)) - lgamma(c - b + 1.0));
-    lr *= fl, li *= fl, ur *= fu, ui *= fu;
-    sr += lr * ur - li * ui;
-    si += lr * ui + li * ur;
+  if (a.mu != nullptr) {
+    ensure_fact_table();
+    if (a.d <= 8)
+      select_kernel<true, 8><<<blocks, threads, 0, s>>>(a);
+    else
+      select_kernel<true, kMaxDisplacedDim><<<blocks, threads, 0, s>>>(a);
+  } else {
+    select_kernel<false><<<blocks, threads, 0, s>>>(a);
   }
-  return make_double2(pre * sr, pre * si);
-}
-
-__global__ void displacement_matrix_kernel(double mr, double mi, int n, double2* out) {
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) out[e] = displacement_element(mr, mi, e / n, e % n);
-}
-
-void launch_displacement_matrix(double mu_re, double mu_im, int n, double2* out, cudaStream_t s) {
-  displacement_matrix_kernel<<<1, 256, 0, s>>>(mu_re, mu_im, n, out);
-}
-
-// One warp per sample: D(mu_n) into shared memory (f64 generation, fp32 apply), then per 128-column
-// tile the transformed components, their Born-weight partials and max (fixed-order warp trees).
-__global__ void __launch_bounds__(256) displace_kernel(const DisplaceArgs a) {
-  __shared__ float2 sD[8][kMaxDisplacedDim * kMaxDisplacedDim];
-  const int wib = threadIdx.x >> 5;
-  const int n = blockIdx.x * 8 + wib;
-  const int lane = threadIdx.x & 31;
-  if (n >= a.count || !a.alive[n]) return;  // warp-uniform
-  const int d = a.d;
-  const double2 mu = a.mu[static_cast<size_t>(n) * a.num_sites + a.site];
-  for (int e = lane; e < d * d; e += 32) {
-    const double2 v = displacement_element(mu.x, mu.y, e / d, e % d);
-    sD[wib][e] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
-  }
-  __syncwarp();
-  const float2* D = sD[wib];
-  float2* row = a.temp + static_cast<size_t>(n) * d * a.chirp;  // [d][chirp]
-  for (int t = 0; t < a.tpk; ++t) {
-    float w[kMaxDisplacedDim], mx[kMaxDisplacedDim];
-#pragma unroll
-    for (int k = 0; k < kMaxDisplacedDim; ++k) w[k] = 0.f, mx[k] = 0.f;
-    for (int j = 0; j < 4; ++j) {
-      const int r = t * 128 + j * 32 + lane;
-      if (r >= a.chir_loc) continue;
-      float2 v[kMaxDisplacedDim];
-#pragma unroll
-      for (int k = 0; k < kMaxDisplacedDim; ++k)
-        if (k < d) v[k] = row[static_cast<size_t>(k) * a.chirp + r];
-      const float wl = a.cinfo[r].y;
-#pragma unroll
-      for (int k = 0; k < kMaxDisplacedDim; ++k) {
-        if (k >= d) break;
-        float orr = 0.f, oi = 0.f;
-#pragma unroll
-        for (int q = 0; q < kMaxDisplacedDim; ++q) {
-          if (q >= d) break;
-          const float2 dk = D[k * d + q];
-          orr = fmaf(dk.x, v[q].x, fmaf(-dk.y, v[q].y, orr));
-          oi = fmaf(dk.x, v[q].y, fmaf(dk.y, v[q].x, oi));
-        }
-        row[static_cast<size_t>(k) * a.chirp + r] = make_float2(orr, oi);
-        w[k] = fmaf(wl, fmaf(orr, orr, oi * oi), w[k]);
-        mx[k] = fmaxf(mx[k], fmaxf(fabsf(orr), fabsf(oi)));
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kMaxDisplacedDim; ++k) {
-      if (k >= d) break;
-      float ws = w[k], ms = mx[k];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        ws += __shfl_xor_sync(0xffffffffu, ws, o);
-        ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
-      }
-      if (lane == 0) a.pstat[static_cast<size_t>(n) * a.nt + k * a.tpk + t] = make_float2(ws, ms);
-    }
-  }
-}
-
-void launch_displace(const DisplaceArgs& a, cudaStream_t s) {
-  displace_kernel<<<(a.count + 7) / 8, 256, 0, s>>>(a);
 }
 
 // ============================================================================================
