@@ -215,6 +215,9 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--schedule-eps", type=float, default=0.0,
+                    help="dynamic bond dimensions: truncate every bond to discarded weight <= eps "
+                         "(dynamic_bond_schedule, edge budgets 100x the centre) before sampling")
     ap.add_argument("--displace", type=float, default=0.0,
                     help="GBS displacement site transform with mu ~ complex normal of this std per "
                          "(sample, site) (0 = none)")
@@ -252,10 +255,18 @@ def main():
     smp, _ = build_synthetic(cfg["M"], cfg["chi"], cfg["d"], seed=42, mode=mode, devices=[local],
                              pass_samples=P_pass, record_site_times=2, host_stream_slots=args.stream_slots,
                              policy=P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX),
-                             scheme={"auto": 0, "3m": 3, "4m": 4}[args.scheme])
+                             scheme={"auto": 0, "3m": 3, "4m": 4}[args.scheme],
+                             schedule=(P.TruncationFilter(chi_max=cfg["chi"], eps_center=args.schedule_eps,
+                                                          edge_factor=100.0) if args.schedule_eps > 0 else None))
     scheme = "3M" if smp.scheme == P.Scheme.M3 else "4M"
     build_s = time.perf_counter() - t0
     macs_per_sample, bonds = chain_macs(cfg["M"], cfg["chi"], cfg["d"])
+    sched_note = None
+    if args.schedule_eps > 0:
+        b = smp.bond_dims
+        sched_macs = sum(b[i] * b[i + 1] * cfg["d"] for i in range(cfg["M"]))
+        sched_note = (f"dynamic bonds, eps_center={args.schedule_eps:g} (edges x101): {sched_macs / macs_per_sample:.3f} "
+                      f"of the full chain's MACs; max chi {max(b)}")
     rows_dev = torch.empty((P_pass, cfg["M"]), dtype=torch.uint8, device="cuda")
 
     mu_host = rows_host = None
@@ -337,7 +348,9 @@ def main():
         smp, _ = build_synthetic(cfg["M"], cfg["chi"], cfg["d"], seed=42, mode=mode, devices=[local],
                                  pass_samples=P_pass, record_site_times=0, host_stream_slots=3,
                                  policy=P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX),
-                                 scheme={"auto": 0, "3m": 3, "4m": 4}[args.scheme])
+                                 scheme={"auto": 0, "3m": 3, "4m": 4}[args.scheme],
+                                 schedule=(P.TruncationFilter(chi_max=cfg["chi"], eps_center=args.schedule_eps,
+                                                              edge_factor=100.0) if args.schedule_eps > 0 else None))
         e2e_build_s = time.perf_counter() - t0
         step(args.warmup + args.steps)  # one untimed warm-up pass of the streamed state
     e2e_s = 0.0
@@ -392,6 +405,7 @@ def main():
                        "M": cfg["M"], "chi": cfg["chi"], "d": cfg["d"], "pass_samples_per_gpu": P_pass,
                        "job_samples": cfg["job"], "job_seconds_at_value": cfg["job"] / value,
                        "mode": args.mode, "scheme": scheme, "parallelism": f"dp{world}",
+                       "bond_schedule": sched_note,
                        "displacement": (f"GBS displacement D(mu) per (sample, site), mu ~ CN(0, {args.displace}^2)"
                                         if args.displace > 0 else None),
                        "l2": f"inputs larger than L2 (compressed MPS {smp.state_bytes / 1e9:.1f} GB)",

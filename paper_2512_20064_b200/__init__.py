@@ -10,6 +10,9 @@ from .sampler import (  # noqa: F401
     BondSchedule,
     ParallelResult,
     apply_schedule,
+    dynamic_bond_schedule,
+    entanglement_entropy,
+    TruncationFilter,
     run_data_parallel,
     run_serial,
     ConfigError,

@@ -205,7 +205,7 @@ class BatchPlan:
 class SamplerOptions:
     policy: PrecisionPolicy = field(default_factory=PrecisionPolicy)
     seed: int = 0
-    schedule: Optional[object] = None        # BondSchedule: not supported on the GPU path
+    schedule: Optional[object] = None        # BondSchedule: applied to the state before upload
     site_transform: Optional[object] = None  # SiteTransform hook: a Displacement, else ConfigError
     record_decay_trace: bool = False
     mode: Mode = Mode.AUTO
@@ -437,6 +437,60 @@ class BondSchedule:
     @staticmethod
     def full(bond_dims, chi_max: int) -> "BondSchedule":
         return BondSchedule(list(bond_dims), chi_max)
+
+
+def entanglement_entropy(lam) -> float:
+    """S = -sum L^2 ln L^2 with 0 ln 0 = 0 (SPEC.md gbs-ops entanglement_entropy; Fig. 6)."""
+    p = np.square(np.asarray(lam, dtype=np.float64))
+    norm = float(p.sum())
+    if abs(norm - 1.0) > 1e-9:
+        raise NumericError(f"entanglement_entropy: Lambda is not normalised (sum L^2 = {norm!r})")
+    nz = p[p > 0]
+    return float(-(nz * np.log(nz)).sum())
+
+
+@dataclass
+class TruncationFilter:
+    """TruncationFilterConfig (SPEC.md gbs-ops): per-bond discarded-weight budgets eps_b with
+    eps_b >= eps_center, equality at the centre bond and nonincreasing toward it (§3.4:
+    "more aggressive at the edges").  eps_b = eps_center * (1 + edge_factor * x^edge_power) with
+    x = |b - M/2| / (M/2) in [0, 1]; `budget` overrides the shape with any callable(b, M)."""
+
+    chi_max: int
+    eps_center: float = 1e-6
+    edge_factor: float = 0.0
+    edge_power: float = 2.0
+    budget: Optional[object] = None
+
+    def eps(self, bond: int, num_sites: int) -> float:
+        if self.budget is not None:
+            return float(self.budget(bond, num_sites))
+        half = num_sites / 2.0
+        x = abs(bond - half) / half if half > 0 else 0.0
+        return self.eps_center * (1.0 + self.edge_factor * x ** self.edge_power)
+
+
+def dynamic_bond_schedule(lambdas, cfg: TruncationFilter, bond_dims=None) -> BondSchedule:
+    """dynamic_bond_schedule (SPEC.md gbs-ops, §3.4 / Table 1): bond b (between sites b-1
+    and b, Lambda vector lambdas[b-1]) keeps the smallest k with sum_{j >= k} L[j]^2 <= eps_b, capped
+    at chi_max (and at the state's own bond); boundary bonds are 1.  The result plugs into
+    SamplerOptions.schedule / apply_schedule (sampler.cpp:173-176, 218-246)."""
+    m = len(lambdas)
+    chi = [1] * (m + 1)
+    for b in range(1, m):
+        lam = np.asarray(lambdas[b - 1], dtype=np.float64)
+        if lam.size == 0:
+            raise ConfigError("dynamic_bond_schedule: empty spectrum")
+        if np.any(np.diff(lam) > 0):
+            raise NumericError("dynamic_bond_schedule: Lambda must be nonincreasing")
+        p = lam * lam
+        tail = np.cumsum(p[::-1])[::-1]  # tail[k] = sum_{j >= k} L[j]^2
+        eps = cfg.eps(b, m)
+        ok = np.nonzero(np.append(tail, 0.0)[1:] <= eps)[0]  # discarded weight when keeping k + 1
+        k = int(ok[0]) + 1 if ok.size else lam.size
+        cap = cfg.chi_max if bond_dims is None else min(cfg.chi_max, int(bond_dims[b]))
+        chi[b] = max(1, min(k, cap))
+    return BondSchedule(chi, cfg.chi_max)
 
 
 def apply_schedule(mps: MpsState, schedule: BondSchedule) -> MpsState:

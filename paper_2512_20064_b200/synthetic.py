@@ -47,8 +47,12 @@ def build_synthetic(num_sites: int, chi: int, d: int, seed: int = 42, level_damp
                     mode: Mode = Mode.AUTO, devices: Optional[Sequence[int]] = None,
                     pass_samples: int = 0, n_base: int = 4, record_site_times: bool = False,
                     keep_host: bool = False, tp_size: int = 1, tp_rank: int = 0,
-                    host_stream_slots: int = 0, scheme: int = 0):
+                    host_stream_slots: int = 0, scheme: int = 0, schedule=None):
     """Build a GpuSampler holding a synthetic chain; returns (sampler, lambdas[, host gammas]).
+
+    schedule: an optional TruncationFilter -- the chain is generated at the capped bonds and then
+    truncated to dynamic_bond_schedule(lambdas) exactly like apply_schedule (sampler.cpp:218-246):
+    Gamma_i[:chi_{i}, :chi_{i+1}, :] and Lambda_i[:chi_{i+1}] (ragged per-site GEMM shapes).
 
     The MPS is generated and compressed site by site on the first device, never materialised in
     host memory (c3: 102 GB compressed, 409 GB as complex128)."""
@@ -62,6 +66,13 @@ def build_synthetic(num_sites: int, chi: int, d: int, seed: int = 42, level_damp
     rng = np.random.default_rng(seed)
     lambdas = [random_lambda(rng, bonds[i + 1], decay) if i + 1 < num_sites else np.ones(1)
                for i in range(num_sites)]
+    full_bonds = list(bonds)
+    if schedule is not None:
+        from .sampler import dynamic_bond_schedule
+        bonds = [min(a, b) for a, b in zip(dynamic_bond_schedule(lambdas, schedule, full_bonds).per_site_chi,
+                                           full_bonds)]
+        bonds[0] = bonds[-1] = 1
+        lambdas = [np.ascontiguousarray(lambdas[i][:bonds[i + 1]]) for i in range(num_sites)]
     gen = torch.Generator(device=device)
     gen.manual_seed(seed)
     bases = {}
@@ -78,11 +89,12 @@ def build_synthetic(num_sites: int, chi: int, d: int, seed: int = 42, level_damp
         lam_prev = torch.ones(1, dtype=torch.float32, device=device)
         for i in range(num_sites):
             cl, cr = bonds[i], bonds[i + 1]
-            key = (cl, cr)
+            fl, fr = full_bonds[i], full_bonds[i + 1]
+            key = (fl, fr)
             if key not in bases:
-                bases[key] = [_isometry(torch, cl, cr * d, d, level_damping, gen, device)
+                bases[key] = [_isometry(torch, fl, fr * d, d, level_damping, gen, device)
                               for _ in range(min(n_base, num_sites))]
-            hb = bases[key][i % len(bases[key])]
+            hb = bases[key][i % len(bases[key])][:cl, :cr * d]  # the scheduled truncation
             phase = torch.exp(2j * np.pi * torch.rand(cr * d, generator=gen, device=device,
                                                       dtype=torch.float32)).to(torch.complex64)
             lam = torch.as_tensor(lambdas[i], dtype=torch.float32, device=device)

@@ -464,3 +464,20 @@ def test_displaced_sampling_bench_dims_and_tp(pkg):
     assert np.array_equal(t[0], t[1])
     assert (t[0] != gpu_rows).any(axis=1).sum() <= 1
     tp.close()
+
+
+def test_dynamic_bond_schedule_ragged_chain(pkg):
+    """A device-generated chi = 512 chain truncated by dynamic_bond_schedule (ragged, non-monotone
+    per-site GEMM shapes, padded K / N tiles): parity vs the oracle on the same truncated chain."""
+    cfg = pkg.TruncationFilter(chi_max=512, eps_center=2e-2, edge_factor=4.0)
+    smp, lams, _ = _synthetic(pkg, 10, 512, 6, schedule=cfg)
+    b = smp.bond_dims
+    assert max(b) < 512 and len(set(b[2:-2])) > 1
+    dec = O.Mps(6, list(b), [smp.decoded_gamma(i) for i in range(10)], list(lams))
+    ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, 64, 7, want_marginals=True)
+    gpu_rows = smp.sample(0, 64, 7)
+    gm = smp.marginals(0, ref_rows)
+    big = ref_marg >= 1e-3
+    assert (np.abs(gm[big] - ref_marg[big]) / ref_marg[big]).max() < MARG_RTOL
+    ndiff, explained = compare_strings(gpu_rows, ref_rows, ref_marg, 7)
+    assert ndiff == explained, (ndiff, explained)

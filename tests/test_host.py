@@ -224,3 +224,40 @@ def test_cpp_dropin_adapter_cpu():
     import subprocess
     r = subprocess.run([ADAPTER, "cpu"], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_dynamic_bond_schedule_spec_examples():
+    """dynamic_bond_schedule / entanglement_entropy (SPEC.md gbs-ops examples, Table 1)."""
+    assert P.entanglement_entropy([1.0]) == 0.0
+    assert abs(P.entanglement_entropy([2 ** -0.5, 2 ** -0.5]) - np.log(2)) < 1e-15
+    with pytest.raises(P.NumericError):
+        P.entanglement_entropy([0.5, 0.5])
+    m = 12
+    # product state: chi = 1 everywhere
+    s = P.dynamic_bond_schedule([np.array([1.0, 0.0, 0.0, 0.0])] * m, P.TruncationFilter(chi_max=4, eps_center=1e-9))
+    assert s.per_site_chi == [1] * (m + 1)
+    assert abs(s.compute_ratio() - 1.0 / 16) < 1e-15
+    # flat spectrum, no budget: chi_max everywhere, step ratio 100%
+    s = P.dynamic_bond_schedule([np.ones(16) / 4.0] * m, P.TruncationFilter(chi_max=16, eps_center=0.0))
+    assert s.per_site_chi[1:-1] == [16] * (m - 1) and s.step_ratio() == 1.0
+    # area-law spectra, edge-aggressive budgets: comp ratio < 1, equivalent chi < chi_max, budgets
+    # nonincreasing toward the centre, smaller eps never lowers chi (schedule monotonicity)
+    rng = np.random.default_rng(0)
+    lams = []
+    for b in range(1, m):
+        rate = 0.05 + 0.3 * abs(b - m / 2) / (m / 2)  # entanglement peaked at the centre
+        lam = np.exp(-rate * np.arange(64)) * (1 + 0.01 * rng.uniform(size=64))
+        lam = np.sort(lam)[::-1]
+        lams.append(lam / np.linalg.norm(lam))
+    lams.append(np.ones(1))
+    cfg = P.TruncationFilter(chi_max=64, eps_center=1e-8, edge_factor=100.0)
+    eps = [cfg.eps(b, m) for b in range(m + 1)]
+    assert min(eps) == eps[m // 2] and all(eps[b] >= eps[b + 1] for b in range(m // 2))
+    s = P.dynamic_bond_schedule(lams, cfg)
+    assert s.compute_ratio() < 1.0 and s.equivalent_chi() < 64
+    tighter = P.dynamic_bond_schedule(lams, P.TruncationFilter(chi_max=64, eps_center=1e-10, edge_factor=100.0))
+    assert all(a >= b for a, b in zip(tighter.per_site_chi, s.per_site_chi))
+    for b in range(1, m):  # the rule itself: minimal k with discarded weight <= eps_b
+        k, lam = s.per_site_chi[b], lams[b - 1]
+        assert (lam[k:] ** 2).sum() <= eps[b] + 1e-18
+        assert k == 1 or (lam[k - 1:] ** 2).sum() > eps[b]

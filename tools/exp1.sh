@@ -1,6 +1,3 @@
 cd $GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 2>&1 | tail -2
-b() { timeout 300 env $1 python bench.py --config c2 $2 --no-cpu-baseline --steps 3 --e2e resident --e2e-steps 1 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['roofline']['gemm_share_of_step'], d['clocks']['sm_mhz'])"; }
-echo "c2 plain"; b X=1 ""
-echo "c2 displaced fused"; b X=1 "--displace 0.5"
-echo "c2 displaced separate"; b MPSG_DISPLACE_SEPARATE=1 "--displace 0.5"
+for e in 0 1e-6 1e-4; do timeout 300 python bench.py --config c3 --schedule-eps $e --no-cpu-baseline --steps 2 --e2e resident --e2e-steps 1 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c3 eps $e', d['value'], d['roofline']['frac'], d['config']['bond_schedule'], d['clocks']['sm_mhz'])"; done
