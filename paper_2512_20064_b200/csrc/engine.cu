@@ -127,7 +127,9 @@ static void part_range(int extent, int parts, int i, int& b, int& e) {
 struct Comm {
   virtual ~Comm() = default;
   // In place: this rank's chunk sits at buf + rank * chunk; afterwards every slot is filled.
-  virtual void allgather(void* buf, size_t chunk, cudaStream_t s) = 0;
+  // lane: the pipeline lane issuing the call; every lane has its own ordered channel (its own NCCL
+  // communicator) so the two lanes' collectives never interleave on one communicator.
+  virtual void allgather(void* buf, size_t chunk, cudaStream_t s, int lane) = 0;
 };
 
 struct NcclApi {
@@ -135,6 +137,7 @@ struct NcclApi {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -149,6 +152,7 @@ static const NcclApi& nccl() {
     api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
     api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(h, "ncclAllGather"));
     api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.commSplit = reinterpret_cast<decltype(api.commSplit)>(dlsym(h, "ncclCommSplit"));
     api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(dlsym(h, "ncclGetErrorString"));
   });
   if (!api.allGather || !api.commInitRank || !api.getUniqueId)
@@ -164,16 +168,21 @@ static const NcclApi& nccl() {
   } while (0)
 
 struct NcclComm : Comm {
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm[2] = {nullptr, nullptr};  // lane 0, lane 1 (split from lane 0 on first use)
   int rank = 0;
   NcclComm(const ncclUniqueId& id, int nranks, int r) : rank(r) {
-    NCCL_OK(nccl().commInitRank(&comm, nranks, id, r));
+    NCCL_OK(nccl().commInitRank(&comm[0], nranks, id, r));
   }
   ~NcclComm() override {
-    if (comm && nccl().commDestroy) nccl().commDestroy(comm);
+    for (auto c : comm)
+      if (c && nccl().commDestroy) nccl().commDestroy(c);
   }
-  void allgather(void* buf, size_t chunk, cudaStream_t s) override {
-    NCCL_OK(nccl().allGather(static_cast<char*>(buf) + rank * chunk, buf, chunk, ncclUint8, comm, s));
+  void allgather(void* buf, size_t chunk, cudaStream_t s, int lane) override {
+    if (lane == 1 && !comm[1]) {  // collective: every rank reaches it at the same point of the sweep
+      if (!nccl().commSplit) throw Error(MPSG_ERR_CUDA, "ncclCommSplit unavailable (needs NCCL >= 2.18)");
+      NCCL_OK(nccl().commSplit(comm[0], 0, rank, &comm[1], nullptr));
+    }
+    NCCL_OK(nccl().allGather(static_cast<char*>(buf) + rank * chunk, buf, chunk, ncclUint8, comm[lane], s));
   }
 };
 
@@ -209,7 +218,8 @@ struct LocalComm : Comm {
   std::shared_ptr<LocalGroup> g;
   int rank;
   LocalComm(std::shared_ptr<LocalGroup> grp, int r) : g(std::move(grp)), rank(r) {}
-  void allgather(void* buf, size_t chunk, cudaStream_t s) override {
+  void allgather(void* buf, size_t chunk, cudaStream_t s, int /*lane*/) override {
+    // host barriers serialise the calls of all lanes in issue order, identical on every rank
     LocalGroup& G = *g;
     G.bufs[rank] = buf;
     CUDA_OK(cudaEventRecord(G.ready[rank], s));
@@ -433,10 +443,12 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     want = std::min<uint64_t>(65536, static_cast<uint64_t>(budget / row_bytes));
   }
   // Two lanes overlap the select kernel with the other lane's contraction; measured neutral under
-  // the 1000 W power cap (c2 +2%, c3 -2.5%), so one lane is the default.
-  int nlanes = 1;
+  // the 1000 W power cap without tensor parallelism (c2 +2%, c3 -2.5%), so one lane is the default.
+  // Tensor parallelism defaults to two lanes: one lane's partial / environment all-gathers and
+  // selection run underneath the other lane's contraction, so the GEMM and the collectives overlap.
+  int nlanes = h.tp > 1 ? 2 : 1;
   if (const char* v = std::getenv("MPSG_LANES")) nlanes = std::max(1, std::min(2, std::atoi(v)));
-  if (h.opts.host_stream_slots != 0 || h.tp != 1) nlanes = 1;
+  if (h.opts.host_stream_slots != 0) nlanes = 1;
   const int lane_cap = std::max(2 * kBM, round_up(static_cast<int>((std::min<uint64_t>(want, 1u << 22) +
                                                                      nlanes - 1) / nlanes), 2 * kBM));
   dc.cap = nlanes * lane_cap;
@@ -859,7 +871,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       } else {  // per-rank (weight, max) per outcome, exchanged, summed in rank order on every rank
         launch_reduce_tiles(ln.pstat, s.nt, s.chirp / kBN, sa.d, rows[L],
                             ln.part + 1ull * h.tp_rank * ln.cap * h.d, ln.stream);
-        h.comm->allgather(ln.part, 1ull * ln.cap * h.d * sizeof(float2), ln.stream);
+        h.comm->allgather(ln.part, 1ull * ln.cap * h.d * sizeof(float2), ln.stream, L);
         sa.parts = h.tp;
         sa.part_base = ln.part;
         sa.part_stride = 1ll * ln.cap * static_cast<long long>(h.d);
@@ -891,7 +903,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       sa.cinfo = cinfo;
       launch_select(sa, ln.stream);
       if (h.tp > 1 && has_next)  // rebuild the full environment from the column shards
-        h.comm->allgather(ln.env, 2ull * h.env_comp * ln.cap * kn * sizeof(__half), ln.stream);
+        h.comm->allgather(ln.env, 2ull * h.env_comp * ln.cap * kn * sizeof(__half), ln.stream, L);
       po.launches += 2;
       po.macs += static_cast<uint64_t>(cnt[L]) * s.chil * s.width * h.d;
       po.wmacs += static_cast<uint64_t>(cnt[L]) * s.width * h.d;
