@@ -481,3 +481,42 @@ def test_dynamic_bond_schedule_ragged_chain(pkg):
     assert (np.abs(gm[big] - ref_marg[big]) / ref_marg[big]).max() < MARG_RTOL
     ndiff, explained = compare_strings(gpu_rows, ref_rows, ref_marg, 7)
     assert ndiff == explained, (ndiff, explained)
+
+
+@pytest.mark.parametrize("scheme", [3, 4])
+def test_randomized_shapes(pkg, scheme):
+    """Seeded fuzz over chain shapes: random M, d, ragged bonds (1..300, not capped), pass sizes and
+    scaling modes; every chain must match the oracle on the decoded tensors (strings up to boundary
+    draws, teacher-forced marginals within 1e-4)."""
+    rng = np.random.default_rng(1234 + scheme)
+    for case in range(16):
+        m = int(rng.integers(2, 9))
+        d = int(rng.integers(1, 13))
+        bonds = [1] + [int(rng.integers(1, 301)) for _ in range(m - 1)] + [1]
+        gam, lam = [], []
+        for i in range(m):
+            cl, cr = bonds[i], bonds[i + 1]
+            g = (rng.standard_normal((cl, cr, d)) + 1j * rng.standard_normal((cl, cr, d))) / np.sqrt(cl * d)
+            gam.append(g)
+            l = np.sort(rng.uniform(0.05, 1.0, cr))[::-1]
+            if case % 5 == 4 and cr > 2:
+                l[cr // 2:] = 0.0  # zero-weight columns (Lambda_r = 0 is legal, mps.cpp:31-35)
+            lam.append(l / np.linalg.norm(l))
+        mps = O.Mps(d, bonds, gam, lam)
+        scaling = [0, 2][case % 2]
+        pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode(scaling))
+        n = int(rng.integers(1, 400))
+        smp = pkg.GpuSampler(to_state(pkg, mps), pol, scheme=pkg.Scheme(scheme),
+                             pass_samples=int(rng.choice([128, 256, 1024])))
+        dec = decoded_mps(smp, mps)
+        seed = int(rng.integers(0, 2**63))
+        ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, n, seed, scaling=scaling, want_marginals=True)
+        got = smp.sample(0, n, seed)
+        ndiff, explained = compare_strings(got, ref_rows, ref_marg, seed)
+        assert ndiff == explained, (case, m, d, bonds, ndiff, explained)
+        gm = smp.marginals(0, ref_rows)
+        big = ref_marg >= 1e-3
+        if big.any():
+            rel = (np.abs(gm[big] - ref_marg[big]) / ref_marg[big]).max()
+            assert rel < MARG_RTOL, (case, m, d, bonds, rel)
+        smp.close()
