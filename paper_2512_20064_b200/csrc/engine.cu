@@ -749,7 +749,11 @@ static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const S
       const char* v = std::getenv("MPSG_3M_EPI");
       return v ? std::atoi(v) : 8;
     }();
-    launch_site_gemm_3m(h.split, epilogue_max(h, s), env_epi, ln.tma_env64[i], *tma_g128, ga,
+    static const bool env_quad = [] {
+      const char* v = std::getenv("MPSG_3M_QUAD");
+      return v && std::atoi(v) != 0;
+    }();
+    launch_site_gemm_3m(h.split, epilogue_max(h, s), env_epi, env_quad, ln.tma_env64[i], *tma_g128, ga,
                         std::min(ctas, dc.num_sms), stream);
     return;
   }

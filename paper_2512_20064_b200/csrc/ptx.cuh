@@ -103,6 +103,18 @@ __device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap* m, uint32_t 
       "l"(policy)
       : "memory");
 }
+// Same, multicast to every CTA in `mask`; each destination's bytes are counted on the barrier at
+// the same offset in that destination's CTA-pair leader.
+__device__ __forceinline__ void tma_load_3d_pair_mc(const CUtensorMap* m, uint32_t leader_bar_addr,
+                                                    void* dst, int32_t c0, int32_t c1, int32_t c2,
+                                                    uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6, %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar_addr), "r"(c0), "r"(c1), "r"(c2), "h"(mask),
+      "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                    smem_u32(dst_smem)),

@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "ptx.cuh"
 #include "sweep.cuh"
 
@@ -49,11 +51,11 @@ int gemm_3m_smem_bytes(bool split) { return split ? Cfg3M<true>::kSmem : Cfg3M<f
 // Unit u -> (Gamma tile m, sample tile t).  Groups of `group` Gamma tiles are swept over all sample
 // tiles (Gamma index fastest), so the group's Gamma planes stay in L2 while each environment tile
 // is fetched from DRAM once per group.
-__device__ __forceinline__ void unit_coords_3m(int u, const Gemm3MArgs& a, int& m, int& t) {
+__device__ __forceinline__ void unit_coords_3m(int u, const Gemm3MArgs& a, int g_tiles, int& m, int& t) {
   const int per_group = a.group * a.s_tiles;
   const int g = u / per_group;
   const int m0 = g * a.group;
-  const int gw = min(a.group, a.g_tiles - m0);
+  const int gw = min(a.group, g_tiles - m0);
   const int r = u - g * per_group;
   t = r / gw;
   m = m0 + (r - t * gw);
@@ -89,7 +91,11 @@ __device__ unsigned long long g_prof3m[8];
 
 // kMax: also the per-(sample, tile) max component (tensor-parallel handles exchange it; otherwise
 // the select kernel takes the max of the chosen slice itself).
-template <bool kSplit, bool kMax, int kEpiWarps>
+// kQuad: 4-CTA clusters = two CTA pairs working on the same sample tile and adjacent Gamma tiles;
+// the pairs share every environment tile through TMA multicast (pair 0 fetches the hi plane, pair 1
+// the lo plane, each for both pairs), cutting the L2 -> SM traffic per MMA by a quarter.  A stage
+// is refilled only when both pairs have consumed it (commits multicast to all four CTAs).
+template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad>
 __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
     site_gemm_3m_kernel(const __grid_constant__ CUtensorMap tma_env64,
                         const __grid_constant__ CUtensorMap tma_g, const Gemm3MArgs a) {
@@ -106,15 +112,19 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int rank = static_cast<int>(ptx::cluster_ctarank());
+  constexpr int kCl = kQuad ? 4 : 2;
+  const int crank = static_cast<int>(ptx::cluster_ctarank());
+  const int rank = crank & 1;  // rank within the CTA pair
+  const int pair = crank >> 1;
   const bool leader = rank == 0;
-  const int cluster = blockIdx.x >> 1;
-  const int num_clusters = gridDim.x >> 1;
+  const int cluster = blockIdx.x / kCl;
+  const int num_clusters = gridDim.x / kCl;
+  const int g_units = kQuad ? (a.g_tiles + 1) >> 1 : a.g_tiles;  // Gamma tile (pairs) per unit row
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&full[s], 1);   // leader: own expect_tx, bytes from both CTAs
-      ptx::mbar_init(&empty[s], 1);  // the leader's multicast commit
+      ptx::mbar_init(&empty[s], kQuad ? 2 : 1);  // the leaders' multicast commits
     }
     for (int j = 0; j < 2; ++j) ptx::mbar_init(&tfull[j], 1);
     for (int j = 0; j < 4; ++j) ptx::mbar_init(&tempty[j], 2 * kEpiWarps);  // epilogue warps x 2 CTAs
@@ -133,7 +143,7 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int units = a.g_tiles * a.s_tiles;
+  const int units = g_units * a.s_tiles;
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs; bytes counted on the leader's barrier) ----------
@@ -144,7 +154,8 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
       uint32_t phase = 0;
       for (int u = cluster; u < units; u += num_clusters) {
         int m, t;
-        unit_coords_3m(u, a, m, t);
+        unit_coords_3m(u, a, g_units, m, t);
+        if (kQuad) m = 2 * m + pair;
         const int grow = m * 2 * kBM + rank * kBM;     // this SM's Gamma rows
         const int erow = t * kBM + rank * (kBM / 2);   // this SM's sample rows
 #pragma unroll 1
@@ -156,10 +167,17 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
             const uint32_t lbar = ptx::leader_bar(&full[stage]);
             if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
             ptx::tma_load_2d_pair(&tma_g, lbar, st, kb * kBK3, c * a.np + grow, pol_g);
+            if constexpr (kQuad) {  // env plane h = pair for both pairs (same rows: same rank)
+              if (pair < C::kHalves)
+                ptx::tma_load_3d_pair_mc(&tma_env64, lbar, st + C::kATile + pair * C::kBTile, kin * kBK3,
+                                         (3 * pair + c) * a.env_cap + erow, shard,
+                                         static_cast<uint16_t>((1u << rank) | (1u << (rank + 2))), pol_env);
+            } else {
 #pragma unroll
-            for (int h = 0; h < C::kHalves; ++h)
-              ptx::tma_load_3d_pair(&tma_env64, lbar, st + C::kATile + h * C::kBTile, kin * kBK3,
-                                    (3 * h + c) * a.env_cap + erow, shard, pol_env);
+              for (int h = 0; h < C::kHalves; ++h)
+                ptx::tma_load_3d_pair(&tma_env64, lbar, st + C::kATile + h * C::kBTile, kin * kBK3,
+                                      (3 * h + c) * a.env_cap + erow, shard, pol_env);
+            }
             if (++stage == C::kStages) {
               stage = 0;
               phase ^= 1;
@@ -210,14 +228,15 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
                 ptx::umma_pair_elect(d, ad + 2 * ks, bd + 2 * ks, kId, accum, false, false);
               }
             }
-            ptx::umma_commit_pair_mc_elect(&empty[stage], 0x3);
+            ptx::umma_commit_pair_mc_elect(&empty[stage], kQuad ? 0xF : 0x3);
             if (++stage == C::kStages) {
               stage = 0;
               phase ^= 1;
             }
           }
         }
-        ptx::umma_commit_pair_mc_elect(&tfull[unit & 1], 0x3);  // all three products of the unit done
+        // all three products of the unit done -> this pair's epilogues
+        ptx::umma_commit_pair_mc_elect(&tfull[unit & 1], static_cast<uint16_t>(0x3u << (2 * pair)));
       }
       if ((a.flags & 32) && lane == 0) {
         atomicAdd(&g_prof3m[2], static_cast<unsigned long long>(w_slot));
@@ -235,10 +254,12 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
     int unit = 0;
     for (int u = cluster; u < units; u += num_clusters, ++unit, gp += 3) {
       int m, t;
-      unit_coords_3m(u, a, m, t);
+      unit_coords_3m(u, a, g_units, m, t);
+      if (kQuad) m = 2 * m + pair;
       const int col0 = m * 2 * kBM + rank * kBM;  // first of this SM's 128 columns (one outcome)
       const int k = col0 / a.chirp;
-      const bool valid = k < a.d;                  // the pair-padding tile has nothing to store
+      // the pair-padding tile (and a quad's phantom odd Gamma tile) has nothing to store
+      const bool valid = k < a.d && m < a.g_tiles;
       const int r = col0 - k * a.chirp + ec;
       const float2 ci = valid ? a.cinfo[col0 + ec] : make_float2(0.f, 0.f);
       const long long e0 = (a.flags & 32) ? clock64() : 0;
@@ -265,9 +286,9 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
           __syncwarp();
           if (a.flags & 32) e2 = clock64();
           if (lane == 0) {
-            ptx::mbar_arrive_remote_relaxed(&tempty[(gp + 0) & 3], 0);
-            ptx::mbar_arrive_remote_relaxed(&tempty[(gp + 1) & 3], 0);
-            ptx::mbar_arrive_remote_relaxed(&tempty[(gp + 2) & 3], 0);
+            ptx::mbar_arrive_remote_relaxed(&tempty[(gp + 0) & 3], 2 * pair);
+            ptx::mbar_arrive_remote_relaxed(&tempty[(gp + 1) & 3], 2 * pair);
+            ptx::mbar_arrive_remote_relaxed(&tempty[(gp + 2) & 3], 2 * pair);
           }
         }
         if (valid) {
@@ -319,48 +340,52 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
   }
 }
 
-template <bool kSplit, bool kMax, int kEpiWarps>
+template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad>
 static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
                         int grid, cudaStream_t s) {
-  auto kern = site_gemm_3m_kernel<kSplit, kMax, kEpiWarps>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg3M<kSplit>::kSmem);
-    attr = true;
-  }
+  auto kern = site_gemm_3m_kernel<kSplit, kMax, kEpiWarps, kQuad>;
+  constexpr int kCl = kQuad ? 4 : 2;
+  static int max_clusters = 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(128 + 32 * kEpiWarps);
   cfg.dynamicSmemBytes = Cfg3M<kSplit>::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.x = kCl;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  if (!max_clusters) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg3M<kSplit>::kSmem);
+    cfg.gridDim = dim3(kCl);
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
+      max_clusters = 148 / kCl;  // 4-CTA clusters: 33 on a B200 (132 SMs)
+  }
+  cfg.gridDim = dim3(kCl * std::max(1, std::min(max_clusters, grid / kCl)));
   cudaLaunchKernelEx(&cfg, kern, tma_env64, tma_g, a);
 }
 
 template <bool kSplit, bool kMax>
-static void launch_3m_w(int epi_warps, const CUtensorMap& e, const CUtensorMap& g, const Gemm3MArgs& a,
-                        int grid, cudaStream_t s) {
-  if (epi_warps == 4)
-    launch_3m_t<kSplit, kMax, 4>(e, g, a, grid, s);
+static void launch_3m_w(int epi_warps, bool quad, const CUtensorMap& e, const CUtensorMap& g,
+                        const Gemm3MArgs& a, int grid, cudaStream_t s) {
+  if (quad)
+    launch_3m_t<kSplit, kMax, 8, true>(e, g, a, grid, s);
+  else if (epi_warps == 4)
+    launch_3m_t<kSplit, kMax, 4, false>(e, g, a, grid, s);
   else
-    launch_3m_t<kSplit, kMax, 8>(e, g, a, grid, s);
+    launch_3m_t<kSplit, kMax, 8, false>(e, g, a, grid, s);
 }
 
-void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, const CUtensorMap& tma_env64,
+void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, const CUtensorMap& tma_env64,
                          const CUtensorMap& tma_g, const Gemm3MArgs& a, int grid, cudaStream_t s) {
-  grid = (grid + 1) & ~1;  // whole CTA pairs
   if (split)
-    with_max ? launch_3m_w<true, true>(epi_warps, tma_env64, tma_g, a, grid, s)
-             : launch_3m_w<true, false>(epi_warps, tma_env64, tma_g, a, grid, s);
+    with_max ? launch_3m_w<true, true>(epi_warps, quad, tma_env64, tma_g, a, grid, s)
+             : launch_3m_w<true, false>(epi_warps, quad, tma_env64, tma_g, a, grid, s);
   else
-    with_max ? launch_3m_w<false, true>(epi_warps, tma_env64, tma_g, a, grid, s)
-             : launch_3m_w<false, false>(epi_warps, tma_env64, tma_g, a, grid, s);
+    with_max ? launch_3m_w<false, true>(epi_warps, quad, tma_env64, tma_g, a, grid, s)
+             : launch_3m_w<false, false>(epi_warps, quad, tma_env64, tma_g, a, grid, s);
 }
 
 }  // namespace mpsg

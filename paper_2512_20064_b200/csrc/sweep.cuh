@@ -128,7 +128,8 @@ int gemm_pair_smem_bytes(bool split);
 // with_max: also the per-(sample, tile) max component in pstat.y (tensor parallelism); otherwise
 // pstat.y is 0 and the select kernel computes the chosen slice's max (SelectArgs::slice_max).
 // epi_warps: 4 or 8 epilogue warps (one or two per TMEM lane quarter).
-void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, const CUtensorMap& tma_env64,
+// quad: 4-CTA clusters sharing the environment tiles by multicast (see site_gemm_3m.cu).
+void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, const CUtensorMap& tma_env64,
                          const CUtensorMap& tma_g, const Gemm3MArgs& a, int grid, cudaStream_t s);
 int gemm_3m_smem_bytes(bool split);
 void launch_select(const SelectArgs& a, cudaStream_t s);
