@@ -212,7 +212,7 @@ def main():
     ap.add_argument("--scheme", default="auto", choices=["auto", "3m", "4m"],
                     help="complex decomposition of the contraction (auto = 3M when the state fits)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--schedule-eps", type=float, default=0.0,
