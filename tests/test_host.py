@@ -261,3 +261,18 @@ def test_dynamic_bond_schedule_spec_examples():
         k, lam = s.per_site_chi[b], lams[b - 1]
         assert (lam[k:] ** 2).sum() <= eps[b] + 1e-18
         assert k == 1 or (lam[k - 1:] ** 2).sum() > eps[b]
+
+
+def test_displacement_transform_host_checks():
+    """Displacement (the GBS SiteTransform): shape checks on the host; other site transforms are
+    rejected like the reference's TP executor rejects options it cannot run (ConfigError)."""
+    d = P.Displacement(np.zeros((10, 4), complex))
+    assert d.amplitudes(2, 5, 4).shape == (5, 4)
+    with pytest.raises(P.DimensionError):
+        d.amplitudes(8, 5, 4)  # beyond the batch
+    with pytest.raises(P.DimensionError):
+        d.amplitudes(0, 5, 3)  # wrong site count
+    mps = P.MpsState(2, 2, [1, 2, 1], [np.ones((1, 2, 2), complex), np.ones((2, 1, 2), complex)],
+                     [np.array([0.8, 0.6]), np.ones(1)])
+    with pytest.raises(P.ConfigError):
+        P.sample_batch(mps, P.BatchPlan(4), P.SamplerOptions(site_transform=lambda *a: None))
