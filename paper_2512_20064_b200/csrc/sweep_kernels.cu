@@ -404,10 +404,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer: one thread of the leader CTA drives both SMs ----------------
-    if (lane == 0 && leader) {
+    // ---------------- MMA issuer: the leader CTA's warp 1 drives both SMs ----------------
+    // The whole warp runs the loop with warp-uniform operands; one elected lane issues (no per-MMA
+    // R2UR waterfall, as in the 3M kernel).
+    if (leader) {
       constexpr uint32_t kId = ptx::idesc_f16_f32(2 * kBM, kBN, false);
       constexpr uint32_t kIdNeg = ptx::idesc_f16_f32(2 * kBM, kBN, true);
+      const uint64_t desc0 = ptx::sdesc_kmajor_sw64(ptx::smem_u32(smem));
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -420,31 +423,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = 0; kb < a.k_blocks; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t st = ptx::smem_u32(smem + stage * C::kStageBytes);
+          const uint64_t st = desc0 + ((stage * C::kStageBytes) >> 4);  // 16 B units
 #pragma unroll
           for (int ks = 0; ks < kBK / 16; ++ks) {
-            const uint32_t off = ks * 32;
-            const uint64_t br = ptx::sdesc_kmajor_sw64(st + C::kAPlanes * C::kATile + off);
-            const uint64_t bi = ptx::sdesc_kmajor_sw64(st + C::kAPlanes * C::kATile + C::kBTile + off);
+            const uint64_t off = 2 * ks;  // 32 B per K16 step inside the 64 B swizzle row
+            const uint64_t br = st + ((C::kAPlanes * C::kATile) >> 4) + off;
+            const uint64_t bi = br + (C::kBTile >> 4);
             const uint32_t accum = (kb | ks) ? 1u : 0u;
 #pragma unroll
             for (int h = 0; h < (kSplit ? 2 : 1); ++h) {
               const uint32_t acc0 = h ? 1u : accum;
-              const uint64_t ar = ptx::sdesc_kmajor_sw64(st + (2 * h + 0) * C::kATile + off);
-              const uint64_t ai = ptx::sdesc_kmajor_sw64(st + (2 * h + 1) * C::kATile + off);
-              ptx::umma_pair_afill(d_re, ar, br, kId, acc0);
-              ptx::umma_pair_alast(d_im, ar, bi, kId, acc0);
-              ptx::umma_pair(d_re, ai, bi, kIdNeg, 1u);
-              ptx::umma_pair(d_im, ai, br, kId, 1u);
+              const uint64_t ar = st + (((2 * h + 0) * C::kATile) >> 4) + off;
+              const uint64_t ai = st + (((2 * h + 1) * C::kATile) >> 4) + off;
+              ptx::umma_pair_elect(d_re, ar, br, kId, acc0, true, false);
+              ptx::umma_pair_elect(d_im, ar, bi, kId, acc0, false, true);
+              ptx::umma_pair_elect(d_re, ai, bi, kIdNeg, 1u, false, false);
+              ptx::umma_pair_elect(d_im, ai, br, kId, 1u, false, false);
             }
           }
-          ptx::umma_commit_pair_mc(&empty[stage], 0x3);
+          ptx::umma_commit_pair_mc_elect(&empty[stage], 0x3);
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::umma_commit_pair_mc(&tfull[acc], 0x3);
+        ptx::umma_commit_pair_mc_elect(&tfull[acc], 0x3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
