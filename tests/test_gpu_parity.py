@@ -520,3 +520,23 @@ def test_randomized_shapes(pkg, scheme):
             rel = (np.abs(gm[big] - ref_marg[big]) / ref_marg[big]).max()
             assert rel < MARG_RTOL, (case, m, d, bonds, rel)
         smp.close()
+
+
+@pytest.mark.parametrize("scheme", [3, 4])
+def test_single_mode_within_reference_f16_envelope(pkg, gold, scheme):
+    """SINGLE (one fp16 pass, compute = TF32 / F16 policies): its marginal error vs the f64 oracle stays
+    within the error envelope of the reference's own F16 compute policy (the oracle's emulated-F16
+    contraction, precision.cpp:23-50 / contract.cpp:53-81) on the same decoded chain."""
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    pol = pkg.PrecisionPolicy(compute=pkg.Precision.F16, scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    smp = pkg.GpuSampler(to_state(pkg, mps), pol, scheme=pkg.Scheme(scheme))
+    dec = decoded_mps(smp, mps)
+    n = 500
+    ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, n, 7, want_marginals=True)
+    _, f16_marg, _ = O.orc_sample_range(dec, 0, n, 7, compute=O.F16, forced=ref_rows, want_marginals=True)
+    gm = smp.marginals(0, ref_rows)
+    big = ref_marg >= 1e-3
+    err_gpu = (np.abs(gm[big] - ref_marg[big]) / ref_marg[big]).max()
+    err_f16 = (np.abs(f16_marg[big] - ref_marg[big]) / ref_marg[big]).max()
+    assert err_gpu <= max(2.0 * err_f16, 1e-3), (err_gpu, err_f16)
