@@ -374,6 +374,8 @@ static void launch_3m_w(int epi_warps, bool quad, const CUtensorMap& e, const CU
     launch_3m_t<kSplit, kMax, 8, true>(e, g, a, grid, s);
   else if (epi_warps == 4)
     launch_3m_t<kSplit, kMax, 4, false>(e, g, a, grid, s);
+  else if (epi_warps == 16)
+    launch_3m_t<kSplit, kMax, 16, false>(e, g, a, grid, s);
   else
     launch_3m_t<kSplit, kMax, 8, false>(e, g, a, grid, s);
 }
