@@ -240,11 +240,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: MPSG_BENCH_SHARE_DEVICE=1 puts every rank on device 0 with a gloo process group, so
+    # the multi-rank bench path can be exercised on a one-GPU box (NCCL rejects two ranks per GPU)
+    share = os.environ.get("MPSG_BENCH_SHARE_DEVICE") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2512_20064_b200 as P
     from paper_2512_20064_b200.synthetic import build_synthetic
@@ -325,7 +333,7 @@ def main():
     clocks = clk.stop()
     t_max = dev_s
     if dist:
-        tt = torch.tensor([dev_s], device="cuda", dtype=torch.float64)
+        tt = torch.tensor([dev_s], device="cpu" if share else "cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
         dist.barrier()
@@ -361,7 +369,7 @@ def main():
         e2e_h2d += st_e2e.h2d_bytes
     e2e = P_pass * args.e2e_steps * world / e2e_s if e2e_s > 0 else None
     if dist and e2e_s > 0:
-        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        tt = torch.tensor([e2e_s], device="cpu" if share else "cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = P_pass * args.e2e_steps * world / float(tt.item())
 
