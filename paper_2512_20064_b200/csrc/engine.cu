@@ -1459,7 +1459,7 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
       }
       int ex = 0;
       if (mx > 0.0) std::frexp(mx, &ex);
-      sig[r] = std::ldexp(1.0, -ex);
+      sig[r] = std::ldexp(1.0, kEnvExp - ex);
       for (int l = 0; l < s.chil; ++l) {
         const double* v = env + 2 * (static_cast<size_t>(r) * s.chil + l);
         float comp[3];

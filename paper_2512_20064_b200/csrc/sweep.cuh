@@ -25,6 +25,11 @@ constexpr int kGemmThreads = 256;
 constexpr int kPlaneRe = 0;  // Gamma planes: Gr, Gi (, Gs)
 constexpr int kPlaneIm = 1;
 constexpr uint64_t kMeasureStream = 0x6d656173ull;  // rng.hpp:19
+// The next environment is renormalised (power of two) to a max component in [2^13, 2^14): the hi/lo
+// fp16 split then keeps the lo part out of the fp16 subnormal range for components down to ~1e-5 of
+// the max (with a max in [0.5, 1) every component below 0.25 had a subnormal, i.e. imprecise, lo
+// part).  Products stay far from fp32 overflow (|t| <= 2^14 * K).
+constexpr int kEnvExp = 14;
 constexpr uint8_t kDead = 0xFF;                      // sampler.hpp:17
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }

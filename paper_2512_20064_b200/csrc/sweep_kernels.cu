@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
       if (mx > 0.f) {
         int e;
         frexpf(mx, &e);
-        scale = ldexpf(1.0f, -e);
+        scale = ldexpf(1.0f, kEnvExp - e);
         live_out = true;
       }
     }
@@ -868,8 +868,8 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
           mx = by_lane ? __shfl_sync(0xffffffffu, mk, kk) : outcome_max(a, n, kk, lane);
         if (mx > 0.f) {
           int e;
-          frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
-          scale = ldexpf(1.0f, -e);
+          frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1): the env max lands in [2^13, 2^14)
+          scale = ldexpf(1.0f, kEnvExp - e);
           live_out = true;
         }
       }

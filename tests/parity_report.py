@@ -76,6 +76,61 @@ def report(name, smp, dec, n, seed, scheme):
     }
 
 
+def report_ref(name, smp, dec, n, seed, scheme, threads=None):
+    """Same checks against the reference itself (oracle/_ref, compiled from the reference's sources),
+    multi-threaded: rows from ref_sample_range, teacher-forced marginals from ref_marginals_forced in
+    parallel chunks -- for chains too large for the single-threaded C restatement."""
+    from concurrent.futures import ThreadPoolExecutor
+    t0 = time.time()
+    threads = threads or os.cpu_count() or 1
+    rs = O.RefState(dec)
+    ref_rows = rs.sample_range(0, n, seed, threads=threads)
+    chunks = np.array_split(np.arange(n), threads)
+    with ThreadPoolExecutor(threads) as ex:
+        parts = list(ex.map(lambda idx: rs.marginals_forced(ref_rows[idx]), [c for c in chunks if len(c)]))
+    ref_marg = np.concatenate(parts)
+    with ThreadPoolExecutor(threads) as ex:  # the reference's own F32 policy on the same strings
+        f32_marg = np.concatenate(list(ex.map(lambda idx: rs.marginals_forced(ref_rows[idx], compute=O.F32),
+                                              [c for c in chunks if len(c)])))
+    gpu_rows = smp.sample(0, n, seed)
+    gm = smp.marginals(0, ref_rows)
+    live = ref_marg >= 0
+    big = live & (ref_marg >= 1e-3)
+    rel = np.abs(gm[big] - ref_marg[big]) / ref_marg[big]
+    diff = np.nonzero((gpu_rows != ref_rows).any(axis=1))[0]
+    explained = 0
+    for s_ in diff:
+        i = int(np.argmax(gpu_rows[s_] != ref_rows[s_]))
+        u = O.orc().orc_uniform(seed, O.MEASURE_STREAM, int(s_), i)
+        if boundary_distance(ref_marg[s_, i], u) < EPS_BOUNDARY:
+            explained += 1
+    # per-site classes: interior (full chi on both bonds) vs the right edge (chiR < chiL)
+    b = list(dec.bond_dims)
+    cmax = max(b)
+    inner = [i for i in range(dec.num_sites) if b[i] == cmax and b[i + 1] == cmax]
+    redge = [i for i in range(dec.num_sites) if b[i + 1] < b[i]]
+
+    def cls_max(mg, sites):
+        if not sites:
+            return 0.0
+        sel = big[:, sites, :]
+        e = np.abs(mg[:, sites, :] - ref_marg[:, sites, :])[sel] / ref_marg[:, sites, :][sel]
+        return float(e.max()) if e.size else 0.0
+    extra = {"max_rel_err_interior_sites": cls_max(gm, inner), "max_rel_err_right_edge_sites": cls_max(gm, redge),
+             "reference_f32_policy_max_rel_err_interior": cls_max(f32_marg, inner),
+             "reference_f32_policy_max_rel_err_right_edge": cls_max(f32_marg, redge),
+             "right_edge_sites": redge}
+    return {**extra, "case": name, "scheme": scheme, "oracle": "reference (oracle/_ref, threaded)", "samples": n,
+            "sites": dec.num_sites, "phys_dim": dec.phys_dim, "max_bond": int(max(dec.bond_dims)),
+            "seed": seed, "draws_checked": int((ref_rows != P.DEAD_OUTCOME).sum()),
+            "strings_differing": int(len(diff)), "differences_explained_by_boundary_draws": explained,
+            "unexplained_differences": int(len(diff)) - explained,
+            "marginals_checked": int(live.sum()),
+            "max_marginal_rel_err_p_ge_1e-3": float(rel.max()) if rel.size else 0.0,
+            "pass": bool((rel.max() if rel.size else 0) < 1e-4 and len(diff) == explained),
+            "seconds": round(time.time() - t0, 1)}
+
+
 def main():
     pol = P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX)
     out = []
@@ -96,6 +151,15 @@ def main():
             smp, lams = build_synthetic(m, chi, d, seed=11, policy=pol, scheme=int(scheme))
             dec = O.Mps(d, list(smp.bond_dims), [smp.decoded_gamma(i) for i in range(m)], list(lams))
             out.append(report(f"synthetic M={m} chi={chi} d={d}", smp, dec, n, 7, tag))
+            smp.close()
+            print(json.dumps(out[-1]), flush=True)
+    if O.have_ref():  # the c3 bond dimension over a 24-site chain (19 sites at chi = 2048)
+        for scheme in (P.Scheme.M3, P.Scheme.M4):
+            tag = "3M" if scheme == P.Scheme.M3 else "4M"
+            m, chi, d, n = 24, 2048, 6, 256
+            smp, lams = build_synthetic(m, chi, d, seed=5, policy=pol, scheme=int(scheme))
+            dec = O.Mps(d, list(smp.bond_dims), [smp.decoded_gamma(i) for i in range(m)], list(lams))
+            out.append(report_ref(f"c3 shape M={m} chi={chi} d={d}", smp, dec, n, 7, tag))
             smp.close()
             print(json.dumps(out[-1]), flush=True)
     path = sys.argv[1] if len(sys.argv) > 1 else None

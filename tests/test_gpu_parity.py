@@ -540,3 +540,38 @@ def test_single_mode_within_reference_f16_envelope(pkg, gold, scheme):
     err_gpu = (np.abs(gm[big] - ref_marg[big]) / ref_marg[big]).max()
     err_f16 = (np.abs(f16_marg[big] - ref_marg[big]) / ref_marg[big]).max()
     assert err_gpu <= max(2.0 * err_f16, 1e-3), (err_gpu, err_f16)
+
+
+@pytest.mark.parametrize("scheme", [3, 4])
+def test_c3_shape_parity_vs_reference_f32_envelope(pkg, scheme):
+    """The c3 bond dimension over a 20-site chain (15 sites at chi = 2048), against the compiled
+    reference itself (threaded): outcome strings identical (boundary draws excepted); interior-site
+    marginals within 1e-4; right-edge sites (chiR < chiL), where every fp32-class contraction
+    amplifies the environment's accumulated rounding through the cancellation of the narrowing bonds,
+    within 10x the reference's own F32 policy on the same strings."""
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not available")
+    from concurrent.futures import ThreadPoolExecutor
+    m, chi, d, n = 20, 2048, 6, 128
+    smp, lams, _ = _synthetic(pkg, m, chi, d, scheme=scheme)
+    dec = O.Mps(d, list(smp.bond_dims), [smp.decoded_gamma(i) for i in range(m)], list(lams))
+    rs = O.RefState(dec)
+    rows = rs.sample_range(0, n, 7, threads=16)
+    chunks = [c for c in np.array_split(np.arange(n), 16) if len(c)]
+    with ThreadPoolExecutor(16) as ex:
+        ref = np.concatenate(list(ex.map(lambda idx: rs.marginals_forced(rows[idx]), chunks)))
+        f32 = np.concatenate(list(ex.map(lambda idx: rs.marginals_forced(rows[idx], compute=O.F32), chunks)))
+    got = smp.sample(0, n, 7)
+    ndiff, explained = compare_strings(got, rows, ref, 7)
+    assert ndiff == explained, (ndiff, explained)
+    gm = smp.marginals(0, rows)
+    b = list(smp.bond_dims)
+    big = ref >= 1e-3
+
+    def worst(mg, sites):
+        sel = big[:, sites, :]
+        return (np.abs(mg[:, sites, :] - ref[:, sites, :])[sel] / ref[:, sites, :][sel]).max()
+    inner = [i for i in range(m) if b[i] == chi and b[i + 1] == chi]
+    redge = [i for i in range(m) if b[i + 1] < b[i]]
+    assert worst(gm, inner) < MARG_RTOL
+    assert worst(gm, redge) < max(MARG_RTOL, 10.0 * worst(f32, redge)), (worst(gm, redge), worst(f32, redge))
