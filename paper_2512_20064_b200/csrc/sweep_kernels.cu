@@ -915,6 +915,45 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
     const float2* src = a.temp + (static_cast<size_t>(n) * a.d + (live_out ? outcome : 0)) * a.chirp;
     const int live_cols = live_out ? a.chir_loc : 0;
     const int C = a.env_comp;
+    if constexpr (!kDisp) {
+      // 8 consecutive columns per lane: four 16 B loads, one 16 B store per plane
+      for (int r = lane * 8; r < a.kp_next; r += 256) {  // kp_next is a multiple of 32
+        float re[8], im[8];
+        if (r + 7 < live_cols) {  // chirp is a multiple of 128: these loads stay inside the row
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 v = *reinterpret_cast<const float4*>(src + r + 2 * j);
+            re[2 * j] = v.x, im[2 * j] = v.y, re[2 * j + 1] = v.z, im[2 * j + 1] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float2 v = r + j < live_cols ? src[r + j] : make_float2(0.f, 0.f);
+            re[j] = v.x, im[j] = v.y;
+          }
+        }
+        float comp[3][8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          comp[0][j] = re[j] * scale;
+          comp[1][j] = im[j] * scale;
+          comp[2][j] = comp[0][j] + comp[1][j];
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (c >= C) break;
+          __align__(16) __half hv[8], lv[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            hv[j] = __float2half_rn(comp[c][j]);
+            lv[j] = __float2half_rn(comp[c][j] - __half2float(hv[j]));
+          }
+          *reinterpret_cast<uint4*>(e0 + c * plane + r) = *reinterpret_cast<const uint4*>(hv);
+          *reinterpret_cast<uint4*>(e0 + (C + c) * plane + r) = *reinterpret_cast<const uint4*>(lv);
+        }
+      }
+      return;
+    }
     for (int r = lane * 4; r < a.kp_next; r += 128) {  // kp_next is a multiple of 32
       float4 v01 = make_float4(0.f, 0.f, 0.f, 0.f), v23 = v01;
       if (kDisp && r < live_cols) {  // displaced: row `outcome` of D applied on the fly
