@@ -1,6 +1,6 @@
 """Diagnostic (needs a B200 and oracle/_ref): dump GPU vs reference marginals at the c3 shape.
 
-usage: python tools/parity_diag.py M CHI D N SCHEME out.npz
+usage: python tests/parity_diag.py M CHI D N SCHEME out.npz
 """
 import os
 import sys
@@ -8,8 +8,8 @@ import sys
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path[:0] = [ROOT, os.path.join(ROOT, "tests"), os.path.join(ROOT, "oracle")]
-import oracle as O  # noqa: E402  (diagnostic tooling, like tests/)
+sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+import oracle as O  # noqa: E402  (test infrastructure: the checker)
 import paper_2512_20064_b200 as P  # noqa: E402
 from paper_2512_20064_b200.synthetic import build_synthetic  # noqa: E402
 from concurrent.futures import ThreadPoolExecutor  # noqa: E402
