@@ -1,4 +1,5 @@
-"""Quick GPU bring-up probe (prints, no asserts): RNG, one contraction, one c1 sweep."""
+"""Quick GPU bring-up probe (test infrastructure; prints, no asserts): RNG, one contraction, one c1
+sweep against the oracle."""
 import os
 import sys
 import time
