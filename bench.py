@@ -208,7 +208,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--pass", dest="pass_samples", type=int, default=0)
-    ap.add_argument("--mode", default="split", choices=["split", "single"])
+    ap.add_argument("--mode", default="split", choices=["split", "single", "precise"])
     ap.add_argument("--scheme", default="auto", choices=["auto", "3m", "4m"],
                     help="complex decomposition of the contraction (auto = 3M when the state fits)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -258,7 +258,7 @@ def main():
     from paper_2512_20064_b200.synthetic import build_synthetic
 
     P_pass = args.pass_samples or DEFAULT_PASS[args.config]
-    mode = P.Mode.SPLIT if args.mode == "split" else P.Mode.SINGLE
+    mode = {"split": P.Mode.SPLIT, "single": P.Mode.SINGLE, "precise": P.Mode.PRECISE}[args.mode]
     t0 = time.perf_counter()
     smp, _ = build_synthetic(cfg["M"], cfg["chi"], cfg["d"], seed=42, mode=mode, devices=[local],
                              pass_samples=P_pass, record_site_times=2, host_stream_slots=args.stream_slots,
@@ -406,8 +406,9 @@ def main():
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
-            "dtype": "f16 x (f16 hi + f16 lo) -> f32 accumulate; f64 CDF" if args.mode == "split" else
-                     "f16 x f16 -> f32 accumulate; f64 CDF",
+            "dtype": {"split": "f16 x (f16 hi + f16 lo) -> f32 accumulate; f64 CDF",
+                      "single": "f16 x f16 -> f32 accumulate; f64 CDF",
+                      "precise": "(f16 hi + f16 lo) x (f16 hi + f16 lo) -> f32 accumulate; f64 CDF"}[args.mode],
             "data": "synthetic random right-canonical MPS generated on device (seed 42), measurement seed 7",
             "config": {"workload": cfg["desc"] + f"; step = one sweep of {P_pass} samples/GPU over all M sites",
                        "M": cfg["M"], "chi": cfg["chi"], "d": cfg["d"], "pass_samples_per_gpu": P_pass,

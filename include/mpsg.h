@@ -58,7 +58,11 @@ enum { MPSG_SCALE_NONE = 0, MPSG_SCALE_GLOBAL_MAX = 1, MPSG_SCALE_PER_SAMPLE_MAX
  *   MPSG_MODE_SINGLE  fp16 Gamma x fp16 environment, one MMA pass; F16-class accuracy.
  *                     Used for compute = TF32 / F16.
  *   MPSG_MODE_AUTO    pick from policy.compute. */
-enum { MPSG_MODE_AUTO = 0, MPSG_MODE_SPLIT = 1, MPSG_MODE_SINGLE = 2 };
+enum { MPSG_MODE_AUTO = 0, MPSG_MODE_SPLIT = 1, MPSG_MODE_SINGLE = 2, MPSG_MODE_PRECISE = 3 };
+/*   MPSG_MODE_PRECISE  SPLIT plus Gamma stored as an exact fp16 hi + lo pair per component (22-bit
+ *                     mantissas instead of 11): the device samples the caller's f64 / f32 Gamma to
+ *                     ~2^-23 instead of ~2^-12 per element, at 3 MMAs per K-step instead of 2 and
+ *                     twice the Gamma bytes (12 B per complex entry).  3M scheme only. */
 /* Complex decomposition of the contraction:
  *   MPSG_SCHEME_3M  Gauss: 3 real products (Gamma planes Gr, Gi, Gr+Gi: 6 bytes per complex entry)
  *   MPSG_SCHEME_4M  4 real products (Gamma planes Gr, Gi: 4 bytes per complex entry)

@@ -338,6 +338,7 @@ struct mpsg_handle_s {
   bool pair = true;                        // K1 variant: CTA-pair UMMA (M=256) vs A-multicast pairs
   bool m3 = false;                         // 3M contraction (Gamma planes Gr, Gi, Gs; env re, im, s)
   int gplanes = 2, env_comp = 2;
+  bool precise = false;                    // Gamma hi + lo planes (MPSG_MODE_PRECISE)
   std::unique_ptr<mpsg::Comm> comm;
   std::mutex mu;
 };
@@ -390,8 +391,12 @@ static void choose_scheme(mpsg_handle_s& h) {
       }
     }
   }
+  if (h.precise) {
+    config_check(h.opts.scheme != MPSG_SCHEME_4M, "MPSG_MODE_PRECISE needs the 3M scheme");
+    m3 = true;
+  }
   h.m3 = m3;
-  h.gplanes = m3 ? 3 : 2;
+  h.gplanes = h.precise ? 6 : (m3 ? 3 : 2);
   h.env_comp = m3 ? 3 : 2;
 }
 
@@ -753,7 +758,7 @@ static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const S
       const char* v = std::getenv("MPSG_3M_QUAD");
       return v && std::atoi(v) != 0;
     }();
-    launch_site_gemm_3m(h.split, epilogue_max(h, s), env_epi, env_quad, ln.tma_env64[i], *tma_g128, ga,
+    launch_site_gemm_3m(h.split, epilogue_max(h, s), env_epi, env_quad, h.precise, ln.tma_env64[i], *tma_g128, ga,
                         std::min(ctas, dc.num_sms), stream);
     return;
   }
@@ -911,7 +916,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       po.launches += 2;
       po.macs += static_cast<uint64_t>(cnt[L]) * s.chil * s.width * h.d;
       po.wmacs += static_cast<uint64_t>(cnt[L]) * s.width * h.d;
-      po.issued += (h.m3 ? 6ull : 8ull) * rows[L] * s.np * s.kp * (h.split ? 2 : 1);
+      po.issued += (h.m3 ? 6ull : 8ull) * rows[L] * s.np * s.kp * (h.precise ? 3 : h.split ? 2 : 1);
     }
     if (timing) CUDA_OK(cudaEventRecord(dc.ev[i + 1], dc.stream));
   }
@@ -1182,7 +1187,8 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
     h->bonds.assign(bond_dims, bond_dims + num_sites + 1);
     h->policy = pol;
     if (opts) h->opts = *opts;
-    config_check(h->opts.mode >= MPSG_MODE_AUTO && h->opts.mode <= MPSG_MODE_SINGLE, "unknown mode");
+    config_check(h->opts.mode >= MPSG_MODE_AUTO && h->opts.mode <= MPSG_MODE_PRECISE, "unknown mode");
+    h->precise = h->opts.mode == MPSG_MODE_PRECISE;
     {
       const char* v = std::getenv("MPSG_GEMM");  // A/B switch for the contraction kernel
       h->pair = !(v && std::string(v) == "cluster");
@@ -1192,7 +1198,7 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
     h->tp_rank = h->opts.tp_rank;
     config_check(h->tp_rank >= 0 && h->tp_rank < h->tp, "tp_rank out of range");
     config_check(h->tp == 1 || ndev <= 1, "a tensor-parallel rank drives exactly one device");
-    h->split = h->opts.mode == MPSG_MODE_SPLIT ||
+    h->split = h->opts.mode == MPSG_MODE_SPLIT || h->opts.mode == MPSG_MODE_PRECISE ||
                (h->opts.mode == MPSG_MODE_AUTO && (pol.compute == MPSG_F64 || pol.compute == MPSG_F32));
     config_check(h->opts.scheme == MPSG_SCHEME_AUTO || h->opts.scheme == MPSG_SCHEME_3M ||
                      h->opts.scheme == MPSG_SCHEME_4M, "unknown contraction scheme");
@@ -1310,8 +1316,16 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
           const double f = static_cast<double>(static_cast<float>(cs[rl * d + k])) * h->gl[site][l] /
                            h->gr[site][r];
           const size_t o = 2 * ((static_cast<size_t>(l) * s.chir + r) * d + k);
-          out[o] = static_cast<double>(__half2float(g[(static_cast<size_t>(kPlaneRe) * s.np + row) * s.kp + lpos[l]])) * f;
-          out[o + 1] = static_cast<double>(__half2float(g[(static_cast<size_t>(kPlaneIm) * s.np + row) * s.kp + lpos[l]])) * f;
+          const size_t ire = (static_cast<size_t>(kPlaneRe) * s.np + row) * s.kp + lpos[l];
+          const size_t iim = (static_cast<size_t>(kPlaneIm) * s.np + row) * s.kp + lpos[l];
+          double gre = __half2float(g[ire]), gim = __half2float(g[iim]);
+          if (h->precise) {  // + the lo planes (3, 4): exact fp16 residuals of the hi grid
+            const size_t lo = 3ull * s.np * s.kp;
+            gre += static_cast<double>(__half2float(g[lo + ire]));
+            gim += static_cast<double>(__half2float(g[lo + iim]));
+          }
+          out[o] = gre * f;
+          out[o + 1] = gim * f;
         }
   });
 }

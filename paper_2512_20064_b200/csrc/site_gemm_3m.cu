@@ -34,13 +34,17 @@
 
 namespace mpsg {
 
-template <bool kSplit>
+// kGlo (MPSG_MODE_PRECISE): Gamma carries a lo plane per component too; stage = [A_hi | A_lo | B_hi |
+// B_lo] and three MMAs per K16 step (A_hi x B_hi, A_hi x B_lo through the A collector, A_lo x B_hi).
+template <bool kSplit, bool kGlo = false>
 struct Cfg3M {
   static constexpr int kHalves = kSplit ? 2 : 1;
+  static constexpr int kAHalves = kGlo ? 2 : 1;
   static constexpr int kATile = kBM * kBK3 * 2;        // 16 KiB: 128 Gamma rows x 128 B
   static constexpr int kBTile = (kBM / 2) * kBK3 * 2;  // 8 KiB: this SM's 64 sample rows
-  static constexpr int kStageBytes = kATile + kHalves * kBTile;
-  static constexpr int kStages = kSplit ? 6 : 8;
+  static constexpr int kBOff = kAHalves * kATile;      // B tiles after the A tile(s)
+  static constexpr int kStageBytes = kAHalves * kATile + kHalves * kBTile;
+  static constexpr int kStages = kGlo ? 4 : (kSplit ? 6 : 8);
   static constexpr int kRedBytes = 4 * kBM * 8;        // [4 lane quarters][128 samples] float2
   static constexpr int kBarBytes = 512;
   static constexpr int kSmem = kStages * kStageBytes + 1024 + kBarBytes + kRedBytes;
@@ -95,11 +99,11 @@ __device__ unsigned long long g_prof3m[8];
 // the pairs share every environment tile through TMA multicast (pair 0 fetches the hi plane, pair 1
 // the lo plane, each for both pairs), cutting the L2 -> SM traffic per MMA by a quarter.  A stage
 // is refilled only when both pairs have consumed it (commits multicast to all four CTAs).
-template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad>
+template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad, bool kGlo = false>
 __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
     site_gemm_3m_kernel(const __grid_constant__ CUtensorMap tma_env64,
                         const __grid_constant__ CUtensorMap tma_g, const Gemm3MArgs a) {
-  using C = Cfg3M<kSplit>;
+  using C = Cfg3M<kSplit, kGlo>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -167,15 +171,17 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
             const uint32_t lbar = ptx::leader_bar(&full[stage]);
             if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
             ptx::tma_load_2d_pair(&tma_g, lbar, st, kb * kBK3, c * a.np + grow, pol_g);
+            if constexpr (kGlo)  // the component's lo plane (planes 3..5)
+              ptx::tma_load_2d_pair(&tma_g, lbar, st + C::kATile, kb * kBK3, (3 + c) * a.np + grow, pol_g);
             if constexpr (kQuad) {  // env plane h = pair for both pairs (same rows: same rank)
               if (pair < C::kHalves)
-                ptx::tma_load_3d_pair_mc(&tma_env64, lbar, st + C::kATile + pair * C::kBTile, kin * kBK3,
+                ptx::tma_load_3d_pair_mc(&tma_env64, lbar, st + C::kBOff + pair * C::kBTile, kin * kBK3,
                                          (3 * pair + c) * a.env_cap + erow, shard,
                                          static_cast<uint16_t>((1u << rank) | (1u << (rank + 2))), pol_env);
             } else {
 #pragma unroll
               for (int h = 0; h < C::kHalves; ++h)
-                ptx::tma_load_3d_pair(&tma_env64, lbar, st + C::kATile + h * C::kBTile, kin * kBK3,
+                ptx::tma_load_3d_pair(&tma_env64, lbar, st + C::kBOff + h * C::kBTile, kin * kBK3,
                                       (3 * h + c) * a.env_cap + erow, shard, pol_env);
             }
             if (++stage == C::kStages) {
@@ -217,13 +223,15 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
             ptx::tc_fence_after();
             // descriptor start addresses are in 16 B units: +32 B per K16 step inside the atom
             const uint64_t ad = desc0 + ((stage * C::kStageBytes) >> 4);
-            const uint64_t bd = ad + (C::kATile >> 4);
+            const uint64_t bd = ad + (C::kBOff >> 4);
 #pragma unroll
             for (int ks = 0; ks < kBK3 / 16; ++ks) {
               const uint32_t accum = (kb | ks) ? 1u : 0u;
               if constexpr (kSplit) {
                 ptx::umma_pair_elect(d, ad + 2 * ks, bd + 2 * ks, kId, accum, true, false);
                 ptx::umma_pair_elect(d, ad + 2 * ks, bd + (C::kBTile >> 4) + 2 * ks, kId, 1u, false, true);
+                if constexpr (kGlo)  // Gamma lo x env hi
+                  ptx::umma_pair_elect(d, ad + (C::kATile >> 4) + 2 * ks, bd + 2 * ks, kId, 1u, false, false);
               } else {
                 ptx::umma_pair_elect(d, ad + 2 * ks, bd + 2 * ks, kId, accum, false, false);
               }
@@ -340,15 +348,16 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
   }
 }
 
-template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad>
+template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad, bool kGlo = false>
 static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
                         int grid, cudaStream_t s) {
-  auto kern = site_gemm_3m_kernel<kSplit, kMax, kEpiWarps, kQuad>;
+  auto kern = site_gemm_3m_kernel<kSplit, kMax, kEpiWarps, kQuad, kGlo>;
+  using Cf = Cfg3M<kSplit, kGlo>;
   constexpr int kCl = kQuad ? 4 : 2;
   static int max_clusters = 0;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(128 + 32 * kEpiWarps);
-  cfg.dynamicSmemBytes = Cfg3M<kSplit>::kSmem;
+  cfg.dynamicSmemBytes = Cf::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -358,7 +367,7 @@ static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (!max_clusters) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg3M<kSplit>::kSmem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem);
     cfg.gridDim = dim3(kCl);
     if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
       max_clusters = 148 / kCl;  // 4-CTA clusters: 33 on a B200 (132 SMs)
@@ -368,8 +377,14 @@ static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, 
 }
 
 template <bool kSplit, bool kMax>
-static void launch_3m_w(int epi_warps, bool quad, const CUtensorMap& e, const CUtensorMap& g,
+static void launch_3m_w(int epi_warps, bool quad, bool glo, const CUtensorMap& e, const CUtensorMap& g,
                         const Gemm3MArgs& a, int grid, cudaStream_t s) {
+  if constexpr (kSplit) {
+    if (glo) {
+      launch_3m_t<kSplit, kMax, 8, false, true>(e, g, a, grid, s);
+      return;
+    }
+  }
   if (quad)
     launch_3m_t<kSplit, kMax, 8, true>(e, g, a, grid, s);
   else if (epi_warps == 4)
@@ -380,14 +395,15 @@ static void launch_3m_w(int epi_warps, bool quad, const CUtensorMap& e, const CU
     launch_3m_t<kSplit, kMax, 8, false>(e, g, a, grid, s);
 }
 
-void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, const CUtensorMap& tma_env64,
-                         const CUtensorMap& tma_g, const Gemm3MArgs& a, int grid, cudaStream_t s) {
+void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, bool glo,
+                         const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
+                         int grid, cudaStream_t s) {
   if (split)
-    with_max ? launch_3m_w<true, true>(epi_warps, quad, tma_env64, tma_g, a, grid, s)
-             : launch_3m_w<true, false>(epi_warps, quad, tma_env64, tma_g, a, grid, s);
+    with_max ? launch_3m_w<true, true>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s)
+             : launch_3m_w<true, false>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s);
   else
-    with_max ? launch_3m_w<false, true>(epi_warps, quad, tma_env64, tma_g, a, grid, s)
-             : launch_3m_w<false, false>(epi_warps, quad, tma_env64, tma_g, a, grid, s);
+    with_max ? launch_3m_w<false, true>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s)
+             : launch_3m_w<false, false>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s);
 }
 
 }  // namespace mpsg

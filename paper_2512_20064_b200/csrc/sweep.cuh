@@ -134,8 +134,10 @@ int gemm_pair_smem_bytes(bool split);
 // pstat.y is 0 and the select kernel computes the chosen slice's max (SelectArgs::slice_max).
 // epi_warps: 4 or 8 epilogue warps (one or two per TMEM lane quarter).
 // quad: 4-CTA clusters sharing the environment tiles by multicast (see site_gemm_3m.cu).
-void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, const CUtensorMap& tma_env64,
-                         const CUtensorMap& tma_g, const Gemm3MArgs& a, int grid, cudaStream_t s);
+// glo: Gamma lo planes present (MPSG_MODE_PRECISE, split only).
+void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, bool glo,
+                         const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
+                         int grid, cudaStream_t s);
 int gemm_3m_smem_bytes(bool split);
 void launch_select(const SelectArgs& a, cudaStream_t s);
 // pstat [rows][nt] -> out [rows][d]: (sum of weights, max) over the tiles of each outcome

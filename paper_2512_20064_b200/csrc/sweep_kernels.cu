@@ -1157,24 +1157,31 @@ template <typename T>
 __global__ void pack_kernel(const void* src, int chil, int chir, int d, int b0, int width, int kp,
                             int chirp, const int* lpos, const double* gl, const double* gr,
                             const double* cs, int gplanes, __half* g_out, int np) {
-  __shared__ __half tre[32][33], tim[32][33], tsm[32][33];
+  // planes: [Gr, Gi (, Gs)] and, for gplanes = 6 (MPSG_MODE_PRECISE), [Gr_lo, Gi_lo, Gs_lo] -- the
+  // residual of the hi grid, itself rounded by quantize_pair, so every plane (and Gs = Gr + Gi per
+  // precision half) is an exact fp16 number
+  __shared__ __half tp[6][32][33];
   const int wcols = width * d;
   const size_t stride = static_cast<size_t>(chir) * d;
   const int j0 = blockIdx.x * 32, l0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
   for (int yy = ty; yy < 32; yy += 8) {
     const int l = l0 + yy, jl = j0 + tx;
-    __half hr = __float2half_rn(0.f), hi = hr, hs = hr;
+    __half h[6];
+#pragma unroll
+    for (int p = 0; p < 6; ++p) h[p] = __float2half_rn(0.f);
     if (l < chil && jl < wcols) {
       const int rl = jl / d, k = jl - rl * d;
       double re, im;
       load_c<T>(src, static_cast<size_t>(l) * stride + static_cast<size_t>(b0 + rl) * d + k, re, im);
       const double f = gr[b0 + rl] / gl[l] / cs[jl];
-      quantize_pair(re * f, im * f, hr, hi, hs);
+      quantize_pair(re * f, im * f, h[0], h[1], h[2]);
+      if (gplanes == 6)
+        quantize_pair(re * f - static_cast<double>(__half2float(h[0])),
+                      im * f - static_cast<double>(__half2float(h[1])), h[3], h[4], h[5]);
     }
-    tre[yy][tx] = hr;
-    tim[yy][tx] = hi;
-    tsm[yy][tx] = hs;
+#pragma unroll
+    for (int p = 0; p < 6; ++p) tp[p][yy][tx] = h[p];
   }
   __syncthreads();
   for (int yy = ty; yy < 32; yy += 8) {
@@ -1183,9 +1190,8 @@ __global__ void pack_kernel(const void* src, int chil, int chir, int d, int b0, 
       const int rl = jl / d, k = jl - rl * d;
       const size_t row = static_cast<size_t>(k) * chirp + rl;
       const size_t col = static_cast<size_t>(lpos[l]);
-      g_out[(static_cast<size_t>(kPlaneRe) * np + row) * kp + col] = tre[tx][yy];
-      g_out[(static_cast<size_t>(kPlaneIm) * np + row) * kp + col] = tim[tx][yy];
-      if (gplanes == 3) g_out[(2ull * np + row) * kp + col] = tsm[tx][yy];
+      for (int p = 0; p < gplanes; ++p)
+        g_out[(static_cast<size_t>(p) * np + row) * kp + col] = tp[p][tx][yy];
     }
   }
 }

@@ -118,6 +118,7 @@ class Mode(enum.IntEnum):
     AUTO = 0
     SPLIT = 1
     SINGLE = 2
+    PRECISE = 3  # SPLIT + Gamma hi / lo planes: samples the caller's Gamma to ~2^-23 (3M only)
 
 
 class Scheme(enum.IntEnum):

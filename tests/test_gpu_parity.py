@@ -575,3 +575,37 @@ def test_c3_shape_parity_vs_reference_f32_envelope(pkg, scheme):
     redge = [i for i in range(m) if b[i + 1] < b[i]]
     assert worst(gm, inner) < MARG_RTOL
     assert worst(gm, redge) < max(MARG_RTOL, 10.0 * worst(f32, redge)), (worst(gm, redge), worst(f32, redge))
+
+
+def test_precise_mode_vs_original_mps(pkg, gold):
+    """MPSG_MODE_PRECISE (Gamma hi + lo planes): the decoded tensor matches the caller's f64 Gamma to
+    ~2^-23, so the GPU agrees with the reference run on the *original* MPS (not the decoded one):
+    marginals within 1e-4 and identical strings; the default format (fp16 Gamma, 2^-12) does not
+    reach that against the original on c1b."""
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    smp = pkg.GpuSampler(to_state(pkg, mps), pol, mode=pkg.Mode.PRECISE)
+    worst = 0.0
+    for i in range(mps.num_sites):
+        g, dg = mps.gammas[i], smp.decoded_gamma(i)
+        colmax = np.maximum(np.abs(g.real), np.abs(g.imag)).max(axis=0, keepdims=True)
+        err = np.maximum(np.abs(g.real - dg.real), np.abs(g.imag - dg.imag))
+        worst = max(worst, float((err / np.where(colmax > 0, colmax, 1)).max()))
+    print("precise decode: max |err| / column max", worst)
+    assert worst < 2.0 ** -16, worst
+    n = 1000
+    ref_rows, ref_marg, _ = O.orc_sample_range(mps, 0, n, 7, want_marginals=True)  # the ORIGINAL chain
+    got = smp.sample(0, n, 7)
+    ndiff, explained = compare_strings(got, ref_rows, ref_marg, 7)
+    assert ndiff == explained, (ndiff, explained)
+    gm = smp.marginals(0, ref_rows)
+    big = ref_marg >= 1e-3
+    rel = (np.abs(gm[big] - ref_marg[big]) / ref_marg[big]).max()
+    print("precise vs original: max marginal rel err", rel)
+    assert rel < MARG_RTOL, rel
+    # the default (fp16 Gamma) handle, same comparison against the original chain, for contrast
+    dflt = pkg.GpuSampler(to_state(pkg, mps), pol)
+    rel_d = (np.abs(dflt.marginals(0, ref_rows)[big] - ref_marg[big]) / ref_marg[big]).max()
+    print("default (fp16 Gamma) vs original: max marginal rel err", rel_d)
+    assert rel_d > rel
