@@ -153,6 +153,16 @@ def main():
             out.append(report(f"synthetic M={m} chi={chi} d={d}", smp, dec, n, 7, tag))
             smp.close()
             print(json.dumps(out[-1]), flush=True)
+    # MPSG_MODE_PRECISE against the ORIGINAL chains (not the decoded ones)
+    for case in ("c1", "c1b"):
+        z = np.load(os.path.join(GOLD, f"{case}.npz"))
+        mps = O.load_npz_mps(z)
+        st = P.MpsState(mps.num_sites, mps.phys_dim, list(mps.bond_dims), list(mps.gammas), list(mps.lambdas))
+        smp = P.GpuSampler(st, pol, mode=P.Mode.PRECISE)
+        r = report(case + " (original MPS)", smp, mps, int(z["n"]), int(z["seed"]), "3M PRECISE")
+        out.append(r)
+        smp.close()
+        print(json.dumps(out[-1]), flush=True)
     if O.have_ref():  # the c3 bond dimension over a 24-site chain (19 sites at chi = 2048)
         for scheme in (P.Scheme.M3, P.Scheme.M4):
             tag = "3M" if scheme == P.Scheme.M3 else "4M"
