@@ -394,11 +394,16 @@ static void choose_scheme(mpsg_handle_s& h) {
   if (h.precise) {
     config_check(h.opts.scheme != MPSG_SCHEME_4M, "MPSG_MODE_PRECISE needs the 3M scheme");
     m3 = true;
-    if (h.opts.host_stream_slots == 0) {  // 6 Gamma planes resident: fail early with the sizes
-      double state6 = 0.0;
-      for (uint64_t i = 0; i < h.M; ++i)
-        state6 += 6.0 * 2.0 * round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN) *
-                  static_cast<double>(h.tp) * round_up((static_cast<int>(h.bonds[i]) + h.tp - 1) / h.tp, kBK3);
+    double state6 = 0.0;  // 6 Gamma planes: fail early with the sizes
+    for (uint64_t i = 0; i < h.M; ++i)
+      state6 += 6.0 * 2.0 * round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN) *
+                static_cast<double>(h.tp) * round_up((static_cast<int>(h.bonds[i]) + h.tp - 1) / h.tp, kBK3);
+    if (h.opts.host_stream_slots != 0) {
+      const double host = static_cast<double>(sysconf(_SC_PHYS_PAGES)) * sysconf(_SC_PAGE_SIZE);
+      config_check(state6 * h.devs.size() <= 0.85 * host,
+                   "MPSG_MODE_PRECISE: the hi + lo Gamma planes need " + std::to_string(state6 / 1e9) +
+                       " GB of pinned host memory per device");
+    } else {
       for (auto& dc : h.devs) {
         size_t free_b = 0, total_b = 0;
         CUDA_OK(cudaSetDevice(dc.device));
