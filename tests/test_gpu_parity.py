@@ -609,3 +609,38 @@ def test_precise_mode_vs_original_mps(pkg, gold):
     rel_d = (np.abs(dflt.marginals(0, ref_rows)[big] - ref_marg[big]) / ref_marg[big]).max()
     print("default (fp16 Gamma) vs original: max marginal rel err", rel_d)
     assert rel_d > rel
+
+
+def test_tensor_parallel_at_c4_bond_dimension(pkg):
+    """The c4 shape (chi = 1e4, d = 4; three sites at the full bond) built directly as two column-
+    sharded ranks (device-generated, same seed) on this GPU with the in-process exchange and two
+    pipeline lanes: both ranks produce identical rows, equal to the unsharded sampler's except draws
+    at a CDF boundary, and their marginals agree with it to F32-class accuracy."""
+    import threading
+    from paper_2512_20064_b200.synthetic import build_synthetic
+    m, chi, d, n = 16, 10000, 4, 1024
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    one, _ = build_synthetic(m, chi, d, seed=3, policy=pol, pass_samples=n)
+    assert max(one.bond_dims) == chi
+    ranks = [build_synthetic(m, chi, d, seed=3, policy=pol, pass_samples=n, tp_size=2, tp_rank=r)[0]
+             for r in range(2)]
+    pkg.sampler.connect_local(ranks)
+    out = [None, None]
+    marg = [None, None]
+    ref_rows = one.sample(0, n, 9)
+
+    def run(r):
+        out[r] = ranks[r].sample(0, n, 9)
+        marg[r] = ranks[r].marginals(0, ref_rows)
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert np.array_equal(out[0], out[1])
+    assert (out[0] != ref_rows).any(axis=1).sum() <= 2
+    gm = one.marginals(0, ref_rows)
+    big = gm >= 1e-3
+    assert (np.abs(marg[0][big] - gm[big]) / gm[big]).max() < 1e-4
+    for s in ranks + [one]:
+        s.close()
