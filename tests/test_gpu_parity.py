@@ -644,3 +644,22 @@ def test_tensor_parallel_at_c4_bond_dimension(pkg):
     assert (np.abs(marg[0][big] - gm[big]) / gm[big]).max() < 1e-4
     for s in ranks + [one]:
         s.close()
+
+
+def test_sample_device_rows_and_stats(pkg, gold):
+    """mpsg_sample_device (rows written to device memory, the bench's device-timed path) equals the
+    host-rows call; RunStats carries the reference's contraction_macs formula (contract.cpp:97-100)."""
+    import torch
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    smp = pkg.GpuSampler(to_state(pkg, mps), pol, pass_samples=256)
+    st = pkg.RunStats()
+    host = smp.sample(5, 700, 7, stats=st)
+    dev = torch.empty((700, mps.num_sites), dtype=torch.uint8, device="cuda")
+    smp.sample_device(5, 700, 7, dev.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(dev.cpu().numpy(), host)
+    b = mps.bond_dims
+    assert st.contraction_macs == 700 * sum(b[i] * b[i + 1] * mps.phys_dim for i in range(mps.num_sites))
+    assert st.issued_mma_flops > 0 and st.d2h_bytes == 700 * mps.num_sites
