@@ -15,7 +15,7 @@ import paper_2512_20064_b200 as P  # noqa: E402
 from paper_2512_20064_b200.synthetic import build_synthetic  # noqa: E402
 
 M, chi, d, N = (int(x) for x in sys.argv[1:5])
-mode = P.Mode.SINGLE if len(sys.argv) > 5 and sys.argv[5] == "single" else P.Mode.SPLIT
+mode = {"single": P.Mode.SINGLE, "precise": P.Mode.PRECISE}.get(sys.argv[5] if len(sys.argv) > 5 else "split", P.Mode.SPLIT)
 ps = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 scheme = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 t = time.time()
