@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define MPSG_ABI_VERSION 1
+#define MPSG_ABI_VERSION 2  /* 2: mpsg_stats gained displacement_macs, measure_pipeline_ops */
 
 enum {
   MPSG_OK = 0,
@@ -113,7 +113,7 @@ typedef struct mpsg_options {
 /* Mirrors mpsamp::RunStats + FlopCounters (sampler.hpp:46-54, contract.hpp:12-25). */
 typedef struct mpsg_stats {
   uint64_t contraction_macs;       /* sum_i count * chiL_i * chiR_i * d (contract.cpp:97-100) */
-  uint64_t measure_weight_macs;    /* sum_i count * chiR_i * d (sampler.cpp:113-116) */
+  uint64_t measure_weight_macs;    /* sum_i live_i * chiR_i * d, live samples only (sampler.cpp:81-90) */
   uint64_t dead_samples;
   double seconds;                  /* wall time of the call */
   double* site_seconds;            /* optional caller array of length M (device time per site) */
@@ -124,6 +124,9 @@ typedef struct mpsg_stats {
   uint64_t kernel_launches;        /* CUDA kernels launched by this call */
   double device_seconds;           /* device time of all passes (CUDA events; record_site_times) */
   double* decay_trace;             /* optional caller array of length M (record_decay_trace) */
+  uint64_t displacement_macs;      /* count * chiR_i * d^2 per displaced site (FlopCounters field of
+                                      contract.hpp:14; the apply of SPEC.md:375-381) */
+  uint64_t measure_pipeline_ops;   /* d per live (sample, site) (sampler.cpp:92-93,114-115) */
 } mpsg_stats;
 
 typedef struct mpsg_handle_s* mpsg_handle;

@@ -77,6 +77,8 @@ class DeviceState {
 inline void merge_stats(const mpsg_stats& s, const std::vector<double>& site, mpsamp::RunStats& rs) {
   rs.flops.contraction_macs += s.contraction_macs;
   rs.flops.measure_weight_macs += s.measure_weight_macs;
+  rs.flops.displacement_macs += s.displacement_macs;
+  rs.flops.measure_pipeline_ops += s.measure_pipeline_ops;
   rs.dead_samples += s.dead_samples;
   if (rs.site_seconds.size() < site.size()) rs.site_seconds.resize(site.size(), 0.0);
   for (size_t i = 0; i < site.size(); ++i) rs.site_seconds[i] += site[i];

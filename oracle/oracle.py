@@ -229,6 +229,21 @@ class RefState:
                                           out.ctypes.data_as(_pu8), C.byref(macs), C.byref(dead)))
         return out, macs.value, dead.value
 
+    def sample_batch_stats(self, n, seed, compute=F64, scaling=SCALE_PER_SAMPLE):
+        """sample_batch with RunStats: (rows, {contraction_macs, displacement_macs,
+        measure_weight_macs, measure_pipeline_ops}, dead_samples)."""
+        out = np.empty((n, self.mps.num_sites), np.uint8)
+        c4 = (_u64 * 4)()
+        dead = _u64()
+        L = ref()
+        L.ref_sample_batch_stats.argtypes = [C.c_void_p, _u64, _u64, _int, _int, _pu8, C.POINTER(_u64),
+                                             C.POINTER(_u64)]
+        L.ref_sample_batch_stats.restype = _int
+        _check_ref(L.ref_sample_batch_stats(self.h, n, seed, compute, scaling, out.ctypes.data_as(_pu8), c4,
+                                            C.byref(dead)))
+        names = ("contraction_macs", "displacement_macs", "measure_weight_macs", "measure_pipeline_ops")
+        return out, dict(zip(names, list(c4))), dead.value
+
     def sample_range(self, first, count, seed, compute=F64, scaling=SCALE_PER_SAMPLE, threads=None):
         threads = threads or os.cpu_count() or 1
         out = np.empty((count, self.mps.num_sites), np.uint8)

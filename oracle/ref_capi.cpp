@@ -169,6 +169,26 @@ int ref_sample_batch(void* h, uint64_t n, uint64_t n1, uint64_t n2, uint64_t see
     }
 }
 
+// sample_batch with the RunStats counters (contract.hpp:12-25, sampler.hpp:46-54):
+// out4 = {contraction_macs, displacement_macs, measure_weight_macs, measure_pipeline_ops}
+int ref_sample_batch_stats(void* h, uint64_t n, uint64_t seed, int compute, int scaling, uint8_t* out,
+                           uint64_t* out4, uint64_t* dead) {
+    try {
+        RunStats st;
+        SampleBatch b = sample_batch(*static_cast<MpsState*>(h), BatchPlan::simple(n),
+                                     make_opts(seed, compute, scaling), &st);
+        std::memcpy(out, b.outcomes.data(), b.outcomes.size());
+        out4[0] = st.flops.contraction_macs;
+        out4[1] = st.flops.displacement_macs;
+        out4[2] = st.flops.measure_weight_macs;
+        out4[3] = st.flops.measure_pipeline_ops;
+        if (dead) *dead = st.dead_samples;
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 // detail::sample_micro_serial sampler.cpp:129 over [first, first+count), run on `threads`
 // host threads over disjoint contiguous sub-ranges (equivalent to run_data_parallel with
 // p1 = threads because draws are keyed by global sample index).  rows: count x M.

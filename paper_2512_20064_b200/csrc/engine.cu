@@ -319,6 +319,7 @@ struct DevCtx {
   std::vector<cudaEvent_t> ev;   // per-site boundaries on lane 0 (M + 1)
   cudaEvent_t pass_end = nullptr;
   double* trace = nullptr;       // [M] sum |env_ref| per site (decay trace, lazy)
+  unsigned long long* live = nullptr;  // [M] live samples measured per site (RunStats counters)
 };
 
 }  // namespace mpsg
@@ -558,6 +559,7 @@ static void free_device(DevCtx& dc) {
   cudaFree(dc.src);
   cudaFree(dc.err);
   cudaFree(dc.trace);
+  cudaFree(dc.live);
   for (auto& s : dc.sites) cudaFree(s.inv_gamma);
   for (auto e : dc.ev) cudaEventDestroy(e);
   if (dc.pass_end) cudaEventDestroy(dc.pass_end);
@@ -727,7 +729,7 @@ static void set_site(mpsg_handle_s& h, uint64_t i, const void* gamma, bool is_de
 // the sweep
 // ---------------------------------------------------------------------------------------------
 struct PassOut {
-  uint64_t macs = 0, wmacs = 0, issued = 0, launches = 0;
+  uint64_t macs = 0, wmacs = 0, issued = 0, launches = 0, dmacs = 0, pops = 0;
   double gemm_s = 0.0, device_s = 0.0;
 };
 
@@ -928,13 +930,14 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       sa.trace = dc.trace ? dc.trace + i : nullptr;
       sa.scaling = h.policy.scaling;
       sa.mu = fuse_displace ? ln.mu : nullptr;
+      sa.live = dc.live + i;
       sa.cinfo = cinfo;
       launch_select(sa, ln.stream);
       if (h.tp > 1 && has_next)  // rebuild the full environment from the column shards
         h.comm->allgather(ln.env, 2ull * h.env_comp * ln.cap * kn * sizeof(__half), ln.stream, L);
       po.launches += 2;
       po.macs += static_cast<uint64_t>(cnt[L]) * s.chil * s.width * h.d;
-      po.wmacs += static_cast<uint64_t>(cnt[L]) * s.width * h.d;
+      if (displaced) po.dmacs += static_cast<uint64_t>(cnt[L]) * s.width * h.d * h.d;
       po.issued += (h.m3 ? 6ull : 8ull) * rows[L] * s.np * s.kp * (h.precise ? 3 : h.split ? 2 : 1);
     }
     if (timing) CUDA_OK(cudaEventRecord(dc.ev[i + 1], dc.stream));
@@ -984,6 +987,9 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
     if (mu_host)
       for (auto& ln : dc.lanes)
         if (!ln.mu) CUDA_OK(cudaMalloc(&ln.mu, sizeof(double2) * ln.cap * h.M));
+    if (!dc.live) CUDA_OK(cudaMalloc(&dc.live, h.M * sizeof(unsigned long long)));
+    CUDA_OK(cudaMemsetAsync(dc.live, 0, h.M * sizeof(unsigned long long), dc.stream));
+    CUDA_OK(cudaStreamSynchronize(dc.stream));
     if (forced_host || marg_host)
       for (auto& ln : dc.lanes)
         if (!ln.forced) {
@@ -1056,6 +1062,13 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
         }
       }
     }
+    // measure's counters over the live samples (sampler.cpp:81-93,114-115)
+    std::vector<unsigned long long> live(h.M);
+    CUDA_OK(cudaMemcpy(live.data(), dc.live, h.M * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < h.M; ++i) {
+      rr.po.wmacs += live[i] * static_cast<uint64_t>(dc.sites[i].width) * h.d;
+      rr.po.pops += live[i] * h.d;
+    }
   } catch (...) {
     rr.err = std::current_exception();
   }
@@ -1092,12 +1105,15 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
     if (r.err) std::rethrow_exception(r.err);
   if (st) {
     st->contraction_macs = st->measure_weight_macs = st->issued_mma_flops = 0;
+    st->displacement_macs = st->measure_pipeline_ops = 0;
     st->kernel_launches = 0;
     st->gemm_seconds = 0.0;
     st->device_seconds = 0.0;
     for (auto& r : rr) {
       st->contraction_macs += r.po.macs;
       st->measure_weight_macs += r.po.wmacs;
+      st->displacement_macs += r.po.dmacs;
+      st->measure_pipeline_ops += r.po.pops;
       st->issued_mma_flops += r.po.issued;
       st->kernel_launches += r.po.launches;
       st->gemm_seconds = std::max(st->gemm_seconds, r.po.gemm_s);  // devices run concurrently

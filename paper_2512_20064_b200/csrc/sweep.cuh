@@ -100,6 +100,7 @@ struct SelectArgs {
   // the gathered slice use D(mu[n]) temp[n, :, r] computed on the fly from the d stored outcomes
   const double2* mu;        // [rows][num_sites] or null
   const float2* cinfo;      // site column info (wl_r = cinfo[r].y) for the displaced weights
+  unsigned long long* live; // optional: += number of live samples measured at this site (RunStats)
 };
 
 // GBS displacement site transform (SPEC.md gbs-ops; the hook of sampler.cpp:143): for every live

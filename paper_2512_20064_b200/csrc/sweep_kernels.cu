@@ -795,6 +795,7 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
   bool live_out = false; // carries into the next site
   float scale = 0.f;
   const float2* D = sD[kDisp ? wib : 0];
+  if (live_in && a.live != nullptr && lane == 0) atomicAdd(a.live, 1ull);  // measure's counters
   if (kDisp && live_in) {
     const double2 mu = a.mu[static_cast<size_t>(n) * a.num_sites + a.site];
     for (int e = lane; e < a.d * a.d; e += 32) {

@@ -239,6 +239,8 @@ class RunStats:
     site_seconds: list = field(default_factory=list)
     total_seconds: float = 0.0
     issued_mma_flops: int = 0
+    displacement_macs: int = 0
+    measure_pipeline_ops: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
 
@@ -357,6 +359,8 @@ class GpuSampler:
             stats.dead_samples += st.dead_samples
             stats.total_seconds += st.seconds
             stats.issued_mma_flops += st.issued_mma_flops
+            stats.displacement_macs += st.displacement_macs
+            stats.measure_pipeline_ops += st.measure_pipeline_ops
             stats.h2d_bytes += st.h2d_bytes
             stats.d2h_bytes += st.d2h_bytes
             stats.site_seconds = list(np.asarray(stats.site_seconds or np.zeros(self.num_sites)) + site_s)

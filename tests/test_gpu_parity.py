@@ -663,3 +663,32 @@ def test_sample_device_rows_and_stats(pkg, gold):
     b = mps.bond_dims
     assert st.contraction_macs == 700 * sum(b[i] * b[i + 1] * mps.phys_dim for i in range(mps.num_sites))
     assert st.issued_mma_flops > 0 and st.d2h_bytes == 700 * mps.num_sites
+
+
+def test_runstats_counters_match_reference(pkg, gold):
+    """RunStats / FlopCounters (sampler.hpp:46-54, contract.hpp:12-25): contraction MACs over every
+    sample, measure's weight MACs and pipeline ops over the live ones only, dead samples — equal to
+    the reference's own counters, on c1b and on a chain where samples die (structural zeros)."""
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not available")
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    g0 = np.zeros((1, 2, 2), complex)
+    g0[0, 0, 0], g0[0, 1, 1] = 1.0, 0.8
+    g1 = np.zeros((2, 2, 2), complex)
+    g1[0, :, :] = [[0.5, 0.2j], [0.3, 0.4]]
+    g2 = np.zeros((2, 1, 2), complex)
+    g2[:, 0, :] = [[1.0, 0.5], [0.25, 1.0]]
+    dying = O.Mps(2, [1, 2, 2, 1], [g0, g1, g2], [np.array([0.8, 0.6]), np.array([0.9, 0.4359]), np.ones(1)])
+    for mps in (O.load_npz_mps(np.load(f"{gold}/c1b.npz")), dying):
+        smp = pkg.GpuSampler(to_state(pkg, mps), pol)
+        dec = decoded_mps(smp, mps)
+        n = 777
+        ref_rows, want, dead = O.RefState(dec).sample_batch_stats(n, 7)
+        st = pkg.RunStats()
+        rows = smp.sample(0, n, 7, stats=st)
+        assert np.array_equal(rows, ref_rows)
+        assert st.contraction_macs == want["contraction_macs"]
+        assert st.measure_weight_macs == want["measure_weight_macs"]
+        assert st.measure_pipeline_ops == want["measure_pipeline_ops"]
+        assert st.dead_samples == dead
+        smp.close()
