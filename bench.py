@@ -58,6 +58,15 @@ def peaks():
         return 1590.0, 1400.0, 6650.0, "fallback"
 
 
+def peak_clock_mhz():
+    """Median SM clock under load while MEASURED_PEAKS.json's sustained bf16 figure was taken."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["clocks_under_load"]["sm_mhz_median"])
+    except Exception:
+        return None
+
+
 def chain_macs(M, chi, d):
     from paper_2512_20064_b200.sampler import capped_bond_dims
     b = capped_bond_dims(M, d, chi)
@@ -344,7 +353,9 @@ def main():
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     e2e_mode = args.e2e
     if e2e_mode == "auto":
-        e2e_mode = "stream" if (not args.stream_slots and host_mem_available() > 1.15 * state_bytes * local_world) \
+        # a 3M state streams its Gr, Gi planes only (Gs is re-formed on the device): 2/3 of the bytes
+        host_need = state_bytes * (2 / 3 if smp.scheme == P.Scheme.M3 else 1)
+        e2e_mode = "stream" if (not args.stream_slots and host_mem_available() > 1.15 * host_need * local_world) \
             else "resident"
     if args.stream_slots:
         e2e_mode = "stream"
@@ -402,6 +413,7 @@ def main():
         cpu = {"value": rate / macs_per_sample, "unit": "samples/s", "cores": threads, "kind": kind,
                "sample": sample, "seconds": round(secs, 2)}
     if rank == 0:
+        pclk = peak_clock_mhz()
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
@@ -432,6 +444,13 @@ def main():
                          "issued_tflops": issued / gemm_s / 1e12 if gemm_s > 0 else None,
                          "issued_frac": issued / gemm_s / 1e12 / sustained if gemm_s > 0 else None,
                          "frac_of_burst": achieved / burst if achieved else None,
+                         # both the kernel and the sustained cuBLAS figure run at the 1000 W power cap:
+                         # the issued rate per SM clock against cuBLAS's per clock separates issue
+                         # efficiency from the operating clock the power cap leaves
+                         "issued_frac_at_equal_clock": (issued / gemm_s / 1e12 / sustained * pclk / clocks["sm_mhz"]
+                                                        if gemm_s > 0 and pclk and clocks and clocks.get("sm_mhz")
+                                                        else None),
+                         "peak_sm_mhz": pclk,
                          "gemm_share_of_step": gemm_s / dev_s if dev_s > 0 else None},
             "cpu_baseline": cpu,
             "host_link": link,

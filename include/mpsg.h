@@ -158,7 +158,9 @@ int mpsg_builder_finish(mpsg_handle h);
 
 void mpsg_destroy(mpsg_handle h);
 
-/* Device bytes held for the compressed state on one device (algorithmic Gamma bytes). */
+/* Bytes of the compressed state held per device: in HBM, or for a host-streamed handle in pinned
+ * host memory (there the 3M sum planes are re-formed on the device after each copy, so a 3M
+ * host-streamed state holds 2/3 of the resident state's bytes). */
 uint64_t mpsg_state_bytes(mpsg_handle h);
 /* The contraction scheme the handle runs: MPSG_SCHEME_3M or MPSG_SCHEME_4M (0 for a null handle). */
 int mpsg_scheme(mpsg_handle h);

@@ -339,6 +339,10 @@ struct mpsg_handle_s {
   bool pair = true;                        // K1 variant: CTA-pair UMMA (M=256) vs A-multicast pairs
   bool m3 = false;                         // 3M contraction (Gamma planes Gr, Gi, Gs; env re, im, s)
   int gplanes = 2, env_comp = 2;
+  // planes kept per site in pinned host memory when Gamma is host-streamed: the 3M sum planes
+  // (Gs = Gr + Gi, exact by construction) are re-formed on the device after the copy, so the host
+  // link carries 4 B per complex entry for 3M as for 4M (PRECISE: 8 of the 12 B)
+  int hplanes = 2;
   bool precise = false;                    // Gamma hi + lo planes (MPSG_MODE_PRECISE)
   std::unique_ptr<mpsg::Comm> comm;
   std::mutex mu;
@@ -382,7 +386,7 @@ static void choose_scheme(mpsg_handle_s& h) {
     }
     if (h.opts.host_stream_slots != 0) {
       const double host = static_cast<double>(sysconf(_SC_PHYS_PAGES)) * sysconf(_SC_PAGE_SIZE);
-      if (state3 * h.devs.size() > 0.8 * host) m3 = false;
+      if (state3 * (2.0 / 3.0) * h.devs.size() > 0.8 * host) m3 = false;  // host keeps Gr, Gi only
     } else {
       for (auto& dc : h.devs) {
         size_t free_b = 0, total_b = 0;
@@ -401,8 +405,8 @@ static void choose_scheme(mpsg_handle_s& h) {
                 static_cast<double>(h.tp) * round_up((static_cast<int>(h.bonds[i]) + h.tp - 1) / h.tp, kBK3);
     if (h.opts.host_stream_slots != 0) {
       const double host = static_cast<double>(sysconf(_SC_PHYS_PAGES)) * sysconf(_SC_PAGE_SIZE);
-      config_check(state6 * h.devs.size() <= 0.85 * host,
-                   "MPSG_MODE_PRECISE: the hi + lo Gamma planes need " + std::to_string(state6 / 1e9) +
+      config_check(state6 * (4.0 / 6.0) * h.devs.size() <= 0.85 * host,
+                   "MPSG_MODE_PRECISE: the hi + lo Gamma planes need " + std::to_string(state6 * 4.0 / 6.0 / 1e9) +
                        " GB of pinned host memory per device");
     } else {
       for (auto& dc : h.devs) {
@@ -417,6 +421,7 @@ static void choose_scheme(mpsg_handle_s& h) {
   }
   h.m3 = m3;
   h.gplanes = h.precise ? 6 : (m3 ? 3 : 2);
+  h.hplanes = m3 ? h.gplanes * 2 / 3 : h.gplanes;
   h.env_comp = m3 ? 3 : 2;
 }
 
@@ -644,11 +649,18 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
     if (h.m3) ln.tma_env64[i] = make_tma_env(ln.env, s.kshard, env_rows, h.tp, kBM / 2, kBK3);
   }
   if (dc.slots) {
+    const size_t pe = static_cast<size_t>(s.np) * s.kp;  // elements per plane
     if (!s.g_host) {
-      CUDA_OK(cudaMallocHost(&s.g_host, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half)));
+      CUDA_OK(cudaMallocHost(&s.g_host, h.hplanes * pe * sizeof(__half)));
       CUDA_OK(cudaMallocHost(&s.cinfo_host, 1ull * s.np * sizeof(float2)));
     }
-    CUDA_OK(cudaMemcpyAsync(s.g_host, s.g, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half), cudaMemcpyDeviceToHost, dc.stream));
+    if (h.hplanes == h.gplanes) {
+      CUDA_OK(cudaMemcpyAsync(s.g_host, s.g, h.gplanes * pe * sizeof(__half), cudaMemcpyDeviceToHost, dc.stream));
+    } else {  // 3M: [Gr, Gi] of each precision half (the Gs planes are re-formed after the H2D copy)
+      for (int hf = 0; hf < h.gplanes / 3; ++hf)
+        CUDA_OK(cudaMemcpyAsync(s.g_host + 2ull * hf * pe, s.g + 3ull * hf * pe, 2 * pe * sizeof(__half),
+                                cudaMemcpyDeviceToHost, dc.stream));
+    }
     CUDA_OK(cudaMemcpyAsync(s.cinfo_host, s.cinfo, 1ull * s.np * sizeof(float2), cudaMemcpyDeviceToHost, dc.stream));
     CUDA_OK(cudaStreamSynchronize(dc.stream));
     s.tma_slot.resize(dc.slots);
@@ -674,8 +686,18 @@ static void issue_loads(mpsg_handle_s& h, DevCtx& dc, uint64_t upto) {
     const int slot = static_cast<int>(q % dc.slots);
     const SiteDev& s = dc.sites[q % h.M];
     CUDA_OK(cudaStreamWaitEvent(dc.copy_stream, dc.freed[slot], 0));  // consume q - slots done
-    const size_t gb = static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half);
-    CUDA_OK(cudaMemcpyAsync(dc.slot_g[slot], s.g_host, gb, cudaMemcpyHostToDevice, dc.copy_stream));
+    const size_t pe = static_cast<size_t>(s.np) * s.kp;
+    const size_t gb = h.hplanes * pe * sizeof(__half);
+    if (h.hplanes == h.gplanes) {
+      CUDA_OK(cudaMemcpyAsync(dc.slot_g[slot], s.g_host, gb, cudaMemcpyHostToDevice, dc.copy_stream));
+    } else {
+      for (int hf = 0; hf < h.gplanes / 3; ++hf) {
+        __half* dst = dc.slot_g[slot] + 3ull * hf * pe;
+        CUDA_OK(cudaMemcpyAsync(dst, s.g_host + 2ull * hf * pe, 2 * pe * sizeof(__half),
+                                cudaMemcpyHostToDevice, dc.copy_stream));
+        launch_sum_plane(dst, pe, dc.copy_stream);  // Gs = Gr + Gi (exact fp16 sums)
+      }
+    }
     CUDA_OK(cudaMemcpyAsync(dc.slot_cinfo[slot], s.cinfo_host, 1ull * s.np * sizeof(float2),
                             cudaMemcpyHostToDevice, dc.copy_stream));
     CUDA_OK(cudaEventRecord(dc.loaded[slot], dc.copy_stream));
@@ -1316,7 +1338,8 @@ void mpsg_destroy(mpsg_handle h) {
 uint64_t mpsg_state_bytes(mpsg_handle h) {
   if (!h || h->devs.empty()) return 0;
   uint64_t b = 0;
-  for (const auto& s : h->devs[0].sites) b += static_cast<size_t>(h->gplanes) * s.np * s.kp * sizeof(__half);
+  const int planes = h->devs[0].slots ? h->hplanes : h->gplanes;
+  for (const auto& s : h->devs[0].sites) b += static_cast<size_t>(planes) * s.np * s.kp * sizeof(__half);
   return b;  // host-streamed: these bytes live in pinned host memory
 }
 
@@ -1329,10 +1352,12 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
     DevCtx& dc = h->devs[0];
     CUDA_OK(cudaSetDevice(dc.device));
     const SiteDev& s = dc.sites[site];
-    std::vector<__half> g(static_cast<size_t>(h->gplanes) * s.np * s.kp);
+    const size_t pe = static_cast<size_t>(s.np) * s.kp;
+    std::vector<__half> g(h->gplanes * pe);
     std::vector<double> cs(std::max<size_t>(1, 1ull * s.width * h->d));
-    if (dc.slots)
-      std::memcpy(g.data(), s.g_host, g.size() * sizeof(__half));
+    if (dc.slots)  // host planes [Gr, Gi] per precision half: place them at their device plane
+      for (int hf = 0; hf < h->hplanes / 2; ++hf)
+        std::memcpy(g.data() + (h->m3 ? 3 : 2) * hf * pe, s.g_host + 2 * hf * pe, 2 * pe * sizeof(__half));
     else
       CUDA_OK(cudaMemcpy(g.data(), s.g, g.size() * sizeof(__half), cudaMemcpyDeviceToHost));
     CUDA_OK(cudaMemcpy(cs.data(), s.cs, cs.size() * sizeof(double), cudaMemcpyDeviceToHost));

@@ -152,6 +152,9 @@ void launch_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, 
                   cudaStream_t s);
 // Compression of one site's column shard [b0, b0 + width) of chiR: src complex (chiL, chiR, d)
 // f64 or f32 interleaved on device; row l goes to padded K position lpos[l].
+// g[2 pe + j] = g[j] + g[pe + j]: re-forms the 3M sum plane Gs = Gr + Gi of a host-streamed site
+// (exact: quantize_pair puts Gr, Gi and their sum on one fp16 grid).  pe % 8 == 0.
+void launch_sum_plane(__half* g, size_t pe, cudaStream_t s);
 void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
                           int width, int kp, int chirp, const int* lpos, const double* gl,
                           const double* gr, const double* wl, int gplanes, __half* g_out,

@@ -1197,6 +1197,31 @@ __global__ void pack_kernel(const void* src, int chil, int chir, int d, int b0, 
   }
 }
 
+__global__ void __launch_bounds__(256) sum_plane_kernel(__half* g, size_t n8, size_t pe) {
+  const uint4* a = reinterpret_cast<const uint4*>(g);
+  const uint4* b = reinterpret_cast<const uint4*>(g + pe);
+  uint4* c = reinterpret_cast<uint4*>(g + 2 * pe);
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint4 x = a[i], y = b[i];
+    uint4 z;
+    const __half2* xh = reinterpret_cast<const __half2*>(&x);
+    const __half2* yh = reinterpret_cast<const __half2*>(&y);
+    __half2* zh = reinterpret_cast<__half2*>(&z);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) zh[q] = __hadd2(xh[q], yh[q]);
+    c[i] = z;
+  }
+}
+
+void launch_sum_plane(__half* g, size_t pe, cudaStream_t s) {
+  const size_t n8 = pe / 8;
+  if (n8 == 0) return;
+  // two CTAs per SM at most: the kernel shares the GPU with the persistent contraction
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((n8 + 255) / 256, 2 * 148));
+  sum_plane_kernel<<<blocks, 256, 0, s>>>(g, n8, pe);
+}
+
 void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
                           int width, int kp, int chirp, const int* lpos, const double* gl,
                           const double* gr, const double* wl, int gplanes, __half* g_out,

@@ -193,6 +193,23 @@ def test_host_streamed_gamma(pkg, gold, slots, scheme):
     b = stm.sample(0, 1000, 7, stats=stats)
     assert np.array_equal(a, b)
     assert np.array_equal(stm.sample(123, 77, 7), a[123:200])
+    if scheme == 3:  # 3M streams Gr, Gi only (Gs re-formed on the device): 2/3 of the planes' bytes
+        assert stm.state_bytes * 3 == res.state_bytes * 2
+
+
+def test_host_streamed_gamma_precise(pkg, gold):
+    """PRECISE mode with Gamma streamed from pinned host memory (hi and lo Gr, Gi planes copied, both
+    sum planes re-formed on the device): identical rows and decoded tensors to the resident sweep."""
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    st = to_state(pkg, mps)
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    res = pkg.GpuSampler(st, pol, pass_samples=256, mode=pkg.Mode.PRECISE)
+    stm = pkg.GpuSampler(st, pol, pass_samples=256, mode=pkg.Mode.PRECISE, host_stream_slots=2)
+    for i in range(mps.num_sites):
+        assert np.array_equal(stm.decoded_gamma(i), res.decoded_gamma(i))
+    assert np.array_equal(stm.sample(0, 700, 7), res.sample(0, 700, 7))
+    assert stm.state_bytes * 6 == res.state_bytes * 4
 
 
 def test_mpsb_files_roundtrip(pkg, gold, tmp_path):
