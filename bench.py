@@ -45,6 +45,7 @@ CONFIGS["c4s"] = dict(M=64, chi=10000, d=4, job=1_000_000, stream=3,
 for _chi in (256, 512, 1024, 2048, 4096):
     CONFIGS[f"c5_{_chi}"] = dict(M=512, chi=_chi, d=4, job=100_000,
                                  desc=f"c5: bond-dimension sweep M=512, chi={_chi}, d=4, N=1e5")
+SLICE = {"auto": 0, "temp": 1, "recompute": 2}
 DEFAULT_PASS = {"c1": 1000, "c2": 32768, "c3": 16384, "c5_256": 65536, "c5_512": 32768,
                 "c5_1024": 32768, "c5_2048": 16384, "c5_4096": 8192, "c4s": 8192}
 
@@ -221,6 +222,9 @@ def main():
     ap.add_argument("--scheme", default="auto", choices=["auto", "3m", "4m"],
                     help="complex decomposition of the contraction (auto = 3M when the state fits)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--slice", default="auto", choices=sorted(SLICE),
+                    help="chosen-slice path: recompute (weights-only contraction + bucketed 1/d slice GEMM), "
+                         "temp (all d outcomes materialised), auto (= temp)")
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -272,7 +276,7 @@ def main():
     smp, _ = build_synthetic(cfg["M"], cfg["chi"], cfg["d"], seed=42, mode=mode, devices=[local],
                              pass_samples=P_pass, record_site_times=2, host_stream_slots=args.stream_slots,
                              policy=P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX),
-                             scheme={"auto": 0, "3m": 3, "4m": 4}[args.scheme],
+                             scheme={"auto": 0, "3m": 3, "4m": 4}[args.scheme], slice=SLICE[args.slice],
                              schedule=(P.TruncationFilter(chi_max=cfg["chi"], eps_center=args.schedule_eps,
                                                           edge_factor=100.0) if args.schedule_eps > 0 else None))
     scheme = "3M" if smp.scheme == P.Scheme.M3 else "4M"
@@ -367,7 +371,7 @@ def main():
         smp, _ = build_synthetic(cfg["M"], cfg["chi"], cfg["d"], seed=42, mode=mode, devices=[local],
                                  pass_samples=P_pass, record_site_times=0, host_stream_slots=3,
                                  policy=P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX),
-                                 scheme={"auto": 0, "3m": 3, "4m": 4}[args.scheme],
+                                 scheme={"auto": 0, "3m": 3, "4m": 4}[args.scheme], slice=SLICE[args.slice],
                                  schedule=(P.TruncationFilter(chi_max=cfg["chi"], eps_center=args.schedule_eps,
                                                               edge_factor=100.0) if args.schedule_eps > 0 else None))
         e2e_build_s = time.perf_counter() - t0
@@ -425,7 +429,7 @@ def main():
             "config": {"workload": cfg["desc"] + f"; step = one sweep of {P_pass} samples/GPU over all M sites",
                        "M": cfg["M"], "chi": cfg["chi"], "d": cfg["d"], "pass_samples_per_gpu": P_pass,
                        "job_samples": cfg["job"], "job_seconds_at_value": cfg["job"] / value,
-                       "mode": args.mode, "scheme": scheme, "parallelism": f"dp{world}",
+                       "mode": args.mode, "scheme": scheme, "slice": args.slice, "parallelism": f"dp{world}",
                        "bond_schedule": sched_note,
                        "displacement": (f"GBS displacement D(mu) per (sample, site), mu ~ CN(0, {args.displace}^2)"
                                         if args.displace > 0 else None),

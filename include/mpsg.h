@@ -108,7 +108,18 @@ typedef struct mpsg_options {
                                       decay_probe :207-216); GlobalMax is traced as None */
   int scheme;                      /* complex decomposition of the contraction: MPSG_SCHEME_AUTO,
                                       MPSG_SCHEME_3M or MPSG_SCHEME_4M (see above) */
+  int slice;                       /* how the chosen slice reaches the next environment (MPSG_SLICE_*) */
 } mpsg_options;
+
+/* MPSG_SLICE_AUTO     = MPSG_SLICE_TEMP (the faster path on every measured configuration)
+ * MPSG_SLICE_TEMP     the contraction materialises all d outcomes (temp) and the selection gathers
+ *                     the chosen slice
+ * MPSG_SLICE_RECOMPUTE  for plain sampling calls on a 3M state without tensor parallelism (d <= 32):
+ *                     the contraction emits only the Born weights, the rows are bucketed by drawn
+ *                     outcome and a 1/d-size GEMM recomputes the chosen slices straight into the
+ *                     next environment (no temp round trip through HBM; same arithmetic, identical
+ *                     outcomes).  Measured 15-32% slower than TEMP. */
+enum { MPSG_SLICE_AUTO = 0, MPSG_SLICE_TEMP = 1, MPSG_SLICE_RECOMPUTE = 2 };
 
 /* Mirrors mpsamp::RunStats + FlopCounters (sampler.hpp:46-54, contract.hpp:12-25). */
 typedef struct mpsg_stats {

@@ -32,6 +32,7 @@ from .sampler import (  # noqa: F401
     SamplerOptions,
     ScalingMode,
     Scheme,
+    Slice,
     capped_bond_dims,
     decay_probe,
     device_draws,

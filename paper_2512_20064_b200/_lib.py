@@ -30,7 +30,7 @@ class Policy(C.Structure):
 class Options(C.Structure):
     _fields_ = [("mode", _int), ("pass_samples", _u64), ("record_site_times", _int),
                 ("tp_size", _int), ("tp_rank", _int), ("host_stream_slots", _int),
-                ("record_decay_trace", _int), ("scheme", _int)]
+                ("record_decay_trace", _int), ("scheme", _int), ("slice", _int)]
 
 
 class Stats(C.Structure):

@@ -293,8 +293,18 @@ struct Lane {
   uint8_t* host_rows = nullptr;   // pinned [cap][M]
   std::vector<CUtensorMap> tma_env;    // per site: the shard-major env map over this lane's env
   std::vector<CUtensorMap> tma_env64;  // same with a 64-row box (3M kernel: env is the B operand)
+  // slice-recompute path (3M, tp = 1): rows bucketed by outcome each site
+  __half* env_perm = nullptr;     // the environment rows in bucket order (slice GEMM B operand)
+  int* perm = nullptr;            // [cap] row -> sample of the pass
+  int* perm2 = nullptr;
+  uint8_t* rowk = nullptr;        // [cap] drawn outcome per row (d = dead from the next site)
+  float* scale = nullptr;         // [cap] renormalisation per row
+  float* scale2 = nullptr;        // [cap] the same in bucket order
+  uint8_t* alive2 = nullptr;
+  int* bcount = nullptr;          // [2 (d + 1)] bucket counts, fill cursors
+  std::vector<CUtensorMap> tma_envp64;  // per site: B maps over env_perm
   cudaEvent_t k1done = nullptr, done = nullptr;
-  std::vector<cudaEvent_t> gev;   // per-site GEMM start/stop (2 M)
+  std::vector<cudaEvent_t> gev;   // per-site contraction start/stop, slice GEMM start/stop (4 M)
 };
 
 struct DevCtx {
@@ -344,6 +354,7 @@ struct mpsg_handle_s {
   // link carries 4 B per complex entry for 3M as for 4M (PRECISE: 8 of the 12 B)
   int hplanes = 2;
   bool precise = false;                    // Gamma hi + lo planes (MPSG_MODE_PRECISE)
+  bool slice_rc = false;                   // slice-recompute path available (3M, tp = 1, d <= 32)
   std::unique_ptr<mpsg::Comm> comm;
   std::mutex mu;
 };
@@ -502,6 +513,17 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     CUDA_OK(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
     ln.tma_env.resize(h.M);
     ln.tma_env64.resize(h.M);
+    if (h.slice_rc) {
+      CUDA_OK(cudaMalloc(&ln.env_perm, 2ull * h.env_comp * ln.cap * kmax * sizeof(__half)));
+      CUDA_OK(cudaMalloc(&ln.perm, ln.cap * sizeof(int)));
+      CUDA_OK(cudaMalloc(&ln.perm2, ln.cap * sizeof(int)));
+      CUDA_OK(cudaMalloc(&ln.rowk, ln.cap));
+      CUDA_OK(cudaMalloc(&ln.scale, ln.cap * sizeof(float)));
+      CUDA_OK(cudaMalloc(&ln.scale2, ln.cap * sizeof(float)));
+      CUDA_OK(cudaMalloc(&ln.alive2, ln.cap));
+      CUDA_OK(cudaMalloc(&ln.bcount, 2 * (h.d + 1) * sizeof(int)));
+      ln.tma_envp64.resize(h.M);
+    }
   }
   CUDA_OK(cudaMalloc(&dc.err, sizeof(int)));
   CUDA_OK(cudaMemset(dc.err, 0, sizeof(int)));
@@ -555,6 +577,14 @@ static void free_device(DevCtx& dc) {
     cudaFree(ln.marg);
     cudaFree(ln.logscale);
     cudaFree(ln.mu);
+    cudaFree(ln.env_perm);
+    cudaFree(ln.perm);
+    cudaFree(ln.perm2);
+    cudaFree(ln.rowk);
+    cudaFree(ln.scale);
+    cudaFree(ln.scale2);
+    cudaFree(ln.alive2);
+    cudaFree(ln.bcount);
     if (ln.host_rows) cudaFreeHost(ln.host_rows);
     if (ln.k1done) cudaEventDestroy(ln.k1done);
     if (ln.done) cudaEventDestroy(ln.done);
@@ -647,6 +677,7 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
     const uint64_t env_rows = 2ull * h.env_comp * ln.cap;
     ln.tma_env[i] = make_tma_env(ln.env, s.kshard, env_rows, h.tp);
     if (h.m3) ln.tma_env64[i] = make_tma_env(ln.env, s.kshard, env_rows, h.tp, kBM / 2, kBK3);
+    if (ln.env_perm) ln.tma_envp64[i] = make_tma_env(ln.env_perm, s.kshard, env_rows, h.tp, kBM / 2, kBK3);
   }
   if (dc.slots) {
     const size_t pe = static_cast<size_t>(s.np) * s.kp;  // elements per plane
@@ -761,13 +792,16 @@ struct PassOut {
 // path: +10% at chi = 512).
 static bool epilogue_max(const mpsg_handle_s& h, const SiteDev& s) { return h.tp > 1 || s.kp >= 1024; }
 
+
 // K1 for `rows` samples of lane `ln` at site i.  tma_g128 / tma_g64: Gamma maps with 128 / 64-row
 // boxes (the 3M kernel loads Gamma as its A operand; the 4M pair kernel as its half-B operand).
+// slice: 0 = K1 (temp + weights), 1 = weights only (slice-recompute path), 2 = the slice GEMM
 static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const SiteDev& s, const Lane& ln,
                                uint64_t i, int rows, const CUtensorMap* tma_g128,
-                               const CUtensorMap& tma_g64, const float2* cinfo, cudaStream_t stream) {
+                               const CUtensorMap& tma_g64, const float2* cinfo, cudaStream_t stream,
+                               int slice = 0, int kp_next = 0) {
   if (h.m3) {
-    Gemm3MArgs ga;
+    Gemm3MArgs ga = {};
     ga.g_tiles = s.np / (2 * kBN);
     ga.s_tiles = rows / kBM;
     ga.k_blocks = s.kp / kBK3;
@@ -790,8 +824,14 @@ static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const S
     ga.group = std::min(ga.g_tiles, env_group);
     ga.flags = env_flags;
     ga.cinfo = cinfo;
-    ga.temp = ln.temp;
-    ga.pstat = ln.pstat;
+    ga.temp = slice == 0 ? ln.temp : nullptr;
+    ga.pstat = slice == 2 ? nullptr : ln.pstat;
+    if (slice == 2) {
+      ga.bcount = ln.bcount;
+      ga.scale = ln.scale2;
+      ga.env_next = ln.env;
+      ga.kp_next = kp_next;
+    }
     const int ctas = 2 * ga.g_tiles * ga.s_tiles;
     static const int env_epi = [] {
       const char* v = std::getenv("MPSG_3M_EPI");
@@ -801,8 +841,9 @@ static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const S
       const char* v = std::getenv("MPSG_3M_QUAD");
       return v && std::atoi(v) != 0;
     }();
-    launch_site_gemm_3m(h.split, epilogue_max(h, s), env_epi, env_quad, h.precise, ln.tma_env64[i], *tma_g128, ga,
-                        std::min(ctas, dc.num_sms), stream);
+    launch_site_gemm_3m(h.split, slice == 1 || epilogue_max(h, s), env_epi, env_quad && slice == 0, h.precise,
+                        slice == 2 ? ln.tma_envp64[i] : ln.tma_env64[i], *tma_g128, ga, std::min(ctas, dc.num_sms),
+                        stream, slice == 2);
     return;
   }
   const int mrow = h.pair ? 2 * kBM : kBM;
@@ -842,13 +883,16 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
   }
   off[1] = cnt[0];
   const int active = cnt[1] > 0 ? 2 : 1;
+  // slice recompute for plain sampling passes (teacher forcing, marginals, displacement and the decay
+  // trace read temp): rows are then permuted by outcome every such site, perm maps them to samples
+  const bool rc_pass = h.slice_rc && !forced && !marg && !displaced && !dc.trace;
   int rows[2];
   for (int L = 0; L < active; ++L) {
     Lane& ln = dc.lanes[L];
     rows[L] = round_up(cnt[L], mrow);
     if (L > 0 && timing) CUDA_OK(cudaStreamWaitEvent(ln.stream, dc.ev[0], 0));  // after the pass-start stamp
     launch_init_env(ln.env, h.env_comp, ln.cap, dc.sites[0].kshard, h.tp, rows[L], cnt[L], ln.alive,
-                    ln.stream, dc.trace ? ln.logscale : nullptr);
+                    ln.stream, dc.trace ? ln.logscale : nullptr, rc_pass ? ln.perm : nullptr);
     po.launches += 1;
   }
   if (dc.slots) issue_loads(h, dc, dc.consumed + dc.slots);
@@ -875,9 +919,11 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
         else if (i > 0)
           CUDA_OK(cudaStreamWaitEvent(ln.stream, dc.lanes[1].k1done, 0));
       }
-      if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[2 * i], ln.stream));
-      launch_contraction(h, dc, s, ln, i, rows[L], tma_g128, *tma_g64, cinfo, ln.stream);
-      if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[2 * i + 1], ln.stream));
+      const bool has_next = i + 1 < h.M;
+      const bool rc = rc_pass && h.opts.slice == MPSG_SLICE_RECOMPUTE;
+      if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[4 * i], ln.stream));
+      launch_contraction(h, dc, s, ln, i, rows[L], tma_g128, *tma_g64, cinfo, ln.stream, rc ? 1 : 0);
+      if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[4 * i + 1], ln.stream));
       // Displacement fused into the selection (one read of temp) unless the weights must be exchanged
       // first (tensor parallelism) or the decay trace reads the transformed slice.
       static const bool no_fuse = std::getenv("MPSG_DISPLACE_SEPARATE") != nullptr;
@@ -902,11 +948,13 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
         po.launches += 1;
       }
       if (active == 2) CUDA_OK(cudaEventRecord(ln.k1done, ln.stream));
-      if (dc.slots) {  // K1 is the only reader of the slot: hand it back to the copy stream
+      auto release_slot = [&] {  // the last reader of the Gamma slot is done: back to the copy stream
+        if (!dc.slots) return;
         CUDA_OK(cudaEventRecord(dc.freed[slot], dc.stream));
         ++dc.consumed;
         issue_loads(h, dc, dc.consumed + dc.slots);
-      }
+      };
+      if (!(rc && has_next)) release_slot();
 
       SelectArgs sa;
       sa.site = static_cast<int>(i);
@@ -933,12 +981,11 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       }
       sa.rows = rows[L];
       sa.count = cnt[L];
-      const bool has_next = i + 1 < h.M;
       const int kn = has_next ? dc.sites[i + 1].kshard : 0;
       sa.kp_next = kn;
       sa.env_cap = ln.cap;
       sa.env_comp = h.env_comp;
-      sa.slice_max = (h.m3 && !epilogue_max(h, s)) ? 1 : 0;
+      sa.slice_max = (h.m3 && !rc && !epilogue_max(h, s)) ? 1 : 0;
       sa.seed = seed;
       sa.first = lfirst;
       sa.temp = ln.temp;
@@ -954,7 +1001,45 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       sa.mu = fuse_displace ? ln.mu : nullptr;
       sa.live = dc.live + i;
       sa.cinfo = cinfo;
+      sa.perm = rc_pass ? ln.perm : nullptr;
+      sa.rowk = rc ? ln.rowk : nullptr;
+      sa.scale_out = ln.scale;
+      sa.bcount = ln.bcount;
+      if (rc) CUDA_OK(cudaMemsetAsync(ln.bcount, 0, 2 * (h.d + 1) * sizeof(int), ln.stream));
       launch_select(sa, ln.stream);
+      if (rc && has_next) {
+        // bucket the rows by outcome, zero the rows dead from here on, recompute the chosen slices
+        PermuteArgs pa;
+        pa.rows = rows[L];
+        pa.d = static_cast<int>(h.d);
+        pa.planes = 2 * h.env_comp;
+        pa.kp = s.kshard;
+        pa.env_cap = ln.cap;
+        pa.rowk = ln.rowk;
+        pa.scale = ln.scale;
+        pa.perm = ln.perm;
+        pa.env = ln.env;
+        pa.bcount = ln.bcount;
+        pa.bfill = ln.bcount + (h.d + 1);
+        pa.rowk2 = nullptr;
+        pa.scale2 = ln.scale2;
+        pa.perm2 = ln.perm2;
+        pa.alive2 = ln.alive2;
+        pa.env2 = ln.env_perm;
+        launch_permute_rows(pa, ln.stream);
+        launch_zero_dead(ln.env, 2 * h.env_comp, ln.cap, kn, rows[L], ln.bcount, static_cast<int>(h.d), ln.stream);
+        if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[4 * i + 2], ln.stream));
+        launch_contraction(h, dc, s, ln, i, rows[L], tma_g128, *tma_g64, cinfo, ln.stream, 2, kn);
+        if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[4 * i + 3], ln.stream));
+        release_slot();
+        std::swap(ln.perm, ln.perm2);
+        std::swap(ln.alive, ln.alive2);
+        po.launches += 4;
+        po.issued += 6ull * (rows[L] + static_cast<uint64_t>(kBM) * h.d) * s.chirp * s.kp * (h.precise ? 3 : h.split ? 2 : 1);
+      } else if (timing >= 2) {
+        CUDA_OK(cudaEventRecord(ln.gev[4 * i + 2], ln.stream));
+        CUDA_OK(cudaEventRecord(ln.gev[4 * i + 3], ln.stream));
+      }
       if (h.tp > 1 && has_next)  // rebuild the full environment from the column shards
         h.comm->allgather(ln.env, 2ull * h.env_comp * ln.cap * kn * sizeof(__half), ln.stream, L);
       po.launches += 2;
@@ -994,7 +1079,7 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
     if (timing >= 2)
       for (auto& ln : dc.lanes)
         if (ln.gev.empty()) {
-          ln.gev.resize(2 * h.M);
+          ln.gev.resize(4 * h.M);
           for (auto& e : ln.gev) CUDA_OK(cudaEventCreate(&e));
         }
     if (timing) rr.site_ms.assign(h.M, 0.0);
@@ -1078,8 +1163,10 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
           if (timing >= 2)
             for (int L = 0; L < 2; ++L) {
               if (cnt[L] <= 0) continue;
-              CUDA_OK(cudaEventElapsedTime(&ms, dc.lanes[L].gev[2 * i], dc.lanes[L].gev[2 * i + 1]));
+              CUDA_OK(cudaEventElapsedTime(&ms, dc.lanes[L].gev[4 * i], dc.lanes[L].gev[4 * i + 1]));
               rr.po.gemm_s += ms * 1e-3;
+              CUDA_OK(cudaEventElapsedTime(&ms, dc.lanes[L].gev[4 * i + 2], dc.lanes[L].gev[4 * i + 3]));
+              rr.po.gemm_s += ms * 1e-3;  // the slice GEMM (0 at temp-path sites)
             }
         }
       }
@@ -1276,6 +1363,9 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
     }
     if (mpsg_device_count() == 0) throw Error(MPSG_ERR_CUDA, "no sm_100 CUDA device visible");
     choose_scheme(*h);
+    config_check(h->opts.slice >= MPSG_SLICE_AUTO && h->opts.slice <= MPSG_SLICE_RECOMPUTE,
+                 "unknown slice option");
+    h->slice_rc = h->m3 && h->tp == 1 && h->d <= 32 && h->opts.slice == MPSG_SLICE_RECOMPUTE;
     try {
       for (auto& dc : h->devs) alloc_device(*h, dc);
     } catch (...) {

@@ -47,7 +47,8 @@ struct Cfg3M {
   static constexpr int kStages = kGlo ? 4 : (kSplit ? 6 : 8);
   static constexpr int kRedBytes = 4 * kBM * 8;        // [4 lane quarters][128 samples] float2
   static constexpr int kBarBytes = 512;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + kBarBytes + kRedBytes;
+  static constexpr int kOffBytes = 256;                // slice GEMM: bucket offsets
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + kBarBytes + kRedBytes + kOffBytes;
 };
 
 int gemm_3m_smem_bytes(bool split) { return split ? Cfg3M<true>::kSmem : Cfg3M<false>::kSmem; }
@@ -99,7 +100,10 @@ __device__ unsigned long long g_prof3m[8];
 // the pairs share every environment tile through TMA multicast (pair 0 fetches the hi plane, pair 1
 // the lo plane, each for both pairs), cutting the L2 -> SM traffic per MMA by a quarter.  A stage
 // is refilled only when both pairs have consumed it (commits multicast to all four CTAs).
-template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad, bool kGlo = false>
+// kSlice: the slice GEMM of the slice-recompute path (Gemm3MArgs::bcount): units whose sample tile
+// misses the bucket of their outcome are skipped by every role alike, and the epilogue writes the
+// next environment's hi / lo planes exactly as the select kernel would from temp.
+template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad, bool kGlo = false, bool kSlice = false>
 __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
     site_gemm_3m_kernel(const __grid_constant__ CUtensorMap tma_env64,
                         const __grid_constant__ CUtensorMap tma_g, const Gemm3MArgs a) {
@@ -113,6 +117,7 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
   uint64_t* tempty = tfull + 2;          // [4] per TMEM slot
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
   float2* red = reinterpret_cast<float2*>(smem + C::kStages * C::kStageBytes + C::kBarBytes);
+  int* boff = reinterpret_cast<int*>(smem + C::kStages * C::kStageBytes + C::kBarBytes + C::kRedBytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -133,6 +138,14 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
     for (int j = 0; j < 2; ++j) ptx::mbar_init(&tfull[j], 1);
     for (int j = 0; j < 4; ++j) ptx::mbar_init(&tempty[j], 2 * kEpiWarps);  // epilogue warps x 2 CTAs
     ptx::fence_mbar_init();
+    if constexpr (kSlice) {  // bucket k = rows [boff[k], boff[k + 1])
+      int o = 0;
+      for (int k = 0; k <= a.d; ++k) {
+        boff[k] = o;
+        o += a.bcount[k];
+      }
+      boff[a.d + 1] = o;
+    }
   }
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tma_env64);
@@ -148,6 +161,20 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int units = g_units * a.s_tiles;
+  // slice GEMM: does Gamma tile pair m (outcome of either SM's 128 columns) meet sample tile t's rows?
+  auto unit_on = [&](int m, int t) -> bool {
+    if constexpr (!kSlice) {
+      return true;
+    } else {
+      const int r0 = t * kBM, r1 = r0 + kBM;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int k = (m * 2 * kBM + hh * kBM) / a.chirp;
+        if (k < a.d && boff[k] < r1 && boff[k + 1] > r0) return true;
+      }
+      return false;
+    }
+  };
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs; bytes counted on the leader's barrier) ----------
@@ -160,6 +187,7 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
         int m, t;
         unit_coords_3m(u, a, g_units, m, t);
         if (kQuad) m = 2 * m + pair;
+        if (!unit_on(m, t)) continue;
         const int grow = m * 2 * kBM + rank * kBM;     // this SM's Gamma rows
         const int erow = t * kBM + rank * (kBM / 2);   // this SM's sample rows
 #pragma unroll 1
@@ -207,7 +235,12 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
       uint32_t phase = 0;
       uint32_t gp = 0;  // running product index: TMEM slot gp % 4
       int unit = 0;
-      for (int u = cluster; u < units; u += num_clusters, ++unit) {
+      for (int u = cluster; u < units; u += num_clusters) {
+        if constexpr (kSlice) {
+          int m, t;
+          unit_coords_3m(u, a, g_units, m, t);
+          if (!unit_on(m, t)) continue;
+        }
 #pragma unroll 1
         for (int c = 0; c < 3; ++c, ++gp) {
           const uint32_t slot = gp & 3;
@@ -245,6 +278,7 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
         }
         // all three products of the unit done -> this pair's epilogues
         ptx::umma_commit_pair_mc_elect(&tfull[unit & 1], static_cast<uint16_t>(0x3u << (2 * pair)));
+        ++unit;
       }
       if ((a.flags & 32) && lane == 0) {
         atomicAdd(&g_prof3m[2], static_cast<unsigned long long>(w_slot));
@@ -260,10 +294,11 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
     const int ec = q * 32 + lane;  // column within the SM's 128
     uint32_t gp = 0;
     int unit = 0;
-    for (int u = cluster; u < units; u += num_clusters, ++unit, gp += 3) {
+    for (int u = cluster; u < units; u += num_clusters) {
       int m, t;
       unit_coords_3m(u, a, g_units, m, t);
       if (kQuad) m = 2 * m + pair;
+      if (!unit_on(m, t)) continue;
       const int col0 = m * 2 * kBM + rank * kBM;  // first of this SM's 128 columns (one outcome)
       const int k = col0 / a.chirp;
       // the pair-padding tile (and a quad's phantom odd Gamma tile) has nothing to store
@@ -299,13 +334,41 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
             ptx::mbar_arrive_remote_relaxed(&tempty[(gp + 2) & 3], 2 * pair);
           }
         }
-        if (valid) {
+        if constexpr (kSlice) {
+          // next environment rows of this SM's outcome bucket: E = temp * scale split hi / lo per
+          // component re, im, re + im (the select kernel's arithmetic, sweep_kernels.cu)
+          if (valid && r < a.kp_next) {
+            const int j0 = t * kBM + c0 + ch * kEpiSamples;
+            const int lo = boff[k], hi = boff[k + 1];
+            const size_t plane = static_cast<size_t>(a.env_cap) * a.kp_next;
+#pragma unroll
+            for (int i = 0; i < kEpiSamples; ++i) {
+              const int j = j0 + i;
+              if (j < lo || j >= hi) continue;
+              const float re = (pr[i] - pi[i]) * ci.x;
+              const float im = (ps[i] - pr[i] - pi[i]) * ci.x;
+              const float sc = a.scale[j];
+              float comp[3];
+              comp[0] = re * sc;
+              comp[1] = im * sc;
+              comp[2] = comp[0] + comp[1];
+              __half* e0 = a.env_next + static_cast<size_t>(j) * a.kp_next + r;
+#pragma unroll
+              for (int cc = 0; cc < 3; ++cc) {
+                const __half hv = __float2half_rn(comp[cc]);
+                e0[cc * plane] = hv;
+                e0[(3 + cc) * plane] = __float2half_rn(comp[cc] - __half2float(hv));
+              }
+            }
+          }
+        } else if (valid) {
 #pragma unroll
           for (int i = 0; i < kEpiSamples; ++i) {
             const float re = (pr[i] - pi[i]) * ci.x;
             const float im = (ps[i] - pr[i] - pi[i]) * ci.x;
-            // streaming store: temp (1.6 GB per c3 site) must not evict the Gamma group from L2
-            __stcs(dst + (ch * kEpiSamples + i) * row_stride, make_float2(re, im));
+            // streaming store: temp (1.6 GB per c3 site) must not evict the Gamma group from L2;
+            // no temp at all on the slice-recompute path (weights only)
+            if (a.temp != nullptr) __stcs(dst + (ch * kEpiSamples + i) * row_stride, make_float2(re, im));
             pr[i] = ci.y * fmaf(re, re, im * im);
             if constexpr (kMax) pi[i] = fmaxf(fabsf(re), fabsf(im));
           }
@@ -315,7 +378,7 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
           if (lane < 16) red[q * kBM + c0 + ch * kEpiSamples + lane] = make_float2(w, mx);
         }
       }
-      if (valid) {
+      if (valid && !kSlice) {
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
         if (h == 0) {  // thread ec reduces sample ec of the unit over the 4 lane quarters, in order
           float2 v = red[ec];
@@ -336,6 +399,8 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
         atomicAdd(&g_prof3m[5], static_cast<unsigned long long>(e2 - e1));
         atomicAdd(&g_prof3m[4], 1ull);
       }
+      ++unit;
+      gp += 3;
     }
   }
 
@@ -348,10 +413,10 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
   }
 }
 
-template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad, bool kGlo = false>
+template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad, bool kGlo = false, bool kSlice = false>
 static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
                         int grid, cudaStream_t s) {
-  auto kern = site_gemm_3m_kernel<kSplit, kMax, kEpiWarps, kQuad, kGlo>;
+  auto kern = site_gemm_3m_kernel<kSplit, kMax, kEpiWarps, kQuad, kGlo, kSlice>;
   using Cf = Cfg3M<kSplit, kGlo>;
   constexpr int kCl = kQuad ? 4 : 2;
   static int max_clusters = 0;
@@ -397,7 +462,15 @@ static void launch_3m_w(int epi_warps, bool quad, bool glo, const CUtensorMap& e
 
 void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, bool glo,
                          const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
-                         int grid, cudaStream_t s) {
+                         int grid, cudaStream_t s, bool slice) {
+  if (slice) {  // slice GEMM: 8 epilogue warps, CTA pairs
+    if (split)
+      glo ? launch_3m_t<true, false, 8, false, true, true>(tma_env64, tma_g, a, grid, s)
+          : launch_3m_t<true, false, 8, false, false, true>(tma_env64, tma_g, a, grid, s);
+    else
+      launch_3m_t<false, false, 8, false, false, true>(tma_env64, tma_g, a, grid, s);
+    return;
+  }
   if (split)
     with_max ? launch_3m_w<true, true>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s)
              : launch_3m_w<true, false>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s);

@@ -64,8 +64,33 @@ struct Gemm3MArgs {
   int group;         // Gamma tiles per raster group
   int flags;         // diagnostics (0 in production): 32 = clock64 timing probes (g_prof3m)
   const float2* cinfo;
-  float2* temp;
+  float2* temp;      // null: weights-only contraction (slice-recompute path, no temp stores)
   float2* pstat;
+  // slice GEMM (slice-recompute path): the environment rows are bucketed by outcome (rows
+  // [off_k, off_k+1) drew outcome k, off = prefix sums of bcount[0..d]); only the units whose
+  // sample tile meets the bucket of their Gamma columns' outcome run, and the epilogue writes the
+  // next environment's hi / lo planes (row scale `scale`) instead of temp / pstat
+  const int* bcount;
+  const float* scale;
+  __half* env_next;  // [2 * 3][env_cap][kp_next]
+  int kp_next;
+};
+
+// Slice-recompute path: rows of the environment scattered into outcome buckets (bucket d = dead
+// from the next site), carrying their sample index, outcome, renormalisation scale and liveness.
+struct PermuteArgs {
+  int rows, d, planes, kp, env_cap;
+  const uint8_t* rowk;
+  const float* scale;
+  const int* perm;
+  const __half* env;
+  const int* bcount;
+  int* bfill;
+  uint8_t* rowk2;
+  float* scale2;
+  int* perm2;
+  uint8_t* alive2;
+  __half* env2;
 };
 
 // Per-(sample, outcome) partials read by the select kernel: element (part, n, k) lives at
@@ -101,6 +126,13 @@ struct SelectArgs {
   const double2* mu;        // [rows][num_sites] or null
   const float2* cinfo;      // site column info (wl_r = cinfo[r].y) for the displaced weights
   unsigned long long* live; // optional: += number of live samples measured at this site (RunStats)
+  // slice-recompute path: row n holds sample perm[n] of the pass (null: identity); with rowk set the
+  // kernel records (outcome or d = dead next, scale) per row and counts the buckets instead of
+  // writing the next environment (the slice GEMM does)
+  const int* perm;
+  uint8_t* rowk;
+  float* scale_out;
+  int* bcount;              // [d + 1]
 };
 
 // GBS displacement site transform (SPEC.md gbs-ops; the hook of sampler.cpp:143): for every live
@@ -136,18 +168,24 @@ int gemm_pair_smem_bytes(bool split);
 // epi_warps: 4 or 8 epilogue warps (one or two per TMEM lane quarter).
 // quad: 4-CTA clusters sharing the environment tiles by multicast (see site_gemm_3m.cu).
 // glo: Gamma lo planes present (MPSG_MODE_PRECISE, split only).
+// slice = true: the slice GEMM of the slice-recompute path (Gemm3MArgs::bcount / scale / env_next)
 void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, bool glo,
                          const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
-                         int grid, cudaStream_t s);
+                         int grid, cudaStream_t s, bool slice = false);
 int gemm_3m_smem_bytes(bool split);
 void launch_select(const SelectArgs& a, cudaStream_t s);
+void launch_permute_rows(const PermuteArgs& a, cudaStream_t s);
+// zeroes rows [sum(bcount[0..d)), rows) of the next environment (the samples dead from there on)
+void launch_zero_dead(__half* env, int planes, int env_cap, int kp, int rows, const int* bcount, int d,
+                      cudaStream_t s);
 // pstat [rows][nt] -> out [rows][d]: (sum of weights, max) over the tiles of each outcome
 void launch_reduce_tiles(const float2* pstat, int nt, int tiles_per_k, int d, int rows,
                          float2* out, cudaStream_t s);
 // Site-0 env in the shard-major layout [shards][2C][cap][kshard]: E[n][0] = 1 (shard 0) in the
 // hi.re plane and, for C = 3, the hi.s plane.
 void launch_init_env(__half* env, int env_comp, int env_cap, int kshard0, int shards, int rows,
-                     int count, uint8_t* alive, cudaStream_t s, double* logscale = nullptr);
+                     int count, uint8_t* alive, cudaStream_t s, double* logscale = nullptr,
+                     int* perm = nullptr);
 void launch_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, double* out,
                   cudaStream_t s);
 // Compression of one site's column shard [b0, b0 + width) of chiR: src complex (chiL, chiR, d)

@@ -790,7 +790,8 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   if (n >= a.rows) return;
-  const bool live_in = n < a.count && a.alive[n];
+  const int sidx = a.perm != nullptr ? a.perm[n] : n;  // sample of this row within the pass
+  const bool live_in = sidx < a.count && a.alive[n];
   int outcome = kDead;   // recorded at this site
   bool live_out = false; // carries into the next site
   float scale = 0.f;
@@ -850,7 +851,7 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
       if (a.forced != nullptr) {
         kk = a.forced[static_cast<size_t>(n) * a.num_sites + a.site];
       } else {
-        const double draw = keyed_uniform(a.seed, kMeasureStream, a.first + n, a.site);
+        const double draw = keyed_uniform(a.seed, kMeasureStream, a.first + sidx, a.site);
         double cum = 0.0;
         kk = 0;
         for (int k = 0; k < a.d; ++k) {  // sampler.cpp:100-106: strict '>', no early break
@@ -880,9 +881,18 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
     double* mrow = a.marg + (static_cast<size_t>(n) * a.num_sites + a.site) * a.d;
     for (int k = 0; k < a.d; ++k) mrow[k] = -1.0;
   }
-  if (lane == 0 && n < a.count) {
-    a.rows_out[static_cast<size_t>(n) * a.num_sites + a.site] = static_cast<uint8_t>(outcome);
+  if (lane == 0 && sidx < a.count) {
+    a.rows_out[static_cast<size_t>(sidx) * a.num_sites + a.site] = static_cast<uint8_t>(outcome);
     a.alive[n] = live_out ? 1 : 0;
+  }
+  if (a.rowk != nullptr) {  // slice-recompute path: bucket the row; the slice GEMM writes its env
+    if (lane == 0) {
+      const int b = live_out ? outcome : a.d;
+      a.rowk[n] = static_cast<uint8_t>(b);
+      a.scale_out[n] = scale;
+      atomicAdd(a.bcount + b, 1);
+    }
+    return;
   }
   if (a.trace != nullptr && outcome != kDead) {
     // reference-scale |env| of the gathered slice: |temp_int| / gamma_r * exp(-logscale)
@@ -1054,7 +1064,7 @@ void launch_select(const SelectArgs& a, cudaStream_t s) {
 // site-0 environment (sampler.cpp:136-138: env = ones(count, 1), all alive)
 // ============================================================================================
 __global__ void init_env_kernel(__half* env, int env_comp, int env_cap, int kshard0, int shards,
-                                int rows, int count, uint8_t* alive, double* logscale) {
+                                int rows, int count, uint8_t* alive, double* logscale, int* perm) {
   const int planes = 2 * env_comp;
   const size_t plane = static_cast<size_t>(env_cap) * kshard0;
   const size_t total = static_cast<size_t>(shards) * planes * plane;
@@ -1069,13 +1079,73 @@ __global__ void init_env_kernel(__half* env, int env_comp, int env_cap, int ksha
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < rows; n += gridDim.x * blockDim.x) {
     alive[n] = n < count ? 1 : 0;
     if (logscale) logscale[n] = 0.0;
+    if (perm) perm[n] = n;
   }
 }
 
 void launch_init_env(__half* env, int env_comp, int env_cap, int kshard0, int shards, int rows,
-                     int count, uint8_t* alive, cudaStream_t s, double* logscale) {
+                     int count, uint8_t* alive, cudaStream_t s, double* logscale, int* perm) {
   init_env_kernel<<<296, 256, 0, s>>>(env, env_comp, env_cap, kshard0, shards, rows, count, alive,
-                                      logscale);
+                                      logscale, perm);
+}
+
+// ============================================================================================
+// Slice-recompute path: bucket scatter of the environment rows by drawn outcome (one warp per
+// row; the order inside a bucket is the atomic arrival order -- every row's arithmetic is
+// independent of its position, so the sampled values are not) and zeroing of the dead rows
+// ============================================================================================
+__device__ __forceinline__ int bucket_offset(const int* bcount, int k) {
+  int o = 0;
+  for (int q = 0; q < k; ++q) o += bcount[q];
+  return o;
+}
+
+__global__ void __launch_bounds__(256) permute_rows_kernel(const PermuteArgs a) {
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= a.rows) return;
+  const int k = a.rowk[j];
+  int dst = 0;
+  if (lane == 0) dst = bucket_offset(a.bcount, k) + atomicAdd(a.bfill + k, 1);
+  dst = __shfl_sync(0xffffffffu, dst, 0);
+  const size_t plane = static_cast<size_t>(a.env_cap) * a.kp;
+  const int v8 = a.kp / 8;  // kp is a multiple of 64
+  for (int p = 0; p < a.planes; ++p) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.env + p * plane + static_cast<size_t>(j) * a.kp);
+    uint4* out = reinterpret_cast<uint4*>(a.env2 + p * plane + static_cast<size_t>(dst) * a.kp);
+    for (int c = lane; c < v8; c += 32) out[c] = src[c];
+  }
+  if (lane == 0) {
+    a.perm2[dst] = a.perm[j];
+    if (a.rowk2 != nullptr) a.rowk2[dst] = static_cast<uint8_t>(k);
+    a.scale2[dst] = a.scale[j];
+    a.alive2[dst] = k < a.d ? 1 : 0;
+  }
+}
+
+void launch_permute_rows(const PermuteArgs& a, cudaStream_t s) {
+  const int blocks = (a.rows * 32 + 255) / 256;
+  permute_rows_kernel<<<blocks, 256, 0, s>>>(a);
+}
+
+__global__ void zero_dead_kernel(__half* env, int planes, int env_cap, int kp, int rows, const int* bcount,
+                                 int d) {
+  __shared__ int r0;
+  if (threadIdx.x == 0) r0 = bucket_offset(bcount, d);
+  __syncthreads();
+  const size_t plane = static_cast<size_t>(env_cap) * kp;
+  const size_t per_plane = static_cast<size_t>(rows - r0) * kp / 8;  // uint4 per plane
+  const size_t total = per_plane * planes;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t p = i / per_plane, rem = i - p * per_plane;
+    reinterpret_cast<uint4*>(env + p * plane + static_cast<size_t>(r0) * kp)[rem] = make_uint4(0, 0, 0, 0);
+  }
+}
+
+void launch_zero_dead(__half* env, int planes, int env_cap, int kp, int rows, const int* bcount, int d,
+                      cudaStream_t s) {
+  zero_dead_kernel<<<148, 256, 0, s>>>(env, planes, env_cap, kp, rows, bcount, d);
 }
 
 __global__ void draws_kernel(uint64_t seed, uint64_t first, uint64_t count, uint64_t site,

@@ -47,7 +47,7 @@ def build_synthetic(num_sites: int, chi: int, d: int, seed: int = 42, level_damp
                     mode: Mode = Mode.AUTO, devices: Optional[Sequence[int]] = None,
                     pass_samples: int = 0, n_base: int = 4, record_site_times: bool = False,
                     keep_host: bool = False, tp_size: int = 1, tp_rank: int = 0,
-                    host_stream_slots: int = 0, scheme: int = 0, schedule=None):
+                    host_stream_slots: int = 0, scheme: int = 0, schedule=None, slice: int = 0):
     """Build a GpuSampler holding a synthetic chain; returns (sampler, lambdas[, host gammas]).
 
     schedule: an optional TruncationFilter -- the chain is generated at the capped bonds and then
@@ -81,7 +81,7 @@ def build_synthetic(num_sites: int, chi: int, d: int, seed: int = 42, level_damp
     bd = (C.c_uint64 * (num_sites + 1))(*bonds)
     pol = _lib.Policy(int(policy.compute), int(policy.storage), int(policy.scaling))
     opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), int(tp_size), int(tp_rank),
-                       int(host_stream_slots), 0, int(scheme))
+                       int(host_stream_slots), 0, int(scheme), int(slice))
     devs, nd = GpuSampler._devices(devices)
     _check(L.mpsg_builder_begin(num_sites, d, bd, C.byref(pol), C.byref(opt), devs, nd, C.byref(h)))
     host = [] if keep_host else None

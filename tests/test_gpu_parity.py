@@ -709,3 +709,57 @@ def test_runstats_counters_match_reference(pkg, gold):
         assert st.measure_pipeline_ops == want["measure_pipeline_ops"]
         assert st.dead_samples == dead
         smp.close()
+
+
+def _dead_chain():
+    g0 = np.zeros((1, 2, 2), complex)
+    g0[0, 0, 0] = 1.0
+    g0[0, 1, 1] = 0.8
+    g1 = np.zeros((2, 2, 2), complex)
+    g1[0, :, :] = [[0.5, 0.2j], [0.3, 0.4]]
+    g2 = np.zeros((2, 1, 2), complex)
+    g2[:, 0, :] = [[1.0, 0.5], [0.25, 1.0]]
+    mps = O.Mps(2, [1, 2, 2, 1], [g0, g1, g2])
+    mps.lambdas = [np.array([0.8, 0.6]), np.array([0.9, 0.4359]), np.ones(1)]
+    return mps
+
+
+@pytest.mark.parametrize("case", ["c1", "c1b", "dead", "chi512_passes", "chi2048", "precise", "single",
+                                  "stream"])
+def test_slice_recompute_identical_to_temp(pkg, gold, case):
+    """The slice-recompute path (weights-only contraction, rows bucketed by outcome, 1/d slice GEMM
+    writing the next environment) produces exactly the temp path's outcome strings and counters:
+    same arithmetic per element, only the row order inside the device changes.  Covers forced
+    recompute at every site, dead samples, several passes with a ragged last pass, PRECISE, SINGLE
+    and a host-streamed state."""
+    from paper_2512_20064_b200.synthetic import build_synthetic
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    n, seed = 1000, 7
+
+    def make(slice_):
+        if case in ("c1", "c1b", "dead", "precise", "single"):
+            mps = _dead_chain() if case == "dead" else O.load_npz_mps(np.load(f"{gold}/{'c1b' if case == 'c1b' else 'c1'}.npz"))
+            mode = {"precise": pkg.Mode.PRECISE, "single": pkg.Mode.SINGLE}.get(case, pkg.Mode.AUTO)
+            return pkg.GpuSampler(to_state(pkg, mps), pol, mode=mode, pass_samples=384, slice=slice_)
+        chi, m = (512, 12) if case != "chi2048" else (2048, 8)
+        kw = dict(pass_samples=384) if case == "chi512_passes" else {}
+        if case == "stream":
+            chi, m, kw = 512, 10, dict(host_stream_slots=2)
+        smp, _ = build_synthetic(m, chi, 6, seed=11, policy=pol, slice=int(slice_), **kw)
+        return smp
+
+    temp = make(pkg.Slice.TEMP)
+    st_t = pkg.RunStats()
+    want = temp.sample(0, n, seed, stats=st_t)
+    temp.close()
+    for sl in (pkg.Slice.RECOMPUTE,):
+        smp = make(sl)
+        st = pkg.RunStats()
+        got = smp.sample(0, n, seed, stats=st)
+        assert np.array_equal(got, want), (case, sl, int((got != want).any(axis=1).sum()))
+        assert st.contraction_macs == st_t.contraction_macs and st.dead_samples == st_t.dead_samples
+        assert st.measure_weight_macs == st_t.measure_weight_macs
+        assert np.array_equal(smp.sample(217, 301, seed), want[217:518])
+        smp.close()
+    if case == "dead":
+        assert 0 < (want[:, -1] == pkg.DEAD_OUTCOME).sum() < n

@@ -1,6 +1,6 @@
 """Perf probe: per-site device times and algorithmic TFLOP/s for a synthetic chain.
 
-usage: python tools/perf_probe.py M CHI D N [mode] [pass] [scheme 0|3|4]
+usage: python tools/perf_probe.py M CHI D N [mode] [pass] [scheme 0|3|4] [slice 0|1|2]
 """
 import os
 import sys
@@ -18,8 +18,10 @@ M, chi, d, N = (int(x) for x in sys.argv[1:5])
 mode = {"single": P.Mode.SINGLE, "precise": P.Mode.PRECISE}.get(sys.argv[5] if len(sys.argv) > 5 else "split", P.Mode.SPLIT)
 ps = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 scheme = int(sys.argv[7]) if len(sys.argv) > 7 else 0
+slice_ = int(sys.argv[8]) if len(sys.argv) > 8 else 0
 t = time.time()
-smp, lams = build_synthetic(M, chi, d, mode=mode, pass_samples=ps or N, record_site_times=True, scheme=scheme)
+smp, lams = build_synthetic(M, chi, d, mode=mode, pass_samples=ps or N, record_site_times=True, scheme=scheme,
+                           slice=slice_)
 print(f"build {time.time()-t:.1f}s state {smp.state_bytes/1e9:.2f} GB scheme {int(smp.scheme)}", flush=True)
 bonds = smp.bond_dims
 rows = torch.empty((N, M), dtype=torch.uint8, device="cuda")
