@@ -1346,6 +1346,8 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
                (h->opts.mode == MPSG_MODE_AUTO && (pol.compute == MPSG_F64 || pol.compute == MPSG_F32));
     config_check(h->opts.scheme == MPSG_SCHEME_AUTO || h->opts.scheme == MPSG_SCHEME_3M ||
                      h->opts.scheme == MPSG_SCHEME_4M, "unknown contraction scheme");
+    config_check(h->opts.slice >= MPSG_SLICE_AUTO && h->opts.slice <= MPSG_SLICE_RECOMPUTE,
+                 "unknown slice option");
     h->gl.resize(num_sites);
     h->gr.resize(num_sites);
     for (uint64_t i = 0; i < num_sites; ++i) {
@@ -1363,8 +1365,6 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
     }
     if (mpsg_device_count() == 0) throw Error(MPSG_ERR_CUDA, "no sm_100 CUDA device visible");
     choose_scheme(*h);
-    config_check(h->opts.slice >= MPSG_SLICE_AUTO && h->opts.slice <= MPSG_SLICE_RECOMPUTE,
-                 "unknown slice option");
     h->slice_rc = h->m3 && h->tp == 1 && h->d <= 32 && h->opts.slice == MPSG_SLICE_RECOMPUTE;
     try {
       for (auto& dc : h->devs) alloc_device(*h, dc);

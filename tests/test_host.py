@@ -81,6 +81,18 @@ def test_abi_scheme_option_validated_before_device():
     assert [int(x) for x in P.Scheme] == [0, 3, 4]
 
 
+def test_abi_slice_option_validated_before_device():
+    """mpsg_options.slice: only AUTO / TEMP / RECOMPUTE are accepted (ConfigError before device work)."""
+    L = _lib.lib()
+    bd = (C.c_uint64 * 3)(1, 4, 1)
+    pol = _lib.Policy(0, 0, 0)
+    for bad in (3, -1, 7):
+        h = C.c_void_p()
+        opt = _lib.Options(slice=bad)
+        assert L.mpsg_builder_begin(2, 2, bd, C.byref(pol), C.byref(opt), None, 0, C.byref(h)) == _lib.MPSG_ERR_CONFIG
+    assert [int(x) for x in P.Slice] == [0, 1, 2]
+
+
 def test_options_struct_layout_matches_header(tmp_path):
     """The ctypes mirrors of mpsg_options / mpsg_stats have the header's layout (gcc offsetof)."""
     import subprocess
