@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define MPSG_ABI_VERSION 2  /* 2: mpsg_stats gained displacement_macs, measure_pipeline_ops */
+#define MPSG_ABI_VERSION 3  /* 2: mpsg_stats gained displacement_macs, measure_pipeline_ops; 3: mpsg_options.slice */
 
 enum {
   MPSG_OK = 0,
