@@ -359,7 +359,9 @@ def main():
     if e2e_mode == "auto":
         # a 3M state streams its Gr, Gi planes only (Gs is re-formed on the device): 2/3 of the bytes
         host_need = state_bytes * (2 / 3 if smp.scheme == P.Scheme.M3 else 1)
-        e2e_mode = "stream" if (not args.stream_slots and host_mem_available() > 1.15 * host_need * local_world) \
+        # several ranks pin their states at once: keep 40% of the host memory free then
+        room = host_mem_available() * (1 / 1.15 if local_world == 1 else 0.6)
+        e2e_mode = "stream" if (not args.stream_slots and room > host_need * local_world) \
             else "resident"
     if args.stream_slots:
         e2e_mode = "stream"
