@@ -483,11 +483,14 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     const double budget = 6.0e9;  // bytes of per-pass working set
     want = std::min<uint64_t>(65536, static_cast<uint64_t>(budget / row_bytes));
   }
-  // Two lanes overlap the select kernel with the other lane's contraction; measured neutral under
-  // the 1000 W power cap without tensor parallelism (c2 +2%, c3 -2.5%), so one lane is the default.
-  // Tensor parallelism defaults to two lanes: one lane's partial / environment all-gathers and
+  // Two lanes overlap the select kernel with the other lane's contraction (a selection block fits
+  // next to the 128-register 3M contraction on an SM).  Measured (profiles/r1_lanes_ab/, one box,
+  // alternating runs): c3 +1.9%, chi = 512 / 256 neutral, so two lanes for chains with chi >= 1024.
+  // Tensor parallelism always uses two lanes: one lane's partial / environment all-gathers and
   // selection run underneath the other lane's contraction, so the GEMM and the collectives overlap.
-  int nlanes = h.tp > 1 ? 2 : 1;
+  uint64_t chi_max = 1;
+  for (uint64_t i = 0; i <= h.M; ++i) chi_max = std::max(chi_max, h.bonds[i]);
+  int nlanes = (h.tp > 1 || (h.m3 && chi_max >= 1024)) ? 2 : 1;
   if (const char* v = std::getenv("MPSG_LANES")) nlanes = std::max(1, std::min(2, std::atoi(v)));
   if (h.opts.host_stream_slots != 0) nlanes = 1;
   const int lane_cap = std::max(2 * kBM, round_up(static_cast<int>((std::min<uint64_t>(want, 1u << 22) +
