@@ -304,6 +304,7 @@ struct Lane {
   int* bcount = nullptr;          // [2 (d + 1)] bucket counts, fill cursors
   std::vector<CUtensorMap> tma_envp64;  // per site: B maps over env_perm
   cudaEvent_t k1done = nullptr, done = nullptr;
+  cudaEvent_t seldone = nullptr;  // this lane's selection of the current site (host-streamed slots)
   std::vector<cudaEvent_t> gev;   // per-site contraction start/stop, slice GEMM start/stop (4 M)
 };
 
@@ -492,7 +493,8 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
   for (uint64_t i = 0; i <= h.M; ++i) chi_max = std::max(chi_max, h.bonds[i]);
   int nlanes = (h.tp > 1 || (h.m3 && chi_max >= 1024)) ? 2 : 1;
   if (const char* v = std::getenv("MPSG_LANES")) nlanes = std::max(1, std::min(2, std::atoi(v)));
-  if (h.opts.host_stream_slots != 0) nlanes = 1;
+  // host-streamed Gamma: both lanes read each slot; the slice-recompute path keeps one lane
+  if (h.opts.host_stream_slots != 0 && h.opts.slice == MPSG_SLICE_RECOMPUTE) nlanes = 1;
   const int lane_cap = std::max(2 * kBM, round_up(static_cast<int>((std::min<uint64_t>(want, 1u << 22) +
                                                                      nlanes - 1) / nlanes), 2 * kBM));
   dc.cap = nlanes * lane_cap;
@@ -514,6 +516,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     CUDA_OK(cudaMallocHost(&ln.host_rows, 1ull * ln.cap * h.M));
     CUDA_OK(cudaEventCreateWithFlags(&ln.k1done, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&ln.seldone, cudaEventDisableTiming));
     ln.tma_env.resize(h.M);
     ln.tma_env64.resize(h.M);
     if (h.slice_rc) {
@@ -591,6 +594,7 @@ static void free_device(DevCtx& dc) {
     if (ln.host_rows) cudaFreeHost(ln.host_rows);
     if (ln.k1done) cudaEventDestroy(ln.k1done);
     if (ln.done) cudaEventDestroy(ln.done);
+    if (ln.seldone) cudaEventDestroy(ln.seldone);
     for (auto e : ln.gev) cudaEventDestroy(e);
   }
   cudaFree(dc.scratch);
@@ -951,13 +955,16 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
         po.launches += 1;
       }
       if (active == 2) CUDA_OK(cudaEventRecord(ln.k1done, ln.stream));
-      auto release_slot = [&] {  // the last reader of the Gamma slot is done: back to the copy stream
-        if (!dc.slots) return;
-        CUDA_OK(cudaEventRecord(dc.freed[slot], dc.stream));
+      // Host-streamed Gamma: the slot (planes and cinfo) is read by the contraction(s), the fused
+      // displacement selection and the slice GEMM of every lane; the last lane hands it back to the
+      // copy stream once all of them are done (lane 1's contraction already follows lane 0's).
+      auto release_slot = [&] {
+        if (!dc.slots || L != active - 1) return;
+        if (active == 2) CUDA_OK(cudaStreamWaitEvent(ln.stream, dc.lanes[0].seldone, 0));
+        CUDA_OK(cudaEventRecord(dc.freed[slot], ln.stream));
         ++dc.consumed;
         issue_loads(h, dc, dc.consumed + dc.slots);
       };
-      if (!(rc && has_next)) release_slot();
 
       SelectArgs sa;
       sa.site = static_cast<int>(i);
@@ -1010,6 +1017,8 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       sa.bcount = ln.bcount;
       if (rc) CUDA_OK(cudaMemsetAsync(ln.bcount, 0, 2 * (h.d + 1) * sizeof(int), ln.stream));
       launch_select(sa, ln.stream);
+      if (dc.slots && active == 2 && L == 0) CUDA_OK(cudaEventRecord(ln.seldone, ln.stream));
+      if (!(rc && has_next)) release_slot();
       if (rc && has_next) {
         // bucket the rows by outcome, zero the rows dead from here on, recompute the chosen slices
         PermuteArgs pa;
