@@ -763,3 +763,20 @@ def test_slice_recompute_identical_to_temp(pkg, gold, case):
         smp.close()
     if case == "dead":
         assert 0 < (want[:, -1] == pkg.DEAD_OUTCOME).sum() < n
+
+
+def test_host_streamed_two_lanes_displaced(pkg):
+    """chi = 1024 (two pipeline lanes) with Gamma streamed through 2 device slots, plain and with the
+    fused displacement selection (which reads the slot's column info): identical rows to the
+    HBM-resident sweep over several passes."""
+    from paper_2512_20064_b200.synthetic import build_synthetic
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    m, chi, d, n = 8, 1024, 4, 1200
+    res, _ = build_synthetic(m, chi, d, seed=5, policy=pol, pass_samples=512)
+    stm, _ = build_synthetic(m, chi, d, seed=5, policy=pol, pass_samples=512, host_stream_slots=2)
+    rng = np.random.default_rng(9)
+    mu = 0.4 * (rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m)))
+    assert np.array_equal(stm.sample(0, n, 7), res.sample(0, n, 7))
+    assert np.array_equal(stm.sample(0, n, 7, mu=mu), res.sample(0, n, 7, mu=mu))
+    stm.close()
+    res.close()
