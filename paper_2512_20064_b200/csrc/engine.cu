@@ -820,15 +820,18 @@ static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const S
     ga.nt = s.nt;
     static const int env_group = [] {
       const char* v = std::getenv("MPSG_3M_GROUP");
-      // 8 Gamma tiles (25 MB at chi = 2048) per raster group: measured 3.5 GB DRAM reads per c3 site
-      // launch vs 4.4 GB with 16 tiles (the larger group does not stay in L2), same duration
-      return v ? std::max(1, std::atoi(v)) : 8;
+      return v ? std::max(1, std::atoi(v)) : 0;
     }();
+    // Gamma tile pairs per raster group: as many as fit ~25 MB of Gamma planes, at least 8 (c3:
+    // 8 pairs = 25 MB -- larger groups measured more DRAM traffic and less speed, profiles/
+    // r1_l2_experiments/; c2 and c5 chi = 1024: the whole site, +2.5%, profiles/r1_group_ab/)
+    const double pair_bytes = 2.0 * kBM * s.kp * sizeof(__half) * h.gplanes;
+    const int auto_group = std::max(8, static_cast<int>(26214400.0 / pair_bytes));
     static const int env_flags = [] {
       const char* v = std::getenv("MPSG_3M_FLAGS");
       return v ? std::atoi(v) : 0;
     }();
-    ga.group = std::min(ga.g_tiles, env_group);
+    ga.group = std::min(ga.g_tiles, env_group > 0 ? env_group : auto_group);
     ga.flags = env_flags;
     ga.cinfo = cinfo;
     ga.temp = slice == 0 ? ln.temp : nullptr;
