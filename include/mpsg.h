@@ -37,7 +37,8 @@
 extern "C" {
 #endif
 
-#define MPSG_ABI_VERSION 3  /* 2: mpsg_stats gained displacement_macs, measure_pipeline_ops; 3: mpsg_options.slice */
+#define MPSG_ABI_VERSION 4  /* 2: mpsg_stats gained displacement_macs, measure_pipeline_ops; 3: mpsg_options.slice;
+                               4: mpsg_stats.near_boundary_draws */
 
 enum {
   MPSG_OK = 0,
@@ -138,6 +139,10 @@ typedef struct mpsg_stats {
   uint64_t displacement_macs;      /* count * chiR_i * d^2 per displaced site (FlopCounters field of
                                       contract.hpp:14; the apply of SPEC.md:375-381) */
   uint64_t measure_pipeline_ops;   /* d per live (sample, site) (sampler.cpp:92-93,114-115) */
+  uint64_t near_boundary_draws;    /* drawn (sample, site) pairs whose uniform lies within 1e-6 of an
+                                      interior CDF boundary cum_k, k < d - 1 (sampler.cpp:100-106):
+                                      the only draws whose outcome may differ from the reference's
+                                      under rounding; counted on the device */
 } mpsg_stats;
 
 typedef struct mpsg_handle_s* mpsg_handle;

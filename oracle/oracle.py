@@ -361,3 +361,56 @@ def ref_apply_schedule(mps: Mps, chi: list, chi_max: int) -> Mps:
         return _mps_from_handle(h)
     finally:
         ref().ref_mps_free(h)
+
+
+class RefSiteSweep:
+    """The reference's per-site sweep body (ref_capi.cpp ref_sweep_*: contract_site ->
+    measurement_draws -> measure -> scale_rows_inplace, sampler.cpp:140-158) driven one site at a
+    time, threaded over contiguous sample chunks.  For full-length parity on chains whose complex128
+    Gamma does not fit in host memory (c3: 409 GB): the caller passes one decoded Gamma_i per call.
+
+    site(i, gamma, lam) -> (outcomes (count,) u8, marginals (count, d) f64, near (count,) bool);
+    with forced (count,) u8 the outcome column is imposed (teacher forcing)."""
+
+    def __init__(self, first, count, seed, compute=F64, scaling=SCALE_PER_SAMPLE, threads=None, eps=1e-6):
+        L = ref()
+        L.ref_sweep_begin.restype = C.c_void_p
+        L.ref_sweep_begin.argtypes = [_u64, _u64, _u64, _int, _int, _int]
+        L.ref_sweep_site.restype = _int
+        L.ref_sweep_site.argtypes = [C.c_void_p, _sz, _pd, _sz, _sz, _sz, _pd, _pu8, _dbl, _pu8, _pd, _pu8]
+        L.ref_sweep_macs.restype = _u64
+        L.ref_sweep_macs.argtypes = [C.c_void_p]
+        L.ref_sweep_end.argtypes = [C.c_void_p]
+        self.count, self.eps = int(count), float(eps)
+        self.h = L.ref_sweep_begin(first, count, seed, compute, scaling, threads or os.cpu_count() or 1)
+
+    def site(self, i, gamma: np.ndarray, lam: np.ndarray, forced=None):
+        g = np.ascontiguousarray(gamma, np.complex128)
+        lam = np.ascontiguousarray(lam, np.float64)
+        chil, chir, d = g.shape
+        out = np.empty(self.count, np.uint8)
+        marg = np.empty((self.count, d), np.float64)
+        near = np.zeros(self.count, np.uint8)
+        fp = None
+        if forced is not None:
+            forced = np.ascontiguousarray(forced, np.uint8)
+            fp = forced.ctypes.data_as(_pu8)
+        _check_ref(ref().ref_sweep_site(self.h, i, g.ctypes.data_as(_pd), chil, chir, d, lam.ctypes.data_as(_pd),
+                                        fp, self.eps, out.ctypes.data_as(_pu8), marg.ctypes.data_as(_pd),
+                                        near.ctypes.data_as(_pu8)))
+        return out, marg, near.astype(bool)
+
+    @property
+    def contraction_macs(self) -> int:
+        return int(ref().ref_sweep_macs(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            ref().ref_sweep_end(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

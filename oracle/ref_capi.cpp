@@ -429,3 +429,139 @@ int ref_decay_probe(void* h, int compute, int scaling, uint64_t count, uint64_t 
     }
 }
 }
+
+// ---- site-streaming sweep (full-length parity on chains larger than host memory) ---------------
+//
+// The per-site body of detail::sample_micro_serial (sampler.cpp:140-158) -- contract_site ->
+// measurement_draws -> measure -> scale_rows_inplace, the reference's own functions -- driven one
+// site at a time, so the caller can hand over one decoded Gamma_i at a time (c3 as complex128 is
+// 409 GB, beyond host memory) and drop it afterwards.  The samples [first, first + count) are split
+// into `threads` contiguous chunks with one environment each (partition-invariant: draws are keyed
+// by global sample index, rng.hpp:7-9).  Per site it also returns the reference's conditional
+// distribution p[n, k] = w[n, k] / total (the weights of sampler.cpp:83-93, evaluated on the same
+// temp) and, per sample, whether the draw lay within `eps` of an interior CDF boundary cum_k
+// (k < d - 1, cum accumulated exactly as sampler.cpp:100-104).  With `forced` the outcome column
+// is given (teacher forcing) and the environment follows it, as ref_marginals_forced does.
+namespace {
+struct SiteSweep {
+    uint64_t first = 0, count = 0, seed = 0;
+    PrecisionPolicy pol;
+    std::vector<uint64_t> a, b;             // chunk ranges (relative to first)
+    std::vector<ComplexTensor> env;         // per chunk (count_t, chiL)
+    std::vector<std::vector<uint8_t>> alive;
+    uint64_t macs = 0;
+};
+}  // namespace
+
+extern "C" {
+void* ref_sweep_begin(uint64_t first, uint64_t count, uint64_t seed, int compute, int scaling, int threads) {
+    auto* s = new SiteSweep();
+    s->first = first;
+    s->count = count;
+    s->seed = seed;
+    s->pol.compute = static_cast<Precision>(compute);
+    s->pol.storage = Precision::F64;
+    s->pol.scaling = static_cast<ScalingMode>(scaling);
+    if (threads < 1) threads = 1;
+    for (int t = 0; t < threads; ++t) {
+        const uint64_t a = count * t / threads, b = count * (t + 1) / threads;
+        if (b <= a) continue;
+        s->a.push_back(a);
+        s->b.push_back(b);
+        ComplexTensor e({b - a, 1});
+        for (uint64_t n = 0; n < b - a; ++n) e[n] = cdouble(1.0, 0.0);  // sampler.cpp:136-137
+        s->env.push_back(std::move(e));
+        s->alive.emplace_back(b - a, 1);
+    }
+    return s;
+}
+
+// gamma: complex128 (chil, chir, d) of site `site`; lambda: chir.  out: count outcomes (0xFF dead);
+// marg: count x d (-1 for samples not alive at this site); near: count flags (may be null).
+int ref_sweep_site(void* hs, size_t site, const double* gamma, size_t chil, size_t chir, size_t d,
+                   const double* lambda, const uint8_t* forced, double eps, uint8_t* out, double* marg,
+                   uint8_t* near) {
+    auto* s = static_cast<SiteSweep*>(hs);
+    try {
+        std::vector<cdouble> g(chil * chir * d);
+        std::memcpy(g.data(), gamma, g.size() * sizeof(cdouble));
+        const ComplexTensor gt({chil, chir, d}, std::move(g));
+        const std::vector<double> lam(lambda, lambda + chir);
+        const size_t T = s->env.size();
+        std::vector<std::exception_ptr> errs(T);
+        std::vector<uint64_t> macs(T, 0);
+        std::vector<std::thread> pool;
+        for (size_t t = 0; t < T; ++t) {
+            pool.emplace_back([&, t] {
+                try {
+                    const uint64_t a = s->a[t], cnt = s->b[t] - s->a[t];
+                    auto& alive = s->alive[t];
+                    FlopCounters fc;
+                    ComplexTensor temp = contract_site(s->env[t], gt, s->pol, &fc);
+                    macs[t] = fc.contraction_macs;
+                    std::vector<double> draws = detail::measurement_draws(s->seed, s->first + a, cnt, site);
+                    std::vector<uint8_t> alive_in = alive;
+                    // the reference's conditional distribution and boundary distance on this temp
+                    std::vector<double> w(d);
+                    for (uint64_t n = 0; n < cnt; ++n) {
+                        double* mrow = marg + (a + n) * d;
+                        if (near) near[a + n] = 0;
+                        if (!alive_in[n] || (forced && forced[a + n] == kDeadOutcome)) {
+                            for (size_t k = 0; k < d; ++k) mrow[k] = -1.0;
+                            continue;
+                        }
+                        std::fill(w.begin(), w.end(), 0.0);
+                        const cdouble* row = temp.data() + n * chir * d;
+                        for (size_t r = 0; r < chir; ++r) {
+                            const double l2 = lam[r] * lam[r];
+                            for (size_t k = 0; k < d; ++k) w[k] += l2 * std::norm(row[r * d + k]);
+                        }
+                        double total = 0.0;
+                        for (size_t k = 0; k < d; ++k) total += w[k];
+                        double cum = 0.0;
+                        bool nb = false;
+                        for (size_t k = 0; k < d; ++k) {
+                            mrow[k] = total == 0.0 ? -1.0 : w[k] / total;
+                            cum += total == 0.0 ? 0.0 : w[k] / total;
+                            if (k + 1 < d && std::fabs(draws[n] - cum) < eps) nb = true;
+                        }
+                        if (near) near[a + n] = nb && !forced ? 1 : 0;
+                    }
+                    if (!forced) {  // the reference's own measure + scaling (sampler.cpp:145-156)
+                        MeasureResult mr = measure(temp, lam, draws, alive, &fc);
+                        s->env[t] = std::move(mr.env);
+                        scale_rows_inplace(s->env[t], s->pol.scaling, alive);
+                        for (uint64_t n = 0; n < cnt; ++n) out[a + n] = mr.outcomes[n];
+                    } else {        // teacher forcing along the given column
+                        ComplexTensor next({cnt, chir});
+                        for (uint64_t n = 0; n < cnt; ++n) {
+                            const uint8_t k_f = forced[a + n];
+                            out[a + n] = alive[n] ? k_f : kDeadOutcome;
+                            if (!alive[n] || k_f == kDeadOutcome || marg[(a + n) * d] < 0.0) {
+                                alive[n] = 0;
+                                continue;
+                            }
+                            const cdouble* row = temp.data() + n * chir * d;
+                            for (size_t r = 0; r < chir; ++r) next.at2(n, r) = row[r * d + k_f];
+                        }
+                        s->env[t] = std::move(next);
+                        scale_rows_inplace(s->env[t], s->pol.scaling, alive);
+                    }
+                } catch (...) {
+                    errs[t] = std::current_exception();
+                }
+            });
+        }
+        for (auto& th : pool) th.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+        for (auto m : macs) s->macs += m;
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+uint64_t ref_sweep_macs(void* hs) { return static_cast<SiteSweep*>(hs)->macs; }
+void ref_sweep_end(void* hs) { delete static_cast<SiteSweep*>(hs); }
+}

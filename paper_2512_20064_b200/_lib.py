@@ -9,7 +9,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MPSG_LIB_PATH") or os.path.join(HERE, "libmpsg.so")
 
-ABI_VERSION = 3  # include/mpsg.h MPSG_ABI_VERSION
+ABI_VERSION = 4  # include/mpsg.h MPSG_ABI_VERSION
 MPSG_OK, MPSG_ERR_INTERNAL, MPSG_ERR_CONFIG, MPSG_ERR_NUMERIC, MPSG_ERR_IO, MPSG_ERR_CUDA = 0, 1, 2, 3, 4, 5
 
 _u64, _int, _dbl = C.c_uint64, C.c_int, C.c_double
@@ -38,7 +38,8 @@ class Stats(C.Structure):
                 ("seconds", _dbl), ("site_seconds", _pd), ("issued_mma_flops", _u64),
                 ("h2d_bytes", _u64), ("d2h_bytes", _u64), ("gemm_seconds", _dbl),
                 ("gemm_flops", _u64), ("kernel_launches", _u64), ("device_seconds", _dbl),
-                ("decay_trace", _pd), ("displacement_macs", _u64), ("measure_pipeline_ops", _u64)]
+                ("decay_trace", _pd), ("displacement_macs", _u64), ("measure_pipeline_ops", _u64),
+                ("near_boundary_draws", _u64)]
 
 
 # (name, restype, argtypes) for every entry point of include/mpsg.h

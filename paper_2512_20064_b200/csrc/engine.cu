@@ -52,6 +52,10 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
       throw Error(MPSG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
   } while (0)
 
+void check_launch(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(MPSG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
 static void config_check(bool ok, const std::string& msg) {
   if (!ok) throw Error(MPSG_ERR_CONFIG, msg);
 }
@@ -331,6 +335,7 @@ struct DevCtx {
   cudaEvent_t pass_end = nullptr;
   double* trace = nullptr;       // [M] sum |env_ref| per site (decay trace, lazy)
   unsigned long long* live = nullptr;  // [M] live samples measured per site (RunStats counters)
+  unsigned long long* near = nullptr;  // [M] draws within kBoundaryEps of a CDF boundary per site
 };
 
 }  // namespace mpsg
@@ -602,6 +607,7 @@ static void free_device(DevCtx& dc) {
   cudaFree(dc.err);
   cudaFree(dc.trace);
   cudaFree(dc.live);
+  cudaFree(dc.near);
   for (auto& s : dc.sites) cudaFree(s.inv_gamma);
   for (auto e : dc.ev) cudaEventDestroy(e);
   if (dc.pass_end) cudaEventDestroy(dc.pass_end);
@@ -760,6 +766,9 @@ static void set_site(mpsg_handle_s& h, uint64_t i, const void* gamma, bool is_de
   config_check(dtype == MPSG_F64 || dtype == MPSG_F32, "gamma dtype must be f64 or f32");
   // the left bond scales of site i derive from Lambda_{i-1}: sites are set in chain order
   config_check(i == 0 || h.site_set[i - 1], "sites must be set in increasing order");
+  // site i's Lambda fixes the left bond scales site i + 1 was compressed with
+  config_check(i + 1 == h.M || !h.site_set[i + 1], "site " + std::to_string(i) +
+                                                       " cannot be set again after site i + 1 was set");
   const size_t chir = h.bonds[i + 1];
   validate_lambda(lambda, chir);
   h.gr[i] = bond_scales(lambda, chir);
@@ -789,7 +798,7 @@ static void set_site(mpsg_handle_s& h, uint64_t i, const void* gamma, bool is_de
 // the sweep
 // ---------------------------------------------------------------------------------------------
 struct PassOut {
-  uint64_t macs = 0, wmacs = 0, issued = 0, launches = 0, dmacs = 0, pops = 0;
+  uint64_t macs = 0, wmacs = 0, issued = 0, launches = 0, dmacs = 0, pops = 0, near = 0;
   double gemm_s = 0.0, device_s = 0.0;
 };
 
@@ -1013,6 +1022,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       sa.scaling = h.policy.scaling;
       sa.mu = fuse_displace ? ln.mu : nullptr;
       sa.live = dc.live + i;
+      sa.near = forced ? nullptr : dc.near + i;
       sa.cinfo = cinfo;
       sa.perm = rc_pass ? ln.perm : nullptr;
       sa.rowk = rc ? ln.rowk : nullptr;
@@ -1110,7 +1120,9 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
       for (auto& ln : dc.lanes)
         if (!ln.mu) CUDA_OK(cudaMalloc(&ln.mu, sizeof(double2) * ln.cap * h.M));
     if (!dc.live) CUDA_OK(cudaMalloc(&dc.live, h.M * sizeof(unsigned long long)));
+    if (!dc.near) CUDA_OK(cudaMalloc(&dc.near, h.M * sizeof(unsigned long long)));
     CUDA_OK(cudaMemsetAsync(dc.live, 0, h.M * sizeof(unsigned long long), dc.stream));
+    CUDA_OK(cudaMemsetAsync(dc.near, 0, h.M * sizeof(unsigned long long), dc.stream));
     CUDA_OK(cudaStreamSynchronize(dc.stream));
     if (forced_host || marg_host)
       for (auto& ln : dc.lanes)
@@ -1193,6 +1205,8 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
       rr.po.wmacs += live[i] * static_cast<uint64_t>(dc.sites[i].width) * h.d;
       rr.po.pops += live[i] * h.d;
     }
+    CUDA_OK(cudaMemcpy(live.data(), dc.near, h.M * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < h.M; ++i) rr.po.near += live[i];
   } catch (...) {
     rr.err = std::current_exception();
   }
@@ -1209,6 +1223,12 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
   std::lock_guard<std::mutex> lk(h.mu);
   const auto t0 = std::chrono::steady_clock::now();
   const size_t nd = rows_dev ? 1 : h.devs.size();
+  // devices that get no samples this call must not contribute an earlier call's trace
+  for (auto& dc : h.devs)
+    if (dc.trace) {
+      CUDA_OK(cudaSetDevice(dc.device));
+      CUDA_OK(cudaMemset(dc.trace, 0, h.M * sizeof(double)));
+    }
   std::vector<RangeResult> rr(nd);
   std::vector<std::thread> th;
   for (size_t k = 0; k < nd; ++k) {
@@ -1230,6 +1250,7 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
   if (st) {
     st->contraction_macs = st->measure_weight_macs = st->issued_mma_flops = 0;
     st->displacement_macs = st->measure_pipeline_ops = 0;
+    st->near_boundary_draws = 0;
     st->kernel_launches = 0;
     st->gemm_seconds = 0.0;
     st->device_seconds = 0.0;
@@ -1238,6 +1259,7 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
       st->measure_weight_macs += r.po.wmacs;
       st->displacement_macs += r.po.dmacs;
       st->measure_pipeline_ops += r.po.pops;
+      st->near_boundary_draws += r.po.near;
       st->issued_mma_flops += r.po.issued;
       st->kernel_launches += r.po.launches;
       st->gemm_seconds = std::max(st->gemm_seconds, r.po.gemm_s);  // devices run concurrently
@@ -1274,6 +1296,16 @@ static void sample_impl(mpsg_handle_s& h, uint64_t seed, uint64_t first, uint64_
   }
 }
 
+// Teacher-forced outcomes index temp: every entry must be an outcome (< d) or the dead sentinel.
+static void check_forced(const mpsg_handle_s& h, const uint8_t* forced, uint64_t count) {
+  const uint64_t n = count * h.M;
+  for (uint64_t j = 0; j < n; ++j)
+    if (forced[j] >= h.d && forced[j] != kDead)
+      throw Error(MPSG_ERR_CONFIG, "forced outcome " + std::to_string(forced[j]) + " at (sample " +
+                                       std::to_string(j / h.M) + ", site " + std::to_string(j % h.M) +
+                                       ") is neither < d nor the dead sentinel 0xFF");
+}
+
 void handle_chain(mpsg_handle h, uint64_t& m, uint64_t& d, std::vector<uint64_t>& bonds,
                   std::vector<const double*>& lambdas) {
   config_check(h->finished, "state not finished");
@@ -1283,6 +1315,8 @@ void handle_chain(mpsg_handle h, uint64_t& m, uint64_t& d, std::vector<uint64_t>
   lambdas.clear();
   for (auto& l : h->lambda) lambdas.push_back(l.data());
 }
+
+int handle_tp_size(mpsg_handle h) { return h ? h->tp : 1; }
 
 }  // namespace mpsg
 
@@ -1559,6 +1593,7 @@ int mpsg_marginals(mpsg_handle h, uint64_t first, uint64_t count, const uint8_t*
   return guarded([&] {
     config_check(h != nullptr && forced != nullptr && marg != nullptr, "null argument");
     config_check(count >= 1, "count must be >= 1");
+    check_forced(*h, forced, count);
     std::vector<uint8_t> rows(count * h->M);
     sample_impl(*h, 0, first, count, rows.data(), nullptr, forced, marg, nullptr);
   });
@@ -1578,6 +1613,7 @@ int mpsg_marginals_displaced(mpsg_handle h, uint64_t first, uint64_t count, cons
   return guarded([&] {
     config_check(h != nullptr && forced != nullptr && marg != nullptr && mu != nullptr, "null argument");
     config_check(count >= 1, "count must be >= 1");
+    check_forced(*h, forced, count);
     std::vector<uint8_t> rows(count * h->M);
     sample_impl(*h, 0, first, count, rows.data(), nullptr, forced, marg, nullptr, mu);
   });

@@ -274,6 +274,10 @@ int mpsg_save_file(mpsg_handle h, const char* path, int storage) {
   try {
     if (!h || !path) throw IoFail(MPSG_ERR_CONFIG, "null argument");
     scalar_bytes(storage);  // rejects tf32 (mps_io.cpp:171)
+    // a tensor-parallel handle holds one column shard of every site: saving it would write the
+    // other ranks' columns as zeros under a valid checksum
+    if (mpsg::handle_tp_size(h) > 1)
+      throw IoFail(MPSG_ERR_CONFIG, "mpsg_save_file: a tensor-parallel handle holds only its column shard");
     uint64_t num_sites = 0, phys_dim = 0;
     std::vector<uint64_t> bonds;
     std::vector<const double*> lambda;

@@ -420,7 +420,7 @@ static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, 
   auto kern = site_gemm_3m_kernel<kSplit, kMax, kEpiWarps, kQuad, kGlo, kSlice>;
   using Cf = Cfg3M<kSplit, kGlo>;
   constexpr int kCl = kQuad ? 4 : 2;
-  static int max_clusters = 0;
+  static PerDevice clusters;  // per device: smem opt-in + occupancy query
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(128 + 32 * kEpiWarps);
   cfg.dynamicSmemBytes = Cf::kSmem;
@@ -432,14 +432,20 @@ static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (!max_clusters) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem);
-    cfg.gridDim = dim3(kCl);
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
-      max_clusters = 148 / kCl;  // 4-CTA clusters: 33 on a B200 (132 SMs)
-  }
+  const int max_clusters = clusters.get([&] {
+    check_launch(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem),
+                 "site_gemm_3m_kernel smem opt-in");
+    cudaLaunchConfig_t q = cfg;
+    q.gridDim = dim3(kCl);
+    int mc = 0;
+    if (cudaOccupancyMaxActiveClusters(&mc, kern, &q) != cudaSuccess || mc < 1) {
+      cudaGetLastError();
+      mc = 148 / kCl;  // 4-CTA clusters: 33 on a B200 (132 SMs)
+    }
+    return mc;
+  });
   cfg.gridDim = dim3(kCl * std::max(1, std::min(max_clusters, grid / kCl)));
-  cudaLaunchKernelEx(&cfg, kern, tma_env64, tma_g, a);
+  check_launch(cudaLaunchKernelEx(&cfg, kern, tma_env64, tma_g, a), "site_gemm_3m_kernel");
 }
 
 template <bool kSplit, bool kMax>

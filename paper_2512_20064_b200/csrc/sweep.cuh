@@ -15,7 +15,34 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 namespace mpsg {
+
+// One-time setup per (call site, device).  The dynamic-shared-memory opt-in
+// (cudaFuncSetAttribute), occupancy queries and __constant__ tables are properties of a device's
+// context, and a multi-device handle drives its devices from concurrent host threads, so every
+// such cache is keyed by the current device and guarded by a mutex.
+constexpr int kMaxDevices = 64;
+struct PerDevice {
+  std::mutex mu;
+  int value[kMaxDevices] = {};
+  bool set[kMaxDevices] = {};
+  template <typename F>
+  int get(F&& init) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = kMaxDevices - 1;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!set[dev]) {
+      value[dev] = init();
+      set[dev] = true;
+    }
+    return value[dev];
+  }
+};
+// Raises the engine's MPSG_ERR_CUDA error when a launch (or a launch attribute) failed.
+void check_launch(cudaError_t e, const char* what);
 
 constexpr int kBM = 128;  // samples per tile (UMMA M)
 constexpr int kBN = 128;  // complex output columns per tile (UMMA N per real plane)
@@ -31,6 +58,9 @@ constexpr uint64_t kMeasureStream = 0x6d656173ull;  // rng.hpp:19
 // part).  Products stay far from fp32 overflow (|t| <= 2^14 * K).
 constexpr int kEnvExp = 14;
 constexpr uint8_t kDead = 0xFF;                      // sampler.hpp:17
+// Parity rule: a draw within this distance of an interior CDF boundary cum_k (k < d - 1) may flip
+// outcome under any rounding difference; such draws are counted on the device (mpsg_stats).
+constexpr double kBoundaryEps = 1e-6;
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
@@ -126,6 +156,8 @@ struct SelectArgs {
   const double2* mu;        // [rows][num_sites] or null
   const float2* cinfo;      // site column info (wl_r = cinfo[r].y) for the displaced weights
   unsigned long long* live; // optional: += number of live samples measured at this site (RunStats)
+  unsigned long long* near; // optional: += number of draws within kBoundaryEps of an interior CDF
+                            // boundary at this site (the north star's "counted and reported" rule)
   // slice-recompute path: row n holds sample perm[n] of the pass (null: identity); with rowk set the
   // kernel records (outcome or d = dead next, scale) per row and counts the buckets instead of
   // writing the next environment (the slice GEMM does)

@@ -261,12 +261,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 template <bool kSplit>
 static void launch_gemm_t(const CUtensorMap& tma_env, const CUtensorMap& tma_g,
                           const SiteGemmArgs& a, int grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(site_gemm_kernel<kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         GemmCfg<kSplit>::kSmem);
-    attr = true;
-  }
+  static PerDevice attr;
+  attr.get([] {
+    check_launch(cudaFuncSetAttribute(site_gemm_kernel<kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      GemmCfg<kSplit>::kSmem), "site_gemm_kernel smem opt-in");
+    return 1;
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGemmThreads);
@@ -279,7 +279,7 @@ static void launch_gemm_t(const CUtensorMap& tma_env, const CUtensorMap& tma_g,
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, site_gemm_kernel<kSplit>, tma_env, tma_g, a);
+  check_launch(cudaLaunchKernelEx(&cfg, site_gemm_kernel<kSplit>, tma_env, tma_g, a), "site_gemm_kernel");
 }
 
 void launch_site_gemm(bool split, const CUtensorMap& tma_env, const CUtensorMap& tma_g,
@@ -514,12 +514,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 template <bool kSplit>
 static void launch_gemm_pair_t(const CUtensorMap& tma_env, const CUtensorMap& tma_g64,
                                const SiteGemmArgs& a, int grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(site_gemm_pair_kernel<kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         PairCfg<kSplit>::kSmem);
-    attr = true;
-  }
+  static PerDevice attr;
+  attr.get([] {
+    check_launch(cudaFuncSetAttribute(site_gemm_pair_kernel<kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      PairCfg<kSplit>::kSmem), "site_gemm_pair_kernel smem opt-in");
+    return 1;
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGemmThreads);
@@ -532,7 +532,7 @@ static void launch_gemm_pair_t(const CUtensorMap& tma_env, const CUtensorMap& tm
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, site_gemm_pair_kernel<kSplit>, tma_env, tma_g64, a);
+  check_launch(cudaLaunchKernelEx(&cfg, site_gemm_pair_kernel<kSplit>, tma_env, tma_g64, a), "site_gemm_pair_kernel");
 }
 
 void launch_site_gemm_pair(bool split, const CUtensorMap& tma_env, const CUtensorMap& tma_g64,
@@ -552,16 +552,18 @@ void launch_site_gemm_pair(bool split, const CUtensorMap& tma_env, const CUtenso
 // of the generator).
 // ============================================================================================
 // c_fact[a][b] = sqrt(a! / b!) / (a - b)! for b <= a <= 64 (the closed-form factors of L and U)
+// (a __constant__ symbol exists once per device: the table is uploaded to every device it runs on)
 __constant__ double c_fact[65][65];
-static bool g_fact_ready = false;
 static void ensure_fact_table() {
-  if (g_fact_ready) return;
-  static double h[65][65];
-  for (int a = 0; a <= 64; ++a)
-    for (int b = 0; b <= 64; ++b)
-      h[a][b] = b <= a ? std::exp(0.5 * (std::lgamma(a + 1.0) - std::lgamma(b + 1.0)) - std::lgamma(a - b + 1.0)) : 0.0;
-  cudaMemcpyToSymbol(c_fact, h, sizeof(h));
-  g_fact_ready = true;
+  static PerDevice ready;
+  ready.get([] {
+    static double h[65][65];
+    for (int a = 0; a <= 64; ++a)
+      for (int b = 0; b <= 64; ++b)
+        h[a][b] = b <= a ? std::exp(0.5 * (std::lgamma(a + 1.0) - std::lgamma(b + 1.0)) - std::lgamma(a - b + 1.0)) : 0.0;
+    check_launch(cudaMemcpyToSymbol(c_fact, h, sizeof(h)), "displacement factorial table upload");
+    return 1;
+  });
 }
 
 __device__ __forceinline__ double2 displacement_element(double mr, double mi, int a, int c) {
@@ -767,13 +769,16 @@ __device__ int select_displaced(const SelectArgs& a, int n, int lane, const floa
     const double draw = keyed_uniform(a.seed, kMeasureStream, a.first + n, a.site);
     double cum = 0.0;
     kk = 0;
+    bool near = false;
 #pragma unroll
     for (int k = 0; k < MAXD; ++k) {  // sampler.cpp:100-106
       if (k >= d) break;
       cum += ws[k] / total;
       if (draw > cum) ++kk;
+      near |= k + 1 < d && fabs(draw - cum) < kBoundaryEps;
     }
     if (kk >= d) kk = d - 1;  // :107
+    if (near && a.near != nullptr && lane == 0) atomicAdd(a.near, 1ull);
   }
   float mx = 0.f;
 #pragma unroll
@@ -854,11 +859,14 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
         const double draw = keyed_uniform(a.seed, kMeasureStream, a.first + sidx, a.site);
         double cum = 0.0;
         kk = 0;
+        bool near = false;  // the draw lies within kBoundaryEps of an interior CDF boundary
         for (int k = 0; k < a.d; ++k) {  // sampler.cpp:100-106: strict '>', no early break
           cum += weight(k) / total;
           if (draw > cum) ++kk;
+          near |= k + 1 < a.d && fabs(draw - cum) < kBoundaryEps;
         }
         if (kk >= a.d) kk = a.d - 1;  // :107
+        if (near && a.near != nullptr && lane == 0) atomicAdd(a.near, 1ull);
       }
       if (kk != kDead) {
         outcome = kk;

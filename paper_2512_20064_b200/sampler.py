@@ -251,6 +251,7 @@ class RunStats:
     issued_mma_flops: int = 0
     displacement_macs: int = 0
     measure_pipeline_ops: int = 0
+    near_boundary_draws: int = 0   # draws within 1e-6 of an interior CDF boundary (device-counted)
     h2d_bytes: int = 0
     d2h_bytes: int = 0
 
@@ -288,14 +289,15 @@ class GpuSampler:
     def from_file(cls, path: str, policy: Optional[PrecisionPolicy] = None, mode: Mode = Mode.AUTO,
                   devices: Optional[Sequence[int]] = None, pass_samples: int = 0,
                   record_site_times: bool = False, host_stream_slots: int = 0,
-                  scheme: Scheme = Scheme.AUTO, slice: Slice = Slice.AUTO) -> "GpuSampler":
+                  scheme: Scheme = Scheme.AUTO, slice: Slice = Slice.AUTO,
+                  record_decay_trace: bool = False) -> "GpuSampler":
         """Build the device state from an MPSB file (the reference's format, mps_io.hpp:17-24)."""
         L = _lib.lib()
         policy = policy or PrecisionPolicy()
         policy.validate()
         pol = _lib.Policy(int(policy.compute), int(policy.storage), int(policy.scaling))
-        opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), 1, 0, int(host_stream_slots), 0,
-                           int(scheme), int(slice))
+        opt = _lib.Options(int(mode), int(pass_samples), int(record_site_times), 1, 0, int(host_stream_slots),
+                           int(record_decay_trace), int(scheme), int(slice))
         devs, nd = cls._devices(devices)
         h = C.c_void_p()
         _check(L.mpsg_create_from_file(path.encode(), C.byref(pol), C.byref(opt), devs, nd, C.byref(h)))
@@ -371,6 +373,7 @@ class GpuSampler:
             stats.issued_mma_flops += st.issued_mma_flops
             stats.displacement_macs += st.displacement_macs
             stats.measure_pipeline_ops += st.measure_pipeline_ops
+            stats.near_boundary_draws += st.near_boundary_draws
             stats.h2d_bytes += st.h2d_bytes
             stats.d2h_bytes += st.d2h_bytes
             stats.site_seconds = list(np.asarray(stats.site_seconds or np.zeros(self.num_sites)) + site_s)
@@ -629,17 +632,29 @@ def run_data_parallel(mps_path: str, plan: BatchPlan, p1: int, opts: SamplerOpti
                       devices: Optional[Sequence[int]] = None) -> ParallelResult:
     """run_data_parallel (parallel.cpp:240-330) on p1 B200s of this process: the file is read once
     (streamed site by site), every device keeps the compressed chain, each sweeps a contiguous
-    share of the samples.  Outcomes equal the serial ones (keyed RNG)."""
+    share of the samples.  Outcomes equal the serial ones (keyed RNG).
+
+    The site transform is applied per sample as in the reference's DP worker (parallel.cpp:291-308);
+    the decay trace is recorded when asked.  A bond schedule raises ConfigError, as the C++ adapter
+    does (include/mpsg_mpsamp.hpp): the file-backed state is built site by site on the device and
+    is not truncated here -- truncate with apply_schedule and use sample_batch."""
     if p1 < 1:
         raise ConfigError("data parallel needs p1 >= 1")
+    if opts.schedule is not None:
+        raise ConfigError("file-backed executors do not apply bond schedules; use apply_schedule + sample_batch")
+    if opts.site_transform is not None and not isinstance(opts.site_transform, Displacement):
+        raise ConfigError("site transforms other than the GBS Displacement are not supported by the GPU sweep")
     opts.policy.validate()
     plan = BatchPlan(plan.total_samples, plan.macro_batch, plan.micro_batch)
     plan.normalize()
     devs = list(devices) if devices else list(range(p1))
-    smp = GpuSampler.from_file(mps_path, opts.policy, opts.mode, devs, opts.pass_samples, scheme=opts.scheme)
+    smp = GpuSampler.from_file(mps_path, opts.policy, opts.mode, devs, opts.pass_samples, scheme=opts.scheme,
+                               record_decay_trace=opts.record_decay_trace)
     try:
         st = RunStats()
-        rows = smp.sample(0, plan.total_samples, opts.seed, stats=st)
+        mu = (opts.site_transform.amplitudes(0, plan.total_samples, smp.num_sites)
+              if opts.site_transform is not None else None)
+        rows = smp.sample(0, plan.total_samples, opts.seed, stats=st, mu=mu)
     finally:
         smp.close()
     st.dead_samples = int((rows[:, -1] == DEAD_OUTCOME).sum())

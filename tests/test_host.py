@@ -40,7 +40,7 @@ def test_library_is_sm100a_only():
 
 def test_abi_basics_without_gpu():
     L = _lib.lib()
-    assert L.mpsg_abi_version() == _lib.ABI_VERSION == 3
+    assert L.mpsg_abi_version() == _lib.ABI_VERSION == 4
     if L.mpsg_device_count() == 0:
         # no CPU fallback: a compute call fails loudly with the CUDA code
         out = np.empty(4)
@@ -273,6 +273,17 @@ def test_dynamic_bond_schedule_spec_examples():
         k, lam = s.per_site_chi[b], lams[b - 1]
         assert (lam[k:] ** 2).sum() <= eps[b] + 1e-18
         assert k == 1 or (lam[k - 1:] ** 2).sum() > eps[b]
+
+
+def test_file_executors_reject_schedule_and_foreign_transforms(tmp_path):
+    """run_serial / run_data_parallel (file-backed) raise ConfigError for a bond schedule -- the
+    file state is built site by site on the device and not truncated, as in the C++ adapter -- and
+    for site transforms other than the GBS Displacement, before touching a device."""
+    opts = P.SamplerOptions(schedule=P.BondSchedule([1, 2, 1], 2))
+    with pytest.raises(P.ConfigError):
+        P.sampler.run_data_parallel(str(tmp_path / "none.mpsb"), P.BatchPlan(10), 1, opts)
+    with pytest.raises(P.ConfigError):
+        P.sampler.run_serial(str(tmp_path / "none.mpsb"), P.BatchPlan(10), P.SamplerOptions(site_transform=len))
 
 
 def test_displacement_transform_host_checks():

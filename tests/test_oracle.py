@@ -127,6 +127,36 @@ def test_live_cross_check_random():
                                    rs.marginals_forced(forced), rtol=1e-12, atol=1e-15)
 
 
+def test_site_streaming_sweep_equals_reference_sampler(gold):
+    """oracle.RefSiteSweep (the reference's per-site body driven one site at a time, threaded over
+    sample chunks; used for the full-length c2 / c3 parity) reproduces the reference's own
+    sample_micro_serial rows and teacher-forced marginals bit for bit, for F64 and F32, free-running
+    and teacher-forced, and its near-boundary flags equal a direct count on the same CDFs."""
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    for name in ("c1", "c1b"):
+        mps = O.load_npz_mps(np.load(os.path.join(gold, f"{name}.npz")))
+        rs = O.RefState(mps)
+        for compute in (O.F64, O.F32):
+            rows = rs.sample_range(0, 1000, 7, compute=compute, threads=4)
+            marg = rs.marginals_forced(rows, compute=compute)
+            sw = O.RefSiteSweep(0, 1000, 7, compute=compute, threads=3, eps=1e-3)
+            tf = O.RefSiteSweep(0, 1000, 7, compute=compute, threads=2)
+            for i in range(mps.num_sites):
+                o, mg, near = sw.site(i, mps.gammas[i], mps.lambdas[i])
+                assert np.array_equal(o, rows[:, i]), (name, compute, i)
+                np.testing.assert_array_equal(mg, marg[:, i])
+                u = np.array([O.orc().orc_uniform(7, O.MEASURE_STREAM, n, i) for n in range(1000)])
+                cum = np.cumsum(mg, axis=1)[:, :-1]
+                want = (np.abs(cum - u[:, None]) < 1e-3).any(axis=1) & (mg[:, 0] >= 0)
+                assert np.array_equal(near, want), (name, i)
+                o2, mg2, _ = tf.site(i, mps.gammas[i], mps.lambdas[i], forced=rows[:, i])
+                assert np.array_equal(o2, rows[:, i])
+                np.testing.assert_array_equal(mg2, marg[:, i])
+            assert sw.contraction_macs == 1000 * sum(mps.bond_dims[i] * mps.bond_dims[i + 1] * mps.phys_dim
+                                                     for i in range(mps.num_sites))
+
+
 # ---- GBS displacement (SPEC.md gbs-ops; the reference's src/gbs.cpp is absent) ---------------
 def test_displacement_closed_form_kats():
     """expm_displacement: mu = 0 -> identity; n = 2 closed form; the closed form
