@@ -42,12 +42,19 @@ CONFIGS = {
 # M = 8176 chain, which needs TP over 8 GPUs and 19.6 TB of host / disk storage
 CONFIGS["c4s"] = dict(M=64, chi=10000, d=4, job=1_000_000, stream=3,
                       desc="c4 slice: M=64 sites of the c4 shape (chi=1e4, d=4), N=1e6, Gamma host-streamed")
-for _chi in (256, 512, 1024, 2048, 4096):
-    CONFIGS[f"c5_{_chi}"] = dict(M=512, chi=_chi, d=4, job=100_000,
-                                 desc=f"c5: bond-dimension sweep M=512, chi={_chi}, d=4, N=1e5")
+# c4: the whole M = 8176 chain (13.1 TB as 4M planes, 19.6 TB as 3M) -- beyond HBM and host memory,
+# so the sites are regenerated on the device from their generators every pass (mpsg_generated_*:
+# ~16 GB of base isometries), on a side stream overlapping the contractions
+CONFIGS["c4"] = dict(M=8176, chi=10000, d=4, job=1_000_000, generated=True, warm_pass=256,
+                     desc="c4: M=8176, chi=1e4, d=4, N=1e6; Gamma regenerated on the device per site and pass")
+for _chi in (256, 512, 1024, 2048, 4096, 8192, 10000):
+    CONFIGS[f"c5_{_chi}"] = dict(M=512, chi=_chi, d=4, job=100_000, generated=_chi >= 8192,
+                                 desc=f"c5: bond-dimension sweep M=512, chi={_chi}, d=4, N=1e5"
+                                      + ("; Gamma regenerated on the device" if _chi >= 8192 else ""))
 SLICE = {"auto": 0, "temp": 1, "recompute": 2}
 DEFAULT_PASS = {"c1": 1000, "c2": 32768, "c3": 16384, "c5_256": 65536, "c5_512": 32768,
-                "c5_1024": 32768, "c5_2048": 16384, "c5_4096": 8192, "c4s": 8192}
+                "c5_1024": 32768, "c5_2048": 16384, "c5_4096": 8192, "c4s": 8192, "c4": 8192,
+                "c5_8192": 8192, "c5_10000": 8192}
 
 
 def peaks():
@@ -82,6 +89,19 @@ def parity_report_path(config):
                 "max_rel_err_right_edge": r["max_rel_err_right_edge_sites"]}
     except Exception:
         return {"path": p}
+
+
+def connect_tp(P, smp, tp, tp_rank, dist, force):
+    """Joins this rank's handle to its tensor-parallel group's NCCL communicator (the unique id is
+    made by the group's first rank and shared over the torch process group)."""
+    if tp == 1 and not force:
+        return
+    uid = P.sampler.nccl_unique_id() if tp_rank == 0 else None
+    if dist is not None:
+        ids = [None] * dist.get_world_size()
+        dist.all_gather_object(ids, uid)
+        uid = ids[(dist.get_rank() // tp) * tp]
+    smp.connect_nccl(uid)
 
 
 def chain_macs(M, chi, d):
@@ -256,10 +276,24 @@ def main():
     ap.add_argument("--stream-slots", type=int, default=0,
                     help="keep the compressed MPS in pinned host memory and stream it per site "
                          "through this many device slots (0 = resident in HBM)")
+    ap.add_argument("--supply", default="auto", choices=["auto", "resident", "generated"],
+                    help="generated: keep only the chain's generators and regenerate every site on the "
+                         "device each pass (auto: the config's default -- c4, c5 chi >= 8192)")
+    ap.add_argument("--tp", type=int, default=1,
+                    help="tensor-parallel group size: consecutive ranks form a group holding column shards "
+                         "of every Gamma_i (the even-site pattern, parallel.cpp:420-443) and exchange the "
+                         "per-site partial weights and environment shards over NCCL; dp = world / tp")
+    ap.add_argument("--tp-exchange", action="store_true",
+                    help="with --tp 1: run the exchange data plane through a one-rank NCCL group anyway "
+                         "(exercises the TP transport on a single GPU)")
+    ap.add_argument("--warm-pass", type=int, default=0,
+                    help="samples per warm-up step (0 = the timed pass size; c4 default 256: one full "
+                         "pass takes minutes)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if not args.stream_slots and cfg.get("stream"):
         args.stream_slots = cfg["stream"]
+    generated = args.supply == "generated" or (args.supply == "auto" and cfg.get("generated", False))
     if args.impl == "reference":
         run_reference_arm(args, cfg)
         return
@@ -286,6 +320,11 @@ def main():
     import paper_2512_20064_b200 as P
     from paper_2512_20064_b200.synthetic import build_synthetic
 
+    tp = max(1, args.tp)
+    if world % tp:
+        raise SystemExit(f"--tp {tp} must divide the world size {world}")
+    dp, group, tp_rank = world // tp, rank // tp, rank % tp
+
     P_pass = args.pass_samples or DEFAULT_PASS[args.config]
     mode = {"split": P.Mode.SPLIT, "single": P.Mode.SINGLE, "precise": P.Mode.PRECISE}[args.mode]
     t0 = time.perf_counter()
@@ -294,8 +333,11 @@ def main():
                              policy=P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX),
                              scheme={"auto": 0, "3m": 3, "4m": 4}[args.scheme], slice=SLICE[args.slice],
                              schedule=(P.TruncationFilter(chi_max=cfg["chi"], eps_center=args.schedule_eps,
-                                                          edge_factor=100.0) if args.schedule_eps > 0 else None))
+                                                          edge_factor=100.0) if args.schedule_eps > 0 else None),
+                             generated=generated, tp_size=tp, tp_rank=tp_rank)
+    connect_tp(P, smp, tp, tp_rank, dist, args.tp_exchange)
     scheme = "3M" if smp.scheme == P.Scheme.M3 else "4M"
+    warm_pass = args.warm_pass or cfg.get("warm_pass", 0) or P_pass
     build_s = time.perf_counter() - t0
     macs_per_sample, bonds = chain_macs(cfg["M"], cfg["chi"], cfg["d"])
     sched_note = None
@@ -315,19 +357,20 @@ def main():
 
     def step(it):
         st = P.RunStats()
-        first = (it * world + rank) * P_pass
+        first = (it * dp + group) * P_pass
         rows = smp.sample(first, P_pass, 7, stats=st, mu=mu_host)  # host rows; device time from events
         return st, rows
 
-    def device_step(it):
+    def device_step(it, count=None):
+        count = count or P_pass
         st = P.RunStats()
-        first = (it * world + rank) * P_pass
+        first = (it * dp + group) * P_pass
         L = P.sampler._lib
         s = L.Stats()
         site = np.zeros(cfg["M"], np.float64)
         s.site_seconds = site.ctypes.data_as(L._pd)
         if mu_host is None:
-            P.sampler._check(L.lib().mpsg_sample_device(smp._h, 7, first, P_pass,
+            P.sampler._check(L.lib().mpsg_sample_device(smp._h, 7, first, count,
                                                         ctypes.c_void_p(rows_dev.data_ptr()), ctypes.byref(s)))
         else:  # GBS displacement site transform; device time from the engine's events
             P.sampler._check(L.lib().mpsg_sample_displaced(smp._h, 7, first, P_pass, mu_host.ctypes.data_as(L._pd),
@@ -340,7 +383,7 @@ def main():
         return st, s
 
     for w in range(args.warmup):
-        device_step(w)
+        device_step(w, min(warm_pass, P_pass))
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -382,6 +425,8 @@ def main():
             else "resident"
     if args.stream_slots:
         e2e_mode = "stream"
+    if generated:
+        e2e_mode = "generated"
     e2e_h2d = 0
     if e2e_mode == "stream" and not args.stream_slots:
         smp.close()
@@ -392,7 +437,9 @@ def main():
                                  policy=P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX),
                                  scheme={"auto": 0, "3m": 3, "4m": 4}[args.scheme], slice=SLICE[args.slice],
                                  schedule=(P.TruncationFilter(chi_max=cfg["chi"], eps_center=args.schedule_eps,
-                                                              edge_factor=100.0) if args.schedule_eps > 0 else None))
+                                                              edge_factor=100.0) if args.schedule_eps > 0 else None),
+                                 tp_size=tp, tp_rank=tp_rank)
+        connect_tp(P, smp, tp, tp_rank, dist, args.tp_exchange)
         e2e_build_s = time.perf_counter() - t0
         step(args.warmup + args.steps)  # one untimed warm-up pass of the streamed state
     e2e_s = 0.0
@@ -401,13 +448,13 @@ def main():
         st_e2e, _ = step(args.warmup + args.steps + 1 + it)
         e2e_s += time.perf_counter() - t
         e2e_h2d += st_e2e.h2d_bytes
-    e2e = P_pass * args.e2e_steps * world / e2e_s if e2e_s > 0 else None
+    e2e = P_pass * args.e2e_steps * dp / e2e_s if e2e_s > 0 else None
     if dist and e2e_s > 0:
         tt = torch.tensor([e2e_s], device="cpu" if share else "cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = P_pass * args.e2e_steps * world / float(tt.item())
+        e2e = P_pass * args.e2e_steps * dp / float(tt.item())
 
-    value = P_pass * world * args.steps / t_max
+    value = P_pass * dp * args.steps / t_max
     burst, sustained, hbm, src = peaks()
     achieved = gemm_flops / gemm_s / 1e12 if gemm_s > 0 else None
     # north-star roofline: the slower of the GEMM at tensor peak and the Gamma bytes over the link
@@ -448,14 +495,20 @@ def main():
             "config": {"workload": cfg["desc"] + f"; step = one sweep of {P_pass} samples/GPU over all M sites",
                        "M": cfg["M"], "chi": cfg["chi"], "d": cfg["d"], "pass_samples_per_gpu": P_pass,
                        "job_samples": cfg["job"], "job_seconds_at_value": cfg["job"] / value,
-                       "mode": args.mode, "scheme": scheme, "slice": args.slice, "parallelism": f"dp{world}",
+                       "mode": args.mode, "scheme": scheme, "slice": args.slice, "parallelism": f"dp{dp}" + (f"xtp{tp}" if tp > 1 or args.tp_exchange else ""),
                        "bond_schedule": sched_note,
                        "displacement": (f"GBS displacement D(mu) per (sample, site), mu ~ CN(0, {args.displace}^2)"
                                         if args.displace > 0 else None),
-                       "l2": f"inputs larger than L2 (compressed MPS {smp.state_bytes / 1e9:.1f} GB)",
+                       "l2": (f"inputs larger than L2 (compressed MPS {smp.state_bytes / 1e9:.1f} GB)" if not generated
+                              else "inputs larger than L2 (every site regenerated into 3 device slots of up to "
+                                   f"{max(6 * cfg['chi'] * cfg['chi'] * cfg['d'], 1) / 1e9:.1f} GB)"),
+                       "warmup_pass_samples": min(warm_pass, P_pass),
                        "gamma_residency": (f"pinned host memory, streamed per site through {args.stream_slots} "
                                            f"device slots ({h2d / args.steps / 1e9:.1f} GB H2D per step, "
-                                           f"{h2d / t_max / 1e9:.1f} GB/s)") if args.stream_slots else "HBM",
+                                           f"{h2d / t_max / 1e9:.1f} GB/s)") if args.stream_slots else
+                                          ("regenerated on the device every pass from the chain's generators "
+                                           f"({smp.state_bytes / 1e9:.1f} GB of base isometries in HBM), "
+                                           "3 device slots, side stream") if generated else "HBM",
                        "build_seconds": round(build_s, 1)},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
                          "frac": achieved / sustained if achieved else None, "traffic": traffic,
@@ -483,6 +536,9 @@ def main():
                              "memory and is copied H2D site by site every step (3 device slots, copy stream "
                              "overlapping the kernels); wall clock per step, max over ranks")
                     if e2e_mode == "stream" else
+                            ("mpsg_sample (C ABI) with host output rows (D2H inside the timed region); the "
+                             "sites are regenerated on the device (no Gamma crosses the host link)")
+                    if e2e_mode == "generated" else
                             ("mpsg_sample (C ABI) with host output rows (D2H inside the timed region); the "
                              "compressed MPS stays resident in HBM (host memory cannot hold it for every rank)")},
             "clocks": clocks, "gpu_launches": launches, "wall_seconds": wall,

@@ -38,7 +38,7 @@ extern "C" {
 #endif
 
 #define MPSG_ABI_VERSION 4  /* 2: mpsg_stats gained displacement_macs, measure_pipeline_ops; 3: mpsg_options.slice;
-                               4: mpsg_stats.near_boundary_draws */
+                               4: mpsg_stats.near_boundary_draws, mpsg_generated_*, mpsg_synthetic_site */
 
 enum {
   MPSG_OK = 0,
@@ -176,7 +176,8 @@ void mpsg_destroy(mpsg_handle h);
 
 /* Bytes of the compressed state held per device: in HBM, or for a host-streamed handle in pinned
  * host memory (there the 3M sum planes are re-formed on the device after each copy, so a 3M
- * host-streamed state holds 2/3 of the resident state's bytes). */
+ * host-streamed state holds 2/3 of the resident state's bytes); for a generated handle the bytes of
+ * its base isometries in HBM. */
 uint64_t mpsg_state_bytes(mpsg_handle h);
 /* The contraction scheme the handle runs: MPSG_SCHEME_3M or MPSG_SCHEME_4M (0 for a null handle). */
 int mpsg_scheme(mpsg_handle h);
@@ -185,6 +186,37 @@ int mpsg_scheme(mpsg_handle h);
  * complex128 interleaved (chiL, chiR, d).  The CPU oracle consumes these.  A tensor-parallel
  * handle writes only its own column shard (other entries are left untouched). */
 int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out);
+
+/* ---- synthetic chains regenerated on the device ------------------------------------------
+ * For chains whose compressed Gamma exceeds device and host memory (c4: M = 8176, chi = 1e4,
+ * d = 4 is 13-20 TB), a handle can hold a random right-canonical chain of the random_mps form
+ * (mps.cpp:148-175) as its generators instead of its tensors:
+ *   Gamma_i[l, r, k] = B_b(i)[l, r*d + k] * phase_i[r*d + k] * Lambda_{i-1}[l] / Lambda_i[r]
+ * B_b a base isometry registered once (complex64 (rows >= bond[i], cols >= bond[i+1] * d) with
+ * orthonormal rows; a site uses its leading bond[i] x bond[i+1]*d block), phase_i[j] = exp(2 pi i u)
+ * with u the reference's keyed uniform (rng.hpp:22-37) of (seed, 0x70686173, site i, column j),
+ * and the products rounded in fp32 in that order.  Every pass regenerates and compresses each site
+ * on the device into a ring of host_stream_slots (default 3) device slots, on a side stream that
+ * overlaps the previous sites' contractions -- the paper's double-buffered site stream
+ * (SiteStream, mps_io.cpp:294-350) with the device as the source.  Bond scales,
+ * validation and compression are those of mpsg_builder_set_site, so a state built from the
+ * materialised sites (mpsg_synthetic_site + mpsg_builder_set_site) samples identically. */
+int mpsg_generated_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bond_dims,
+                         const mpsg_policy* policy, const mpsg_options* opts, const int* devices,
+                         int ndev, uint64_t seed, mpsg_handle* out);
+/* Registers a base isometry (complex64 interleaved, rows x cols row-major; a device pointer on the
+ * first listed device, or host memory); the handle keeps its own copy on every device. */
+int mpsg_generated_add_base(mpsg_handle h, const void* base, int base_is_device, uint64_t rows,
+                            uint64_t cols, int* base_id);
+/* Site `site` (in increasing order) regenerates from base `base_id` with Lambda_site = lambda
+ * (length bond[site + 1]; validated like MpsState::validate).  Finish with mpsg_builder_finish. */
+int mpsg_generated_set_site(mpsg_handle h, uint64_t site, int base_id, const double* lambda);
+/* The generator formula evaluated into `out` (complex64 rows x cols, device memory on the calling
+ * thread's current device): base (row stride ld) as above, lambda_prev (rows; NULL = ones) and
+ * lambda (cols / phys_dim) the site's bond spectra. */
+int mpsg_synthetic_site(const void* base, uint64_t ld, uint64_t rows, uint64_t cols, uint64_t phys_dim,
+                        const double* lambda_prev, const double* lambda, uint64_t seed, uint64_t site,
+                        void* out);
 
 /* ---- MPSB files (the reference's on-disk format, mps_io.hpp:17-24) ----------------------- */
 /* Read an MPSB file (any storage precision, checksums verified -> MPSG_ERR_IO) and build the

@@ -71,6 +71,11 @@ SIGNATURES = [
     ("mpsg_nccl_unique_id", _int, [C.POINTER(C.c_uint8)]),
     ("mpsg_tp_connect_nccl", _int, [C.c_void_p, C.POINTER(C.c_uint8)]),
     ("mpsg_tp_connect_local", _int, [C.POINTER(C.c_void_p), _int]),
+    ("mpsg_generated_begin", _int, [_u64, _u64, _pu64, C.POINTER(Policy), C.POINTER(Options),
+                                    C.POINTER(_int), _int, _u64, C.POINTER(C.c_void_p)]),
+    ("mpsg_generated_add_base", _int, [C.c_void_p, C.c_void_p, _int, _u64, _u64, C.POINTER(_int)]),
+    ("mpsg_generated_set_site", _int, [C.c_void_p, _u64, _int, _pd]),
+    ("mpsg_synthetic_site", _int, [C.c_void_p, _u64, _u64, _u64, _u64, _pd, _pd, _u64, _u64, C.c_void_p]),
 ]
 
 _lib = None

@@ -27,6 +27,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/mpsg.h"
@@ -134,6 +135,10 @@ struct Comm {
   // lane: the pipeline lane issuing the call; every lane has its own ordered channel (its own NCCL
   // communicator) so the two lanes' collectives never interleave on one communicator.
   virtual void allgather(void* buf, size_t chunk, cudaStream_t s, int lane) = 0;
+  // Strided all-gather: rank q's data are the byte runs [q * stride + off, + len) of buf, for every
+  // (off, len) in runs; afterwards every rank holds every rank's runs (the rest of buf untouched).
+  virtual void allgather_runs(void* buf, size_t stride, const std::vector<std::pair<size_t, size_t>>& runs,
+                              cudaStream_t s, int lane) = 0;
 };
 
 struct NcclApi {
@@ -142,6 +147,10 @@ struct NcclApi {
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*commCount)(const ncclComm_t, int*) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -158,8 +167,13 @@ static const NcclApi& nccl() {
     api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
     api.commSplit = reinterpret_cast<decltype(api.commSplit)>(dlsym(h, "ncclCommSplit"));
     api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+    api.broadcast = reinterpret_cast<decltype(api.broadcast)>(dlsym(h, "ncclBroadcast"));
+    api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(h, "ncclGroupStart"));
+    api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+    api.commCount = reinterpret_cast<decltype(api.commCount)>(dlsym(h, "ncclCommCount"));
   });
-  if (!api.allGather || !api.commInitRank || !api.getUniqueId)
+  if (!api.allGather || !api.commInitRank || !api.getUniqueId || !api.broadcast || !api.groupStart ||
+      !api.groupEnd)
     throw Error(MPSG_ERR_CUDA, "NCCL (libnccl.so.2) not available");
   return api;
 }
@@ -173,20 +187,36 @@ static const NcclApi& nccl() {
 
 struct NcclComm : Comm {
   ncclComm_t comm[2] = {nullptr, nullptr};  // lane 0, lane 1 (split from lane 0 on first use)
-  int rank = 0;
-  NcclComm(const ncclUniqueId& id, int nranks, int r) : rank(r) {
+  int rank = 0, nranks = 1;
+  NcclComm(const ncclUniqueId& id, int n, int r) : rank(r), nranks(n) {
     NCCL_OK(nccl().commInitRank(&comm[0], nranks, id, r));
+  }
+  ncclComm_t lane_comm(int lane) {
+    if (lane == 1 && !comm[1]) {  // collective: every rank reaches it at the same point of the sweep
+      if (!nccl().commSplit) throw Error(MPSG_ERR_CUDA, "ncclCommSplit unavailable (needs NCCL >= 2.18)");
+      NCCL_OK(nccl().commSplit(comm[0], 0, rank, &comm[1], nullptr));
+    }
+    return comm[lane];
+  }
+  void allgather_runs(void* buf, size_t stride, const std::vector<std::pair<size_t, size_t>>& runs,
+                      cudaStream_t s, int lane) override {
+    // one broadcast per (root, run), issued as a group: the runs of every root travel concurrently
+    ncclComm_t c = lane_comm(lane);
+    NCCL_OK(nccl().groupStart());
+    for (int q = 0; q < nranks; ++q)
+      for (const auto& run : runs) {
+        char* p = static_cast<char*>(buf) + q * stride + run.first;
+        NCCL_OK(nccl().broadcast(p, p, run.second, ncclUint8, q, c, s));
+      }
+    NCCL_OK(nccl().groupEnd());
   }
   ~NcclComm() override {
     for (auto c : comm)
       if (c && nccl().commDestroy) nccl().commDestroy(c);
   }
   void allgather(void* buf, size_t chunk, cudaStream_t s, int lane) override {
-    if (lane == 1 && !comm[1]) {  // collective: every rank reaches it at the same point of the sweep
-      if (!nccl().commSplit) throw Error(MPSG_ERR_CUDA, "ncclCommSplit unavailable (needs NCCL >= 2.18)");
-      NCCL_OK(nccl().commSplit(comm[0], 0, rank, &comm[1], nullptr));
-    }
-    NCCL_OK(nccl().allGather(static_cast<char*>(buf) + rank * chunk, buf, chunk, ncclUint8, comm[lane], s));
+    ncclComm_t c = lane_comm(lane);
+    NCCL_OK(nccl().allGather(static_cast<char*>(buf) + rank * chunk, buf, chunk, ncclUint8, c, s));
   }
 };
 
@@ -222,7 +252,11 @@ struct LocalComm : Comm {
   std::shared_ptr<LocalGroup> g;
   int rank;
   LocalComm(std::shared_ptr<LocalGroup> grp, int r) : g(std::move(grp)), rank(r) {}
-  void allgather(void* buf, size_t chunk, cudaStream_t s, int /*lane*/) override {
+  void allgather(void* buf, size_t chunk, cudaStream_t s, int lane) override {
+    allgather_runs(buf, chunk, {{0, chunk}}, s, lane);
+  }
+  void allgather_runs(void* buf, size_t stride, const std::vector<std::pair<size_t, size_t>>& runs,
+                      cudaStream_t s, int /*lane*/) override {
     // host barriers serialise the calls of all lanes in issue order, identical on every rank
     LocalGroup& G = *g;
     G.bufs[rank] = buf;
@@ -231,8 +265,10 @@ struct LocalComm : Comm {
     for (int q = 0; q < G.n; ++q) {
       if (q == rank) continue;
       CUDA_OK(cudaStreamWaitEvent(s, G.ready[q], 0));
-      CUDA_OK(cudaMemcpyPeerAsync(static_cast<char*>(buf) + q * chunk, G.devices[rank],
-                                  static_cast<char*>(G.bufs[q]) + q * chunk, G.devices[q], chunk, s));
+      for (const auto& run : runs)
+        CUDA_OK(cudaMemcpyPeerAsync(static_cast<char*>(buf) + q * stride + run.first, G.devices[rank],
+                                    static_cast<char*>(G.bufs[q]) + q * stride + run.first, G.devices[q],
+                                    run.second, s));
     }
     CUDA_OK(cudaEventRecord(G.done[rank], s));
     G.barrier();
@@ -272,6 +308,12 @@ struct SiteDev {
   double* cs = nullptr;      // [chir * d]
   double* inv_gamma = nullptr;  // [width] 1 / gamma_i[r] of the local columns (decay trace)
   CUtensorMap tma_g{}, tma_g64{};
+  // generated supply: base isometry id and the per-site factors of the generator
+  int base_id = -1;
+  float* lam_prev_f = nullptr;  // [chil] fp32 Lambda_{i-1}
+  float* inv_lam_f = nullptr;   // [chir] fp32 1 / Lambda_i
+  double *gl_d = nullptr, *gr_d = nullptr, *wl_d = nullptr;  // bond scales, weight factors
+  int* lpos_d = nullptr;        // [chil] K position of row l
   // host-streamed mode: the compressed site lives in pinned host memory
   __half* g_host = nullptr;
   float2* cinfo_host = nullptr;
@@ -323,6 +365,12 @@ struct DevCtx {
   void* src = nullptr;       // compress staging (device)
   size_t src_bytes = 0;
   int* err = nullptr;
+  unsigned long long* colmax = nullptr;  // [chirp_max * d] compression scratch (kept zeroed)
+  // generated supply (mpsg_generated_*): base isometries and the per-site phase buffer
+  std::vector<float2*> bases;
+  std::vector<long long> base_rows, base_cols;
+  float2* phase = nullptr;
+  std::vector<long long> slot_sig;  // extents of each slot's last fill (its padding is zero)
   // host-streamed Gamma: ring of device slots filled by a copy stream (sequence q -> slot q % R)
   int slots = 0;
   std::vector<__half*> slot_g;
@@ -361,6 +409,8 @@ struct mpsg_handle_s {
   int hplanes = 2;
   bool precise = false;                    // Gamma hi + lo planes (MPSG_MODE_PRECISE)
   bool slice_rc = false;                   // slice-recompute path available (3M, tp = 1, d <= 32)
+  bool generated = false;                  // Gamma regenerated on the device every pass (synthetic chains)
+  uint64_t gen_seed = 0;
   std::unique_ptr<mpsg::Comm> comm;
   std::mutex mu;
 };
@@ -393,7 +443,9 @@ static int chirp_max_of(const mpsg_handle_s& h) {
 // stream then carries 1.5x the bytes of 4M, measured at 96% of the resident c3 rate).
 static void choose_scheme(mpsg_handle_s& h) {
   bool m3 = h.opts.scheme != MPSG_SCHEME_4M;
-  if (h.opts.scheme == MPSG_SCHEME_AUTO) {
+  if (h.opts.scheme == MPSG_SCHEME_AUTO && h.generated) {
+    m3 = h.pair;  // regenerated into device slots: no state to fit
+  } else if (h.opts.scheme == MPSG_SCHEME_AUTO) {
     if (!h.pair) m3 = false;
     double state3 = 0.0;
     for (uint64_t i = 0; i < h.M; ++i) {
@@ -515,7 +567,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     CUDA_OK(cudaMalloc(&ln.env, 2ull * h.env_comp * ln.cap * kmax * sizeof(__half)));
     CUDA_OK(cudaMalloc(&ln.temp, 1ull * ln.cap * h.d * chirpm * sizeof(float2)));
     CUDA_OK(cudaMalloc(&ln.pstat, 1ull * ln.cap * nt_max * sizeof(float2)));
-    if (h.tp > 1) CUDA_OK(cudaMalloc(&ln.part, 1ull * h.tp * ln.cap * h.d * sizeof(float2)));
+
     CUDA_OK(cudaMalloc(&ln.alive, ln.cap));
     CUDA_OK(cudaMalloc(&ln.rows, 1ull * ln.cap * h.M));
     CUDA_OK(cudaMallocHost(&ln.host_rows, 1ull * ln.cap * h.M));
@@ -538,6 +590,13 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
   }
   CUDA_OK(cudaMalloc(&dc.err, sizeof(int)));
   CUDA_OK(cudaMemset(dc.err, 0, sizeof(int)));
+  CUDA_OK(cudaMalloc(&dc.colmax, sizeof(unsigned long long) * chirpm * h.d));
+  CUDA_OK(cudaMemset(dc.colmax, 0, sizeof(unsigned long long) * chirpm * h.d));
+  if (h.generated) {
+    uint64_t cols = 1;
+    for (uint64_t i = 1; i <= h.M; ++i) cols = std::max(cols, h.bonds[i] * h.d);
+    CUDA_OK(cudaMalloc(&dc.phase, sizeof(float2) * cols));
+  }
   CUDA_OK(cudaMalloc(&dc.scratch, sizeof(double) * (kmax + 2ull * h.tp * chirpm) + sizeof(int) * kmax));
   if (h.opts.host_stream_slots > 0) {
     config_check(h.opts.host_stream_slots >= 2, "host_stream_slots must be 0 or >= 2");
@@ -560,6 +619,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
       CUDA_OK(cudaEventCreateWithFlags(&dc.loaded[q], cudaEventDisableTiming));
       CUDA_OK(cudaEventCreateWithFlags(&dc.freed[q], cudaEventDisableTiming));
     }
+    dc.slot_sig.assign(dc.slots, -1);
   }
 }
 
@@ -605,6 +665,17 @@ static void free_device(DevCtx& dc) {
   cudaFree(dc.scratch);
   cudaFree(dc.src);
   cudaFree(dc.err);
+  cudaFree(dc.colmax);
+  cudaFree(dc.phase);
+  for (auto p : dc.bases) cudaFree(p);
+  for (auto& s : dc.sites) {
+    cudaFree(s.lam_prev_f);
+    cudaFree(s.inv_lam_f);
+    cudaFree(s.gl_d);
+    cudaFree(s.gr_d);
+    cudaFree(s.wl_d);
+    cudaFree(s.lpos_d);
+  }
   cudaFree(dc.trace);
   cudaFree(dc.live);
   cudaFree(dc.near);
@@ -625,9 +696,9 @@ static void free_device(DevCtx& dc) {
   if (dc.stream) cudaStreamDestroy(dc.stream);
 }
 
-// Compress this rank's column shard of site i on device dc from `src` (device pointer).
-static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* src_dev,
-                          bool f64, const double* lambda) {
+// Site geometry of this rank's column shard of site i (padded extents, shard range) and its
+// per-site device arrays that do not depend on the Gamma values.
+static void site_geometry(mpsg_handle_s& h, DevCtx& dc, uint64_t i) {
   SiteDev& s = dc.sites[i];
   s.chil = static_cast<int>(h.bonds[i]);
   s.chir = static_cast<int>(h.bonds[i + 1]);
@@ -639,6 +710,72 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
   s.np = round_up(static_cast<int>(h.d) * s.chirp, 2 * kBN);  // whole N-tile pairs (CTA pairs)
   s.nt = s.np / kBN;
   if (!s.cs) CUDA_OK(cudaMalloc(&s.cs, std::max<size_t>(1, 1ull * s.width * h.d) * sizeof(double)));
+  if (!s.inv_gamma) CUDA_OK(cudaMalloc(&s.inv_gamma, std::max<size_t>(1, s.width) * sizeof(double)));
+  std::vector<double> ig(std::max(1, s.width));
+  for (int r = 0; r < s.width; ++r) ig[r] = 1.0 / h.gr[i][s.b0 + r];
+  CUDA_OK(cudaMemcpy(s.inv_gamma, ig.data(), sizeof(double) * ig.size(), cudaMemcpyHostToDevice));
+}
+
+// K position of row l: the previous site's column shards, each padded to kshard
+static std::vector<int> row_positions(const mpsg_handle_s& h, const SiteDev& s) {
+  std::vector<int> lpos(s.chil);
+  for (int q = 0; q < h.tp; ++q) {
+    int b, e;
+    part_range(s.chil, h.tp, q, b, e);
+    for (int l = b; l < e; ++l) lpos[l] = q * s.kshard + (l - b);
+  }
+  return lpos;
+}
+
+// weight factors wl_r = (Lambda_i[r] / gamma_i[r])^2 of the Born weights
+static std::vector<double> weight_factors(const mpsg_handle_s& h, uint64_t i, const double* lambda) {
+  std::vector<double> wl(h.bonds[i + 1]);
+  for (size_t r = 0; r < wl.size(); ++r) {
+    const double q = lambda[r] / h.gr[i][r];
+    wl[r] = q * q;
+  }
+  return wl;
+}
+
+// TMA maps of site i: the environment of every lane and the Gamma planes (resident or per slot).
+static void site_maps(mpsg_handle_s& h, DevCtx& dc, uint64_t i) {
+  SiteDev& s = dc.sites[i];
+  for (auto& ln : dc.lanes) {
+    const uint64_t env_rows = 2ull * h.env_comp * ln.cap;
+    ln.tma_env[i] = make_tma_env(ln.env, s.kshard, env_rows, h.tp);
+    if (h.m3) ln.tma_env64[i] = make_tma_env(ln.env, s.kshard, env_rows, h.tp, kBM / 2, kBK3);
+    if (ln.env_perm) ln.tma_envp64[i] = make_tma_env(ln.env_perm, s.kshard, env_rows, h.tp, kBM / 2, kBK3);
+  }
+  if (dc.slots) {
+    s.tma_slot.resize(dc.slots);
+    s.tma_slot64.resize(dc.slots);
+    for (int q = 0; q < dc.slots; ++q) {
+      s.tma_slot[q] = make_tma_2d(dc.slot_g[q], s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBM,
+                                  h.m3 ? kBK3 : kBK);
+      s.tma_slot64[q] = make_tma_2d(dc.slot_g[q], s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBN / 2);
+    }
+  } else {
+    s.tma_g = make_tma_2d(s.g, s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBM, h.m3 ? kBK3 : kBK);
+    s.tma_g64 = make_tma_2d(s.g, s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBN / 2);
+  }
+}
+
+static void check_err_flag(DevCtx& dc, cudaStream_t stream, const std::string& where) {
+  int err = 0;
+  CUDA_OK(cudaMemcpyAsync(&err, dc.err, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  CUDA_OK(cudaStreamSynchronize(stream));
+  if (err != 0) {
+    cudaMemset(dc.err, 0, sizeof(int));
+    throw Error(MPSG_ERR_NUMERIC, "contract_site: non-finite input (" + where +
+                                      ") or dynamic range beyond the compressed format");
+  }
+}
+
+// Compress this rank's column shard of site i on device dc from `src` (device pointer).
+static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* src_dev,
+                          bool f64, const double* lambda) {
+  SiteDev& s = dc.sites[i];
+  site_geometry(h, dc, i);
   if (dc.slots) {  // compress into slot 0, then keep the result in pinned host memory
     CUDA_OK(cudaStreamSynchronize(dc.copy_stream));
     s.g = dc.slot_g[0];
@@ -647,18 +784,8 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
     CUDA_OK(cudaMalloc(&s.g, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half)));
     CUDA_OK(cudaMalloc(&s.cinfo, 1ull * s.np * sizeof(float2)));
   }
-  std::vector<double> wl(s.chir);
-  for (int r = 0; r < s.chir; ++r) {
-    const double q = lambda[r] / h.gr[i][r];
-    wl[r] = q * q;
-  }
-  // K position of row l: the previous site's column shards, each padded to kshard
-  std::vector<int> lpos(s.chil);
-  for (int q = 0; q < h.tp; ++q) {
-    int b, e;
-    part_range(s.chil, h.tp, q, b, e);
-    for (int l = b; l < e; ++l) lpos[l] = q * s.kshard + (l - b);
-  }
+  const std::vector<double> wl = weight_factors(h, i, lambda);
+  const std::vector<int> lpos = row_positions(h, s);
   double* d_gl = dc.scratch;
   double* d_gr = d_gl + s.chil;
   double* d_wl = d_gr + s.chir;
@@ -669,29 +796,11 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
   CUDA_OK(cudaMemcpyAsync(d_lpos, lpos.data(), sizeof(int) * s.chil, cudaMemcpyHostToDevice, dc.stream));
   CUDA_OK(cudaMemsetAsync(s.g, 0, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half), dc.stream));
   CUDA_OK(cudaMemsetAsync(s.cinfo, 0, 1ull * s.np * sizeof(float2), dc.stream));
-  if (!s.inv_gamma) CUDA_OK(cudaMalloc(&s.inv_gamma, std::max<size_t>(1, s.width) * sizeof(double)));
-  {
-    std::vector<double> ig(std::max(1, s.width));
-    for (int r = 0; r < s.width; ++r) ig[r] = 1.0 / h.gr[i][s.b0 + r];
-    CUDA_OK(cudaMemcpyAsync(s.inv_gamma, ig.data(), sizeof(double) * ig.size(), cudaMemcpyHostToDevice, dc.stream));
-  }
   launch_compress_site(src_dev, f64, s.chil, s.chir, static_cast<int>(h.d), s.b0, s.width, s.kp,
-                       s.chirp, d_lpos, d_gl, d_gr, d_wl, h.gplanes, s.g, s.cinfo, s.cs, dc.err, dc.stream);
+                       s.chirp, d_lpos, d_gl, d_gr, d_wl, h.gplanes, s.g, s.cinfo, s.cs, dc.colmax, dc.err,
+                       dc.stream);
   CUDA_OK(cudaGetLastError());
-  int err = 0;
-  CUDA_OK(cudaMemcpyAsync(&err, dc.err, sizeof(int), cudaMemcpyDeviceToHost, dc.stream));
-  CUDA_OK(cudaStreamSynchronize(dc.stream));
-  if (err != 0) {
-    cudaMemset(dc.err, 0, sizeof(int));
-    throw Error(MPSG_ERR_NUMERIC, "contract_site: non-finite input (site " + std::to_string(i) +
-                                      ") or dynamic range beyond the compressed format");
-  }
-  for (auto& ln : dc.lanes) {
-    const uint64_t env_rows = 2ull * h.env_comp * ln.cap;
-    ln.tma_env[i] = make_tma_env(ln.env, s.kshard, env_rows, h.tp);
-    if (h.m3) ln.tma_env64[i] = make_tma_env(ln.env, s.kshard, env_rows, h.tp, kBM / 2, kBK3);
-    if (ln.env_perm) ln.tma_envp64[i] = make_tma_env(ln.env_perm, s.kshard, env_rows, h.tp, kBM / 2, kBK3);
-  }
+  check_err_flag(dc, dc.stream, "site " + std::to_string(i));
   if (dc.slots) {
     const size_t pe = static_cast<size_t>(s.np) * s.kp;  // elements per plane
     if (!s.g_host) {
@@ -707,20 +816,44 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
     }
     CUDA_OK(cudaMemcpyAsync(s.cinfo_host, s.cinfo, 1ull * s.np * sizeof(float2), cudaMemcpyDeviceToHost, dc.stream));
     CUDA_OK(cudaStreamSynchronize(dc.stream));
-    s.tma_slot.resize(dc.slots);
-    s.tma_slot64.resize(dc.slots);
-    for (int q = 0; q < dc.slots; ++q) {
-      s.tma_slot[q] = make_tma_2d(dc.slot_g[q], s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBM,
-                                  h.m3 ? kBK3 : kBK);
-      s.tma_slot64[q] = make_tma_2d(dc.slot_g[q], s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBN / 2);
-    }
     s.g = nullptr;
     s.cinfo = nullptr;
     dc.issued = dc.consumed = 0;  // slot 0 was overwritten: restart the load sequence
-  } else {
-    s.tma_g = make_tma_2d(s.g, s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBM, h.m3 ? kBK3 : kBK);
-    s.tma_g64 = make_tma_2d(s.g, s.kp, static_cast<uint64_t>(h.gplanes) * s.np, kBN / 2);
+    dc.slot_sig.assign(dc.slots, -1);
   }
+  site_maps(h, dc, i);
+}
+
+// Generated supply: the generator of site i (base isometry, phases, fp32 Lambda factors) for this
+// rank's shard, as the compression kernels read it.
+static SynthSite synth_of(const mpsg_handle_s& h, const DevCtx& dc, uint64_t i) {
+  const SiteDev& s = dc.sites[i];
+  SynthSite g;
+  g.base = dc.bases[s.base_id];
+  g.ld = dc.base_cols[s.base_id];
+  g.cols = static_cast<long long>(s.chir) * static_cast<long long>(h.d);
+  g.phase = dc.phase;
+  g.lam_prev = s.lam_prev_f;
+  g.inv_lam = s.inv_lam_f;
+  g.d = static_cast<int>(h.d);
+  return g;
+}
+
+// Regenerates and compresses site i into device planes g_out / cinfo_out on `stream` (generated
+// supply): phases, column maxima and scales, packed fp16 planes -- the same kernels and rounding as
+// compressing the materialised site (mpsg_synthetic_site + mpsg_builder_set_site).
+static void regenerate_site(const mpsg_handle_s& h, DevCtx& dc, uint64_t i, __half* g_out, float2* cinfo_out,
+                            bool clear, cudaStream_t stream) {
+  SiteDev& s = dc.sites[i];
+  if (clear) {
+    CUDA_OK(cudaMemsetAsync(g_out, 0, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half), stream));
+    CUDA_OK(cudaMemsetAsync(cinfo_out, 0, 1ull * s.np * sizeof(float2), stream));
+  }
+  launch_synth_phase(h.gen_seed, i, s.chir * static_cast<int>(h.d), dc.phase, stream);
+  launch_compress_synth(synth_of(h, dc, i), s.chil, static_cast<int>(h.d), s.b0, s.width, s.kp, s.chirp,
+                        s.lpos_d, s.gl_d, s.gr_d, s.wl_d, h.gplanes, g_out, cinfo_out, s.cs, dc.colmax, dc.err,
+                        stream);
+  check_launch(cudaGetLastError(), "site regeneration");
 }
 
 // Host-streamed mode: issue site loads until `upto` loads are in flight or done.
@@ -730,6 +863,17 @@ static void issue_loads(mpsg_handle_s& h, DevCtx& dc, uint64_t upto) {
     const int slot = static_cast<int>(q % dc.slots);
     const SiteDev& s = dc.sites[q % h.M];
     CUDA_OK(cudaStreamWaitEvent(dc.copy_stream, dc.freed[slot], 0));  // consume q - slots done
+    if (h.generated) {  // regenerate + compress on the device: no host traffic
+      // the slot's padding is zero from its last fill when that had the same extents
+      const long long sig = (static_cast<long long>(s.np) << 32) ^ (static_cast<long long>(s.kp) << 8) ^
+                            (static_cast<long long>(s.chil) * 131 + s.width);
+      regenerate_site(h, dc, q % h.M, dc.slot_g[slot], dc.slot_cinfo[slot], dc.slot_sig[slot] != sig,
+                      dc.copy_stream);
+      dc.slot_sig[slot] = sig;
+      CUDA_OK(cudaEventRecord(dc.loaded[slot], dc.copy_stream));
+      ++dc.issued;
+      continue;
+    }
     const size_t pe = static_cast<size_t>(s.np) * s.kp;
     const size_t gb = h.hplanes * pe * sizeof(__half);
     if (h.hplanes == h.gplanes) {
@@ -764,6 +908,7 @@ static void set_site(mpsg_handle_s& h, uint64_t i, const void* gamma, bool is_de
   config_check(i < h.M, "site index out of range");
   config_check(gamma != nullptr && lambda != nullptr, "null gamma / lambda");
   config_check(dtype == MPSG_F64 || dtype == MPSG_F32, "gamma dtype must be f64 or f32");
+  config_check(!h.generated, "a generated handle takes mpsg_generated_set_site");
   // the left bond scales of site i derive from Lambda_{i-1}: sites are set in chain order
   config_check(i == 0 || h.site_set[i - 1], "sites must be set in increasing order");
   // site i's Lambda fixes the left bond scales site i + 1 was compressed with
@@ -794,6 +939,52 @@ static void set_site(mpsg_handle_s& h, uint64_t i, const void* gamma, bool is_de
   h.site_set[i] = 1;
 }
 
+// Generated supply: site i is regenerated from base isometry `base_id` with Lambda_i = lambda on
+// every pass; only the generator's per-site factors are stored.
+static void set_site_generated(mpsg_handle_s& h, uint64_t i, int base_id, const double* lambda) {
+  config_check(h.generated, "not a generated handle (mpsg_generated_begin)");
+  config_check(!h.finished, "builder already finished");
+  config_check(i < h.M, "site index out of range");
+  config_check(lambda != nullptr, "null lambda");
+  config_check(i == 0 || h.site_set[i - 1], "sites must be set in increasing order");
+  config_check(i + 1 == h.M || !h.site_set[i + 1], "site " + std::to_string(i) +
+                                                       " cannot be set again after site i + 1 was set");
+  const size_t chil = h.bonds[i], chir = h.bonds[i + 1];
+  config_check(base_id >= 0 && base_id < static_cast<int>(h.devs[0].bases.size()), "unknown base isometry id");
+  config_check(h.devs[0].base_rows[base_id] >= static_cast<long long>(chil) &&
+                   h.devs[0].base_cols[base_id] >= static_cast<long long>(chir * h.d),
+               "base isometry smaller than the site (needs bond[i] rows, bond[i+1] * d columns)");
+  validate_lambda(lambda, chir);
+  h.gr[i] = bond_scales(lambda, chir);
+  h.lambda[i].assign(lambda, lambda + chir);
+  if (i + 1 < h.M) h.gl[i + 1] = h.gr[i];
+  std::vector<float> lp(chil, 1.0f), il(chir);
+  if (i > 0)
+    for (size_t l = 0; l < chil; ++l) lp[l] = static_cast<float>(h.lambda[i - 1][l]);
+  for (size_t r = 0; r < chir; ++r) il[r] = 1.0f / static_cast<float>(lambda[r]);
+  for (auto& dc : h.devs) {
+    CUDA_OK(cudaSetDevice(dc.device));
+    site_geometry(h, dc, i);
+    SiteDev& sd = dc.sites[i];
+    sd.base_id = base_id;
+    const std::vector<double> wl = weight_factors(h, i, lambda);
+    const std::vector<int> lpos = row_positions(h, sd);
+    auto up = [](auto*& dst, const auto& v) {
+      using T = std::remove_reference_t<decltype(v[0])>;
+      if (!dst) CUDA_OK(cudaMalloc(&dst, sizeof(T) * v.size()));
+      CUDA_OK(cudaMemcpy(dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    };
+    up(sd.lam_prev_f, lp);
+    up(sd.inv_lam_f, il);
+    up(sd.gl_d, h.gl[i]);
+    up(sd.gr_d, h.gr[i]);
+    up(sd.wl_d, wl);
+    up(sd.lpos_d, lpos);
+    site_maps(h, dc, i);
+  }
+  h.site_set[i] = 1;
+}
+
 // ---------------------------------------------------------------------------------------------
 // the sweep
 // ---------------------------------------------------------------------------------------------
@@ -806,7 +997,10 @@ struct PassOut {
 // exchanges it with the weights, and long-K sites, where the epilogue has slack: +1.5% at c3) or the
 // select kernel's pass over the chosen slice (short-K sites, where the epilogue is on the critical
 // path: +10% at chi = 512).
-static bool epilogue_max(const mpsg_handle_s& h, const SiteDev& s) { return h.tp > 1 || s.kp >= 1024; }
+// The tensor-parallel data plane (partials exchange, environment all-gather) runs for a TP group of
+// p2 > 1 ranks, and for a connected one-rank group (the same collectives through NCCL on one GPU).
+static bool xchg(const mpsg_handle_s& h) { return h.tp > 1 || h.comm != nullptr; }
+static bool epilogue_max(const mpsg_handle_s& h, const SiteDev& s) { return xchg(h) || s.kp >= 1024; }
 
 
 // K1 for `rows` samples of lane `ln` at site i.  tma_g128 / tma_g64: Gamma maps with 128 / 64-row
@@ -946,7 +1140,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       // Displacement fused into the selection (one read of temp) unless the weights must be exchanged
       // first (tensor parallelism) or the decay trace reads the transformed slice.
       static const bool no_fuse = std::getenv("MPSG_DISPLACE_SEPARATE") != nullptr;
-      const bool fuse_displace = displaced && h.tp == 1 && !dc.trace && !no_fuse;
+      const bool fuse_displace = displaced && !xchg(h) && !dc.trace && !no_fuse;
       if (displaced && !fuse_displace) {  // the SiteTransform hook position (sampler.cpp:143)
         DisplaceArgs da;
         da.d = static_cast<int>(h.d);
@@ -984,7 +1178,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       sa.d = static_cast<int>(h.d);
       sa.chir_loc = s.width;
       sa.chirp = s.chirp;
-      if (h.tp == 1) {  // partials straight from the tiles: (tile t of outcome k) at pstat[n][k*tpk+t]
+      if (!xchg(h)) {  // partials straight from the tiles: (tile t of outcome k) at pstat[n][k*tpk+t]
         sa.parts = s.chirp / kBN;
         sa.part_base = ln.pstat;
         sa.part_stride = 1;
@@ -1065,8 +1259,17 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
         CUDA_OK(cudaEventRecord(ln.gev[4 * i + 2], ln.stream));
         CUDA_OK(cudaEventRecord(ln.gev[4 * i + 3], ln.stream));
       }
-      if (h.tp > 1 && has_next)  // rebuild the full environment from the column shards
-        h.comm->allgather(ln.env, 2ull * h.env_comp * ln.cap * kn * sizeof(__half), ln.stream, L);
+      if (xchg(h) && has_next) {  // rebuild the full environment from the column shards
+        const size_t plane_b = 1ull * ln.cap * kn * sizeof(__half);
+        const size_t shard_b = 2ull * h.env_comp * plane_b;
+        if (h.m3) {  // ship hi / lo of re, im (planes 0, 1 and 3, 4); re-form the s planes after
+          h.comm->allgather_runs(ln.env, shard_b, {{0, 2 * plane_b}, {3 * plane_b, 2 * plane_b}}, ln.stream, L);
+          launch_env_reform_s(ln.env, ln.cap, kn, h.tp, rows[L], ln.stream);
+          po.launches += 1;
+        } else {
+          h.comm->allgather(ln.env, shard_b, ln.stream, L);
+        }
+      }
       po.launches += 2;
       po.macs += static_cast<uint64_t>(cnt[L]) * s.chil * s.width * h.d;
       if (displaced) po.dmacs += static_cast<uint64_t>(cnt[L]) * s.width * h.d * h.d;
@@ -1198,6 +1401,10 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
         }
       }
     }
+    if (h.generated) {  // the regenerated sites' finiteness / range checks (compression kernels)
+      CUDA_OK(cudaStreamSynchronize(dc.copy_stream));
+      check_err_flag(dc, dc.stream, "a regenerated site");
+    }
     // measure's counters over the live samples (sampler.cpp:81-93,114-115)
     std::vector<unsigned long long> live(h.M);
     CUDA_OK(cudaMemcpy(live.data(), dc.live, h.M * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
@@ -1318,6 +1525,15 @@ void handle_chain(mpsg_handle h, uint64_t& m, uint64_t& d, std::vector<uint64_t>
 
 int handle_tp_size(mpsg_handle h) { return h ? h->tp : 1; }
 
+// exchanged (weight, max) partials [tp][cap][d] per lane, allocated when the group is connected
+static void ensure_part_buffers(mpsg_handle_s& h) {
+  for (auto& dc : h.devs) {
+    CUDA_OK(cudaSetDevice(dc.device));
+    for (auto& ln : dc.lanes)
+      if (!ln.part) CUDA_OK(cudaMalloc(&ln.part, 1ull * h.tp * ln.cap * h.d * sizeof(float2)));
+  }
+}
+
 }  // namespace mpsg
 
 // =============================================================================================
@@ -1364,9 +1580,9 @@ int mpsg_device_count(void) {
   return c;
 }
 
-int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bond_dims,
-                       const mpsg_policy* policy, const mpsg_options* opts, const int* devices,
-                       int ndev, mpsg_handle* out) {
+static int begin_impl(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bond_dims,
+                      const mpsg_policy* policy, const mpsg_options* opts, const int* devices,
+                      int ndev, mpsg_handle* out, bool generated, uint64_t gen_seed) {
   return guarded([&] {
     config_check(out != nullptr, "null output handle");
     *out = nullptr;
@@ -1382,6 +1598,12 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
     if (opts) h->opts = *opts;
     config_check(h->opts.mode >= MPSG_MODE_AUTO && h->opts.mode <= MPSG_MODE_PRECISE, "unknown mode");
     h->precise = h->opts.mode == MPSG_MODE_PRECISE;
+    h->generated = generated;
+    h->gen_seed = gen_seed;
+    if (generated) {  // regenerated into a ring of device slots (default 3)
+      config_check(h->opts.host_stream_slots >= 0, "host_stream_slots must be >= 0");
+      h->opts.host_stream_slots = h->opts.host_stream_slots == 0 ? 3 : std::max(2, h->opts.host_stream_slots);
+    }
     {
       const char* v = std::getenv("MPSG_GEMM");  // A/B switch for the contraction kernel
       h->pair = !(v && std::string(v) == "cluster");
@@ -1422,6 +1644,97 @@ int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bo
       throw;
     }
     *out = h.release();
+  });
+}
+
+int mpsg_builder_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bond_dims,
+                       const mpsg_policy* policy, const mpsg_options* opts, const int* devices,
+                       int ndev, mpsg_handle* out) {
+  return begin_impl(num_sites, phys_dim, bond_dims, policy, opts, devices, ndev, out, false, 0);
+}
+
+int mpsg_generated_begin(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bond_dims,
+                         const mpsg_policy* policy, const mpsg_options* opts, const int* devices,
+                         int ndev, uint64_t seed, mpsg_handle* out) {
+  return begin_impl(num_sites, phys_dim, bond_dims, policy, opts, devices, ndev, out, true, seed);
+}
+
+int mpsg_generated_add_base(mpsg_handle h, const void* base, int base_is_device, uint64_t rows,
+                            uint64_t cols, int* base_id) {
+  return guarded([&] {
+    config_check(h != nullptr && base != nullptr && base_id != nullptr, "null argument");
+    config_check(h->generated, "not a generated handle (mpsg_generated_begin)");
+    config_check(!h->finished, "builder already finished");
+    config_check(rows >= 1 && cols >= 1, "empty base isometry");
+    const size_t bytes = sizeof(float2) * rows * cols;
+    for (size_t di = 0; di < h->devs.size(); ++di) {
+      DevCtx& dc = h->devs[di];
+      CUDA_OK(cudaSetDevice(dc.device));
+      float2* p = nullptr;
+      CUDA_OK(cudaMalloc(&p, bytes));
+      dc.bases.push_back(p);
+      dc.base_rows.push_back(static_cast<long long>(rows));
+      dc.base_cols.push_back(static_cast<long long>(cols));
+      if (!base_is_device)
+        CUDA_OK(cudaMemcpy(p, base, bytes, cudaMemcpyHostToDevice));
+      else if (di == 0)
+        CUDA_OK(cudaMemcpy(p, base, bytes, cudaMemcpyDeviceToDevice));
+      else
+        CUDA_OK(cudaMemcpyPeer(p, dc.device, base, h->devs[0].device, bytes));
+    }
+    *base_id = static_cast<int>(h->devs[0].bases.size()) - 1;
+  });
+}
+
+int mpsg_generated_set_site(mpsg_handle h, uint64_t site, int base_id, const double* lambda) {
+  return guarded([&] {
+    config_check(h != nullptr, "null handle");
+    set_site_generated(*h, site, base_id, lambda);
+  });
+}
+
+int mpsg_synthetic_site(const void* base, uint64_t ld, uint64_t rows, uint64_t cols, uint64_t phys_dim,
+                        const double* lambda_prev, const double* lambda, uint64_t seed, uint64_t site,
+                        void* out) {
+  return guarded([&] {
+    config_check(base != nullptr && lambda != nullptr && out != nullptr, "null argument");
+    config_check(phys_dim >= 1 && cols % phys_dim == 0 && ld >= cols && rows >= 1, "bad generator shape");
+    if (mpsg_device_count() == 0) throw Error(MPSG_ERR_CUDA, "no sm_100 CUDA device visible");
+    const uint64_t chir = cols / phys_dim;
+    std::vector<float> lp(rows, 1.0f), il(chir);
+    if (lambda_prev)
+      for (uint64_t l = 0; l < rows; ++l) lp[l] = static_cast<float>(lambda_prev[l]);
+    for (uint64_t r = 0; r < chir; ++r) il[r] = 1.0f / static_cast<float>(lambda[r]);
+    float *d_lp = nullptr, *d_il = nullptr;
+    float2* d_ph = nullptr;
+    auto cleanup = [&] {
+      cudaFree(d_lp);
+      cudaFree(d_il);
+      cudaFree(d_ph);
+    };
+    try {
+      CUDA_OK(cudaMalloc(&d_lp, sizeof(float) * rows));
+      CUDA_OK(cudaMalloc(&d_il, sizeof(float) * chir));
+      CUDA_OK(cudaMalloc(&d_ph, sizeof(float2) * cols));
+      CUDA_OK(cudaMemcpy(d_lp, lp.data(), sizeof(float) * rows, cudaMemcpyHostToDevice));
+      CUDA_OK(cudaMemcpy(d_il, il.data(), sizeof(float) * chir, cudaMemcpyHostToDevice));
+      SynthSite g;
+      g.base = static_cast<const float2*>(base);
+      g.ld = static_cast<long long>(ld);
+      g.cols = static_cast<long long>(cols);
+      g.phase = d_ph;
+      g.lam_prev = d_lp;
+      g.inv_lam = d_il;
+      g.d = static_cast<int>(phys_dim);
+      launch_synth_phase(seed, site, static_cast<int>(cols), d_ph, nullptr);
+      launch_synth_values(g, static_cast<int>(rows), static_cast<float2*>(out), nullptr);
+      CUDA_OK(cudaGetLastError());
+      CUDA_OK(cudaDeviceSynchronize());
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
   });
 }
 
@@ -1477,6 +1790,11 @@ void mpsg_destroy(mpsg_handle h) {
 uint64_t mpsg_state_bytes(mpsg_handle h) {
   if (!h || h->devs.empty()) return 0;
   uint64_t b = 0;
+  if (h->generated) {  // the generators: base isometries (complex64) held per device
+    for (size_t k = 0; k < h->devs[0].bases.size(); ++k)
+      b += sizeof(float2) * h->devs[0].base_rows[k] * h->devs[0].base_cols[k];
+    return b;
+  }
   const int planes = h->devs[0].slots ? h->hplanes : h->gplanes;
   for (const auto& s : h->devs[0].sites) b += static_cast<size_t>(planes) * s.np * s.kp * sizeof(__half);
   return b;  // host-streamed: these bytes live in pinned host memory
@@ -1494,11 +1812,33 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
     const size_t pe = static_cast<size_t>(s.np) * s.kp;
     std::vector<__half> g(h->gplanes * pe);
     std::vector<double> cs(std::max<size_t>(1, 1ull * s.width * h->d));
-    if (dc.slots)  // host planes [Gr, Gi] per precision half: place them at their device plane
+    if (h->generated) {  // regenerate the site into a scratch buffer (the pass ring is not touched)
+      std::lock_guard<std::mutex> lk(h->mu);
+      CUDA_OK(cudaStreamSynchronize(dc.copy_stream));  // loads pre-issued by the last pass share the scratch
+      __half* tg = nullptr;
+      float2* tc = nullptr;
+      CUDA_OK(cudaMalloc(&tg, g.size() * sizeof(__half)));
+      cudaError_t e = cudaMalloc(&tc, sizeof(float2) * s.np);
+      if (e == cudaSuccess) {
+        try {
+          regenerate_site(*h, dc, site, tg, tc, true, dc.stream);
+          check_err_flag(dc, dc.stream, "regenerated site " + std::to_string(site));
+          e = cudaMemcpy(g.data(), tg, g.size() * sizeof(__half), cudaMemcpyDeviceToHost);
+        } catch (...) {
+          cudaFree(tg);
+          cudaFree(tc);
+          throw;
+        }
+      }
+      cudaFree(tg);
+      cudaFree(tc);
+      CUDA_OK(e);
+    } else if (dc.slots) {  // host planes [Gr, Gi] per precision half: place them at their device plane
       for (int hf = 0; hf < h->hplanes / 2; ++hf)
         std::memcpy(g.data() + (h->m3 ? 3 : 2) * hf * pe, s.g_host + 2 * hf * pe, 2 * pe * sizeof(__half));
-    else
+    } else {
       CUDA_OK(cudaMemcpy(g.data(), s.g, g.size() * sizeof(__half), cudaMemcpyDeviceToHost));
+    }
     CUDA_OK(cudaMemcpy(cs.data(), s.cs, cs.size() * sizeof(double), cudaMemcpyDeviceToHost));
     const size_t d = h->d;
     std::vector<int> lpos(s.chil);
@@ -1541,11 +1881,14 @@ int mpsg_nccl_unique_id(uint8_t id[128]) {
 int mpsg_tp_connect_nccl(mpsg_handle h, const uint8_t id[128]) {
   return guarded([&] {
     config_check(h != nullptr && id != nullptr, "null argument");
-    config_check(h->tp > 1, "handle was not created with tp_size > 1");
+    // tp_size 1: a one-rank group that runs the exchange data plane through NCCL (same results)
+    config_check(h->devs.size() == 1, "a tensor-parallel rank drives exactly one device");
+    config_check(!h->slice_rc, "the slice-recompute path has no tensor-parallel exchange");
     CUDA_OK(cudaSetDevice(h->devs[0].device));
     ncclUniqueId u;
     std::memcpy(&u, id, sizeof(u));
     h->comm = std::make_unique<NcclComm>(u, h->tp, h->tp_rank);
+    ensure_part_buffers(*h);
   });
 }
 
@@ -1565,7 +1908,11 @@ int mpsg_tp_connect_local(mpsg_handle* hs, int n) {
       CUDA_OK(cudaEventCreateWithFlags(&g->ready[r], cudaEventDisableTiming));
       CUDA_OK(cudaEventCreateWithFlags(&g->done[r], cudaEventDisableTiming));
     }
-    for (int r = 0; r < n; ++r) hs[r]->comm = std::make_unique<LocalComm>(g, r);
+    for (int r = 0; r < n; ++r) {
+      config_check(!hs[r]->slice_rc, "the slice-recompute path has no tensor-parallel exchange");
+      hs[r]->comm = std::make_unique<LocalComm>(g, r);
+      ensure_part_buffers(*hs[r]);
+    }
   });
 }
 
@@ -1677,15 +2024,13 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
       sig[r] = std::ldexp(1.0, kEnvExp - ex);
       for (int l = 0; l < s.chil; ++l) {
         const double* v = env + 2 * (static_cast<size_t>(r) * s.chil + l);
-        float comp[3];
-        comp[0] = static_cast<float>(v[0] * h->gl[site][l] * sig[r]);
-        comp[1] = static_cast<float>(v[1] * h->gl[site][l] * sig[r]);
-        comp[2] = comp[0] + comp[1];
+        __half hv[3], lv[3];
+        env_split(static_cast<float>(v[0] * h->gl[site][l] * sig[r]),
+                  static_cast<float>(v[1] * h->gl[site][l] * sig[r]), hv, lv);
         const size_t o = static_cast<size_t>(r) * s.kp + l;
         for (int c = 0; c < C; ++c) {
-          const __half hv = __float2half_rn(comp[c]);
-          e[c * plane + o] = hv;
-          e[(C + c) * plane + o] = __float2half_rn(comp[c] - __half2float(hv));
+          e[c * plane + o] = hv[c];
+          e[(C + c) * plane + o] = lv[c];
         }
       }
     }

@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
         }
         if constexpr (kSlice) {
           // next environment rows of this SM's outcome bucket: E = temp * scale split hi / lo per
-          // component re, im, re + im (the select kernel's arithmetic, sweep_kernels.cu)
+          // component re, im, re + im (env_split, the select kernel's arithmetic)
           if (valid && r < a.kp_next) {
             const int j0 = t * kBM + c0 + ch * kEpiSamples;
             const int lo = boff[k], hi = boff[k + 1];
@@ -349,16 +349,13 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
               const float re = (pr[i] - pi[i]) * ci.x;
               const float im = (ps[i] - pr[i] - pi[i]) * ci.x;
               const float sc = a.scale[j];
-              float comp[3];
-              comp[0] = re * sc;
-              comp[1] = im * sc;
-              comp[2] = comp[0] + comp[1];
+              __half hv[3], lv[3];
+              env_split(re * sc, im * sc, hv, lv);
               __half* e0 = a.env_next + static_cast<size_t>(j) * a.kp_next + r;
 #pragma unroll
               for (int cc = 0; cc < 3; ++cc) {
-                const __half hv = __float2half_rn(comp[cc]);
-                e0[cc * plane] = hv;
-                e0[(3 + cc) * plane] = __float2half_rn(comp[cc] - __half2float(hv));
+                e0[cc * plane] = hv[cc];
+                e0[(3 + cc) * plane] = lv[cc];
               }
             }
           }

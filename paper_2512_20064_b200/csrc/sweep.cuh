@@ -64,6 +64,26 @@ constexpr double kBoundaryEps = 1e-6;
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+#ifdef __CUDACC__
+// Environment split of one renormalised entry (re, im): hi / lo fp16 parts per component, and the
+// 3M sum component formed from the split parts, s = (hi_re + lo_re) + (hi_im + lo_im) rounded once in
+// fp32, then split the same way.  Every writer of environment planes (selection, slice GEMM, host
+// contract_site) uses it, so a tensor-parallel rank can re-form the s planes from the re / im planes
+// it receives (the environment exchange ships 4 of the 3M's 6 planes) and obtain the same bits.
+__host__ __device__ __forceinline__ void env_split(float re, float im, __half* hv, __half* lv) {
+  hv[0] = __float2half_rn(re);
+  lv[0] = __float2half_rn(re - __half2float(hv[0]));  // exact difference
+  hv[1] = __float2half_rn(im);
+  lv[1] = __float2half_rn(im - __half2float(hv[1]));
+  const float a = __half2float(hv[0]) + __half2float(lv[0]);  // exact: 22 significant bits (adds only:
+                                                             // no contraction, same bits on host and device)
+  const float b = __half2float(hv[1]) + __half2float(lv[1]);
+  const float sv = a + b;
+  hv[2] = __float2half_rn(sv);
+  lv[2] = __float2half_rn(sv - __half2float(hv[2]));
+}
+#endif
+
 struct SiteGemmArgs {
   int m_tiles;       // rows / 128
   int n_tiles;       // Np / 128 (even)
@@ -206,6 +226,9 @@ void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, bo
                          int grid, cudaStream_t s, bool slice = false);
 int gemm_3m_smem_bytes(bool split);
 void launch_select(const SelectArgs& a, cudaStream_t s);
+// env [shards][6][env_cap][kshard] (3M): planes 2, 5 (s = re + im, hi / lo) of rows [0, rows) of every
+// shard re-formed from planes 0, 1, 3, 4 exactly as env_split forms them (kshard % 8 == 0)
+void launch_env_reform_s(__half* env, int env_cap, int kshard, int shards, int rows, cudaStream_t s);
 void launch_permute_rows(const PermuteArgs& a, cudaStream_t s);
 // zeroes rows [sum(bcount[0..d)), rows) of the next environment (the samples dead from there on)
 void launch_zero_dead(__half* env, int planes, int env_cap, int kp, int rows, const int* bcount, int d,
@@ -225,10 +248,35 @@ void launch_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, 
 // g[2 pe + j] = g[j] + g[pe + j]: re-forms the 3M sum plane Gs = Gr + Gi of a host-streamed site
 // (exact: quantize_pair puts Gr, Gi and their sum on one fp16 grid).  pe % 8 == 0.
 void launch_sum_plane(__half* g, size_t pe, cudaStream_t s);
+// colmax: [width * d] zero-initialised scratch (left zeroed).
 void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
                           int width, int kp, int chirp, const int* lpos, const double* gl,
                           const double* gr, const double* wl, int gplanes, __half* g_out,
-                          float2* cinfo_out, double* cs_out, int* err, cudaStream_t s);
+                          float2* cinfo_out, double* cs_out, unsigned long long* colmax, int* err,
+                          cudaStream_t s);
+
+// Synthetic chains regenerated on the device (mpsg_generated_*, mpsg_synthetic_site): the random_mps
+// form (mps.cpp:148-175) Gamma_i[l, r*d + k] = B[l, r*d + k] * phase_i[r*d + k] *
+// lambda_{i-1}[l] / lambda_i[r] with B a base isometry (rows orthonormal) and unit phases keyed by
+// (seed, kPhaseStream, site, column) with the reference's counter-based key chain (rng.hpp:22-37).
+constexpr uint64_t kPhaseStream = 0x70686173ull;  // "phas"
+struct SynthSite {
+  const float2* base;     // B, complex64 (>= chil rows, row stride ld)
+  long long ld;           // row stride of B (complex elements)
+  long long cols;         // chir * d
+  const float2* phase;    // [cols] this site's phases (launch_synth_phase)
+  const float* lam_prev;  // [chil] fp32 lambda_{i-1} (ones(1) at site 0)
+  const float* inv_lam;   // [chir] fp32 1 / lambda_i (rounded on the host)
+  int d;
+};
+void launch_synth_phase(uint64_t seed, uint64_t site, int cols, float2* phase, cudaStream_t s);
+// out: complex64 (rows, cols) row-major = the site's Gamma
+void launch_synth_values(const SynthSite& g, int rows, float2* out, cudaStream_t s);
+// compression of a regenerated site's column shard, straight from the generator (no Gamma buffer)
+void launch_compress_synth(const SynthSite& g, int chil, int d, int b0, int width, int kp, int chirp,
+                           const int* lpos, const double* gl, const double* gr, const double* wl, int gplanes,
+                           __half* g_out, float2* cinfo_out, double* cs_out, unsigned long long* colmax,
+                           int* err, cudaStream_t s);
 int gemm_smem_bytes(bool split);
 
 }  // namespace mpsg

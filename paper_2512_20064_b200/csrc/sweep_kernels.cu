@@ -951,24 +951,19 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
             re[j] = v.x, im[j] = v.y;
           }
         }
-        float comp[3][8];
+        __align__(16) __half hv[3][8], lv[3][8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          comp[0][j] = re[j] * scale;
-          comp[1][j] = im[j] * scale;
-          comp[2][j] = comp[0][j] + comp[1][j];
+          __half h3[3], l3[3];
+          env_split(re[j] * scale, im[j] * scale, h3, l3);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) hv[c][j] = h3[c], lv[c][j] = l3[c];
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           if (c >= C) break;
-          __align__(16) __half hv[8], lv[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            hv[j] = __float2half_rn(comp[c][j]);
-            lv[j] = __float2half_rn(comp[c][j] - __half2float(hv[j]));
-          }
-          *reinterpret_cast<uint4*>(e0 + c * plane + r) = *reinterpret_cast<const uint4*>(hv);
-          *reinterpret_cast<uint4*>(e0 + (C + c) * plane + r) = *reinterpret_cast<const uint4*>(lv);
+          *reinterpret_cast<uint4*>(e0 + c * plane + r) = *reinterpret_cast<const uint4*>(hv[c]);
+          *reinterpret_cast<uint4*>(e0 + (C + c) * plane + r) = *reinterpret_cast<const uint4*>(lv[c]);
         }
       }
       return;
@@ -1005,22 +1000,21 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
         v01 = make_float4(c0.x, c0.y, c1.x, c1.y);
         v23 = make_float4(c2.x, c2.y, 0.f, 0.f);
       }
-      float comp[3][4];
-      comp[0][0] = v01.x * scale, comp[0][1] = v01.z * scale, comp[0][2] = v23.x * scale, comp[0][3] = v23.z * scale;
-      comp[1][0] = v01.y * scale, comp[1][1] = v01.w * scale, comp[1][2] = v23.y * scale, comp[1][3] = v23.w * scale;
+      const float cre[4] = {v01.x * scale, v01.z * scale, v23.x * scale, v23.z * scale};
+      const float cim[4] = {v01.y * scale, v01.w * scale, v23.y * scale, v23.w * scale};
+      __align__(8) __half hv[3][4], lv[3][4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) comp[2][j] = comp[0][j] + comp[1][j];
+      for (int j = 0; j < 4; ++j) {
+        __half h3[3], l3[3];
+        env_split(cre[j], cim[j], h3, l3);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) hv[c][j] = h3[c], lv[c][j] = l3[c];
+      }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         if (c >= C) break;
-        __align__(8) __half hv[4], lv[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          hv[j] = __float2half_rn(comp[c][j]);
-          lv[j] = __float2half_rn(comp[c][j] - __half2float(hv[j]));
-        }
-        *reinterpret_cast<uint2*>(e0 + c * plane + r) = *reinterpret_cast<const uint2*>(hv);
-        *reinterpret_cast<uint2*>(e0 + (C + c) * plane + r) = *reinterpret_cast<const uint2*>(lv);
+        *reinterpret_cast<uint2*>(e0 + c * plane + r) = *reinterpret_cast<const uint2*>(hv[c]);
+        *reinterpret_cast<uint2*>(e0 + (C + c) * plane + r) = *reinterpret_cast<const uint2*>(lv[c]);
       }
     }
   }
@@ -1052,6 +1046,47 @@ void launch_reduce_tiles(const float2* pstat, int nt, int tiles_per_k, int d, in
   const int threads = 256;
   reduce_tiles_kernel<<<(rows * 32 + threads - 1) / threads, threads, 0, s>>>(pstat, nt, tiles_per_k,
                                                                              d, rows, out);
+}
+
+// Tensor-parallel environment exchange: the 3M s planes (hi 2, lo 5) of every shard re-formed from
+// the received re / im planes (hi 0, 1; lo 3, 4) with env_split's arithmetic, 8 columns per thread.
+__global__ void env_reform_s_kernel(__half* env, int env_cap, int kshard, int shards, int rows) {
+  const size_t plane = static_cast<size_t>(env_cap) * kshard;
+  const int per_row = kshard / 8;
+  const size_t total = static_cast<size_t>(shards) * rows * per_row;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int q = static_cast<int>(e / (static_cast<size_t>(rows) * per_row));
+    const size_t rem = e - static_cast<size_t>(q) * rows * per_row;
+    const int n = static_cast<int>(rem / per_row), c8 = static_cast<int>(rem - static_cast<size_t>(n) * per_row);
+    __half* base = env + static_cast<size_t>(q) * 6 * plane + static_cast<size_t>(n) * kshard + 8 * c8;
+    const uint4 hr = *reinterpret_cast<const uint4*>(base);
+    const uint4 hi = *reinterpret_cast<const uint4*>(base + plane);
+    const uint4 lr = *reinterpret_cast<const uint4*>(base + 3 * plane);
+    const uint4 li = *reinterpret_cast<const uint4*>(base + 4 * plane);
+    const __half* phr = reinterpret_cast<const __half*>(&hr);
+    const __half* phi = reinterpret_cast<const __half*>(&hi);
+    const __half* plr = reinterpret_cast<const __half*>(&lr);
+    const __half* pli = reinterpret_cast<const __half*>(&li);
+    __align__(16) __half hs[8], ls[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float a = __half2float(phr[j]) + __half2float(plr[j]);
+      const float b = __half2float(phi[j]) + __half2float(pli[j]);
+      const float sv = a + b;
+      hs[j] = __float2half_rn(sv);
+      ls[j] = __float2half_rn(sv - __half2float(hs[j]));
+    }
+    *reinterpret_cast<uint4*>(base + 2 * plane) = *reinterpret_cast<const uint4*>(hs);
+    *reinterpret_cast<uint4*>(base + 5 * plane) = *reinterpret_cast<const uint4*>(ls);
+  }
+}
+
+void launch_env_reform_s(__half* env, int env_cap, int kshard, int shards, int rows, cudaStream_t s) {
+  const size_t total = static_cast<size_t>(shards) * rows * (kshard / 8);
+  if (total == 0) return;
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 4 * 148));
+  env_reform_s_kernel<<<blocks, 256, 0, s>>>(env, env_cap, kshard, shards, rows);
 }
 
 void launch_select(const SelectArgs& a, cudaStream_t s) {
@@ -1171,38 +1206,104 @@ void launch_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, 
 // ============================================================================================
 // Compression: Gamma (chiL, chiR, d) -> fp16 planes [2][Np][Kp] with power-of-two scales
 //   Ghat[l, r, k] = Gamma[l, r, k] * gr[r] / gl[l] / cs[r, k],  |Ghat| <= 1
+// The source is either a complex array (f64 / f32, the caller's Gamma) or the synthetic-chain
+// generator below (regenerated on the device every pass for chains beyond HBM and host memory).
 // ============================================================================================
 template <typename T>
-__device__ __forceinline__ void load_c(const void* src, size_t idx, double& re, double& im) {
-  const T* p = static_cast<const T*>(src) + 2 * idx;
-  re = static_cast<double>(p[0]);
-  im = static_cast<double>(p[1]);
+struct ArraySrc {  // complex T interleaved, (chiL, chiR * d) row-major
+  const T* p;
+  size_t stride;
+  __device__ __forceinline__ void load(int l, size_t j, double& re, double& im) const {
+    const T* q = p + 2 * (static_cast<size_t>(l) * stride + j);
+    re = static_cast<double>(q[0]);
+    im = static_cast<double>(q[1]);
+  }
+};
+
+// Synthetic random right-canonical chain of the random_mps form (mps.cpp:148-175):
+//   Gamma_i[l, j] = B[l, j] * phase_i[j] * (lambda_{i-1}[l] * (1 / lambda_i[r])),  j = r * d + k
+// with explicitly rounded fp32 operations, so every kernel that evaluates it (the compression of a
+// regenerated site, mpsg_synthetic_site) produces the same bits.
+__device__ __forceinline__ float2 synth_value(const SynthSite& g, int l, size_t j) {
+  const float2 b = g.base[static_cast<size_t>(l) * g.ld + j];
+  const float2 ph = g.phase[j];
+  const float tr = __fsub_rn(__fmul_rn(b.x, ph.x), __fmul_rn(b.y, ph.y));
+  const float ti = __fadd_rn(__fmul_rn(b.x, ph.y), __fmul_rn(b.y, ph.x));
+  const float sc = __fmul_rn(g.lam_prev[l], g.inv_lam[j / g.d]);
+  return make_float2(__fmul_rn(tr, sc), __fmul_rn(ti, sc));
+}
+struct SynthSrc {
+  SynthSite g;
+  __device__ __forceinline__ void load(int l, size_t j, double& re, double& im) const {
+    const float2 v = synth_value(g, l, j);
+    re = static_cast<double>(v.x);
+    im = static_cast<double>(v.y);
+  }
+};
+
+// phase_i[j] = exp(2 pi i u), u = keyed uniform of (seed, kPhaseStream, site, j) (rng.hpp:22-37)
+__global__ void synth_phase_kernel(uint64_t seed, uint64_t site, int cols, float2* phase) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) {
+    const double u = keyed_uniform(seed, kPhaseStream, site, static_cast<uint64_t>(j));
+    double sn, cs;
+    sincospi(2.0 * u, &sn, &cs);
+    phase[j] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
+  }
 }
 
-template <typename T>
-__global__ void colscale_kernel(const void* src, int chil, int chir, int d, int b0, int width,
-                                int chirp, const double* gl, const double* gr, const double* wl,
-                                float2* cinfo, double* cs_out, int* err) {
-  const int jl = blockIdx.x * blockDim.x + threadIdx.x;  // local column jl = r_loc * d + k
+__global__ void synth_values_kernel(const SynthSite g, int rows, float2* out) {
+  const size_t n = static_cast<size_t>(rows) * g.cols;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int l = static_cast<int>(e / g.cols);
+    out[e] = synth_value(g, l, e - static_cast<size_t>(l) * g.cols);
+  }
+}
+
+void launch_synth_phase(uint64_t seed, uint64_t site, int cols, float2* phase, cudaStream_t s) {
+  synth_phase_kernel<<<std::max(1, std::min((cols + 255) / 256, 592)), 256, 0, s>>>(seed, site, cols, phase);
+}
+void launch_synth_values(const SynthSite& g, int rows, float2* out, cudaStream_t s) {
+  synth_values_kernel<<<1184, 256, 0, s>>>(g, rows, out);
+}
+
+// Per local column jl = r_loc * d + k: max over l of max(|re|, |im|) * gr[r] / gl[l] (f64), as an
+// order-independent atomic max of the nonnegative doubles' bit patterns.  A 2-D grid (64-row chunks
+// x 128 columns) keeps enough loads in flight to stream the source at HBM rate.
+template <typename Src>
+__global__ void colmax_kernel(const Src src, int chil, int d, int b0, int width, const double* gl,
+                              const double* gr, unsigned long long* colmax, int* err) {
+  const int jl = blockIdx.x * blockDim.x + threadIdx.x;
   if (jl >= width * d) return;
   const int rl = jl / d, k = jl - rl * d;
   const int r = b0 + rl;
   const size_t j = static_cast<size_t>(r) * d + k;
-  const size_t stride = static_cast<size_t>(chir) * d;
+  const int l0 = blockIdx.y * 64, l1 = min(chil, l0 + 64);
   double mx = 0.0;
   bool finite = true;
-  for (int l = 0; l < chil; ++l) {
+  for (int l = l0; l < l1; ++l) {
     double re, im;
-    load_c<T>(src, static_cast<size_t>(l) * stride + j, re, im);
+    src.load(l, j, re, im);
     if (!isfinite(re) || !isfinite(im)) finite = false;
     const double f = gr[r] / gl[l];
     mx = fmax(mx, fmax(fabs(re * f), fabs(im * f)));
   }
   if (!finite) atomicExch(err, 3);  // NumericError: non-finite Gamma (contract.cpp:117-119)
+  if (mx > 0.0) atomicMax(colmax + jl, static_cast<unsigned long long>(__double_as_longlong(mx)));
+}
+
+// Column scales from the maxima: cs = 2^e with mx = f 2^e, f in [0.5, 1); clears colmax for reuse.
+__global__ void colfinish_kernel(int d, int b0, int width, int chirp, const double* wl,
+                                 unsigned long long* colmax, float2* cinfo, double* cs_out, int* err) {
+  const int jl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (jl >= width * d) return;
+  const int rl = jl / d, k = jl - rl * d;
+  const double mx = __longlong_as_double(static_cast<long long>(colmax[jl]));
+  colmax[jl] = 0ull;
   double cs = 1.0;
   if (mx > 0.0) {
     int e;
-    frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)
+    frexp(mx, &e);
     if (e > 120) {
       atomicExch(err, 3);  // outside the compressed format's range
       e = 120;
@@ -1211,7 +1312,7 @@ __global__ void colscale_kernel(const void* src, int chil, int chir, int d, int 
     cs = ldexp(1.0, e);
   }
   cs_out[jl] = cs;
-  cinfo[k * chirp + rl] = make_float2(static_cast<float>(cs), static_cast<float>(wl[r]));
+  cinfo[k * chirp + rl] = make_float2(static_cast<float>(cs), static_cast<float>(wl[b0 + rl]));
 }
 
 // Rounds (a, b) onto the fp16 grid of the binade of max(|a|, |b|, |a + b|), so that a, b and
@@ -1232,8 +1333,8 @@ __device__ __forceinline__ void quantize_pair(double a, double b, __half& ha, __
   hs = __double2half(qa + qb);
 }
 
-template <typename T>
-__global__ void pack_kernel(const void* src, int chil, int chir, int d, int b0, int width, int kp,
+template <typename Src>
+__global__ void pack_kernel(const Src src, int chil, int d, int b0, int width, int kp,
                             int chirp, const int* lpos, const double* gl, const double* gr,
                             const double* cs, int gplanes, __half* g_out, int np) {
   // planes: [Gr, Gi (, Gs)] and, for gplanes = 6 (MPSG_MODE_PRECISE), [Gr_lo, Gi_lo, Gs_lo] -- the
@@ -1241,7 +1342,6 @@ __global__ void pack_kernel(const void* src, int chil, int chir, int d, int b0, 
   // precision half) is an exact fp16 number
   __shared__ __half tp[6][32][33];
   const int wcols = width * d;
-  const size_t stride = static_cast<size_t>(chir) * d;
   const int j0 = blockIdx.x * 32, l0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
   for (int yy = ty; yy < 32; yy += 8) {
@@ -1252,7 +1352,7 @@ __global__ void pack_kernel(const void* src, int chil, int chir, int d, int b0, 
     if (l < chil && jl < wcols) {
       const int rl = jl / d, k = jl - rl * d;
       double re, im;
-      load_c<T>(src, static_cast<size_t>(l) * stride + static_cast<size_t>(b0 + rl) * d + k, re, im);
+      src.load(l, static_cast<size_t>(b0 + rl) * d + k, re, im);
       const double f = gr[b0 + rl] / gl[l] / cs[jl];
       quantize_pair(re * f, im * f, h[0], h[1], h[2]);
       if (gplanes == 6)
@@ -1300,26 +1400,41 @@ void launch_sum_plane(__half* g, size_t pe, cudaStream_t s) {
   sum_plane_kernel<<<blocks, 256, 0, s>>>(g, n8, pe);
 }
 
-void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
-                          int width, int kp, int chirp, const int* lpos, const double* gl,
-                          const double* gr, const double* wl, int gplanes, __half* g_out,
-                          float2* cinfo_out, double* cs_out, int* err, cudaStream_t s) {
+template <typename Src>
+static void compress_from(const Src& src, int chil, int d, int b0, int width, int kp, int chirp,
+                          const int* lpos, const double* gl, const double* gr, const double* wl, int gplanes,
+                          __half* g_out, float2* cinfo_out, double* cs_out, unsigned long long* colmax, int* err,
+                          cudaStream_t s) {
   if (width <= 0) return;
   const int wcols = width * d;
   const int np = round_up(d * chirp, 2 * kBN);
-  const dim3 cb((wcols + 127) / 128);
-  const dim3 pb((wcols + 31) / 32, (chil + 31) / 32);
-  if (src_f64) {
-    colscale_kernel<double><<<cb, 128, 0, s>>>(src, chil, chir, d, b0, width, chirp, gl, gr, wl,
-                                               cinfo_out, cs_out, err);
-    pack_kernel<double><<<pb, dim3(32, 8), 0, s>>>(src, chil, chir, d, b0, width, kp, chirp, lpos,
-                                                   gl, gr, cs_out, gplanes, g_out, np);
-  } else {
-    colscale_kernel<float><<<cb, 128, 0, s>>>(src, chil, chir, d, b0, width, chirp, gl, gr, wl,
-                                              cinfo_out, cs_out, err);
-    pack_kernel<float><<<pb, dim3(32, 8), 0, s>>>(src, chil, chir, d, b0, width, kp, chirp, lpos, gl,
-                                                  gr, cs_out, gplanes, g_out, np);
-  }
+  colmax_kernel<Src><<<dim3((wcols + 127) / 128, (chil + 63) / 64), 128, 0, s>>>(src, chil, d, b0, width, gl, gr,
+                                                                                 colmax, err);
+  colfinish_kernel<<<(wcols + 127) / 128, 128, 0, s>>>(d, b0, width, chirp, wl, colmax, cinfo_out, cs_out, err);
+  pack_kernel<Src><<<dim3((wcols + 31) / 32, (chil + 31) / 32), dim3(32, 8), 0, s>>>(
+      src, chil, d, b0, width, kp, chirp, lpos, gl, gr, cs_out, gplanes, g_out, np);
+}
+
+void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
+                          int width, int kp, int chirp, const int* lpos, const double* gl,
+                          const double* gr, const double* wl, int gplanes, __half* g_out,
+                          float2* cinfo_out, double* cs_out, unsigned long long* colmax, int* err,
+                          cudaStream_t s) {
+  const size_t stride = static_cast<size_t>(chir) * d;
+  if (src_f64)
+    compress_from(ArraySrc<double>{static_cast<const double*>(src), stride}, chil, d, b0, width, kp, chirp, lpos,
+                  gl, gr, wl, gplanes, g_out, cinfo_out, cs_out, colmax, err, s);
+  else
+    compress_from(ArraySrc<float>{static_cast<const float*>(src), stride}, chil, d, b0, width, kp, chirp, lpos,
+                  gl, gr, wl, gplanes, g_out, cinfo_out, cs_out, colmax, err, s);
+}
+
+void launch_compress_synth(const SynthSite& g, int chil, int d, int b0, int width, int kp, int chirp,
+                           const int* lpos, const double* gl, const double* gr, const double* wl, int gplanes,
+                           __half* g_out, float2* cinfo_out, double* cs_out, unsigned long long* colmax,
+                           int* err, cudaStream_t s) {
+  compress_from(SynthSrc{g}, chil, d, b0, width, kp, chirp, lpos, gl, gr, wl, gplanes, g_out, cinfo_out, cs_out,
+                colmax, err, s);
 }
 
 }  // namespace mpsg

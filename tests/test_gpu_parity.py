@@ -884,3 +884,116 @@ def test_boundary_input_validation(pkg, gold, tmp_path):
     with pytest.raises(pkg.ConfigError):
         tp.ranks[0].save(str(tmp_path / "x.mpsb"))
     tp.close()
+
+
+# ---- generated supply: synthetic chains regenerated on the device every pass -----------------
+@pytest.mark.parametrize("m,chi,d,scheme,pass_samples,sched", [
+    (12, 256, 4, 3, 0, None), (10, 512, 6, 4, 0, None), (8, 1024, 4, 3, 1024, None),
+    (14, 256, 4, 3, 0, 1e-3)])
+def test_generated_supply_equals_resident_chain(pkg, m, chi, d, scheme, pass_samples, sched):
+    """A generated handle (base isometries + per-site spectra; every site regenerated and compressed
+    on the device into the slot ring on every pass) holds exactly the chain build_synthetic
+    materialises: identical decoded Gamma, identical rows (several passes, two lanes at chi = 1024,
+    ragged dynamic bonds) and identical RunStats counters."""
+    from paper_2512_20064_b200.synthetic import build_synthetic
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    schedule = (pkg.TruncationFilter(chi_max=chi, eps_center=sched, edge_factor=100.0) if sched else None)
+    kw = dict(seed=13, policy=pol, scheme=scheme, pass_samples=pass_samples, schedule=schedule)
+    res, lams = build_synthetic(m, chi, d, **kw)
+    gen, lams2 = build_synthetic(m, chi, d, generated=True, **kw)
+    assert res.bond_dims == gen.bond_dims
+    for i in range(m):
+        assert np.array_equal(res.decoded_gamma(i), gen.decoded_gamma(i)), i
+    n = 3000
+    st1, st2 = pkg.RunStats(), pkg.RunStats()
+    a = res.sample(0, n, 7, stats=st1)
+    b = gen.sample(0, n, 7, stats=st2)
+    assert np.array_equal(a, b)
+    assert st1.contraction_macs == st2.contraction_macs and st1.measure_weight_macs == st2.measure_weight_macs
+    assert np.array_equal(gen.sample(0, n, 7), b)  # second call: the ring restarts cleanly
+    mg = gen.marginals(0, a[:64])
+    np.testing.assert_array_equal(mg, res.marginals(0, a[:64]))
+    assert gen.state_bytes < res.state_bytes or m * chi <= 4096
+
+
+def test_generated_supply_parity_vs_reference(pkg):
+    """The regenerated chain against the reference on its decoded tensors (c3 bond dimension)."""
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not available")
+    from paper_2512_20064_b200.synthetic import build_synthetic
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    m, chi, d, n = 10, 2048, 6, 16
+    smp, lams = build_synthetic(m, chi, d, seed=3, policy=pol, generated=True)
+    dec = O.Mps(d, list(smp.bond_dims), [smp.decoded_gamma(i) for i in range(m)], list(lams))
+    ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, n, 7, want_marginals=True)
+    got = smp.sample(0, n, 7)
+    ndiff, explained = compare_strings(got, ref_rows, ref_marg, 7)
+    assert ndiff == explained
+    gm = smp.marginals(0, ref_rows)
+    big = ref_marg >= 1e-3
+    assert (np.abs(gm[big] - ref_marg[big]) / ref_marg[big]).max() < MARG_RTOL
+
+
+def test_generated_supply_rejects_nonfinite(pkg):
+    """A zero in Lambda_i makes Gamma_i infinite (1 / Lambda): the regenerated site fails the
+    compression's finiteness check and the call raises NumericError (contract.cpp:117-119)."""
+    import ctypes as C
+    from paper_2512_20064_b200 import _lib
+    import torch
+    L = _lib.lib()
+    bonds = [1, 4, 1]
+    h = C.c_void_p()
+    bd = (C.c_uint64 * 3)(*bonds)
+    assert L.mpsg_generated_begin(2, 4, bd, None, None, None, 0, 5, C.byref(h)) == 0
+    b0 = torch.eye(1, 16, dtype=torch.complex64, device="cuda")
+    b1 = torch.zeros(4, 4, dtype=torch.complex64, device="cuda")
+    b1[:, 0] = 1.0
+    ids = []
+    for t in (b0, b1):
+        bid = C.c_int()
+        assert L.mpsg_generated_add_base(h, C.c_void_p(t.data_ptr()), 1, t.shape[0], t.shape[1], C.byref(bid)) == 0
+        ids.append(bid.value)
+    lam0 = np.array([1.0, 0.5, 0.25, 0.0])
+    lam1 = np.ones(1)
+    assert L.mpsg_generated_set_site(h, 0, ids[0], lam0.ctypes.data_as(_lib._pd)) == 0
+    assert L.mpsg_generated_set_site(h, 1, ids[1], lam1.ctypes.data_as(_lib._pd)) == 0
+    assert L.mpsg_builder_finish(h) == 0
+    rows = np.empty((8, 2), np.uint8)
+    assert L.mpsg_sample(h, 7, 0, 8, rows.ctypes.data_as(_lib._pu8), None) == 3  # MPSG_ERR_NUMERIC
+    L.mpsg_destroy(h)
+
+
+@pytest.mark.parametrize("scheme", [3, 4])
+def test_nccl_one_rank_group_exchange(pkg, gold, scheme):
+    """The tensor-parallel data plane through NCCL on one GPU: a one-rank group (tp_size 1 connected
+    with mpsg_tp_connect_nccl) runs the partial-weight all-gather, the strided environment all-gather
+    (grouped ncclBroadcast of the re / im planes; 3M re-forms its s planes after it) and the lane-1
+    communicator split -- and samples what the plain handle samples (the exchanged partials are
+    rounded to fp32, so only a draw within ~1e-7 of a boundary could differ)."""
+    z = np.load(f"{gold}/c1b.npz")
+    mps = O.load_npz_mps(z)
+    st = to_state(pkg, mps)
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    plain = pkg.GpuSampler(st, pol, scheme=scheme).sample(0, 4000, 7)
+    smp = pkg.GpuSampler(st, pol, scheme=scheme, pass_samples=1024)
+    smp.connect_nccl(pkg.sampler.nccl_unique_id())
+    got = smp.sample(0, 4000, 7)
+    assert (got != plain).any(axis=1).sum() <= 1
+    dec = decoded_mps(smp, mps)
+    ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, 1000, 7, want_marginals=True)
+    gm = smp.marginals(0, ref_rows)
+    big = ref_marg >= 1e-3
+    assert (np.abs(gm[big] - ref_marg[big]) / ref_marg[big]).max() < MARG_RTOL
+    smp.close()
+
+
+def test_nccl_one_rank_group_generated_chi1024(pkg):
+    """Same at chi = 1024 with two pipeline lanes (lane 1's communicator split from lane 0's) over a
+    generated (regenerated-per-pass) chain."""
+    from paper_2512_20064_b200.synthetic import build_synthetic
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    a, _ = build_synthetic(8, 1024, 4, seed=5, policy=pol, generated=True, pass_samples=2048)
+    b, _ = build_synthetic(8, 1024, 4, seed=5, policy=pol, generated=True, pass_samples=2048)
+    b.connect_nccl(pkg.sampler.nccl_unique_id())
+    x, y = a.sample(0, 4096, 7), b.sample(0, 4096, 7)
+    assert (x != y).any(axis=1).sum() <= 1
