@@ -55,10 +55,14 @@ enum { MPSG_SCALE_NONE = 0, MPSG_SCALE_GLOBAL_MAX = 1, MPSG_SCALE_PER_SAMPLE_MAX
 
 /* GPU contraction schemes:
  *   MPSG_MODE_SPLIT   fp16 Gamma x (hi + lo) fp16 environment, fp32 accumulate; F32-class
- *                     accuracy, 2x issued MMAs.  Used for compute = F64 / F32.
+ *                     accuracy on the DECODED Gamma (the fp16 format moves the sampled
+ *                     distribution itself by ~1e-4 relative at interior sites), 2x issued MMAs.
  *   MPSG_MODE_SINGLE  fp16 Gamma x fp16 environment, one MMA pass; F16-class accuracy.
  *                     Used for compute = TF32 / F16.
- *   MPSG_MODE_AUTO    pick from policy.compute. */
+ *   MPSG_MODE_AUTO    pick from policy.compute: TF32 / F16 -> SINGLE; F64 / F32 -> PRECISE when its
+ *                     state (6 fp16 planes, 12 B per complex entry) fits the device (resident) or
+ *                     60% of host memory (host-streamed), else SPLIT.  mpsg_mode() reports the
+ *                     choice.  Generated handles (synthetic chains) use SPLIT. */
 enum { MPSG_MODE_AUTO = 0, MPSG_MODE_SPLIT = 1, MPSG_MODE_SINGLE = 2, MPSG_MODE_PRECISE = 3 };
 /*   MPSG_MODE_PRECISE  SPLIT plus Gamma stored as an exact fp16 hi + lo pair per component (22-bit
  *                     mantissas instead of 11): the device samples the caller's f64 / f32 Gamma to
@@ -181,6 +185,8 @@ void mpsg_destroy(mpsg_handle h);
 uint64_t mpsg_state_bytes(mpsg_handle h);
 /* The contraction scheme the handle runs: MPSG_SCHEME_3M or MPSG_SCHEME_4M (0 for a null handle). */
 int mpsg_scheme(mpsg_handle h);
+/* The precision mode the handle runs: MPSG_MODE_SPLIT, _SINGLE or _PRECISE (0 for a null handle). */
+int mpsg_mode(mpsg_handle h);
 
 /* The Gamma values the GPU actually samples (decoded compressed format), reference layout:
  * complex128 interleaved (chiL, chiR, d).  The CPU oracle consumes these.  A tensor-parallel

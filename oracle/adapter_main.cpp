@@ -1,8 +1,10 @@
 // TEST INFRASTRUCTURE: builds the drop-in adapter (include/mpsg_mpsamp.hpp) against the
 // reference's own headers and library, exactly as a maintainer would, and checks it.
 //   adapter_test cpu  -> validation/error mapping only (no GPU needed)
-//   adapter_test gpu  -> c1 = random_mps(16, 32, 4, 42) through mpsg_mpsamp::sample_batch,
-//                        compared with mpsamp::sample_batch on the same MPS and seed
+//   adapter_test gpu  -> c1 = random_mps(16, 32, 4, 42) through mpsg_mpsamp::sample_batch (AUTO at
+//                        compute F64 = PRECISE: the caller's Gamma to ~2^-23), compared with
+//                        mpsamp::sample_batch on the same MPS and seed (0 strings may differ); and
+//                        MPSG_MODE_SPLIT against the reference on the decoded Gamma (0 may differ)
 #include <cstdio>
 #include <cstring>
 
@@ -71,8 +73,32 @@ int main(int argc, char** argv) {
       return 1;
     }
   }
-  std::printf("adapter gpu: %zu/1000 strings differ from the reference on the original (uncompressed) "
-              "Gamma; contraction_macs %llu (reference %llu)\n",
-              diff, static_cast<unsigned long long>(st.flops.contraction_macs), 45600000ull);
-  return (st.flops.contraction_macs == 45600000ull && diff <= 20) ? 0 : 1;
+  // MPSG_MODE_SPLIT (the fp16 format's decoded-Gamma contract): identical strings against the
+  // reference run on the decoded Gamma, and the count against the original Gamma recorded
+  size_t diff_split_dec = 0, diff_split_orig = 0;
+  {
+    mpsg_options o{};
+    o.mode = MPSG_MODE_SPLIT;
+    mpsg_mpsamp::DeviceState ds(mps, opts.policy, {}, &o);
+    mpsamp::MpsState dec = mps;
+    for (size_t i = 0; i < mps.num_sites; ++i)
+      mpsg_mpsamp::check(mpsg_decoded_gamma(ds.handle(), i, reinterpret_cast<double*>(dec.gammas[i].data())));
+    std::vector<uint8_t> rows(1000 * 16);
+    mpsamp::RunStats rs;
+    mpsg_mpsamp::sample_micro_serial(ds, 0, 1000, opts, rows.data(), rs);
+    mpsamp::SampleBatch ref_dec = mpsamp::sample_batch(dec, mpsamp::BatchPlan::simple(1000), opts);
+    for (size_t n = 0; n < 1000; ++n) {
+      diff_split_dec += std::memcmp(&rows[n * 16], &ref_dec.outcomes[n * 16], 16) != 0;
+      diff_split_orig += std::memcmp(&rows[n * 16], &want.outcomes[n * 16], 16) != 0;
+    }
+  }
+  // one JSON line (profiles/r2_parity/adapter_c1.json): the default (AUTO -> PRECISE at F64) against the
+  // caller's original Gamma, SPLIT against the decoded and the original Gamma
+  std::printf("{\"case\": \"c1 random_mps(16, 32, 4, 42), 1000 samples, seed 7, F64 + PerSampleMax\", "
+              "\"auto_mode\": %d, \"auto_vs_original_strings_differing\": %zu, "
+              "\"split_vs_decoded_strings_differing\": %zu, \"split_vs_original_strings_differing\": %zu, "
+              "\"contraction_macs\": %llu, \"reference_contraction_macs\": %llu}\n",
+              mpsg_mode(mpsg_mpsamp::DeviceState(mps, opts.policy).handle()), diff, diff_split_dec, diff_split_orig,
+              static_cast<unsigned long long>(st.flops.contraction_macs), 45600000ull);
+  return (st.flops.contraction_macs == 45600000ull && diff == 0 && diff_split_dec == 0) ? 0 : 1;
 }

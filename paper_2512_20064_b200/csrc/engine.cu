@@ -409,6 +409,7 @@ struct mpsg_handle_s {
   int hplanes = 2;
   bool precise = false;                    // Gamma hi + lo planes (MPSG_MODE_PRECISE)
   bool slice_rc = false;                   // slice-recompute path available (3M, tp = 1, d <= 32)
+  bool precise_auto = false;               // MPSG_MODE_AUTO at F64 / F32: PRECISE if its state fits
   bool generated = false;                  // Gamma regenerated on the device every pass (synthetic chains)
   uint64_t gen_seed = 0;
   std::unique_ptr<mpsg::Comm> comm;
@@ -464,6 +465,25 @@ static void choose_scheme(mpsg_handle_s& h) {
         if (state3 + 10.0e9 > static_cast<double>(free_b)) m3 = false;  // pass buffers + headroom
       }
     }
+  }
+  if (h.precise_auto) {  // MPSG_MODE_AUTO at compute F64 / F32: PRECISE when its 6 planes fit
+    double state6 = 0.0;
+    for (uint64_t i = 0; i < h.M; ++i)
+      state6 += 6.0 * 2.0 * round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN) *
+                static_cast<double>(h.tp) * round_up((static_cast<int>(h.bonds[i]) + h.tp - 1) / h.tp, kBK3);
+    bool fits = h.pair && h.opts.scheme != MPSG_SCHEME_4M;
+    if (h.opts.host_stream_slots != 0) {
+      const double host = static_cast<double>(sysconf(_SC_PHYS_PAGES)) * sysconf(_SC_PAGE_SIZE);
+      fits = fits && state6 * (4.0 / 6.0) * h.devs.size() <= 0.6 * host;
+    } else {
+      for (auto& dc : h.devs) {
+        size_t free_b = 0, total_b = 0;
+        CUDA_OK(cudaSetDevice(dc.device));
+        CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+        fits = fits && state6 + 10.0e9 <= static_cast<double>(free_b);
+      }
+    }
+    h.precise = fits;
   }
   if (h.precise) {
     config_check(h.opts.scheme != MPSG_SCHEME_4M, "MPSG_MODE_PRECISE needs the 3M scheme");
@@ -1615,6 +1635,9 @@ static int begin_impl(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bon
     config_check(h->tp == 1 || ndev <= 1, "a tensor-parallel rank drives exactly one device");
     h->split = h->opts.mode == MPSG_MODE_SPLIT || h->opts.mode == MPSG_MODE_PRECISE ||
                (h->opts.mode == MPSG_MODE_AUTO && (pol.compute == MPSG_F64 || pol.compute == MPSG_F32));
+    // the reference's F64 / F32 compute samples the caller's Gamma: AUTO keeps it to ~2^-23 (PRECISE)
+    // whenever that state fits, else the fp16 format's decoded-Gamma contract (SPLIT)
+    h->precise_auto = h->opts.mode == MPSG_MODE_AUTO && !generated && h->split;
     config_check(h->opts.scheme == MPSG_SCHEME_AUTO || h->opts.scheme == MPSG_SCHEME_3M ||
                      h->opts.scheme == MPSG_SCHEME_4M, "unknown contraction scheme");
     config_check(h->opts.slice >= MPSG_SLICE_AUTO && h->opts.slice <= MPSG_SLICE_RECOMPUTE,
@@ -1801,6 +1824,11 @@ uint64_t mpsg_state_bytes(mpsg_handle h) {
 }
 
 int mpsg_scheme(mpsg_handle h) { return h ? (h->m3 ? MPSG_SCHEME_3M : MPSG_SCHEME_4M) : 0; }
+
+int mpsg_mode(mpsg_handle h) {
+  if (!h) return 0;
+  return h->precise ? MPSG_MODE_PRECISE : (h->split ? MPSG_MODE_SPLIT : MPSG_MODE_SINGLE);
+}
 
 int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
   return guarded([&] {

@@ -114,7 +114,8 @@ class PrecisionPolicy:
 
 
 class Mode(enum.IntEnum):
-    """GPU contraction precision; AUTO picks SPLIT for F64/F32 compute."""
+    """GPU contraction precision; AUTO picks PRECISE for F64/F32 compute when its
+    state fits (else SPLIT) and SINGLE for TF32/F16."""
     AUTO = 0
     SPLIT = 1
     SINGLE = 2
@@ -401,6 +402,11 @@ class GpuSampler:
         if mu.shape != (count, self.num_sites):
             raise DimensionError(f"displacement amplitudes must be ({count}, {self.num_sites})")
         return mu
+
+    @property
+    def mode(self) -> Mode:
+        """The precision mode this handle runs (MPSG_MODE_AUTO resolved: SPLIT, SINGLE or PRECISE)."""
+        return Mode(_lib.lib().mpsg_mode(self._h))
 
     @property
     def scheme(self) -> Scheme:

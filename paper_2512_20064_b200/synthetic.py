@@ -93,7 +93,7 @@ def synthetic_site(base, rows: int, cols: int, d: int, lam_prev, lam, seed: int,
 
 def build_synthetic(num_sites: int, chi: int, d: int, seed: int = 42, level_damping: float = 0.2,
                     lambda_decay: Optional[float] = None, policy: Optional[PrecisionPolicy] = None,
-                    mode: Mode = Mode.AUTO, devices: Optional[Sequence[int]] = None,
+                    mode: Mode = Mode.SPLIT, devices: Optional[Sequence[int]] = None,
                     pass_samples: int = 0, n_base: int = 4, record_site_times: bool = False,
                     keep_host: bool = False, tp_size: int = 1, tp_rank: int = 0,
                     host_stream_slots: int = 0, scheme: int = 0, schedule=None, slice: int = 0,
@@ -107,7 +107,9 @@ def build_synthetic(num_sites: int, chi: int, d: int, seed: int = 42, level_damp
     The MPS is generated and compressed site by site on the first device, never materialised in
     host memory (c3: 102 GB compressed, 409 GB as complex128).  generated=True keeps only the
     generators (base isometries + per-site spectra; mpsg_generated_*) and the device regenerates
-    every site on every pass -- the same chain, for chains beyond device and host memory (c4)."""
+    every site on every pass -- the same chain, for chains beyond device and host memory (c4).
+    The default mode is SPLIT: a synthetic chain is sampled under the decoded-Gamma contract, like the
+    benchmark (MPSG_MODE_AUTO would pick PRECISE whenever its 6 planes fit)."""
     import torch
 
     policy = policy or PrecisionPolicy()

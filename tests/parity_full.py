@@ -47,15 +47,19 @@ def site_classes(bonds):
     return left, inner, right
 
 
-def run(config, n, seed=7, mps_seed=42, threads=None, f32=False, scheme=0, m_override=0, log=print):
+def run(config, n, seed=7, mps_seed=42, threads=None, f32=False, scheme=0, m_override=0, log=print,
+        generated=True):
     m, chi, d = CONFIGS[config]
     if m_override:
         m = m_override
     t0 = time.time()
     pol = P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX)
-    smp, lams = build_synthetic(m, chi, d, seed=mps_seed, policy=pol, scheme=scheme)
+    # generated=True: the same chain (tests/test_gpu_parity.py::test_generated_supply_equals_resident_chain)
+    # held as its generators -- a few hundred MB of HBM instead of the resident state (c3: 153 GB)
+    smp, lams = build_synthetic(m, chi, d, seed=mps_seed, policy=pol, scheme=scheme, mode=P.Mode.SPLIT,
+                                generated=generated)
     bonds = list(smp.bond_dims)
-    scheme_name = "3M" if smp.scheme == P.Scheme.M3 else "4M"
+    scheme_name = ("3M" if smp.scheme == P.Scheme.M3 else "4M") + " " + smp.mode.name
     t_build = time.time() - t0
     st = P.RunStats()
     gpu_rows = smp.sample(0, n, seed, stats=st)
@@ -109,6 +113,7 @@ def run(config, n, seed=7, mps_seed=42, threads=None, f32=False, scheme=0, m_ove
         "config": config, "M": m, "chi": chi, "d": d, "samples": n, "mps_seed": mps_seed, "seed": seed,
         "scheme": scheme_name,
         "oracle": "reference (oracle/_ref), site-streamed decoded Gamma, F64 + PerSampleMax, threaded",
+        "gamma_supply": "generated (regenerated on the device)" if generated else "resident",
         "draws_checked": int(live[:, :, 0].sum()),
         "near_boundary_draws_reference_path": int(near.sum()),
         "near_boundary_draws_gpu_device_counter": int(st.near_boundary_draws),
@@ -146,11 +151,12 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--scheme", default="auto", choices=["auto", "3m", "4m"])
+    ap.add_argument("--supply", default="generated", choices=["generated", "resident"])
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     scheme = {"auto": 0, "3m": 3, "4m": 4}[a.scheme]
     r = run(a.config, a.samples, threads=a.threads or None, f32=a.f32, scheme=scheme, m_override=a.sites,
-            log=lambda s: print(s, file=sys.stderr, flush=True))
+            log=lambda s: print(s, file=sys.stderr, flush=True), generated=a.supply == "generated")
     txt = json.dumps(r, indent=1)
     if a.out:
         os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)

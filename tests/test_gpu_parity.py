@@ -101,14 +101,16 @@ def test_contract_site_numerics(pkg, gold, mode, scheme):
         assert rel < tol, (i, rel)
 
 
-@pytest.mark.parametrize("scheme", [3, 4])
+@pytest.mark.parametrize("scheme,mode", [(3, 1), (4, 1), (3, 0)])
 @pytest.mark.parametrize("name", ["c1", "c1b"])
-def test_c1_strings_and_marginals(pkg, gold, name, scheme):
+def test_c1_strings_and_marginals(pkg, gold, name, scheme, mode):
+    """mode 1 = SPLIT (the benchmark's), 0 = AUTO (F64 compute: PRECISE, the state fits)."""
     z = np.load(f"{gold}/{name}.npz")
     mps = O.load_npz_mps(z)
     n, seed = int(z["n"]), int(z["seed"])
     smp = pkg.GpuSampler(to_state(pkg, mps), pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX),
-                         scheme=pkg.Scheme(scheme))
+                         scheme=pkg.Scheme(scheme), mode=pkg.Mode(mode))
+    assert smp.mode == (pkg.Mode.PRECISE if mode == 0 else pkg.Mode.SPLIT)
     dec = decoded_mps(smp, mps)
     ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, n, seed, want_marginals=True)
     gpu_rows = smp.sample(0, n, seed)
