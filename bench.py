@@ -467,6 +467,22 @@ def main():
         link = {"h2d_gb_per_step": h2d / args.steps / 1e9, "link_peak_gbs": link_gbs,
                 "achieved_gbs": h2d / t_max / 1e9, "t_link_s": t_link, "t_tensor_s": t_tensor,
                 "bound": "link" if t_link > t_tensor else "tensor"}
+    supply = None
+    if generated:
+        # every pass regenerates each site of this rank's column shard: the generator reads its base
+        # block twice (column maxima, then the packed planes) and writes the fp16 planes
+        b = smp.bond_dims
+        planes = 3 if scheme == "3M" else 2
+        per_pass = 0
+        for i in range(cfg["M"]):
+            w = -(-b[i + 1] // tp)
+            per_pass += 2 * 8 * b[i] * w * cfg["d"] + planes * 2 * b[i] * w * cfg["d"]
+        t_tensor = gemm_flops / args.steps / (sustained * 1e12)
+        t_hbm = per_pass / (hbm * 1e9)
+        supply = {"kind": "generated on the device (mpsg_generated_*)", "bytes_per_step": per_pass,
+                  "hbm_peak_gbs": hbm, "achieved_gbs": per_pass * args.steps / t_max / 1e9,
+                  "t_supply_s_at_hbm_peak": t_hbm, "t_tensor_s_at_peak": t_tensor,
+                  "bound": "hbm" if t_hbm > t_tensor else "tensor"}
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.mode}_p{P_pass}.json")
     if os.path.exists(prof):
@@ -530,6 +546,7 @@ def main():
                          "gemm_share_of_step": gemm_s / dev_s if dev_s > 0 else None},
             "cpu_baseline": cpu,
             "host_link": link,
+            "gamma_supply": supply,
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": e2e_h2d // max(args.e2e_steps, 1),
                     "d2h_bytes_per_step": P_pass * cfg["M"], "mode": e2e_mode,
                     "note": ("mpsg_sample (C ABI) with host output rows; the compressed MPS lives in pinned host "

@@ -1056,6 +1056,13 @@ static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const S
     }();
     ga.group = std::min(ga.g_tiles, env_group > 0 ? env_group : auto_group);
     ga.flags = env_flags;
+    // L2 reuse across raster groups (snake) and, for the second lane, across the lanes' launches
+    static const int env_raster = [] {
+      const char* v = std::getenv("MPSG_3M_RASTER");
+      return v ? std::atoi(v) : 3;
+    }();
+    const bool lane1 = &ln != &dc.lanes[0];
+    ga.raster = (env_raster & 1) | ((env_raster & 2) && lane1 && ga.g_tiles % ga.group == 0 ? 2 : 0);
     ga.cinfo = cinfo;
     ga.temp = slice == 0 ? ln.temp : nullptr;
     ga.pstat = slice == 2 ? nullptr : ln.pstat;

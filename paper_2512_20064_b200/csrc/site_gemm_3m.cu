@@ -56,14 +56,20 @@ int gemm_3m_smem_bytes(bool split) { return split ? Cfg3M<true>::kSmem : Cfg3M<f
 // Unit u -> (Gamma tile m, sample tile t).  Groups of `group` Gamma tiles are swept over all sample
 // tiles (Gamma index fastest), so the group's Gamma planes stay in L2 while each environment tile
 // is fetched from DRAM once per group.
+// raster & 1 (snake): every other group sweeps the sample tiles in reverse, so it starts on the tiles
+// the previous group touched last -- still in L2 -- instead of re-fetching them from DRAM.
+// raster & 2 (reversed groups, whole groups only): the groups run last-to-first, so the second
+// pipeline lane's launch starts on the Gamma group the first lane's launch left in L2.
 __device__ __forceinline__ void unit_coords_3m(int u, const Gemm3MArgs& a, int g_tiles, int& m, int& t) {
   const int per_group = a.group * a.s_tiles;
-  const int g = u / per_group;
+  const int gi = u / per_group;  // processing order
+  const int g = ((a.raster & 2) && g_tiles % a.group == 0) ? (g_tiles / a.group - 1 - gi) : gi;
   const int m0 = g * a.group;
   const int gw = min(a.group, g_tiles - m0);
-  const int r = u - g * per_group;
+  const int r = u - gi * per_group;
   t = r / gw;
   m = m0 + (r - t * gw);
+  if ((a.raster & 1) && (gi & 1)) t = a.s_tiles - 1 - t;
 }
 
 // warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4.. epilogue (kEpiWarps = 4 or 8)

@@ -113,6 +113,7 @@ struct Gemm3MArgs {
   int nt;            // Np / 128: pstat row stride
   int group;         // Gamma tiles per raster group
   int flags;         // diagnostics (0 in production): 32 = clock64 timing probes (g_prof3m)
+  int raster;        // unit order: 1 = snake over sample tiles, 2 = groups last-to-first (site_gemm_3m.cu)
   const float2* cinfo;
   float2* temp;      // null: weights-only contraction (slice-recompute path, no temp stores)
   float2* pstat;

@@ -627,7 +627,7 @@ def test_precise_mode_vs_original_mps(pkg, gold):
     print("precise vs original: max marginal rel err", rel)
     assert rel < MARG_RTOL, rel
     # the default (fp16 Gamma) handle, same comparison against the original chain, for contrast
-    dflt = pkg.GpuSampler(to_state(pkg, mps), pol)
+    dflt = pkg.GpuSampler(to_state(pkg, mps), pol, mode=pkg.Mode.SPLIT)
     rel_d = (np.abs(dflt.marginals(0, ref_rows)[big] - ref_marg[big]) / ref_marg[big]).max()
     print("default (fp16 Gamma) vs original: max marginal rel err", rel_d)
     assert rel_d > rel
@@ -999,3 +999,76 @@ def test_nccl_one_rank_group_generated_chi1024(pkg):
     b.connect_nccl(pkg.sampler.nccl_unique_id())
     x, y = a.sample(0, 4096, 7), b.sample(0, 4096, 7)
     assert (x != y).any(axis=1).sum() <= 1
+
+
+# ---- multi-rank paths through libmpsg (gloo process group; ranks share the one GPU) --------------
+def _dp_gpu_worker(rank, world, port, gold, q):
+    import os
+    import torch.distributed as dist
+    import paper_2512_20064_b200 as P
+    from paper_2512_20064_b200.parallel import run_data_parallel
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    z = np.load(os.path.join(gold, "c1.npz"))
+    mps = O.load_npz_mps(z)
+    st = P.MpsState(mps.num_sites, mps.phys_dim, list(mps.bond_dims), list(mps.gammas), list(mps.lambdas))
+    smp = P.GpuSampler(st, P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX), mode=P.Mode.SPLIT)
+    out = run_data_parallel(smp.sample, 0, 5000, 7, mps.num_sites)
+    if rank == 0:
+        q.put(out)
+    smp.close()
+    dist.destroy_process_group()
+
+
+def test_data_parallel_two_ranks_libmpsg(pkg, gold):
+    """parallel.run_data_parallel with two processes, each sampling its share on the GPU through
+    libmpsg (gloo for the final gather): the merged rows equal one process's sweep."""
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_dp_gpu_worker, args=(r, 2, port, gold, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = q.get(timeout=300)
+    for p in ps:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in ps)
+    z = np.load(f"{gold}/c1.npz")
+    st = to_state(pkg, O.load_npz_mps(z))
+    one = pkg.GpuSampler(st, pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX),
+                         mode=pkg.Mode.SPLIT).sample(0, 5000, 7)
+    assert np.array_equal(got, one)
+
+
+def test_torchrun_bench_two_ranks_shared_device():
+    """bench.py under torchrun with two ranks (MPSG_BENCH_SHARE_DEVICE=1: both on GPU 0, gloo):
+    whole-job value over both ranks, max-over-ranks timing, one JSON line from rank 0; the
+    reference arm prints from rank 0 only."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MPSG_BENCH_SHARE_DEVICE="1")
+    def cmd(port, *extra):
+        return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
+                "--gpus", "2", "--config", "c2", "--steps", "2", "--warmup", "3", *extra]
+    r = subprocess.run(cmd(29517, "--no-cpu-baseline", "--e2e", "resident", "--e2e-steps", "1"),
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "dp2"
+    assert d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
+    r = subprocess.run(cmd(29518, "--impl", "reference", "--ref-seconds", "1"),
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and json.loads(lines[0])["impl"] == "reference"

@@ -1,6 +1,7 @@
 """Perf probe: per-site device times and algorithmic TFLOP/s for a synthetic chain.
 
 usage: python tools/perf_probe.py M CHI D N [mode] [pass] [scheme 0|3|4] [slice 0|1|2]
+MPSG_PROBE_SUPPLY=generated|stream|resident (default resident) selects the Gamma supply.
 """
 import os
 import sys
@@ -20,9 +21,11 @@ ps = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 scheme = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 slice_ = int(sys.argv[8]) if len(sys.argv) > 8 else 0
 t = time.time()
+supply = os.environ.get("MPSG_PROBE_SUPPLY", "resident")
 smp, lams = build_synthetic(M, chi, d, mode=mode, pass_samples=ps or N, record_site_times=True, scheme=scheme,
-                           slice=slice_)
-print(f"build {time.time()-t:.1f}s state {smp.state_bytes/1e9:.2f} GB scheme {int(smp.scheme)}", flush=True)
+                           slice=slice_, generated=supply == "generated",
+                           host_stream_slots=3 if supply == "stream" else 0)
+print(f"build {time.time()-t:.1f}s state {smp.state_bytes/1e9:.2f} GB scheme {int(smp.scheme)} supply {supply}", flush=True)
 bonds = smp.bond_dims
 rows = torch.empty((N, M), dtype=torch.uint8, device="cuda")
 for rep in range(3):
