@@ -101,7 +101,10 @@ typedef struct mpsg_options {
                                       2: also time every contraction kernel (gemm_seconds) */
   int tp_size;                     /* tensor-parallel group size (0/1 = none): this handle holds
                                       column shard tp_rank of every Gamma_i (balanced_partition of
-                                      chiR, collective.cpp:80-92), the even-site pattern of
+                                      chiR, collective.cpp:80-92, rounded to whole contraction K
+                                      blocks: 64 columns for 3M, 32 for 4M -- so the sharded sweep
+                                      accumulates the unsharded sweep's K blocks in the same order
+                                      and samples bit-identically), the even-site pattern of
                                       parallel.cpp:420-443 applied at every site */
   int tp_rank;
   int host_stream_slots;           /* 0: compressed Gamma resident in HBM.  >= 2: Gamma kept in

@@ -119,11 +119,21 @@ static CUtensorMap make_tma_env(const void* base, uint64_t kshard, uint64_t rows
   return m;
 }
 
-// balanced_partition (collective.cpp:80-92): [begin, end) of part `i` of `extent` over `parts`.
-static void part_range(int extent, int parts, int i, int& b, int& e) {
-  const int base = extent / parts, rem = extent % parts;
-  b = i * base + std::min(i, rem);
-  e = b + base + (i < rem ? 1 : 0);
+// Column shard [begin, end) of part `i` of `extent` over `parts`: the reference's balanced_partition
+// (collective.cpp:80-92) rounded to whole K blocks of `granule` columns -- every shard but the last
+// has round_up(ceil(extent / parts), granule) columns.  A shard of site i's columns is the env K
+// shard of site i + 1; with block-aligned shards the K position of every row l is l itself, so the
+// contraction accumulates exactly the K blocks of the unsharded sweep in the same order (zero
+// blocks appended at most) and a tensor-parallel handle samples bit-identically to an unsharded one.
+static void part_range(int extent, int parts, int i, int& b, int& e, int granule) {
+  if (parts <= 1) {
+    b = 0;
+    e = extent;
+    return;
+  }
+  const int a = round_up((extent + parts - 1) / parts, granule);
+  b = std::min(i * a, extent);
+  e = std::min(b + a, extent);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -422,8 +432,10 @@ namespace mpsg {
 // L2 across the M sweep while the env tiles are re-read once per group.
 constexpr int kGroupPairs = 16;
 
+// K block of the contraction: env shards and Gamma column shards are aligned to it (part_range)
+static int kgran(const mpsg_handle_s& h) { return h.m3 ? kBK3 : kBK; }
 static int kshard_of(const mpsg_handle_s& h, uint64_t bond) {
-  return round_up((static_cast<int>(bond) + h.tp - 1) / h.tp, h.m3 ? kBK3 : kBK);
+  return round_up((static_cast<int>(bond) + h.tp - 1) / h.tp, kgran(h));
 }
 static int kshard_max_of(const mpsg_handle_s& h) {
   int k = kBK;
@@ -722,7 +734,7 @@ static void site_geometry(mpsg_handle_s& h, DevCtx& dc, uint64_t i) {
   SiteDev& s = dc.sites[i];
   s.chil = static_cast<int>(h.bonds[i]);
   s.chir = static_cast<int>(h.bonds[i + 1]);
-  part_range(s.chir, h.tp, h.tp_rank, s.b0, s.width);
+  part_range(s.chir, h.tp, h.tp_rank, s.b0, s.width, kgran(h));
   s.width -= s.b0;
   s.kshard = kshard_of(h, h.bonds[i]);
   s.kp = h.tp * s.kshard;
@@ -741,7 +753,7 @@ static std::vector<int> row_positions(const mpsg_handle_s& h, const SiteDev& s) 
   std::vector<int> lpos(s.chil);
   for (int q = 0; q < h.tp; ++q) {
     int b, e;
-    part_range(s.chil, h.tp, q, b, e);
+    part_range(s.chil, h.tp, q, b, e, kgran(h));
     for (int l = b; l < e; ++l) lpos[l] = q * s.kshard + (l - b);
   }
   return lpos;
@@ -1879,7 +1891,7 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
     std::vector<int> lpos(s.chil);
     for (int q = 0; q < h->tp; ++q) {
       int b, e;
-      part_range(s.chil, h->tp, q, b, e);
+      part_range(s.chil, h->tp, q, b, e, kgran(*h));
       for (int l = b; l < e; ++l) lpos[l] = q * s.kshard + (l - b);
     }
     for (int l = 0; l < s.chil; ++l)

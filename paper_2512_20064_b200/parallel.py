@@ -1,8 +1,9 @@
 """Multi-GPU executors (one process per GPU, torch.distributed for the plumbing).
 
 Tensor parallel — the reference's even-site double-site scheme (parallel.cpp:420-443) applied at
-every site: each rank of a group of p2 holds the column shard balanced_partition(chiR, p2)[rank]
-of every Gamma_i (so chi >= 4096 chains are split across HBMs), contracts it against the full
+every site: each rank of a group of p2 holds the column shard tp_partition(chiR, p2, granule)[rank]
+of every Gamma_i (balanced_partition rounded to whole contraction K blocks, so that a sharded
+sweep accumulates exactly the unsharded sweep's K blocks and samples bit-identically to it) (so chi >= 4096 chains are split across HBMs), contracts it against the full
 environment, exchanges the small per-(sample, outcome) (weight, max) partials and draws the same
 outcome on every rank, then all-gathers the environment shards.  The exchange runs inside libmpsg
 (NCCL, or an in-process group for ranks sharing a process); ``tp_connect_nccl`` shares the NCCL id
@@ -32,6 +33,22 @@ def balanced_partition(extent: int, parts: int) -> List[Tuple[int, int]]:
         out.append((at, at + n))
         at += n
     return out
+
+
+def tp_partition(extent: int, parts: int, granule: int) -> List[Tuple[int, int]]:
+    """Column shards of a tensor-parallel group (engine.cu part_range): balanced_partition
+    (collective.cpp:80-92) rounded to whole K blocks of `granule` columns (64 for the 3M scheme,
+    32 for 4M); every shard but the last holds round_up(ceil(extent / parts), granule) columns,
+    trailing shards may be empty."""
+    if parts <= 1:
+        return [(0, extent)]
+    a = -(-(-(-extent // parts)) // granule) * granule
+    return [(min(i * a, extent), min(i * a + a, extent)) for i in range(parts)]
+
+
+def tp_granule(scheme: int) -> int:
+    """K block of a handle's contraction scheme (MPSG_SCHEME_3M: 64, MPSG_SCHEME_4M: 32)."""
+    return 64 if scheme == 3 else 32
 
 
 def rank_range(first: int, count: int, rank: int, world: int) -> Tuple[int, int]:
@@ -126,7 +143,8 @@ class TensorParallelLocal:
         for r, s in enumerate(self.ranks):
             part = np.zeros_like(full)
             _check(_lib.lib().mpsg_decoded_gamma(s._h, site, part.ctypes.data_as(_lib._pd)))
-            c0, c1 = balanced_partition(b[site + 1], len(self.ranks))[r]
+            gran = tp_granule(_lib.lib().mpsg_scheme(s._h))
+            c0, c1 = tp_partition(b[site + 1], len(self.ranks), gran)[r]
             full[:, c0:c1, :] = part[:, c0:c1, :]
         return full
 
