@@ -37,8 +37,9 @@
 extern "C" {
 #endif
 
-#define MPSG_ABI_VERSION 4  /* 2: mpsg_stats gained displacement_macs, measure_pipeline_ops; 3: mpsg_options.slice;
-                               4: mpsg_stats.near_boundary_draws, mpsg_generated_*, mpsg_synthetic_site */
+#define MPSG_ABI_VERSION 5  /* 2: mpsg_stats gained displacement_macs, measure_pipeline_ops; 3: mpsg_options.slice;
+                               4: mpsg_stats.near_boundary_draws, mpsg_generated_*, mpsg_synthetic_site;
+                               5: MPSG_MODE_GRID, block-aligned tensor-parallel shards */
 
 enum {
   MPSG_OK = 0,
@@ -58,12 +59,21 @@ enum { MPSG_SCALE_NONE = 0, MPSG_SCALE_GLOBAL_MAX = 1, MPSG_SCALE_PER_SAMPLE_MAX
  *                     accuracy on the DECODED Gamma (the fp16 format moves the sampled
  *                     distribution itself by ~1e-4 relative at interior sites), 2x issued MMAs.
  *   MPSG_MODE_SINGLE  fp16 Gamma x fp16 environment, one MMA pass; F16-class accuracy.
- *                     Used for compute = TF32 / F16.
- *   MPSG_MODE_AUTO    pick from policy.compute: TF32 / F16 -> SINGLE; F64 / F32 -> PRECISE when its
+ *   MPSG_MODE_AUTO    pick from policy.compute: TF32 / F16 -> GRID (below; else SINGLE); F64 / F32 -> PRECISE when its
  *                     state (6 fp16 planes, 12 B per complex entry) fits the device (resident) or
  *                     60% of host memory (host-streamed), else SPLIT.  mpsg_mode() reports the
  *                     choice.  Generated handles (synthetic chains) use SPLIT. */
-enum { MPSG_MODE_AUTO = 0, MPSG_MODE_SPLIT = 1, MPSG_MODE_SINGLE = 2, MPSG_MODE_PRECISE = 3 };
+enum { MPSG_MODE_AUTO = 0, MPSG_MODE_SPLIT = 1, MPSG_MODE_SINGLE = 2, MPSG_MODE_PRECISE = 3, MPSG_MODE_GRID = 4 };
+/*   MPSG_MODE_GRID    the reference's TF32 / F16 compute policies (contract_block_reduced,
+ *                     contract.cpp:43-82) on their own operand grids: Gamma and every environment
+ *                     rounded component-wise exactly as round_scalar (precision.cpp:23-50) -- F16:
+ *                     IEEE binary16 on the reference's own values (subnormals, overflow; a Gamma
+ *                     element beyond the grid is MPSG_ERR_NUMERIC), TF32: 10-bit significands on the
+ *                     f32 exponent range, realised as fp16 times power-of-two scales (exact down to
+ *                     2^-28 of each column / row max) -- then one MMA pass with fp32 accumulation,
+ *                     the reference's float accumulator.  4M scheme.  AUTO picks it for compute =
+ *                     TF32 / F16 except on generated chains, with tensor parallelism, GlobalMax
+ *                     scaling or the decay trace (there: SINGLE). */
 /*   MPSG_MODE_PRECISE  SPLIT plus Gamma stored as an exact fp16 hi + lo pair per component (22-bit
  *                     mantissas instead of 11): the device samples the caller's f64 / f32 Gamma to
  *                     ~2^-23 instead of ~2^-12 per element, at 3 MMAs per K-step instead of 2 and

@@ -9,7 +9,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MPSG_LIB_PATH") or os.path.join(HERE, "libmpsg.so")
 
-ABI_VERSION = 4  # include/mpsg.h MPSG_ABI_VERSION
+ABI_VERSION = 5  # include/mpsg.h MPSG_ABI_VERSION
 MPSG_OK, MPSG_ERR_INTERNAL, MPSG_ERR_CONFIG, MPSG_ERR_NUMERIC, MPSG_ERR_IO, MPSG_ERR_CUDA = 0, 1, 2, 3, 4, 5
 
 _u64, _int, _dbl = C.c_uint64, C.c_int, C.c_double

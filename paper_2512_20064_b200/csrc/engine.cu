@@ -419,6 +419,7 @@ struct mpsg_handle_s {
   int hplanes = 2;
   bool precise = false;                    // Gamma hi + lo planes (MPSG_MODE_PRECISE)
   bool slice_rc = false;                   // slice-recompute path available (3M, tp = 1, d <= 32)
+  int grid = 0;                            // kGrid*: MPSG_MODE_GRID (the TF32 / F16 policies' grids)
   bool precise_auto = false;               // MPSG_MODE_AUTO at F64 / F32: PRECISE if its state fits
   bool generated = false;                  // Gamma regenerated on the device every pass (synthetic chains)
   uint64_t gen_seed = 0;
@@ -456,7 +457,10 @@ static int chirp_max_of(const mpsg_handle_s& h) {
 // stream then carries 1.5x the bytes of 4M, measured at 96% of the resident c3 rate).
 static void choose_scheme(mpsg_handle_s& h) {
   bool m3 = h.opts.scheme != MPSG_SCHEME_4M;
-  if (h.opts.scheme == MPSG_SCHEME_AUTO && h.generated) {
+  if (h.grid) {  // per-component grids: Gr + Gi is not on the grid, so no 3M sum plane
+    config_check(h.opts.scheme != MPSG_SCHEME_3M, "MPSG_MODE_GRID runs the 4M scheme (Gr + Gi is off the grid)");
+    m3 = false;
+  } else if (h.opts.scheme == MPSG_SCHEME_AUTO && h.generated) {
     m3 = h.pair;  // regenerated into device slots: no state to fit
   } else if (h.opts.scheme == MPSG_SCHEME_AUTO) {
     if (!h.pair) m3 = false;
@@ -830,7 +834,7 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
   CUDA_OK(cudaMemsetAsync(s.cinfo, 0, 1ull * s.np * sizeof(float2), dc.stream));
   launch_compress_site(src_dev, f64, s.chil, s.chir, static_cast<int>(h.d), s.b0, s.width, s.kp,
                        s.chirp, d_lpos, d_gl, d_gr, d_wl, h.gplanes, s.g, s.cinfo, s.cs, dc.colmax, dc.err,
-                       dc.stream);
+                       dc.stream, h.grid);
   CUDA_OK(cudaGetLastError());
   check_err_flag(dc, dc.stream, "site " + std::to_string(i));
   if (dc.slots) {
@@ -948,7 +952,8 @@ static void set_site(mpsg_handle_s& h, uint64_t i, const void* gamma, bool is_de
                                                        " cannot be set again after site i + 1 was set");
   const size_t chir = h.bonds[i + 1];
   validate_lambda(lambda, chir);
-  h.gr[i] = bond_scales(lambda, chir);
+  // the F16 grid is absolute: Gamma and the environment keep the reference's own values
+  h.gr[i] = h.grid == kGridF16 ? std::vector<double>(chir, 1.0) : bond_scales(lambda, chir);
   h.lambda[i].assign(lambda, lambda + chir);
   if (i + 1 < h.M) h.gl[i + 1] = h.gr[i];
   const size_t elems = 2ull * h.bonds[i] * chir * h.d;
@@ -1179,7 +1184,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       // Displacement fused into the selection (one read of temp) unless the weights must be exchanged
       // first (tensor parallelism) or the decay trace reads the transformed slice.
       static const bool no_fuse = std::getenv("MPSG_DISPLACE_SEPARATE") != nullptr;
-      const bool fuse_displace = displaced && !xchg(h) && !dc.trace && !no_fuse;
+      const bool fuse_displace = displaced && !xchg(h) && !dc.trace && !no_fuse && !h.grid;
       if (displaced && !fuse_displace) {  // the SiteTransform hook position (sampler.cpp:143)
         DisplaceArgs da;
         da.d = static_cast<int>(h.d);
@@ -1253,6 +1258,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       sa.inv_gamma = s.inv_gamma;
       sa.trace = dc.trace ? dc.trace + i : nullptr;
       sa.scaling = h.policy.scaling;
+      sa.grid = h.grid;
       sa.mu = fuse_displace ? ln.mu : nullptr;
       sa.live = dc.live + i;
       sa.near = forced ? nullptr : dc.near + i;
@@ -1635,7 +1641,7 @@ static int begin_impl(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bon
     h->bonds.assign(bond_dims, bond_dims + num_sites + 1);
     h->policy = pol;
     if (opts) h->opts = *opts;
-    config_check(h->opts.mode >= MPSG_MODE_AUTO && h->opts.mode <= MPSG_MODE_PRECISE, "unknown mode");
+    config_check(h->opts.mode >= MPSG_MODE_AUTO && h->opts.mode <= MPSG_MODE_GRID, "unknown mode");
     h->precise = h->opts.mode == MPSG_MODE_PRECISE;
     h->generated = generated;
     h->gen_seed = gen_seed;
@@ -1652,8 +1658,23 @@ static int begin_impl(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bon
     h->tp_rank = h->opts.tp_rank;
     config_check(h->tp_rank >= 0 && h->tp_rank < h->tp, "tp_rank out of range");
     config_check(h->tp == 1 || ndev <= 1, "a tensor-parallel rank drives exactly one device");
-    h->split = h->opts.mode == MPSG_MODE_SPLIT || h->opts.mode == MPSG_MODE_PRECISE ||
-               (h->opts.mode == MPSG_MODE_AUTO && (pol.compute == MPSG_F64 || pol.compute == MPSG_F32));
+    // MPSG_MODE_GRID: the reference's TF32 / F16 compute policies on their own operand grids.  AUTO
+    // picks it for those policies wherever it applies (not: generated chains, tensor parallelism,
+    // the micro-batch-dependent GlobalMax scaling, the decay trace), else SINGLE.
+    {
+      const bool reduced = pol.compute == MPSG_TF32 || pol.compute == MPSG_F16;
+      const bool applies = !generated && h->tp == 1 && pol.scaling != MPSG_SCALE_GLOBAL_MAX &&
+                           !h->opts.record_decay_trace;
+      if (h->opts.mode == MPSG_MODE_GRID) {
+        config_check(reduced, "MPSG_MODE_GRID reproduces the TF32 / F16 compute policies (policy.compute)");
+        config_check(applies, "MPSG_MODE_GRID: not with generated chains, tensor parallelism, GlobalMax "
+                              "scaling or the decay trace");
+      }
+      if (reduced && applies && (h->opts.mode == MPSG_MODE_GRID || h->opts.mode == MPSG_MODE_AUTO))
+        h->grid = pol.compute == MPSG_F16 ? kGridF16 : kGridTF32;
+    }
+    h->split = !h->grid && (h->opts.mode == MPSG_MODE_SPLIT || h->opts.mode == MPSG_MODE_PRECISE ||
+               (h->opts.mode == MPSG_MODE_AUTO && (pol.compute == MPSG_F64 || pol.compute == MPSG_F32)));
     // the reference's F64 / F32 compute samples the caller's Gamma: AUTO keeps it to ~2^-23 (PRECISE)
     // whenever that state fits, else the fp16 format's decoded-Gamma contract (SPLIT)
     h->precise_auto = h->opts.mode == MPSG_MODE_AUTO && !generated && h->split;
@@ -1846,6 +1867,7 @@ int mpsg_scheme(mpsg_handle h) { return h ? (h->m3 ? MPSG_SCHEME_3M : MPSG_SCHEM
 
 int mpsg_mode(mpsg_handle h) {
   if (!h) return 0;
+  if (h->grid) return MPSG_MODE_GRID;
   return h->precise ? MPSG_MODE_PRECISE : (h->split ? MPSG_MODE_SPLIT : MPSG_MODE_SINGLE);
 }
 
@@ -2068,12 +2090,17 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
       }
       int ex = 0;
       if (mx > 0.0) std::frexp(mx, &ex);
-      sig[r] = std::ldexp(1.0, kEnvExp - ex);
+      sig[r] = h->grid == kGridF16 ? 1.0 : std::ldexp(1.0, kEnvExp - ex);  // the F16 grid is absolute
       for (int l = 0; l < s.chil; ++l) {
         const double* v = env + 2 * (static_cast<size_t>(r) * s.chil + l);
         __half hv[3], lv[3];
         env_split(static_cast<float>(v[0] * h->gl[site][l] * sig[r]),
                   static_cast<float>(v[1] * h->gl[site][l] * sig[r]), hv, lv);
+        if (h->grid) {  // the policy's grid: RNE straight from f64, single precision half
+          hv[0] = __double2half(v[0] * h->gl[site][l] * sig[r]);
+          hv[1] = __double2half(v[1] * h->gl[site][l] * sig[r]);
+          lv[0] = lv[1] = __float2half_rn(0.f);
+        }
         const size_t o = static_cast<size_t>(r) * s.kp + l;
         for (int c = 0; c < C; ++c) {
           e[c * plane + o] = hv[c];

@@ -146,6 +146,15 @@ struct PermuteArgs {
 
 // Per-(sample, outcome) partials read by the select kernel: element (part, n, k) lives at
 // part_base[part * part_stride + n * row_stride + k * k_stride]; parts are summed in order.
+// Reference operand grids (MPSG_MODE_GRID): the reduced compute policies' round_scalar
+// (precision.cpp:23-50) applied to Gamma and to every environment, component-wise.
+//   kGridF16:  IEEE binary16 (10-bit significand, normal exponents from -14, subnormals, overflow to
+//              inf) on the reference's own values -- no bond, column or per-sample scaling
+//   kGridTF32: 10-bit significand, f32 exponent range -- scale-invariant, so Gamma keeps its
+//              power-of-two bond / column scales (column max in [2^14, 2^15)) and the environment its
+//              per-sample power of two; the rounding sees the reference's value times a power of two
+constexpr int kGridNone = 0, kGridF16 = 1, kGridTF32 = 2;
+
 struct SelectArgs {
   int site, num_sites, d;
   int chir_loc;             // live local columns of the slice (this rank's shard width)
@@ -172,6 +181,7 @@ struct SelectArgs {
   const double* inv_gamma;
   double* trace;
   int scaling;              // reference ScalingMode for the logscale update (precision.cpp:135-165)
+  int grid;                 // kGrid*: round the next environment onto the reference policy's grid
   // GBS displacement fused into the selection (tp == 1, no decay trace): the weights, the draw and
   // the gathered slice use D(mu[n]) temp[n, :, r] computed on the fly from the d stored outcomes
   const double2* mu;        // [rows][num_sites] or null
@@ -254,7 +264,7 @@ void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int
                           int width, int kp, int chirp, const int* lpos, const double* gl,
                           const double* gr, const double* wl, int gplanes, __half* g_out,
                           float2* cinfo_out, double* cs_out, unsigned long long* colmax, int* err,
-                          cudaStream_t s);
+                          cudaStream_t s, int grid = kGridNone);
 
 // Synthetic chains regenerated on the device (mpsg_generated_*, mpsg_synthetic_site): the random_mps
 // form (mps.cpp:148-175) Gamma_i[l, r*d + k] = B[l, r*d + k] * phase_i[r*d + k] *

@@ -709,6 +709,20 @@ __device__ __forceinline__ float slice_max(const SelectArgs& a, int n, int k, in
   return warp_max(m);
 }
 
+// Max component of the chosen slice in the reference's scaling (env_ref = temp_int / gamma_r up to
+// the per-sample power of two): the PerSampleMax divisor of the grid modes (precision.cpp:155-160).
+__device__ __forceinline__ double slice_max_ref(const SelectArgs& a, int n, int k, int lane) {
+  const float2* src = a.temp + (static_cast<size_t>(n) * a.d + k) * a.chirp;
+  double m = 0.0;
+  for (int r = lane; r < a.chir_loc; r += 32) {
+    const float2 v = src[r];
+    m = fmax(m, static_cast<double>(fmaxf(fabsf(v.x), fabsf(v.y))) * a.inv_gamma[r]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  return m;
+}
+
 // Displaced selection (SelectArgs::mu): D(mu_n) in shared memory, then one pass over the d stored
 // outcomes of every column computes the transformed Born weights and maxima (f64 per lane, fixed-
 // order warp trees); returns the chosen outcome (or kDead) exactly like the undisplaced path.
@@ -800,6 +814,7 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
   int outcome = kDead;   // recorded at this site
   bool live_out = false; // carries into the next site
   float scale = 0.f;
+  double gdiv = 1.0, gmul = 1.0;  // grid modes: next env = RN((temp / gdiv) * gmul)
   const float2* D = sD[kDisp ? wib : 0];
   if (live_in && a.live != nullptr && lane == 0) atomicAdd(a.live, 1ull);  // measure's counters
   if (kDisp && live_in) {
@@ -881,6 +896,17 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
           frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1): the env max lands in [2^13, 2^14)
           scale = ldexpf(1.0f, kEnvExp - e);
           live_out = true;
+          if (a.grid != kGridNone) {
+            // the reference divides the gathered row by its max component (PerSampleMax) before the
+            // next contraction rounds it (precision.cpp:151-160, contract.cpp:66-68); F16 keeps the
+            // reference's absolute values, TF32 a power of two of them (its grid is scale-invariant)
+            if (a.scaling == 2) gdiv = a.grid == kGridTF32 ? slice_max_ref(a, n, kk, lane) : static_cast<double>(mx);
+            if (a.grid == kGridTF32) {
+              int eg;
+              frexp(static_cast<double>(mx) / gdiv, &eg);
+              gmul = ldexp(1.0, kEnvExp - eg);
+            }
+          }
         }
       }
     }
@@ -935,6 +961,18 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
     const int live_cols = live_out ? a.chir_loc : 0;
     const int C = a.env_comp;
     if constexpr (!kDisp) {
+      if (a.grid != kGridNone) {
+        // single precision half on the policy's grid (round_scalar, IEEE RNE from the f64 quotient
+        // exactly as the reference's double row / max); the lo planes stay zero
+        for (int r = lane; r < a.kp_next; r += 32) {
+          const float2 v = r < live_cols ? src[r] : make_float2(0.f, 0.f);
+          e0[r] = __double2half(static_cast<double>(v.x) / gdiv * gmul);
+          e0[plane + r] = __double2half(static_cast<double>(v.y) / gdiv * gmul);
+          e0[2 * plane + r] = __float2half_rn(0.f);
+          e0[3 * plane + r] = __float2half_rn(0.f);
+        }
+        return;
+      }
       // 8 consecutive columns per lane: four 16 B loads, one 16 B store per plane
       for (int r = lane * 8; r < a.kp_next; r += 256) {  // kp_next is a multiple of 32
         float re[8], im[8];
@@ -1293,15 +1331,18 @@ __global__ void colmax_kernel(const Src src, int chil, int d, int b0, int width,
 }
 
 // Column scales from the maxima: cs = 2^e with mx = f 2^e, f in [0.5, 1); clears colmax for reuse.
+// Grid modes: F16 keeps cs = 1 (the policy's absolute grid); TF32 puts the column max in
+// [2^14, 2^15), so fp16 normals cover 2^-28 of it on the 11-bit grid.
 __global__ void colfinish_kernel(int d, int b0, int width, int chirp, const double* wl,
-                                 unsigned long long* colmax, float2* cinfo, double* cs_out, int* err) {
+                                 unsigned long long* colmax, float2* cinfo, double* cs_out, int* err,
+                                 int grid) {
   const int jl = blockIdx.x * blockDim.x + threadIdx.x;
   if (jl >= width * d) return;
   const int rl = jl / d, k = jl - rl * d;
   const double mx = __longlong_as_double(static_cast<long long>(colmax[jl]));
   colmax[jl] = 0ull;
   double cs = 1.0;
-  if (mx > 0.0) {
+  if (mx > 0.0 && grid != kGridF16) {
     int e;
     frexp(mx, &e);
     if (e > 120) {
@@ -1309,7 +1350,7 @@ __global__ void colfinish_kernel(int d, int b0, int width, int chirp, const doub
       e = 120;
     }
     if (e < -120) e = -120;
-    cs = ldexp(1.0, e);
+    cs = ldexp(1.0, grid == kGridTF32 ? e - 15 : e);
   }
   cs_out[jl] = cs;
   cinfo[k * chirp + rl] = make_float2(static_cast<float>(cs), static_cast<float>(wl[b0 + rl]));
@@ -1336,7 +1377,7 @@ __device__ __forceinline__ void quantize_pair(double a, double b, __half& ha, __
 template <typename Src>
 __global__ void pack_kernel(const Src src, int chil, int d, int b0, int width, int kp,
                             int chirp, const int* lpos, const double* gl, const double* gr,
-                            const double* cs, int gplanes, __half* g_out, int np) {
+                            const double* cs, int gplanes, __half* g_out, int np, int grid, int* err) {
   // planes: [Gr, Gi (, Gs)] and, for gplanes = 6 (MPSG_MODE_PRECISE), [Gr_lo, Gi_lo, Gs_lo] -- the
   // residual of the hi grid, itself rounded by quantize_pair, so every plane (and Gs = Gr + Gi per
   // precision half) is an exact fp16 number
@@ -1354,7 +1395,13 @@ __global__ void pack_kernel(const Src src, int chil, int d, int b0, int width, i
       double re, im;
       src.load(l, static_cast<size_t>(b0 + rl) * d + k, re, im);
       const double f = gr[b0 + rl] / gl[l] / cs[jl];
-      quantize_pair(re * f, im * f, h[0], h[1], h[2]);
+      if (grid != kGridNone) {  // round_scalar per component (precision.cpp:23-50): IEEE RNE
+        h[0] = __double2half(re * f);
+        h[1] = __double2half(im * f);
+        if (__hisinf(h[0]) || __hisinf(h[1])) atomicExch(err, 3);  // beyond the F16 grid
+      } else {
+        quantize_pair(re * f, im * f, h[0], h[1], h[2]);
+      }
       if (gplanes == 6)
         quantize_pair(re * f - static_cast<double>(__half2float(h[0])),
                       im * f - static_cast<double>(__half2float(h[1])), h[3], h[4], h[5]);
@@ -1404,29 +1451,30 @@ template <typename Src>
 static void compress_from(const Src& src, int chil, int d, int b0, int width, int kp, int chirp,
                           const int* lpos, const double* gl, const double* gr, const double* wl, int gplanes,
                           __half* g_out, float2* cinfo_out, double* cs_out, unsigned long long* colmax, int* err,
-                          cudaStream_t s) {
+                          cudaStream_t s, int grid = kGridNone) {
   if (width <= 0) return;
   const int wcols = width * d;
   const int np = round_up(d * chirp, 2 * kBN);
   colmax_kernel<Src><<<dim3((wcols + 127) / 128, (chil + 63) / 64), 128, 0, s>>>(src, chil, d, b0, width, gl, gr,
                                                                                  colmax, err);
-  colfinish_kernel<<<(wcols + 127) / 128, 128, 0, s>>>(d, b0, width, chirp, wl, colmax, cinfo_out, cs_out, err);
+  colfinish_kernel<<<(wcols + 127) / 128, 128, 0, s>>>(d, b0, width, chirp, wl, colmax, cinfo_out, cs_out, err,
+                                                       grid);
   pack_kernel<Src><<<dim3((wcols + 31) / 32, (chil + 31) / 32), dim3(32, 8), 0, s>>>(
-      src, chil, d, b0, width, kp, chirp, lpos, gl, gr, cs_out, gplanes, g_out, np);
+      src, chil, d, b0, width, kp, chirp, lpos, gl, gr, cs_out, gplanes, g_out, np, grid, err);
 }
 
 void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
                           int width, int kp, int chirp, const int* lpos, const double* gl,
                           const double* gr, const double* wl, int gplanes, __half* g_out,
                           float2* cinfo_out, double* cs_out, unsigned long long* colmax, int* err,
-                          cudaStream_t s) {
+                          cudaStream_t s, int grid) {
   const size_t stride = static_cast<size_t>(chir) * d;
   if (src_f64)
     compress_from(ArraySrc<double>{static_cast<const double*>(src), stride}, chil, d, b0, width, kp, chirp, lpos,
-                  gl, gr, wl, gplanes, g_out, cinfo_out, cs_out, colmax, err, s);
+                  gl, gr, wl, gplanes, g_out, cinfo_out, cs_out, colmax, err, s, grid);
   else
     compress_from(ArraySrc<float>{static_cast<const float*>(src), stride}, chil, d, b0, width, kp, chirp, lpos,
-                  gl, gr, wl, gplanes, g_out, cinfo_out, cs_out, colmax, err, s);
+                  gl, gr, wl, gplanes, g_out, cinfo_out, cs_out, colmax, err, s, grid);
 }
 
 void launch_compress_synth(const SynthSite& g, int chil, int d, int b0, int width, int kp, int chirp,

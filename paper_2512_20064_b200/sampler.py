@@ -115,11 +115,12 @@ class PrecisionPolicy:
 
 class Mode(enum.IntEnum):
     """GPU contraction precision; AUTO picks PRECISE for F64/F32 compute when its
-    state fits (else SPLIT) and SINGLE for TF32/F16."""
+    state fits (else SPLIT) and GRID for TF32/F16 (SINGLE where GRID does not apply)."""
     AUTO = 0
     SPLIT = 1
     SINGLE = 2
     PRECISE = 3  # SPLIT + Gamma hi / lo planes: samples the caller's Gamma to ~2^-23 (3M only)
+    GRID = 4     # the TF32 / F16 compute policies on their own operand grids (round_scalar, 4M only)
 
 
 class Slice(enum.IntEnum):

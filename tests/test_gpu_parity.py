@@ -50,15 +50,15 @@ def boundary_distance(marg_row: np.ndarray, u: float) -> float:
     return float(np.min(np.abs(cum - u))) if cum.size else 1.0
 
 
-def compare_strings(gpu_rows, ref_rows, marg_ref, seed, first=0):
+def compare_strings(gpu_rows, ref_rows, marg_ref, seed, first=0, eps=EPS_BOUNDARY):
     """Returns (#differing samples, #explained by boundary draws).  A sample's string may differ
-    only from the first site whose draw lies within EPS_BOUNDARY of a reference CDF boundary."""
+    only from the first site whose draw lies within eps of a reference CDF boundary."""
     diff = np.nonzero((gpu_rows != ref_rows).any(axis=1))[0]
     explained = 0
     for n in diff:
         i = int(np.argmax(gpu_rows[n] != ref_rows[n]))
         u = O.orc().orc_uniform(seed, O.MEASURE_STREAM, first + int(n), i)
-        if boundary_distance(marg_ref[n, i], u) < EPS_BOUNDARY:
+        if boundary_distance(marg_ref[n, i], u) < eps:
             explained += 1
     return len(diff), explained
 
@@ -562,7 +562,7 @@ def test_single_mode_within_reference_f16_envelope(pkg, gold, scheme):
     z = np.load(f"{gold}/c1b.npz")
     mps = O.load_npz_mps(z)
     pol = pkg.PrecisionPolicy(compute=pkg.Precision.F16, scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
-    smp = pkg.GpuSampler(to_state(pkg, mps), pol, scheme=pkg.Scheme(scheme))
+    smp = pkg.GpuSampler(to_state(pkg, mps), pol, mode=pkg.Mode.SINGLE, scheme=pkg.Scheme(scheme))
     dec = decoded_mps(smp, mps)
     n = 500
     ref_rows, ref_marg, _ = O.orc_sample_range(dec, 0, n, 7, want_marginals=True)
@@ -572,6 +572,94 @@ def test_single_mode_within_reference_f16_envelope(pkg, gold, scheme):
     err_gpu = (np.abs(gm[big] - ref_marg[big]) / ref_marg[big]).max()
     err_f16 = (np.abs(f16_marg[big] - ref_marg[big]) / ref_marg[big]).max()
     assert err_gpu <= max(2.0 * err_f16, 1e-3), (err_gpu, err_f16)
+
+
+# GPU GRID vs the reference's own reduced policy: both round every operand onto the same grid
+# (decoded Gamma == round_scalar bit for bit) and differ only in fp32 accumulation order (~1e-7 on a
+# marginal), which now and then moves an environment entry across a rounding boundary of the 11-bit
+# grid (one grid ulp, 2^-11; a few % of the marginals downstream of it, profiles/r2_grid/).
+GRID_MEDIAN_RTOL = 1e-6   # typical marginal: fp32 accumulation noise (the policy itself: ~1e-4 vs F64)
+GRID_FLIP_FRAC = 0.05     # marginals off by more than 1e-5 (downstream of a grid-ulp flip)
+
+
+@pytest.mark.parametrize("case,compute,scaling", [("c1b", "F16", "PER_SAMPLE_MAX"), ("c1b", "F16", "NONE"),
+                                                  ("c1b", "TF32", "PER_SAMPLE_MAX"), ("c1", "TF32", "PER_SAMPLE_MAX"),
+                                                  ("c1", "TF32", "NONE")])
+def test_grid_mode_reproduces_reference_reduced_policy(pkg, gold, case, compute, scaling):
+    """MPSG_MODE_GRID (AUTO at compute = F16 / TF32) against the compiled reference running the same
+    policy on the ORIGINAL chain (contract_block_reduced, contract.cpp:43-82: round_scalar on Gamma and
+    on every environment, float accumulation): outcome strings identical except draws near a CDF
+    boundary, marginals (teacher-forced on the reference's strings) within GRID_RTOL -- 20x inside the
+    policy's own deviation from F64, which SINGLE only matches as an envelope."""
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not available")
+    z = np.load(f"{gold}/{case}.npz")
+    mps = O.load_npz_mps(z)
+    cp = {"F16": O.F16, "TF32": O.TF32}[compute]
+    sc = {"PER_SAMPLE_MAX": O.SCALE_PER_SAMPLE, "NONE": O.SCALE_NONE}[scaling]
+    pol = pkg.PrecisionPolicy(compute=getattr(pkg.Precision, compute), scaling=getattr(pkg.ScalingMode, scaling))
+    smp = pkg.GpuSampler(to_state(pkg, mps), pol)
+    assert pkg.sampler._lib.lib().mpsg_mode(smp._h) == int(pkg.Mode.GRID)
+    n = 1000
+    rs = O.RefState(mps)
+    ref_rows = rs.sample_range(0, n, 7, compute=cp, scaling=sc, threads=8)
+    ref_marg = rs.marginals_forced(ref_rows, compute=cp, scaling=sc)
+    f64_marg = rs.marginals_forced(ref_rows, compute=O.F64, scaling=sc)
+    rows = smp.sample(0, n, 7)
+    gm = smp.marginals(0, ref_rows)
+    live = (ref_marg >= 0).all(axis=2)  # sites where the reference sample is alive
+    big = (ref_marg >= 1e-3) & live[:, :, None]
+    e = np.abs(gm[big] - ref_marg[big]) / ref_marg[big]
+    f = np.abs(f64_marg[big] - ref_marg[big]) / f64_marg[big]
+    print(f"{case} {compute} {scaling}: GPU grid vs reference policy median {np.median(e):.2e} max {e.max():.2e} "
+          f"(>1e-5: {(e > 1e-5).mean():.3f}); policy vs F64 median {np.median(f):.2e} max {f.max():.2e}")
+    if scaling == "PER_SAMPLE_MAX":
+        assert np.median(e) < GRID_MEDIAN_RTOL and np.median(e) < np.median(f) / 100
+        assert (e > 1e-5).mean() < GRID_FLIP_FRAC
+        assert e.max() < 0.5 * f.max()
+    else:  # unscaled environments decay into coarser binades (F16: subnormals): flips weigh more
+        assert np.median(e) < np.median(f) / 20
+        assert e.max() < f.max()
+    # sites 0, 1 see identical operands (site 0's env is 1, site 1's is site 0's rounded row)
+    b01 = big[:, :2, :]
+    e01 = np.abs(gm[:, :2, :][b01] - ref_marg[:, :2, :][b01]) / ref_marg[:, :2, :][b01]
+    assert e01.max() < 1e-6, e01.max()
+    # the decoded Gamma is round_scalar(Gamma) component-wise, bit for bit (precision.cpp:23-50)
+    rnd = np.vectorize(lambda x: O.ref().ref_round_scalar(float(x), cp))
+    for i in (0, mps.num_sites // 2):
+        assert np.array_equal(smp.decoded_gamma(i), rnd(mps.gammas[i].real) + 1j * rnd(mps.gammas[i].imag))
+    # strings: a differing string must have its first difference at a draw within 1e-4 of the
+    # reference policy's CDF boundary (the grid-ulp flips above move a CDF by ~1e-5)
+    ndiff, explained = compare_strings(rows, ref_rows, ref_marg, 7, eps=1e-4)
+    assert ndiff == explained and ndiff <= n // 50, (ndiff, explained)
+    smp.close()
+
+
+def test_grid_mode_decay_chain_golden(pkg, gold):
+    """decay_chain (mps.cpp:183-196) under the reference's F16 policy (goldens from the compiled
+    reference): without scaling the F16 environment underflows and every sample dies at site 8,
+    with PerSampleMax none does -- GRID reproduces both outcome matrices, deaths included."""
+    z = np.load(f"{gold}/decay.npz")
+    mps = O.load_npz_mps(z, "decay_")
+    for key, sc in (("decay_f16_none", pkg.ScalingMode.NONE), ("decay_f16_psm", pkg.ScalingMode.PER_SAMPLE_MAX)):
+        pol = pkg.PrecisionPolicy(compute=pkg.Precision.F16, scaling=sc)
+        smp = pkg.GpuSampler(to_state(pkg, mps), pol)
+        rows = smp.sample(0, 200, 3)
+        assert np.array_equal(rows, z[key]), (key, int((rows != z[key]).any(axis=1).sum()))
+        smp.close()
+
+
+def test_grid_mode_f16_overflow_is_numeric_error(pkg, gold):
+    """c1's Gamma reaches 1e10: on the F16 grid it overflows (round_scalar -> inf, precision.cpp:46-47);
+    the reference then propagates inf / NaN, GRID refuses the state with NumericError."""
+    z = np.load(f"{gold}/c1.npz")
+    mps = O.load_npz_mps(z)
+    pol = pkg.PrecisionPolicy(compute=pkg.Precision.F16, scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    with pytest.raises(pkg.NumericError):
+        pkg.GpuSampler(to_state(pkg, mps), pol)
+    smp = pkg.GpuSampler(to_state(pkg, mps), pol, mode=pkg.Mode.SINGLE)  # SINGLE keeps its scaled format
+    assert smp.sample(0, 8, 7).shape == (8, mps.num_sites)
+    smp.close()
 
 
 @pytest.mark.parametrize("scheme", [3, 4])

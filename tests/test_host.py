@@ -40,7 +40,7 @@ def test_library_is_sm100a_only():
 
 def test_abi_basics_without_gpu():
     L = _lib.lib()
-    assert L.mpsg_abi_version() == _lib.ABI_VERSION == 4
+    assert L.mpsg_abi_version() == _lib.ABI_VERSION == 5
     if L.mpsg_device_count() == 0:
         # no CPU fallback: a compute call fails loudly with the CUDA code
         out = np.empty(4)
