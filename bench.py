@@ -276,7 +276,9 @@ def main():
     ap.add_argument("--stream-slots", type=int, default=0,
                     help="keep the compressed MPS in pinned host memory and stream it per site "
                          "through this many device slots (0 = resident in HBM)")
-    ap.add_argument("--supply", default="auto", choices=["auto", "resident", "generated"],
+    ap.add_argument("--file-storage", default="f16", choices=["f64", "f32", "f16"],
+                    help="--supply file: storage precision of the MPSB file written and streamed back")
+    ap.add_argument("--supply", default="auto", choices=["auto", "resident", "generated", "file"],
                     help="generated: keep only the chain's generators and regenerate every site on the "
                          "device each pass (auto: the config's default -- c4, c5 chi >= 8192)")
     ap.add_argument("--tp", type=int, default=1,
@@ -336,6 +338,19 @@ def main():
                                                           edge_factor=100.0) if args.schedule_eps > 0 else None),
                              generated=generated, tp_size=tp, tp_rank=tp_rank)
     connect_tp(P, smp, tp, tp_rank, dist, args.tp_exchange)
+    file_path = None
+    if args.supply == "file":
+        # the chain as an MPSB file (the reference's format), then a handle that re-reads it from
+        # storage every pass (mpsg_create_from_file_streamed: reader thread, pinned staging, device
+        # compression) -- the reference's SiteStream path for chains beyond device and host memory
+        if tp > 1:
+            raise SystemExit("--supply file: not with --tp")
+        file_path = os.path.join(os.environ.get("MPSG_BENCH_DIR", "/tmp"), f"mpsg_bench_{args.config}_r{rank}.mpsb")
+        smp.save(file_path, {"f64": P.Precision.F64, "f32": P.Precision.F32, "f16": P.Precision.F16}[args.file_storage])
+        smp.close()
+        smp = P.GpuSampler.from_file(file_path, P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX), mode=mode,
+                                     devices=[local], pass_samples=P_pass, record_site_times=2,
+                                     scheme=P.Scheme({"auto": 0, "3m": 3, "4m": 4}[args.scheme]), streamed=True)
     scheme = "3M" if smp.scheme == P.Scheme.M3 else "4M"
     warm_pass = args.warm_pass or cfg.get("warm_pass", 0) or P_pass
     build_s = time.perf_counter() - t0
@@ -427,6 +442,8 @@ def main():
         e2e_mode = "stream"
     if generated:
         e2e_mode = "generated"
+    if file_path:
+        e2e_mode = "file"
     e2e_h2d = 0
     if e2e_mode == "stream" and not args.stream_slots:
         smp.close()
@@ -483,13 +500,15 @@ def main():
                   "hbm_peak_gbs": hbm, "achieved_gbs": per_pass * args.steps / t_max / 1e9,
                   "t_supply_s_at_hbm_peak": t_hbm, "t_tensor_s_at_peak": t_tensor,
                   "bound": "hbm" if t_hbm > t_tensor else "tensor"}
-    traffic = None
+    traffic = traffic_alg = traffic_src = None
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.mode}_p{P_pass}.json")
     if os.path.exists(prof):
         with open(prof) as f:
             tj = json.load(f)
         if tj.get("kernel", "").startswith("site_gemm_3m") == (scheme == "3M"):
             traffic = tj.get("bytes_per_launch")
+            traffic_alg = tj.get("algorithmic_bytes")
+            traffic_src = os.path.relpath(prof, ROOT)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # the reference's per-MAC rate is flat in chi at this size; a chi <= 4096 site keeps host memory
@@ -524,10 +543,16 @@ def main():
                                            f"{h2d / t_max / 1e9:.1f} GB/s)") if args.stream_slots else
                                           ("regenerated on the device every pass from the chain's generators "
                                            f"({smp.state_bytes / 1e9:.1f} GB of base isometries in HBM), "
-                                           "3 device slots, side stream") if generated else "HBM",
+                                           "3 device slots, side stream") if generated else
+                                          (f"streamed from storage every pass: MPSB {args.file_storage} file "
+                                           f"({smp.state_bytes / 1e9:.1f} GB of Gamma scalars) re-read by a reader "
+                                           "thread into pinned staging, uploaded and compressed on the device "
+                                           f"into 3 slots ({h2d / t_max / 1e9:.1f} GB/s from the file)")
+                                          if file_path else "HBM",
                        "build_seconds": round(build_s, 1)},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
                          "frac": achieved / sustained if achieved else None, "traffic": traffic,
+                         "traffic_algorithmic_bytes": traffic_alg, "traffic_source": traffic_src,
                          "peak_kind": f"bf16 dense sustained ({src})",
                          "kernel": ("site_gemm_3m_kernel" if scheme == "3M" else "site_gemm_pair_kernel")
                                    + " (tcgen05, all sites of the sweep)",
@@ -556,6 +581,9 @@ def main():
                             ("mpsg_sample (C ABI) with host output rows (D2H inside the timed region); the "
                              "sites are regenerated on the device (no Gamma crosses the host link)")
                     if e2e_mode == "generated" else
+                            ("mpsg_sample (C ABI) with host output rows (D2H inside the timed region); every "
+                             "site is read from the MPSB file, uploaded and compressed inside the timed region")
+                    if e2e_mode == "file" else
                             ("mpsg_sample (C ABI) with host output rows (D2H inside the timed region); the "
                              "compressed MPS stays resident in HBM (host memory cannot hold it for every rank)")},
             "clocks": clocks, "gpu_launches": launches, "wall_seconds": wall,

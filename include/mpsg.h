@@ -39,7 +39,8 @@ extern "C" {
 
 #define MPSG_ABI_VERSION 5  /* 2: mpsg_stats gained displacement_macs, measure_pipeline_ops; 3: mpsg_options.slice;
                                4: mpsg_stats.near_boundary_draws, mpsg_generated_*, mpsg_synthetic_site;
-                               5: MPSG_MODE_GRID, block-aligned tensor-parallel shards */
+                               5: MPSG_MODE_GRID, block-aligned tensor-parallel shards,
+                               mpsg_create_from_file_streamed */
 
 enum {
   MPSG_OK = 0,
@@ -244,6 +245,17 @@ int mpsg_synthetic_site(const void* base, uint64_t ld, uint64_t rows, uint64_t c
  * (parallel.hpp:24-52) become mpsg_create_from_file + mpsg_sample. */
 int mpsg_create_from_file(const char* path, const mpsg_policy* policy, const mpsg_options* opts,
                           const int* devices, int ndev, mpsg_handle* out);
+/* The same file, streamed from storage on every pass instead of held: for chains larger than device
+ * and host memory (c4: 13-26 TB).  Only the header and the Lambda vectors are read here; each pass a
+ * reader thread preads the site payloads in chain order into pinned staging buffers and verifies
+ * their checksums (the reference's SiteStream, mps_io.cpp:294-350, checksum as mps_io.cpp:120-146),
+ * the copy stream uploads the raw Gamma scalars (f64 / f32 / f16 storage) and the compression
+ * kernels pack them into the ring of host_stream_slots device slots (default 3) the sweep consumes.
+ * Samples and marginals equal those of mpsg_create_from_file on the same file bit for bit.  A payload
+ * whose checksum fails surfaces as MPSG_ERR_IO from the sampling call (the handle is then unusable).
+ * mpsg_state_bytes reports the Gamma bytes read per pass. */
+int mpsg_create_from_file_streamed(const char* path, const mpsg_policy* policy, const mpsg_options* opts,
+                                   const int* devices, int ndev, mpsg_handle* out);
 /* Write the state as an MPSB file (save_mps, mps_io.cpp:167-210): the decoded Gamma values at
  * `storage` precision (MPSG_F64 / F32 / F16) and the Lambda vectors. */
 int mpsg_save_file(mpsg_handle h, const char* path, int storage);

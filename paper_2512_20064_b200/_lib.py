@@ -68,6 +68,8 @@ SIGNATURES = [
     ("mpsg_contract_site", _int, [C.c_void_p, _u64, _pd, _u64, _pd]),
     ("mpsg_create_from_file", _int, [C.c_char_p, C.POINTER(Policy), C.POINTER(Options),
                                      C.POINTER(_int), _int, C.POINTER(C.c_void_p)]),
+    ("mpsg_create_from_file_streamed", _int, [C.c_char_p, C.POINTER(Policy), C.POINTER(Options),
+                                     C.POINTER(_int), _int, C.POINTER(C.c_void_p)]),
     ("mpsg_save_file", _int, [C.c_void_p, C.c_char_p, _int]),
     ("mpsg_nccl_unique_id", _int, [C.POINTER(C.c_uint8)]),
     ("mpsg_tp_connect_nccl", _int, [C.c_void_p, C.POINTER(C.c_uint8)]),

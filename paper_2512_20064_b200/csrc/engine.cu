@@ -12,6 +12,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <unistd.h>
 #include <nccl.h>
 
@@ -307,6 +308,143 @@ static std::vector<double> bond_scales(const double* lambda, size_t n) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// storage-streamed Gamma (mpsg_create_from_file_streamed): the reference's SiteStream
+// (mps_io.cpp:294-350) as a pass-by-pass supply.  A reader thread preads the MPSB site payloads in
+// chain order (sites 0..M-1, repeated every pass) into a ring of pinned staging buffers and verifies
+// their FNV-1a checksums (mps_io.cpp:120-146); the copy stream uploads the raw Gamma scalars and the
+// compression kernels pack them into the device slot the sweep consumes next.
+// ---------------------------------------------------------------------------------------------
+struct FileMeta {
+  std::string path;
+  std::vector<uint64_t> off, bytes, check;  // per site: payload offset, payload bytes, checksum
+  std::vector<int> prec;                    // per site: storage precision (MPSG_F64 / F32 / F16)
+  std::vector<uint64_t> gbytes;             // per site: Gamma scalar bytes (payload minus Lambda)
+};
+
+static uint64_t fnv1a64(const uint8_t* p, size_t n) {  // mps_io.cpp:18-25
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+// pread of one site payload + checksum verification; throws Error(MPSG_ERR_IO)
+static void read_payload(int fd, const FileMeta& fm, uint64_t i, uint8_t* dst) {
+  size_t got = 0;
+  const size_t want = fm.bytes[i];
+  while (got < want) {
+    const ssize_t r = ::pread(fd, dst + got, want - got, static_cast<off_t>(fm.off[i] + got));
+    if (r <= 0) throw Error(MPSG_ERR_IO, "mps file truncated at site " + std::to_string(i) + ": " + fm.path);
+    got += static_cast<size_t>(r);
+  }
+  if (fnv1a64(dst, want) != fm.check[i])
+    throw Error(MPSG_ERR_IO, "mps file corrupt: checksum mismatch at site " + std::to_string(i));
+}
+
+struct FileReader {
+  const FileMeta* fm = nullptr;
+  int device = 0;
+  int fd = -1;
+  int R = 2;
+  std::vector<uint8_t*> stage;       // pinned, max payload bytes each
+  std::vector<cudaEvent_t> copied;   // the upload from stage[b] is done (recorded by the consumer)
+  std::vector<long long> holds;      // load sequence number held by stage[b] (-1: none)
+  long long next = 0;                // the next sequence number the consumer takes
+  bool stop = false;
+  std::string err;
+  uint64_t bytes_read = 0;
+  double read_seconds = 0.0;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::thread th;
+
+  FileReader(const FileMeta& meta, int dev, int ring) : fm(&meta), device(dev), R(ring) {
+    fd = ::open(meta.path.c_str(), O_RDONLY);
+    if (fd < 0) throw Error(MPSG_ERR_IO, "cannot open: " + meta.path);
+    (void)::posix_fadvise(fd, 0, 0, POSIX_FADV_SEQUENTIAL);
+    uint64_t mx = 1;
+    for (uint64_t b : meta.bytes) mx = std::max(mx, b);
+    stage.assign(R, nullptr);
+    copied.assign(R, nullptr);
+    holds.assign(R, -1);
+    for (int b = 0; b < R; ++b) {
+      CUDA_OK(cudaMallocHost(&stage[b], mx));
+      CUDA_OK(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+    }
+    th = std::thread([this] { run(); });
+  }
+  ~FileReader() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    if (th.joinable()) th.join();
+    for (int b = 0; b < R; ++b) {
+      if (stage[b]) cudaFreeHost(stage[b]);
+      if (copied[b]) cudaEventDestroy(copied[b]);
+    }
+    if (fd >= 0) ::close(fd);
+  }
+  void run() {
+    cudaSetDevice(device);
+    const long long m = static_cast<long long>(fm->off.size());
+    for (;;) {
+      long long q = 0;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        auto pick = [&] {
+          for (q = next; q < next + R; ++q)
+            if (holds[q % R] != q) return true;
+          return false;
+        };
+        cv.wait(lk, [&] { return stop || (err.empty() && pick()); });
+        if (stop) return;
+        holds[q % R] = -1;
+      }
+      const int b = static_cast<int>(q % R);
+      std::string e;
+      try {
+        CUDA_OK(cudaEventSynchronize(copied[b]));  // the previous upload from this buffer is done
+        const auto t0 = std::chrono::steady_clock::now();
+        read_payload(fd, *fm, static_cast<uint64_t>(q % m), stage[b]);
+        read_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        bytes_read += fm->bytes[q % m];
+      } catch (const std::exception& x) {
+        e = x.what();
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        if (e.empty())
+          holds[b] = q;
+        else
+          err = e;
+      }
+      cv.notify_all();
+    }
+  }
+  // Blocks until the payload of load q (site q % M) is staged; q must be the next in sequence.
+  const uint8_t* take(long long q) {
+    std::unique_lock<std::mutex> lk(mu);
+    if (q != next) throw Error(MPSG_ERR_INTERNAL, "file site stream out of sequence");
+    cv.wait(lk, [&] { return holds[q % R] == q || !err.empty(); });
+    if (holds[q % R] != q) throw Error(MPSG_ERR_IO, err);
+    return stage[q % R];
+  }
+  // The upload from load q's staging buffer was enqueued on `s`.
+  void taken(long long q, cudaStream_t s) {
+    CUDA_OK(cudaEventRecord(copied[q % R], s));
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      next = q + 1;
+    }
+    cv.notify_all();
+  }
+};
+
+// ---------------------------------------------------------------------------------------------
 // state
 // ---------------------------------------------------------------------------------------------
 struct SiteDev {
@@ -381,6 +519,9 @@ struct DevCtx {
   std::vector<long long> base_rows, base_cols;
   float2* phase = nullptr;
   std::vector<long long> slot_sig;  // extents of each slot's last fill (its padding is zero)
+  // storage-streamed supply (mpsg_create_from_file_streamed): staging reader + raw device buffers
+  std::unique_ptr<FileReader> reader;
+  std::vector<void*> slot_raw;
   // host-streamed Gamma: ring of device slots filled by a copy stream (sequence q -> slot q % R)
   int slots = 0;
   std::vector<__half*> slot_g;
@@ -423,6 +564,8 @@ struct mpsg_handle_s {
   bool precise_auto = false;               // MPSG_MODE_AUTO at F64 / F32: PRECISE if its state fits
   bool generated = false;                  // Gamma regenerated on the device every pass (synthetic chains)
   uint64_t gen_seed = 0;
+  bool file = false;                       // Gamma streamed from an MPSB file every pass
+  mpsg::FileMeta fmeta;
   std::unique_ptr<mpsg::Comm> comm;
   std::mutex mu;
 };
@@ -460,8 +603,8 @@ static void choose_scheme(mpsg_handle_s& h) {
   if (h.grid) {  // per-component grids: Gr + Gi is not on the grid, so no 3M sum plane
     config_check(h.opts.scheme != MPSG_SCHEME_3M, "MPSG_MODE_GRID runs the 4M scheme (Gr + Gi is off the grid)");
     m3 = false;
-  } else if (h.opts.scheme == MPSG_SCHEME_AUTO && h.generated) {
-    m3 = h.pair;  // regenerated into device slots: no state to fit
+  } else if (h.opts.scheme == MPSG_SCHEME_AUTO && (h.generated || h.file)) {
+    m3 = h.pair;  // regenerated / streamed into device slots: no state to fit
   } else if (h.opts.scheme == MPSG_SCHEME_AUTO) {
     if (!h.pair) m3 = false;
     double state3 = 0.0;
@@ -488,7 +631,9 @@ static void choose_scheme(mpsg_handle_s& h) {
       state6 += 6.0 * 2.0 * round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN) *
                 static_cast<double>(h.tp) * round_up((static_cast<int>(h.bonds[i]) + h.tp - 1) / h.tp, kBK3);
     bool fits = h.pair && h.opts.scheme != MPSG_SCHEME_4M;
-    if (h.opts.host_stream_slots != 0) {
+    if (h.file) {
+      // streamed from storage: only the slot ring is resident, whatever the chain's size
+    } else if (h.opts.host_stream_slots != 0) {
       const double host = static_cast<double>(sysconf(_SC_PHYS_PAGES)) * sysconf(_SC_PAGE_SIZE);
       fits = fits && state6 * (4.0 / 6.0) * h.devs.size() <= 0.6 * host;
     } else {
@@ -508,7 +653,9 @@ static void choose_scheme(mpsg_handle_s& h) {
     for (uint64_t i = 0; i < h.M; ++i)
       state6 += 6.0 * 2.0 * round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN) *
                 static_cast<double>(h.tp) * round_up((static_cast<int>(h.bonds[i]) + h.tp - 1) / h.tp, kBK3);
-    if (h.opts.host_stream_slots != 0) {
+    if (h.file) {
+      // only the slot ring is resident
+    } else if (h.opts.host_stream_slots != 0) {
       const double host = static_cast<double>(sysconf(_SC_PHYS_PAGES)) * sysconf(_SC_PAGE_SIZE);
       config_check(state6 * (4.0 / 6.0) * h.devs.size() <= 0.85 * host,
                    "MPSG_MODE_PRECISE: the hi + lo Gamma planes need " + std::to_string(state6 * 4.0 / 6.0 / 1e9) +
@@ -656,12 +803,23 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
       CUDA_OK(cudaEventCreateWithFlags(&dc.freed[q], cudaEventDisableTiming));
     }
     dc.slot_sig.assign(dc.slots, -1);
+    if (h.file) {  // raw Gamma scalars of a site as stored in the file, one buffer per slot
+      uint64_t rmax = 1;
+      for (uint64_t g : h.fmeta.gbytes) rmax = std::max(rmax, g);
+      dc.slot_raw.assign(dc.slots, nullptr);
+      for (int q = 0; q < dc.slots; ++q) CUDA_OK(cudaMalloc(&dc.slot_raw[q], rmax));
+      dc.reader = std::make_unique<FileReader>(h.fmeta, dc.device, 2);
+    }
   }
 }
 
 static void free_device(DevCtx& dc) {
   cudaSetDevice(dc.device);
   if (dc.stream) cudaStreamSynchronize(dc.stream);
+  if (dc.copy_stream) cudaStreamSynchronize(dc.copy_stream);
+  dc.reader.reset();  // joins the reader thread
+  for (auto p : dc.slot_raw) cudaFree(p);
+  dc.slot_raw.clear();
   for (auto& s : dc.sites) {
     if (!dc.slots) {
       cudaFree(s.g);
@@ -832,7 +990,7 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
   CUDA_OK(cudaMemcpyAsync(d_lpos, lpos.data(), sizeof(int) * s.chil, cudaMemcpyHostToDevice, dc.stream));
   CUDA_OK(cudaMemsetAsync(s.g, 0, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half), dc.stream));
   CUDA_OK(cudaMemsetAsync(s.cinfo, 0, 1ull * s.np * sizeof(float2), dc.stream));
-  launch_compress_site(src_dev, f64, s.chil, s.chir, static_cast<int>(h.d), s.b0, s.width, s.kp,
+  launch_compress_site(src_dev, f64 ? kSrcF64 : kSrcF32, s.chil, s.chir, static_cast<int>(h.d), s.b0, s.width, s.kp,
                        s.chirp, d_lpos, d_gl, d_gr, d_wl, h.gplanes, s.g, s.cinfo, s.cs, dc.colmax, dc.err,
                        dc.stream, h.grid);
   CUDA_OK(cudaGetLastError());
@@ -899,6 +1057,28 @@ static void issue_loads(mpsg_handle_s& h, DevCtx& dc, uint64_t upto) {
     const int slot = static_cast<int>(q % dc.slots);
     const SiteDev& s = dc.sites[q % h.M];
     CUDA_OK(cudaStreamWaitEvent(dc.copy_stream, dc.freed[slot], 0));  // consume q - slots done
+    if (h.file) {  // storage -> pinned staging (reader thread) -> device raw -> compressed slot
+      const uint64_t i = q % h.M;
+      const uint8_t* raw = dc.reader->take(static_cast<long long>(q));
+      CUDA_OK(cudaMemcpyAsync(dc.slot_raw[slot], raw, h.fmeta.gbytes[i], cudaMemcpyHostToDevice, dc.copy_stream));
+      dc.reader->taken(static_cast<long long>(q), dc.copy_stream);
+      const long long sig = (static_cast<long long>(s.np) << 32) ^ (static_cast<long long>(s.kp) << 8) ^
+                            (static_cast<long long>(s.chil) * 131 + s.width);
+      if (dc.slot_sig[slot] != sig) {
+        CUDA_OK(cudaMemsetAsync(dc.slot_g[slot], 0, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half),
+                                dc.copy_stream));
+        CUDA_OK(cudaMemsetAsync(dc.slot_cinfo[slot], 0, 1ull * s.np * sizeof(float2), dc.copy_stream));
+      }
+      dc.slot_sig[slot] = sig;
+      launch_compress_site(dc.slot_raw[slot], h.fmeta.prec[i], s.chil, s.chir, static_cast<int>(h.d), s.b0,
+                           s.width, s.kp, s.chirp, s.lpos_d, s.gl_d, s.gr_d, s.wl_d, h.gplanes, dc.slot_g[slot],
+                           dc.slot_cinfo[slot], s.cs, dc.colmax, dc.err, dc.copy_stream, h.grid);
+      check_launch(cudaGetLastError(), "file site compression");
+      CUDA_OK(cudaEventRecord(dc.loaded[slot], dc.copy_stream));
+      dc.h2d_bytes += h.fmeta.gbytes[i];
+      ++dc.issued;
+      continue;
+    }
     if (h.generated) {  // regenerate + compress on the device: no host traffic
       // the slot's padding is zero from its last fill when that had the same extents
       const long long sig = (static_cast<long long>(s.np) << 32) ^ (static_cast<long long>(s.kp) << 8) ^
@@ -1013,6 +1193,36 @@ static void set_site_generated(mpsg_handle_s& h, uint64_t i, int base_id, const 
     };
     up(sd.lam_prev_f, lp);
     up(sd.inv_lam_f, il);
+    up(sd.gl_d, h.gl[i]);
+    up(sd.gr_d, h.gr[i]);
+    up(sd.wl_d, wl);
+    up(sd.lpos_d, lpos);
+    site_maps(h, dc, i);
+  }
+  h.site_set[i] = 1;
+}
+
+// Storage-streamed supply: site i's bond scales, weight factors and K positions (from Lambda_i, read
+// with the header); its Gamma is read from the file and compressed on every pass.
+static void set_site_file(mpsg_handle_s& h, uint64_t i, const double* lambda) {
+  config_check(h.file, "not a file-streamed handle");
+  config_check(i < h.M && (i == 0 || h.site_set[i - 1]), "sites must be set in increasing order");
+  const size_t chir = h.bonds[i + 1];
+  validate_lambda(lambda, chir);
+  h.gr[i] = h.grid == kGridF16 ? std::vector<double>(chir, 1.0) : bond_scales(lambda, chir);
+  h.lambda[i].assign(lambda, lambda + chir);
+  if (i + 1 < h.M) h.gl[i + 1] = h.gr[i];
+  for (auto& dc : h.devs) {
+    CUDA_OK(cudaSetDevice(dc.device));
+    site_geometry(h, dc, i);
+    SiteDev& sd = dc.sites[i];
+    const std::vector<double> wl = weight_factors(h, i, lambda);
+    const std::vector<int> lpos = row_positions(h, sd);
+    auto up = [](auto*& dst, const auto& v) {
+      using T = std::remove_reference_t<decltype(v[0])>;
+      if (!dst) CUDA_OK(cudaMalloc(&dst, sizeof(T) * v.size()));
+      CUDA_OK(cudaMemcpy(dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    };
     up(sd.gl_d, h.gl[i]);
     up(sd.gr_d, h.gr[i]);
     up(sd.wl_d, wl);
@@ -1446,9 +1656,9 @@ static void run_range(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t firs
         }
       }
     }
-    if (h.generated) {  // the regenerated sites' finiteness / range checks (compression kernels)
+    if (h.generated || h.file) {  // the supplied sites' finiteness / range checks (compression kernels)
       CUDA_OK(cudaStreamSynchronize(dc.copy_stream));
-      check_err_flag(dc, dc.stream, "a regenerated site");
+      check_err_flag(dc, dc.stream, h.file ? "a site streamed from the file" : "a regenerated site");
     }
     // measure's counters over the live samples (sampler.cpp:81-93,114-115)
     std::vector<unsigned long long> live(h.M);
@@ -1627,7 +1837,8 @@ int mpsg_device_count(void) {
 
 static int begin_impl(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bond_dims,
                       const mpsg_policy* policy, const mpsg_options* opts, const int* devices,
-                      int ndev, mpsg_handle* out, bool generated, uint64_t gen_seed) {
+                      int ndev, mpsg_handle* out, bool generated, uint64_t gen_seed,
+                      const FileMeta* fmeta = nullptr) {
   return guarded([&] {
     config_check(out != nullptr, "null output handle");
     *out = nullptr;
@@ -1645,7 +1856,9 @@ static int begin_impl(uint64_t num_sites, uint64_t phys_dim, const uint64_t* bon
     h->precise = h->opts.mode == MPSG_MODE_PRECISE;
     h->generated = generated;
     h->gen_seed = gen_seed;
-    if (generated) {  // regenerated into a ring of device slots (default 3)
+    h->file = fmeta != nullptr;
+    if (fmeta) h->fmeta = *fmeta;
+    if (generated || h->file) {  // regenerated / streamed into a ring of device slots (default 3)
       config_check(h->opts.host_stream_slots >= 0, "host_stream_slots must be >= 0");
       h->opts.host_stream_slots = h->opts.host_stream_slots == 0 ? 3 : std::max(2, h->opts.host_stream_slots);
     }
@@ -1809,6 +2022,7 @@ int mpsg_builder_set_site(mpsg_handle h, uint64_t site, const void* gamma, int g
   });
 }
 
+
 int mpsg_builder_finish(mpsg_handle h) {
   return guarded([&] {
     config_check(h != nullptr, "null handle");
@@ -1858,6 +2072,10 @@ uint64_t mpsg_state_bytes(mpsg_handle h) {
       b += sizeof(float2) * h->devs[0].base_rows[k] * h->devs[0].base_cols[k];
     return b;
   }
+  if (h->file) {  // the Gamma bytes read from storage per pass (nothing of the state is resident)
+    for (uint64_t g : h->fmeta.gbytes) b += g;
+    return b;
+  }
   const int planes = h->devs[0].slots ? h->hplanes : h->gplanes;
   for (const auto& s : h->devs[0].sites) b += static_cast<size_t>(planes) * s.np * s.kp * sizeof(__half);
   return b;  // host-streamed: these bytes live in pinned host memory
@@ -1881,7 +2099,7 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
     const size_t pe = static_cast<size_t>(s.np) * s.kp;
     std::vector<__half> g(h->gplanes * pe);
     std::vector<double> cs(std::max<size_t>(1, 1ull * s.width * h->d));
-    if (h->generated) {  // regenerate the site into a scratch buffer (the pass ring is not touched)
+    if (h->generated || h->file) {  // supply the site into a scratch buffer (the pass ring is not touched)
       std::lock_guard<std::mutex> lk(h->mu);
       CUDA_OK(cudaStreamSynchronize(dc.copy_stream));  // loads pre-issued by the last pass share the scratch
       __half* tg = nullptr;
@@ -1890,8 +2108,29 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
       cudaError_t e = cudaMalloc(&tc, sizeof(float2) * s.np);
       if (e == cudaSuccess) {
         try {
-          regenerate_site(*h, dc, site, tg, tc, true, dc.stream);
-          check_err_flag(dc, dc.stream, "regenerated site " + std::to_string(site));
+          if (h->file) {  // read + verify the payload, compress it exactly as a pass does
+            std::vector<uint8_t> raw(h->fmeta.bytes[site]);
+            const int fd = ::open(h->fmeta.path.c_str(), O_RDONLY);
+            if (fd < 0) throw Error(MPSG_ERR_IO, "cannot open: " + h->fmeta.path);
+            try {
+              read_payload(fd, h->fmeta, site, raw.data());
+            } catch (...) {
+              ::close(fd);
+              throw;
+            }
+            ::close(fd);
+            ensure_src(dc, h->fmeta.gbytes[site]);
+            CUDA_OK(cudaMemcpy(dc.src, raw.data(), h->fmeta.gbytes[site], cudaMemcpyHostToDevice));
+            CUDA_OK(cudaMemset(tg, 0, g.size() * sizeof(__half)));
+            CUDA_OK(cudaMemset(tc, 0, sizeof(float2) * s.np));
+            launch_compress_site(dc.src, h->fmeta.prec[site], s.chil, s.chir, static_cast<int>(h->d), s.b0,
+                                 s.width, s.kp, s.chirp, s.lpos_d, s.gl_d, s.gr_d, s.wl_d, h->gplanes, tg, tc,
+                                 s.cs, dc.colmax, dc.err, dc.stream, h->grid);
+            check_err_flag(dc, dc.stream, "site " + std::to_string(site) + " of the file");
+          } else {
+            regenerate_site(*h, dc, site, tg, tc, true, dc.stream);
+            check_err_flag(dc, dc.stream, "regenerated site " + std::to_string(site));
+          }
           e = cudaMemcpy(g.data(), tg, g.size() * sizeof(__half), cudaMemcpyDeviceToHost);
         } catch (...) {
           cudaFree(tg);
@@ -2130,3 +2369,31 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
 
 #pragma GCC visibility pop
 }  // extern "C"
+
+namespace mpsg {
+int file_streamed_create(const std::string& path, uint64_t m, uint64_t d, const std::vector<uint64_t>& bonds,
+                         const std::vector<int>& storage, const std::vector<uint64_t>& offsets,
+                         const std::vector<uint64_t>& bytes, const std::vector<uint64_t>& checks,
+                         const std::vector<std::vector<double>>& lambdas, const mpsg_policy* policy,
+                         const mpsg_options* opts, const int* devices, int ndev, mpsg_handle* out) {
+  FileMeta fm;
+  fm.path = path;
+  fm.off = offsets;
+  fm.bytes = bytes;
+  fm.check = checks;
+  fm.prec = storage;
+  fm.gbytes.resize(m);
+  for (uint64_t i = 0; i < m; ++i) fm.gbytes[i] = bytes[i] - 8ull * bonds[i + 1];
+  int rc = begin_impl(m, d, bonds.data(), policy, opts, devices, ndev, out, false, 0, &fm);
+  if (rc) return rc;
+  rc = guarded([&] {
+    for (uint64_t i = 0; i < m; ++i) set_site_file(**out, i, lambdas[i].data());
+    (*out)->finished = true;
+  });
+  if (rc) {
+    mpsg_destroy(*out);
+    *out = nullptr;
+  }
+  return rc;
+}
+}  // namespace mpsg

@@ -270,6 +270,40 @@ int mpsg_create_from_file(const char* path, const mpsg_policy* policy, const mps
   }
 }
 
+int mpsg_create_from_file_streamed(const char* path, const mpsg_policy* policy, const mpsg_options* opts,
+                                   const int* devices, int ndev, mpsg_handle* out) {
+  try {
+    if (!path || !out) throw IoFail(MPSG_ERR_CONFIG, "null argument");
+    *out = nullptr;
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw IoFail(MPSG_ERR_IO, std::string("cannot open: ") + path);
+    const Info in = read_info(f, path);
+    // only Lambda is read now (the tail of each payload); the Gamma scalars are read, checksum-verified
+    // and compressed on every pass by the handle's reader (SiteStream, mps_io.cpp:294-350)
+    std::vector<std::vector<double>> lambdas(in.m);
+    for (uint64_t i = 0; i < in.m; ++i) {
+      const uint64_t chir = in.bonds[i + 1];
+      std::vector<uint8_t> raw(8 * chir);
+      f.seekg(static_cast<std::streamoff>(in.offsets[i] + in.bytes[i] - 8 * chir));
+      f.read(reinterpret_cast<char*>(raw.data()), static_cast<std::streamsize>(raw.size()));
+      if (!f) throw IoFail(MPSG_ERR_IO, "mps file truncated");
+      lambdas[i].resize(chir);
+      for (uint64_t r = 0; r < chir; ++r) {
+        const uint64_t u = get_u64(raw.data() + 8 * r);
+        std::memcpy(&lambdas[i][r], &u, 8);
+      }
+    }
+    return mpsg::file_streamed_create(path, in.m, in.d, in.bonds, in.storage, in.offsets, in.bytes, in.checksums,
+                                      lambdas, policy, opts, devices, ndev, out);
+  } catch (const IoFail& e) {
+    mpsg::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    mpsg::set_last_error(e.what());
+    return MPSG_ERR_INTERNAL;
+  }
+}
+
 int mpsg_save_file(mpsg_handle h, const char* path, int storage) {
   try {
     if (!h || !path) throw IoFail(MPSG_ERR_CONFIG, "null argument");

@@ -259,8 +259,10 @@ void launch_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, 
 // g[2 pe + j] = g[j] + g[pe + j]: re-forms the 3M sum plane Gs = Gr + Gi of a host-streamed site
 // (exact: quantize_pair puts Gr, Gi and their sum on one fp16 grid).  pe % 8 == 0.
 void launch_sum_plane(__half* g, size_t pe, cudaStream_t s);
-// colmax: [width * d] zero-initialised scratch (left zeroed).
-void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
+// colmax: [width * d] zero-initialised scratch (left zeroed).  src_prec: the source scalars, complex
+// interleaved -- kSrcF64 / kSrcF32 / kSrcF16 (the MPSB storage precisions, mps_io.cpp:167-199).
+constexpr int kSrcF64 = 0, kSrcF32 = 1, kSrcF16 = 3;  // = MPSG_F64, MPSG_F32, MPSG_F16
+void launch_compress_site(const void* src, int src_prec, int chil, int chir, int d, int b0,
                           int width, int kp, int chirp, const int* lpos, const double* gl,
                           const double* gr, const double* wl, int gplanes, __half* g_out,
                           float2* cinfo_out, double* cs_out, unsigned long long* colmax, int* err,

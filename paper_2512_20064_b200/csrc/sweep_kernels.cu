@@ -1251,10 +1251,13 @@ template <typename T>
 struct ArraySrc {  // complex T interleaved, (chiL, chiR * d) row-major
   const T* p;
   size_t stride;
+  __device__ __forceinline__ static double wide(double x) { return x; }
+  __device__ __forceinline__ static double wide(float x) { return static_cast<double>(x); }
+  __device__ __forceinline__ static double wide(__half x) { return static_cast<double>(__half2float(x)); }
   __device__ __forceinline__ void load(int l, size_t j, double& re, double& im) const {
     const T* q = p + 2 * (static_cast<size_t>(l) * stride + j);
-    re = static_cast<double>(q[0]);
-    im = static_cast<double>(q[1]);
+    re = wide(q[0]);
+    im = wide(q[1]);
   }
 };
 
@@ -1463,17 +1466,20 @@ static void compress_from(const Src& src, int chil, int d, int b0, int width, in
       src, chil, d, b0, width, kp, chirp, lpos, gl, gr, cs_out, gplanes, g_out, np, grid, err);
 }
 
-void launch_compress_site(const void* src, bool src_f64, int chil, int chir, int d, int b0,
+void launch_compress_site(const void* src, int src_prec, int chil, int chir, int d, int b0,
                           int width, int kp, int chirp, const int* lpos, const double* gl,
                           const double* gr, const double* wl, int gplanes, __half* g_out,
                           float2* cinfo_out, double* cs_out, unsigned long long* colmax, int* err,
                           cudaStream_t s, int grid) {
   const size_t stride = static_cast<size_t>(chir) * d;
-  if (src_f64)
+  if (src_prec == kSrcF64)
     compress_from(ArraySrc<double>{static_cast<const double*>(src), stride}, chil, d, b0, width, kp, chirp, lpos,
                   gl, gr, wl, gplanes, g_out, cinfo_out, cs_out, colmax, err, s, grid);
-  else
+  else if (src_prec == kSrcF32)
     compress_from(ArraySrc<float>{static_cast<const float*>(src), stride}, chil, d, b0, width, kp, chirp, lpos,
+                  gl, gr, wl, gplanes, g_out, cinfo_out, cs_out, colmax, err, s, grid);
+  else  // IEEE binary16 bits (MPSB f16 storage): exact in f64
+    compress_from(ArraySrc<__half>{static_cast<const __half*>(src), stride}, chil, d, b0, width, kp, chirp, lpos,
                   gl, gr, wl, gplanes, g_out, cinfo_out, cs_out, colmax, err, s, grid);
 }
 

@@ -292,8 +292,11 @@ class GpuSampler:
                   devices: Optional[Sequence[int]] = None, pass_samples: int = 0,
                   record_site_times: bool = False, host_stream_slots: int = 0,
                   scheme: Scheme = Scheme.AUTO, slice: Slice = Slice.AUTO,
-                  record_decay_trace: bool = False) -> "GpuSampler":
-        """Build the device state from an MPSB file (the reference's format, mps_io.hpp:17-24)."""
+                  record_decay_trace: bool = False, streamed: bool = False) -> "GpuSampler":
+        """Build the device state from an MPSB file (the reference's format, mps_io.hpp:17-24).
+        streamed=True keeps only the header and Lambda: every pass re-reads the site payloads from
+        storage (checksum-verified) and compresses them on the device -- the reference's SiteStream
+        (mps_io.cpp:294-350) for chains beyond device and host memory (mpsg_create_from_file_streamed)."""
         L = _lib.lib()
         policy = policy or PrecisionPolicy()
         policy.validate()
@@ -302,7 +305,8 @@ class GpuSampler:
                            int(record_decay_trace), int(scheme), int(slice))
         devs, nd = cls._devices(devices)
         h = C.c_void_p()
-        _check(L.mpsg_create_from_file(path.encode(), C.byref(pol), C.byref(opt), devs, nd, C.byref(h)))
+        create = L.mpsg_create_from_file_streamed if streamed else L.mpsg_create_from_file
+        _check(create(path.encode(), C.byref(pol), C.byref(opt), devs, nd, C.byref(h)))
         m, d, bonds = _read_mpsb_shape(path)
         self = cls.from_builder(h, m, d, bonds, policy)
         return self

@@ -267,6 +267,48 @@ def test_mpsb_files_roundtrip(pkg, gold, tmp_path):
         pkg.GpuSampler.from_file(bad, pol)
 
 
+@pytest.mark.parametrize("storage,scheme,mode", [("F64", 3, "AUTO"), ("F32", 4, "AUTO"), ("F16", 3, "AUTO"),
+                                                  ("F64", 4, "GRID")])
+def test_mpsb_file_streamed_equals_resident(pkg, gold, tmp_path, storage, scheme, mode):
+    """mpsg_create_from_file_streamed (the reference's SiteStream, mps_io.cpp:294-350, as a per-pass
+    supply): the site payloads are re-read from storage, checksum-verified and compressed on the device
+    every pass, and the samples, marginals and decoded Gamma equal the resident state built from the
+    same file bit for bit -- over several passes (the load sequence wraps the chain) and several calls."""
+    mb = O.load_npz_mps(np.load(f"{gold}/c1b.npz"))
+    path = str(tmp_path / f"c1b_{storage}.mpsb")
+    O.ref_save_mps(mb, path, getattr(O, storage))
+    comp = pkg.Precision.F16 if mode == "GRID" else pkg.Precision.F64
+    pol = pkg.PrecisionPolicy(compute=comp, scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    kw = dict(scheme=pkg.Scheme(scheme) if mode != "GRID" else pkg.Scheme.AUTO, pass_samples=256)
+    res = pkg.GpuSampler.from_file(path, pol, **kw)
+    st = pkg.GpuSampler.from_file(path, pol, streamed=True, host_stream_slots=2 if scheme == 4 else 0, **kw)
+    assert pkg.sampler._lib.lib().mpsg_scheme(st._h) == pkg.sampler._lib.lib().mpsg_scheme(res._h)
+    assert pkg.sampler._lib.lib().mpsg_mode(st._h) == pkg.sampler._lib.lib().mpsg_mode(res._h)
+    for i in (0, 7, mb.num_sites - 1):
+        assert np.array_equal(st.decoded_gamma(i), res.decoded_gamma(i)), i
+    for first, n in ((0, 700), (3, 300)):  # 700 = three passes of 256 rows
+        rows = st.sample(first, n, 7)
+        assert np.array_equal(rows, res.sample(first, n, 7))
+        assert np.array_equal(st.marginals(first, rows), res.marginals(first, rows))
+    res.close()
+    st.close()
+
+
+def test_mpsb_file_streamed_corrupt_payload(pkg, gold, tmp_path):
+    """A payload whose checksum fails surfaces as IoError from the sampling call that reads it."""
+    mb = O.load_npz_mps(np.load(f"{gold}/c1b.npz"))
+    path = str(tmp_path / "c1b.mpsb")
+    O.ref_save_mps(mb, path, O.F64)
+    raw = bytearray(open(path, "rb").read())
+    raw[-100] ^= 0x40  # a Gamma scalar of the last site
+    open(path, "wb").write(bytes(raw))
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    st = pkg.GpuSampler.from_file(path, pol, streamed=True)  # header + Lambda only: accepted
+    with pytest.raises(pkg.IoError, match="checksum"):
+        st.sample(0, 64, 7)
+    st.close()
+
+
 def test_bond_schedule(pkg, gold):
     """sample_batch with a BondSchedule (sampler.cpp:173-176): the truncated chain, sampled on the GPU,
     matches the oracle on the same truncated (decoded) chain."""
@@ -1013,7 +1055,10 @@ def test_generated_supply_equals_resident_chain(pkg, m, chi, d, scheme, pass_sam
     assert np.array_equal(gen.sample(0, n, 7), b)  # second call: the ring restarts cleanly
     mg = gen.marginals(0, a[:64])
     np.testing.assert_array_equal(mg, res.marginals(0, a[:64]))
-    assert gen.state_bytes < res.state_bytes or m * chi <= 4096
+    # the generators (a few chi x d chi complex64 bases) undercut the resident planes once the chain
+    # holds more full-chi sites than it has bases (c4: 11 GB of bases for a 13-20 TB chain)
+    if sum(1 for i in range(m) if res.bond_dims[i] == chi and res.bond_dims[i + 1] == chi) >= 8:
+        assert gen.state_bytes < res.state_bytes
 
 
 def test_generated_supply_parity_vs_reference(pkg):

@@ -299,3 +299,20 @@ def test_displacement_transform_host_checks():
                      [np.array([0.8, 0.6]), np.ones(1)])
     with pytest.raises(P.ConfigError):
         P.sample_batch(mps, P.BatchPlan(4), P.SamplerOptions(site_transform=lambda *a: None))
+
+
+def test_file_streamed_entry_without_gpu(tmp_path):
+    """mpsg_create_from_file_streamed parses the MPSB header and Lambda on the host (IoError for a
+    missing or foreign file) and fails loudly with MPSG_ERR_CUDA where no B200 is visible."""
+    L = _lib.lib()
+    h = C.c_void_p()
+    assert L.mpsg_create_from_file_streamed(str(tmp_path / "none.mpsb").encode(), None, None, None, 0,
+                                            C.byref(h)) == _lib.MPSG_ERR_IO
+    junk = tmp_path / "junk.mpsb"
+    junk.write_bytes(b"NOTMPSB" * 8)
+    assert L.mpsg_create_from_file_streamed(str(junk).encode(), None, None, None, 0, C.byref(h)) == _lib.MPSG_ERR_IO
+    if L.mpsg_device_count() == 0 and O.have_ref():
+        mps = O.ref_random_mps(4, 4, 2, 5)
+        path = str(tmp_path / "small.mpsb")
+        O.ref_save_mps(mps, path, O.F64)
+        assert L.mpsg_create_from_file_streamed(path.encode(), None, None, None, 0, C.byref(h)) == _lib.MPSG_ERR_CUDA
