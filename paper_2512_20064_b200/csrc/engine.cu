@@ -343,6 +343,9 @@ static void read_payload(int fd, const FileMeta& fm, uint64_t i, uint8_t* dst) {
     throw Error(MPSG_ERR_IO, "mps file corrupt: checksum mismatch at site " + std::to_string(i));
 }
 
+// R staging buffers and R reader threads: load q (site q % M) goes to buffer q % R, and the threads
+// work on the R loads after the consumer's position concurrently -- the per-payload FNV-1a is a
+// byte-serial chain (~1 GB/s per thread), so one reader would cap the stream at ~1 GB/s.
 struct FileReader {
   const FileMeta* fm = nullptr;
   int device = 0;
@@ -351,29 +354,31 @@ struct FileReader {
   std::vector<uint8_t*> stage;       // pinned, max payload bytes each
   std::vector<cudaEvent_t> copied;   // the upload from stage[b] is done (recorded by the consumer)
   std::vector<long long> holds;      // load sequence number held by stage[b] (-1: none)
+  std::vector<long long> inflight;   // load sequence number being read into stage[b] (-1: none)
   long long next = 0;                // the next sequence number the consumer takes
   bool stop = false;
   std::string err;
-  uint64_t bytes_read = 0;
-  double read_seconds = 0.0;
   std::mutex mu;
   std::condition_variable cv;
-  std::thread th;
+  std::vector<std::thread> th;
 
-  FileReader(const FileMeta& meta, int dev, int ring) : fm(&meta), device(dev), R(ring) {
+  FileReader(const FileMeta& meta, int dev) : fm(&meta), device(dev) {
     fd = ::open(meta.path.c_str(), O_RDONLY);
     if (fd < 0) throw Error(MPSG_ERR_IO, "cannot open: " + meta.path);
     (void)::posix_fadvise(fd, 0, 0, POSIX_FADV_SEQUENTIAL);
     uint64_t mx = 1;
     for (uint64_t b : meta.bytes) mx = std::max(mx, b);
+    // up to 8 buffers / threads within 8 GiB of pinned staging, at least 2 (double buffering)
+    R = static_cast<int>(std::max<uint64_t>(2, std::min<uint64_t>(8, (8ull << 30) / mx)));
     stage.assign(R, nullptr);
     copied.assign(R, nullptr);
     holds.assign(R, -1);
+    inflight.assign(R, -1);
     for (int b = 0; b < R; ++b) {
       CUDA_OK(cudaMallocHost(&stage[b], mx));
       CUDA_OK(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
     }
-    th = std::thread([this] { run(); });
+    for (int t = 0; t < R; ++t) th.emplace_back([this] { run(); });
   }
   ~FileReader() {
     {
@@ -381,7 +386,8 @@ struct FileReader {
       stop = true;
     }
     cv.notify_all();
-    if (th.joinable()) th.join();
+    for (auto& t : th)
+      if (t.joinable()) t.join();
     for (int b = 0; b < R; ++b) {
       if (stage[b]) cudaFreeHost(stage[b]);
       if (copied[b]) cudaEventDestroy(copied[b]);
@@ -397,26 +403,25 @@ struct FileReader {
         std::unique_lock<std::mutex> lk(mu);
         auto pick = [&] {
           for (q = next; q < next + R; ++q)
-            if (holds[q % R] != q) return true;
+            if (holds[q % R] != q && inflight[q % R] != q) return true;
           return false;
         };
         cv.wait(lk, [&] { return stop || (err.empty() && pick()); });
         if (stop) return;
         holds[q % R] = -1;
+        inflight[q % R] = q;
       }
       const int b = static_cast<int>(q % R);
       std::string e;
       try {
         CUDA_OK(cudaEventSynchronize(copied[b]));  // the previous upload from this buffer is done
-        const auto t0 = std::chrono::steady_clock::now();
         read_payload(fd, *fm, static_cast<uint64_t>(q % m), stage[b]);
-        read_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        bytes_read += fm->bytes[q % m];
       } catch (const std::exception& x) {
         e = x.what();
       }
       {
         std::lock_guard<std::mutex> lk(mu);
+        inflight[b] = -1;
         if (e.empty())
           holds[b] = q;
         else
@@ -522,6 +527,7 @@ struct DevCtx {
   // storage-streamed supply (mpsg_create_from_file_streamed): staging reader + raw device buffers
   std::unique_ptr<FileReader> reader;
   std::vector<void*> slot_raw;
+  std::vector<cudaEvent_t> raw_ready;  // the raw upload into slot_raw[q] is done (copy stream)
   // host-streamed Gamma: ring of device slots filled by a copy stream (sequence q -> slot q % R)
   int slots = 0;
   std::vector<__half*> slot_g;
@@ -807,8 +813,12 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
       uint64_t rmax = 1;
       for (uint64_t g : h.fmeta.gbytes) rmax = std::max(rmax, g);
       dc.slot_raw.assign(dc.slots, nullptr);
-      for (int q = 0; q < dc.slots; ++q) CUDA_OK(cudaMalloc(&dc.slot_raw[q], rmax));
-      dc.reader = std::make_unique<FileReader>(h.fmeta, dc.device, 2);
+      dc.raw_ready.assign(dc.slots, nullptr);
+      for (int q = 0; q < dc.slots; ++q) {
+        CUDA_OK(cudaMalloc(&dc.slot_raw[q], rmax));
+        CUDA_OK(cudaEventCreateWithFlags(&dc.raw_ready[q], cudaEventDisableTiming));
+      }
+      dc.reader = std::make_unique<FileReader>(h.fmeta, dc.device);
     }
   }
 }
@@ -820,6 +830,8 @@ static void free_device(DevCtx& dc) {
   dc.reader.reset();  // joins the reader thread
   for (auto p : dc.slot_raw) cudaFree(p);
   dc.slot_raw.clear();
+  for (auto e : dc.raw_ready) cudaEventDestroy(e);
+  dc.raw_ready.clear();
   for (auto& s : dc.sites) {
     if (!dc.slots) {
       cudaFree(s.g);
@@ -1051,42 +1063,53 @@ static void regenerate_site(const mpsg_handle_s& h, DevCtx& dc, uint64_t i, __ha
 }
 
 // Host-streamed mode: issue site loads until `upto` loads are in flight or done.
+// Stream of the supply's compression kernels (regeneration, file-site packing).  Inline (default):
+// the engine's lane-0 stream, between the sites' contractions.  On the side copy stream those kernels
+// would interleave with the persistent contraction, whose CTAs own whole SMs with a static unit split:
+// CTAs that start late behind a compression block stretch the whole launch (chi = 8192 regenerated:
+// +38% per site on the side stream against the kernels' own 1.7 ms, profiles/r2_bigchi/).
+static cudaStream_t supply_stream(const DevCtx& dc) {
+  static const bool side = [] {
+    const char* v = std::getenv("MPSG_SUPPLY_STREAM");
+    return v && std::string(v) == "side";
+  }();
+  return side ? dc.copy_stream : dc.stream;
+}
+
 static void issue_loads(mpsg_handle_s& h, DevCtx& dc, uint64_t upto) {
   while (dc.issued < upto) {
     const uint64_t q = dc.issued;
     const int slot = static_cast<int>(q % dc.slots);
     const SiteDev& s = dc.sites[q % h.M];
     CUDA_OK(cudaStreamWaitEvent(dc.copy_stream, dc.freed[slot], 0));  // consume q - slots done
-    if (h.file) {  // storage -> pinned staging (reader thread) -> device raw -> compressed slot
-      const uint64_t i = q % h.M;
-      const uint8_t* raw = dc.reader->take(static_cast<long long>(q));
-      CUDA_OK(cudaMemcpyAsync(dc.slot_raw[slot], raw, h.fmeta.gbytes[i], cudaMemcpyHostToDevice, dc.copy_stream));
-      dc.reader->taken(static_cast<long long>(q), dc.copy_stream);
-      const long long sig = (static_cast<long long>(s.np) << 32) ^ (static_cast<long long>(s.kp) << 8) ^
-                            (static_cast<long long>(s.chil) * 131 + s.width);
-      if (dc.slot_sig[slot] != sig) {
-        CUDA_OK(cudaMemsetAsync(dc.slot_g[slot], 0, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half),
-                                dc.copy_stream));
-        CUDA_OK(cudaMemsetAsync(dc.slot_cinfo[slot], 0, 1ull * s.np * sizeof(float2), dc.copy_stream));
-      }
-      dc.slot_sig[slot] = sig;
-      launch_compress_site(dc.slot_raw[slot], h.fmeta.prec[i], s.chil, s.chir, static_cast<int>(h.d), s.b0,
-                           s.width, s.kp, s.chirp, s.lpos_d, s.gl_d, s.gr_d, s.wl_d, h.gplanes, dc.slot_g[slot],
-                           dc.slot_cinfo[slot], s.cs, dc.colmax, dc.err, dc.copy_stream, h.grid);
-      check_launch(cudaGetLastError(), "file site compression");
-      CUDA_OK(cudaEventRecord(dc.loaded[slot], dc.copy_stream));
-      dc.h2d_bytes += h.fmeta.gbytes[i];
-      ++dc.issued;
-      continue;
-    }
-    if (h.generated) {  // regenerate + compress on the device: no host traffic
+    if (h.file || h.generated) {  // compressed on the device into the slot
+      const cudaStream_t ss = supply_stream(dc);
+      if (ss != dc.copy_stream) CUDA_OK(cudaStreamWaitEvent(ss, dc.freed[slot], 0));
       // the slot's padding is zero from its last fill when that had the same extents
       const long long sig = (static_cast<long long>(s.np) << 32) ^ (static_cast<long long>(s.kp) << 8) ^
                             (static_cast<long long>(s.chil) * 131 + s.width);
-      regenerate_site(h, dc, q % h.M, dc.slot_g[slot], dc.slot_cinfo[slot], dc.slot_sig[slot] != sig,
-                      dc.copy_stream);
+      if (h.file) {  // storage -> pinned staging (reader threads) -> device raw -> compressed slot
+        const uint64_t i = q % h.M;
+        const uint8_t* raw = dc.reader->take(static_cast<long long>(q));
+        CUDA_OK(cudaMemcpyAsync(dc.slot_raw[slot], raw, h.fmeta.gbytes[i], cudaMemcpyHostToDevice, dc.copy_stream));
+        dc.reader->taken(static_cast<long long>(q), dc.copy_stream);
+        CUDA_OK(cudaEventRecord(dc.raw_ready[slot], dc.copy_stream));
+        CUDA_OK(cudaStreamWaitEvent(ss, dc.raw_ready[slot], 0));
+        if (dc.slot_sig[slot] != sig) {
+          CUDA_OK(cudaMemsetAsync(dc.slot_g[slot], 0, static_cast<size_t>(h.gplanes) * s.np * s.kp * sizeof(__half),
+                                  ss));
+          CUDA_OK(cudaMemsetAsync(dc.slot_cinfo[slot], 0, 1ull * s.np * sizeof(float2), ss));
+        }
+        launch_compress_site(dc.slot_raw[slot], h.fmeta.prec[i], s.chil, s.chir, static_cast<int>(h.d), s.b0,
+                             s.width, s.kp, s.chirp, s.lpos_d, s.gl_d, s.gr_d, s.wl_d, h.gplanes, dc.slot_g[slot],
+                             dc.slot_cinfo[slot], s.cs, dc.colmax, dc.err, ss, h.grid);
+        check_launch(cudaGetLastError(), "file site compression");
+        dc.h2d_bytes += h.fmeta.gbytes[i];
+      } else {  // regenerate + compress on the device: no host traffic
+        regenerate_site(h, dc, q % h.M, dc.slot_g[slot], dc.slot_cinfo[slot], dc.slot_sig[slot] != sig, ss);
+      }
       dc.slot_sig[slot] = sig;
-      CUDA_OK(cudaEventRecord(dc.loaded[slot], dc.copy_stream));
+      CUDA_OK(cudaEventRecord(dc.loaded[slot], ss));
       ++dc.issued;
       continue;
     }

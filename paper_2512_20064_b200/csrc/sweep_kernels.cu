@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include <cmath>
+#include <type_traits>
 
 #include "ptx.cuh"
 
@@ -1249,6 +1250,8 @@ void launch_draws(uint64_t seed, uint64_t first, uint64_t count, uint64_t site, 
 // ============================================================================================
 template <typename T>
 struct ArraySrc {  // complex T interleaved, (chiL, chiR * d) row-major
+  // fp32 / fp16 sources: every scaled value is an exact float (see quantize_pair_f32)
+  static constexpr bool kExactF32 = !std::is_same<T, double>::value;
   const T* p;
   size_t stride;
   __device__ __forceinline__ static double wide(double x) { return x; }
@@ -1274,6 +1277,7 @@ __device__ __forceinline__ float2 synth_value(const SynthSite& g, int l, size_t 
   return make_float2(__fmul_rn(tr, sc), __fmul_rn(ti, sc));
 }
 struct SynthSrc {
+  static constexpr bool kExactF32 = true;  // fp32 generator values
   SynthSite g;
   __device__ __forceinline__ void load(int l, size_t j, double& re, double& im) const {
     const float2 v = synth_value(g, l, j);
@@ -1308,6 +1312,11 @@ void launch_synth_values(const SynthSite& g, int rows, float2* out, cudaStream_t
   synth_values_kernel<<<1184, 256, 0, s>>>(g, rows, out);
 }
 
+// 1 / x for a power of two x (the bond and column scales): exact, and a few integer ops instead of an
+// f64 division (the divisions made the compression kernels FP64-bound: pack 1.5 ms per chi = 8192
+// site, the regenerated supply's main overhead).
+__device__ __forceinline__ double inv_pow2(double x) { return ldexp(1.0, -ilogb(x)); }
+
 // Per local column jl = r_loc * d + k: max over l of max(|re|, |im|) * gr[r] / gl[l] (f64), as an
 // order-independent atomic max of the nonnegative doubles' bit patterns.  A 2-D grid (64-row chunks
 // x 128 columns) keeps enough loads in flight to stream the source at HBM rate.
@@ -1326,7 +1335,7 @@ __global__ void colmax_kernel(const Src src, int chil, int d, int b0, int width,
     double re, im;
     src.load(l, j, re, im);
     if (!isfinite(re) || !isfinite(im)) finite = false;
-    const double f = gr[r] / gl[l];
+    const double f = gr[r] * inv_pow2(gl[l]);
     mx = fmax(mx, fmax(fabs(re * f), fabs(im * f)));
   }
   if (!finite) atomicExch(err, 3);  // NumericError: non-finite Gamma (contract.cpp:117-119)
@@ -1371,10 +1380,32 @@ __device__ __forceinline__ void quantize_pair(double a, double b, __half& ha, __
   int e;
   frexp(m, &e);  // m in [2^(e-1), 2^e): fp16 spacing there is 2^(e-11)
   const double u = ldexp(1.0, max(e - 11, -24));
-  const double qa = rint(a / u) * u, qb = rint(b / u) * u;  // RNE; |qa + qb| <= 2^e
+  const double iu = ldexp(1.0, -max(e - 11, -24));
+  const double qa = rint(a * iu) * u, qb = rint(b * iu) * u;  // RNE; |qa + qb| <= 2^e
   ha = __double2half(qa);
   hb = __double2half(qb);
   hs = __double2half(qa + qb);
+}
+
+// quantize_pair for fp32-exact inputs, in fp32 / integer arithmetic with the same result bit for bit:
+// the binade of max(|a|, |b|, |a + b|) is taken from the round-toward-zero fp32 sum (RZ never crosses
+// a power of two upward, and a power of two is representable, so the exponent equals the exact sum's),
+// a * 2^-k, rint and the re-scaling are exact, and qa + qb (a multiple of u below 2^(e+1)) is exact.
+// The f64 original is FP64-bound (pack took 1.3 ms per chi = 8192 regenerated site).
+__device__ __forceinline__ void quantize_pair_f32(float a, float b, __half& ha, __half& hb, __half& hs) {
+  const float m = fmaxf(fmaxf(fabsf(a), fabsf(b)), fabsf(__fadd_rz(a, b)));
+  if (m == 0.f) {
+    ha = hb = hs = __float2half_rn(0.f);
+    return;
+  }
+  int e;
+  frexpf(m, &e);
+  const int ue = max(e - 11, -24);
+  const float u = ldexpf(1.f, ue), iu = ldexpf(1.f, -ue);
+  const float qa = rintf(a * iu) * u, qb = rintf(b * iu) * u;
+  ha = __float2half_rn(qa);
+  hb = __float2half_rn(qb);
+  hs = __float2half_rn(qa + qb);
 }
 
 template <typename Src>
@@ -1383,12 +1414,13 @@ __global__ void pack_kernel(const Src src, int chil, int d, int b0, int width, i
                             const double* cs, int gplanes, __half* g_out, int np, int grid, int* err) {
   // planes: [Gr, Gi (, Gs)] and, for gplanes = 6 (MPSG_MODE_PRECISE), [Gr_lo, Gi_lo, Gs_lo] -- the
   // residual of the hi grid, itself rounded by quantize_pair, so every plane (and Gs = Gr + Gi per
-  // precision half) is an exact fp16 number
-  __shared__ __half tp[6][32][33];
+  // precision half) is an exact fp16 number.  Tile: 64 rows l x 32 columns j; read along j
+  // (coalesced source rows), written along l as half2 (the K-major planes, 128 B per warp store).
+  __shared__ __half tp[6][64][33];
   const int wcols = width * d;
-  const int j0 = blockIdx.x * 32, l0 = blockIdx.y * 32;
+  const int j0 = blockIdx.x * 32, l0 = blockIdx.y * 64;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-  for (int yy = ty; yy < 32; yy += 8) {
+  for (int yy = ty; yy < 64; yy += 8) {
     const int l = l0 + yy, jl = j0 + tx;
     __half h[6];
 #pragma unroll
@@ -1397,30 +1429,42 @@ __global__ void pack_kernel(const Src src, int chil, int d, int b0, int width, i
       const int rl = jl / d, k = jl - rl * d;
       double re, im;
       src.load(l, static_cast<size_t>(b0 + rl) * d + k, re, im);
-      const double f = gr[b0 + rl] / gl[l] / cs[jl];
+      const double f = gr[b0 + rl] * inv_pow2(gl[l]) * inv_pow2(cs[jl]);
       if (grid != kGridNone) {  // round_scalar per component (precision.cpp:23-50): IEEE RNE
         h[0] = __double2half(re * f);
         h[1] = __double2half(im * f);
         if (__hisinf(h[0]) || __hisinf(h[1])) atomicExch(err, 3);  // beyond the F16 grid
+      } else if constexpr (Src::kExactF32) {
+        const float a = static_cast<float>(re * f), b = static_cast<float>(im * f);  // exact
+        quantize_pair_f32(a, b, h[0], h[1], h[2]);
+        if (gplanes == 6)  // residuals of the hi grid: exact in fp32 (below half a grid step)
+          quantize_pair_f32(a - __half2float(h[0]), b - __half2float(h[1]), h[3], h[4], h[5]);
       } else {
         quantize_pair(re * f, im * f, h[0], h[1], h[2]);
+        if (gplanes == 6)
+          quantize_pair(re * f - static_cast<double>(__half2float(h[0])),
+                        im * f - static_cast<double>(__half2float(h[1])), h[3], h[4], h[5]);
       }
-      if (gplanes == 6)
-        quantize_pair(re * f - static_cast<double>(__half2float(h[0])),
-                      im * f - static_cast<double>(__half2float(h[1])), h[3], h[4], h[5]);
     }
 #pragma unroll
     for (int p = 0; p < 6; ++p) tp[p][yy][tx] = h[p];
   }
   __syncthreads();
   for (int yy = ty; yy < 32; yy += 8) {
-    const int jl = j0 + yy, l = l0 + tx;
-    if (jl < wcols && l < chil) {
-      const int rl = jl / d, k = jl - rl * d;
-      const size_t row = static_cast<size_t>(k) * chirp + rl;
-      const size_t col = static_cast<size_t>(lpos[l]);
-      for (int p = 0; p < gplanes; ++p)
-        g_out[(static_cast<size_t>(p) * np + row) * kp + col] = tp[p][tx][yy];
+    const int jl = j0 + yy, l = l0 + 2 * tx;
+    if (jl >= wcols || l >= chil) continue;
+    const int rl = jl / d, k = jl - rl * d;
+    const size_t row = static_cast<size_t>(k) * chirp + rl;
+    const int c0 = lpos[l];
+    const bool pair = l + 1 < chil && lpos[l + 1] == c0 + 1 && (c0 & 1) == 0;
+    for (int p = 0; p < gplanes; ++p) {
+      __half* dst = g_out + (static_cast<size_t>(p) * np + row) * kp;
+      if (pair) {
+        *reinterpret_cast<__half2*>(dst + c0) = __halves2half2(tp[p][2 * tx][yy], tp[p][2 * tx + 1][yy]);
+      } else {
+        dst[c0] = tp[p][2 * tx][yy];
+        if (l + 1 < chil) dst[lpos[l + 1]] = tp[p][2 * tx + 1][yy];
+      }
     }
   }
 }
@@ -1462,7 +1506,7 @@ static void compress_from(const Src& src, int chil, int d, int b0, int width, in
                                                                                  colmax, err);
   colfinish_kernel<<<(wcols + 127) / 128, 128, 0, s>>>(d, b0, width, chirp, wl, colmax, cinfo_out, cs_out, err,
                                                        grid);
-  pack_kernel<Src><<<dim3((wcols + 31) / 32, (chil + 31) / 32), dim3(32, 8), 0, s>>>(
+  pack_kernel<Src><<<dim3((wcols + 31) / 32, (chil + 63) / 64), dim3(32, 8), 0, s>>>(
       src, chil, d, b0, width, kp, chirp, lpos, gl, gr, cs_out, gplanes, g_out, np, grid, err);
 }
 
