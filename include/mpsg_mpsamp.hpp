@@ -138,12 +138,15 @@ inline mpsamp::SampleBatch sample_batch(const mpsamp::MpsState& mps_in, const mp
 // run_serial / run_data_parallel (parallel.hpp:24-52) on an MPSB file: the file is streamed into
 // the compressed device state (mpsg_create_from_file) and sampled on `p1` B200s (devices 0..p1-1
 // unless given).  Returns the batch and merged RunStats like ParallelResult (no CommStats: the
-// data path has no collective).
+// data path has no collective).  from_storage: keep only the header and Lambda and re-read the site
+// payloads from the file on every pass (mpsg_create_from_file_streamed, the reference's SiteStream)
+// -- for chains beyond device and host memory.
 inline mpsamp::SampleBatch run_data_parallel_file(const std::string& mps_path,
                                                   const mpsamp::BatchPlan& plan_in, size_t p1,
                                                   const mpsamp::SamplerOptions& opts,
                                                   mpsamp::RunStats* stats_out = nullptr,
-                                                  std::vector<int> devices = {}) {
+                                                  std::vector<int> devices = {},
+                                                  bool from_storage = false) {
   if (p1 < 1) throw mpsamp::ConfigError("data parallel needs p1 >= 1");
   opts.policy.validate();
   if (opts.site_transform || opts.schedule)
@@ -157,8 +160,8 @@ inline mpsamp::SampleBatch run_data_parallel_file(const std::string& mps_path,
   mpsg_options o{};
   o.record_site_times = stats_out ? 1 : 0;
   mpsg_handle h = nullptr;
-  check(mpsg_create_from_file(mps_path.c_str(), &pol, &o, devices.data(),
-                              static_cast<int>(devices.size()), &h));
+  check((from_storage ? mpsg_create_from_file_streamed : mpsg_create_from_file)(
+      mps_path.c_str(), &pol, &o, devices.data(), static_cast<int>(devices.size()), &h));
   std::unique_ptr<mpsg_handle_s, void (*)(mpsg_handle)> guard(h, mpsg_destroy);
   // chain shape from the file header (read_mps_info, mps_io.cpp:212-254)
   mpsamp::MpsFileInfo info = mpsamp::read_mps_info(mps_path);

@@ -72,6 +72,14 @@ int main(int argc, char** argv) {
       std::printf("FAIL: file executor differs from in-memory\n");
       return 1;
     }
+    // the same file streamed from storage every pass (mpsg_create_from_file_streamed)
+    mpsamp::SampleBatch fs = mpsg_mpsamp::run_data_parallel_file("/tmp/mpsg_adapter_c1.mpsb",
+                                                                 mpsamp::BatchPlan::simple(1000), 1, opts,
+                                                                 nullptr, {}, true);
+    if (fs.outcomes != got.outcomes) {
+      std::printf("FAIL: storage-streamed file executor differs from in-memory\n");
+      return 1;
+    }
   }
   // MPSG_MODE_SPLIT (the fp16 format's decoded-Gamma contract): identical strings against the
   // reference run on the decoded Gamma, and the count against the original Gamma recorded

@@ -634,13 +634,14 @@ class ParallelResult:
     stats: RunStats = None
 
 
-def run_serial(mps_path: str, plan: BatchPlan, opts: SamplerOptions) -> ParallelResult:
-    """run_serial (parallel.cpp:232-238): load the MPSB file and sample on one B200."""
-    return run_data_parallel(mps_path, plan, 1, opts)
+def run_serial(mps_path: str, plan: BatchPlan, opts: SamplerOptions, from_storage: bool = False) -> ParallelResult:
+    """run_serial (parallel.cpp:232-238): load (or, from_storage, stream) the MPSB file and sample on
+    one B200."""
+    return run_data_parallel(mps_path, plan, 1, opts, from_storage=from_storage)
 
 
 def run_data_parallel(mps_path: str, plan: BatchPlan, p1: int, opts: SamplerOptions,
-                      devices: Optional[Sequence[int]] = None) -> ParallelResult:
+                      devices: Optional[Sequence[int]] = None, from_storage: bool = False) -> ParallelResult:
     """run_data_parallel (parallel.cpp:240-330) on p1 B200s of this process: the file is read once
     (streamed site by site), every device keeps the compressed chain, each sweeps a contiguous
     share of the samples.  Outcomes equal the serial ones (keyed RNG).
@@ -648,7 +649,9 @@ def run_data_parallel(mps_path: str, plan: BatchPlan, p1: int, opts: SamplerOpti
     The site transform is applied per sample as in the reference's DP worker (parallel.cpp:291-308);
     the decay trace is recorded when asked.  A bond schedule raises ConfigError, as the C++ adapter
     does (include/mpsg_mpsamp.hpp): the file-backed state is built site by site on the device and
-    is not truncated here -- truncate with apply_schedule and use sample_batch."""
+    is not truncated here -- truncate with apply_schedule and use sample_batch.  from_storage=True
+    re-reads the payloads from the file on every pass instead of holding the chain
+    (mpsg_create_from_file_streamed: chains beyond device and host memory)."""
     if p1 < 1:
         raise ConfigError("data parallel needs p1 >= 1")
     if opts.schedule is not None:
@@ -660,7 +663,7 @@ def run_data_parallel(mps_path: str, plan: BatchPlan, p1: int, opts: SamplerOpti
     plan.normalize()
     devs = list(devices) if devices else list(range(p1))
     smp = GpuSampler.from_file(mps_path, opts.policy, opts.mode, devs, opts.pass_samples, scheme=opts.scheme,
-                               record_decay_trace=opts.record_decay_trace)
+                               record_decay_trace=opts.record_decay_trace, streamed=from_storage)
     try:
         st = RunStats()
         mu = (opts.site_transform.amplitudes(0, plan.total_samples, smp.num_sites)

@@ -259,6 +259,8 @@ def test_mpsb_files_roundtrip(pkg, gold, tmp_path):
         assert np.array_equal(back.lambdas[i], mps.lambdas[i])
     res = pkg.run_data_parallel(f64, pkg.BatchPlan(500), 1, pkg.SamplerOptions(policy=pol, seed=7))
     assert np.array_equal(res.batch.outcomes, want)
+    res = pkg.run_serial(f64, pkg.BatchPlan(500), pkg.SamplerOptions(policy=pol, seed=7), from_storage=True)
+    assert np.array_equal(res.batch.outcomes, want)
     raw = bytearray(open(f64, "rb").read())
     raw[-100] ^= 0x40  # flip a bit in the last site's payload
     bad = str(tmp_path / "bad.mpsb")
