@@ -2,6 +2,8 @@
 
     python tests/parity_full.py --config c2 --samples 1024 --out profiles/r2_parity/c2_full.json
     python tests/parity_full.py --config c3 --samples 64 --f32 --out profiles/r2_parity/c3_full.json
+    python tests/parity_full.py --config c2 --samples 1024 --mode precise --against original --f32 \
+        --out profiles/r2_parity/c2_full_precise_original.json
 
 The chain is the benchmark's own synthetic chain (bench.py: build_synthetic(M, chi, d, seed=42)) at
 its full length.  The GPU sweep (through the C ABI) is compared with the reference itself
@@ -48,7 +50,7 @@ def site_classes(bonds):
 
 
 def run(config, n, seed=7, mps_seed=42, threads=None, f32=False, scheme=0, m_override=0, log=print,
-        generated=True):
+        generated=True, mode="split", against="decoded"):
     m, chi, d = CONFIGS[config]
     if m_override:
         m = m_override
@@ -56,8 +58,18 @@ def run(config, n, seed=7, mps_seed=42, threads=None, f32=False, scheme=0, m_ove
     pol = P.PrecisionPolicy(scaling=P.ScalingMode.PER_SAMPLE_MAX)
     # generated=True: the same chain (tests/test_gpu_parity.py::test_generated_supply_equals_resident_chain)
     # held as its generators -- a few hundred MB of HBM instead of the resident state (c3: 153 GB)
-    smp, lams = build_synthetic(m, chi, d, seed=mps_seed, policy=pol, scheme=scheme, mode=P.Mode.SPLIT,
-                                generated=generated)
+    # against="original": the reference runs on the chain's own values (the generator's complex64
+    # sites, widened to f64) instead of the device's decoded Gamma -- the caller's-MPS contract that
+    # MPSG_MODE_PRECISE (AUTO at F64 / F32) targets
+    pmode = {"split": P.Mode.SPLIT, "precise": P.Mode.PRECISE}[mode]
+    host = None
+    if against == "original":
+        smp, lams, host = build_synthetic(m, chi, d, seed=mps_seed, policy=pol, scheme=scheme, mode=pmode,
+                                          keep_host=True)
+        generated = False
+    else:
+        smp, lams = build_synthetic(m, chi, d, seed=mps_seed, policy=pol, scheme=scheme, mode=pmode,
+                                    generated=generated)
     bonds = list(smp.bond_dims)
     scheme_name = ("3M" if smp.scheme == P.Scheme.M3 else "4M") + " " + smp.mode.name
     t_build = time.time() - t0
@@ -72,7 +84,7 @@ def run(config, n, seed=7, mps_seed=42, threads=None, f32=False, scheme=0, m_ove
     near = np.zeros((n, m), bool)
     t1 = time.time()
     for i in range(m):
-        g = smp.decoded_gamma(i)
+        g = host[i] if host is not None else smp.decoded_gamma(i)
         o, mg, nb = ref.site(i, g, lams[i])
         ref_rows[:, i], ref_marg[:, i], near[:, i] = o, mg, nb
         if f32:
@@ -112,7 +124,9 @@ def run(config, n, seed=7, mps_seed=42, threads=None, f32=False, scheme=0, m_ove
     out = {
         "config": config, "M": m, "chi": chi, "d": d, "samples": n, "mps_seed": mps_seed, "seed": seed,
         "scheme": scheme_name,
-        "oracle": "reference (oracle/_ref), site-streamed decoded Gamma, F64 + PerSampleMax, threaded",
+        "oracle": ("reference (oracle/_ref), site-streamed " +
+                   ("original (generator) Gamma" if host is not None else "decoded Gamma") +
+                   ", F64 + PerSampleMax, threaded"),
         "gamma_supply": "generated (regenerated on the device)" if generated else "resident",
         "draws_checked": int(live[:, :, 0].sum()),
         "near_boundary_draws_reference_path": int(near.sum()),
@@ -152,11 +166,15 @@ def main():
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--scheme", default="auto", choices=["auto", "3m", "4m"])
     ap.add_argument("--supply", default="generated", choices=["generated", "resident"])
+    ap.add_argument("--mode", default="split", choices=["split", "precise"])
+    ap.add_argument("--against", default="decoded", choices=["decoded", "original"],
+                    help="original: the reference on the chain's own values (PRECISE's contract)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     scheme = {"auto": 0, "3m": 3, "4m": 4}[a.scheme]
     r = run(a.config, a.samples, threads=a.threads or None, f32=a.f32, scheme=scheme, m_override=a.sites,
-            log=lambda s: print(s, file=sys.stderr, flush=True), generated=a.supply == "generated")
+            log=lambda s: print(s, file=sys.stderr, flush=True), generated=a.supply == "generated",
+            mode=a.mode, against=a.against)
     txt = json.dumps(r, indent=1)
     if a.out:
         os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)
