@@ -237,6 +237,11 @@ int mpsg_generated_set_site(mpsg_handle h, uint64_t site, int base_id, const dou
 int mpsg_synthetic_site(const void* base, uint64_t ld, uint64_t rows, uint64_t cols, uint64_t phys_dim,
                         const double* lambda_prev, const double* lambda, uint64_t seed, uint64_t site,
                         void* out);
+/* The ORIGINAL values of site `site` of a generated handle -- the generator itself, before the
+ * device compression (mpsg_decoded_gamma returns what the device samples) -- as complex128 (chiL,
+ * chiR, d) in host memory: the chain a caller of the reference would hold (parity against the
+ * caller's MPS, e.g. MPSG_MODE_PRECISE at the c3 / c4 shapes that exceed host memory as complex128). */
+int mpsg_generated_site_values(mpsg_handle h, uint64_t site, double* out);
 
 /* ---- MPSB files (the reference's on-disk format, mps_io.hpp:17-24) ----------------------- */
 /* Read an MPSB file (any storage precision, checksums verified -> MPSG_ERR_IO) and build the

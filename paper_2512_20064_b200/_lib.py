@@ -68,6 +68,7 @@ SIGNATURES = [
     ("mpsg_contract_site", _int, [C.c_void_p, _u64, _pd, _u64, _pd]),
     ("mpsg_create_from_file", _int, [C.c_char_p, C.POINTER(Policy), C.POINTER(Options),
                                      C.POINTER(_int), _int, C.POINTER(C.c_void_p)]),
+    ("mpsg_generated_site_values", _int, [C.c_void_p, _u64, _pd]),
     ("mpsg_create_from_file_streamed", _int, [C.c_char_p, C.POINTER(Policy), C.POINTER(Options),
                                      C.POINTER(_int), _int, C.POINTER(C.c_void_p)]),
     ("mpsg_save_file", _int, [C.c_void_p, C.c_char_p, _int]),

@@ -2037,6 +2037,42 @@ int mpsg_synthetic_site(const void* base, uint64_t ld, uint64_t rows, uint64_t c
   });
 }
 
+int mpsg_generated_site_values(mpsg_handle h, uint64_t site, double* out) {
+  return guarded([&] {
+    config_check(h != nullptr && out != nullptr, "null argument");
+    config_check(h->generated, "not a generated handle (mpsg_generated_begin)");
+    config_check(site < h->M && h->site_set[site], "site not set");
+    std::lock_guard<std::mutex> lk(h->mu);
+    DevCtx& dc = h->devs[0];
+    CUDA_OK(cudaSetDevice(dc.device));
+    const SiteDev& s = dc.sites[site];
+    const size_t n = static_cast<size_t>(s.chil) * s.chir * h->d;
+    float2* buf = nullptr;
+    CUDA_OK(cudaMalloc(&buf, std::max<size_t>(1, n) * sizeof(float2)));
+    std::vector<float2> v(n);
+    cudaError_t e = cudaSuccess;
+    try {
+      CUDA_OK(cudaStreamSynchronize(dc.stream));  // the phase buffer is shared with the pass's loads
+      CUDA_OK(cudaStreamSynchronize(dc.copy_stream));
+      launch_synth_phase(h->gen_seed, site, s.chir * static_cast<int>(h->d), dc.phase, dc.stream);
+      SynthSite g = synth_of(*h, dc, site);
+      launch_synth_values(g, s.chil, buf, dc.stream);
+      CUDA_OK(cudaGetLastError());
+      e = cudaMemcpyAsync(v.data(), buf, n * sizeof(float2), cudaMemcpyDeviceToHost, dc.stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(dc.stream);
+    } catch (...) {
+      cudaFree(buf);
+      throw;
+    }
+    cudaFree(buf);
+    CUDA_OK(e);
+    for (size_t j = 0; j < n; ++j) {
+      out[2 * j] = static_cast<double>(v[j].x);
+      out[2 * j + 1] = static_cast<double>(v[j].y);
+    }
+  });
+}
+
 int mpsg_builder_set_site(mpsg_handle h, uint64_t site, const void* gamma, int gamma_is_device,
                           int dtype, const double* lambda) {
   return guarded([&] {

@@ -1420,7 +1420,6 @@ __global__ void pack_kernel(const Src src, int chil, int d, int b0, int width, i
   const int wcols = width * d;
   const int j0 = blockIdx.x * 32, l0 = blockIdx.y * 64;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-#pragma unroll  // the 8 rows' source loads in flight together
   for (int yy = ty; yy < 64; yy += 8) {
     const int l = l0 + yy, jl = j0 + tx;
     __half h[6];
@@ -1452,7 +1451,6 @@ __global__ void pack_kernel(const Src src, int chil, int d, int b0, int width, i
       if (p < gplanes) tp[p][yy][tx] = h[p];
   }
   __syncthreads();
-#pragma unroll
   for (int yy = ty; yy < 32; yy += 8) {
     const int jl = j0 + yy, l = l0 + 2 * tx;
     if (jl >= wcols || l >= chil) continue;

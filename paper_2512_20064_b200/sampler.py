@@ -424,6 +424,14 @@ class GpuSampler:
         _check(_lib.lib().mpsg_decoded_gamma(self._h, site, out.ctypes.data_as(_lib._pd)))
         return out
 
+    def original_gamma(self, site: int) -> np.ndarray:
+        """A generated handle's own (uncompressed) site values: the generator evaluated in fp32,
+        widened to complex128 (mpsg_generated_site_values) -- the chain the reference would hold."""
+        b = self.bond_dims
+        out = np.empty((b[site], b[site + 1], self.phys_dim), np.complex128)
+        _check(_lib.lib().mpsg_generated_site_values(self._h, site, out.ctypes.data_as(_lib._pd)))
+        return out
+
     def contract_site(self, site: int, env: np.ndarray) -> np.ndarray:
         env = np.ascontiguousarray(env, np.complex128)
         b = self.bond_dims

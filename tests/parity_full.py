@@ -63,13 +63,13 @@ def run(config, n, seed=7, mps_seed=42, threads=None, f32=False, scheme=0, m_ove
     # MPSG_MODE_PRECISE (AUTO at F64 / F32) targets
     pmode = {"split": P.Mode.SPLIT, "precise": P.Mode.PRECISE}[mode]
     host = None
-    if against == "original":
+    if against == "original" and not generated:
         smp, lams, host = build_synthetic(m, chi, d, seed=mps_seed, policy=pol, scheme=scheme, mode=pmode,
                                           keep_host=True)
-        generated = False
-    else:
+    else:  # generated: the original sites come from the generator on demand (original_gamma)
         smp, lams = build_synthetic(m, chi, d, seed=mps_seed, policy=pol, scheme=scheme, mode=pmode,
                                     generated=generated)
+    original = against == "original"
     bonds = list(smp.bond_dims)
     scheme_name = ("3M" if smp.scheme == P.Scheme.M3 else "4M") + " " + smp.mode.name
     t_build = time.time() - t0
@@ -84,7 +84,7 @@ def run(config, n, seed=7, mps_seed=42, threads=None, f32=False, scheme=0, m_ove
     near = np.zeros((n, m), bool)
     t1 = time.time()
     for i in range(m):
-        g = host[i] if host is not None else smp.decoded_gamma(i)
+        g = host[i] if host is not None else (smp.original_gamma(i) if original else smp.decoded_gamma(i))
         o, mg, nb = ref.site(i, g, lams[i])
         ref_rows[:, i], ref_marg[:, i], near[:, i] = o, mg, nb
         if f32:
@@ -125,7 +125,7 @@ def run(config, n, seed=7, mps_seed=42, threads=None, f32=False, scheme=0, m_ove
         "config": config, "M": m, "chi": chi, "d": d, "samples": n, "mps_seed": mps_seed, "seed": seed,
         "scheme": scheme_name,
         "oracle": ("reference (oracle/_ref), site-streamed " +
-                   ("original (generator) Gamma" if host is not None else "decoded Gamma") +
+                   ("original (generator) Gamma" if original else "decoded Gamma") +
                    ", F64 + PerSampleMax, threaded"),
         "gamma_supply": "generated (regenerated on the device)" if generated else "resident",
         "draws_checked": int(live[:, :, 0].sum()),

@@ -296,6 +296,26 @@ def test_mpsb_file_streamed_equals_resident(pkg, gold, tmp_path, storage, scheme
     st.close()
 
 
+def test_generated_precise_and_original_values(pkg):
+    """A generated handle in MPSG_MODE_PRECISE (6 planes regenerated every pass) samples exactly like
+    the resident PRECISE handle of the same chain, and mpsg_generated_site_values returns the chain's
+    own (uncompressed) values -- the sites build_synthetic materialises for the resident handle."""
+    from paper_2512_20064_b200.synthetic import build_synthetic
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    kw = dict(seed=5, policy=pol, mode=pkg.Mode.PRECISE, pass_samples=512)
+    res, _, host = build_synthetic(10, 256, 4, keep_host=True, **kw)
+    gen, _ = build_synthetic(10, 256, 4, generated=True, **kw)
+    assert pkg.sampler._lib.lib().mpsg_mode(gen._h) == int(pkg.Mode.PRECISE)
+    for i in range(10):
+        assert np.array_equal(gen.original_gamma(i), host[i]), i
+        assert np.array_equal(gen.decoded_gamma(i), res.decoded_gamma(i)), i
+    rows = gen.sample(0, 1200, 7)
+    assert np.array_equal(rows, res.sample(0, 1200, 7))
+    assert np.array_equal(gen.marginals(0, rows[:64]), res.marginals(0, rows[:64]))
+    res.close()
+    gen.close()
+
+
 def test_mpsb_file_streamed_corrupt_payload(pkg, gold, tmp_path):
     """A payload whose checksum fails surfaces as IoError from the sampling call that reads it."""
     mb = O.load_npz_mps(np.load(f"{gold}/c1b.npz"))
