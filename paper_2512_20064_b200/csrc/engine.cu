@@ -637,8 +637,8 @@ static void choose_scheme(mpsg_handle_s& h) {
       state6 += 6.0 * 2.0 * round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN) *
                 static_cast<double>(h.tp) * round_up((static_cast<int>(h.bonds[i]) + h.tp - 1) / h.tp, kBK3);
     bool fits = h.pair && h.opts.scheme != MPSG_SCHEME_4M;
-    if (h.file) {
-      // streamed from storage: only the slot ring is resident, whatever the chain's size
+    if (h.file || h.generated) {
+      // streamed from storage / regenerated: only the slot ring is resident, whatever the chain's size
     } else if (h.opts.host_stream_slots != 0) {
       const double host = static_cast<double>(sysconf(_SC_PHYS_PAGES)) * sysconf(_SC_PAGE_SIZE);
       fits = fits && state6 * (4.0 / 6.0) * h.devs.size() <= 0.6 * host;
@@ -659,7 +659,7 @@ static void choose_scheme(mpsg_handle_s& h) {
     for (uint64_t i = 0; i < h.M; ++i)
       state6 += 6.0 * 2.0 * round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN) *
                 static_cast<double>(h.tp) * round_up((static_cast<int>(h.bonds[i]) + h.tp - 1) / h.tp, kBK3);
-    if (h.file) {
+    if (h.file || h.generated) {
       // only the slot ring is resident
     } else if (h.opts.host_stream_slots != 0) {
       const double host = static_cast<double>(sysconf(_SC_PHYS_PAGES)) * sysconf(_SC_PAGE_SIZE);
