@@ -316,3 +316,28 @@ def test_file_streamed_entry_without_gpu(tmp_path):
         path = str(tmp_path / "small.mpsb")
         O.ref_save_mps(mps, path, O.F64)
         assert L.mpsg_create_from_file_streamed(path.encode(), None, None, None, 0, C.byref(h)) == _lib.MPSG_ERR_CUDA
+
+
+def test_tp_partition_block_aligned():
+    """Tensor-parallel column shards (engine.cu part_range / parallel.tp_partition): contiguous,
+    covering [0, extent), every boundary on a K-block multiple, at most one partial (last non-empty)
+    shard, balanced to within one block, and the identity for one rank -- the alignment that makes a
+    sharded contraction accumulate the unsharded K blocks in order."""
+    from paper_2512_20064_b200.parallel import tp_granule, tp_partition
+    assert tp_granule(3) == 64 and tp_granule(4) == 32
+    for extent in (1, 4, 16, 63, 64, 65, 100, 512, 1296, 2048, 4095, 10000):
+        for parts in (1, 2, 3, 4, 8):
+            for gran in (32, 64):
+                sh = tp_partition(extent, parts, gran)
+                assert len(sh) == parts and sh[0][0] == 0 and sh[-1][1] == extent
+                for (b0, e0), (b1, e1) in zip(sh, sh[1:]):
+                    assert e0 == b1 and b0 <= e0
+                if parts == 1:
+                    assert sh == [(0, extent)]
+                    continue
+                widths = [e - b for b, e in sh]
+                assert all(b % gran == 0 for b, _ in sh if b < extent)
+                full = -(-(-(-extent // parts)) // gran) * gran
+                last = max(i for i, w in enumerate(widths) if w > 0)  # the last non-empty shard
+                assert all(w == full for w in widths[:last]) and 0 < widths[last] <= full
+                assert all(w == 0 for w in widths[last + 1:])
