@@ -316,6 +316,21 @@ def test_generated_precise_and_original_values(pkg):
     gen.close()
 
 
+def test_mpsb_file_streamed_two_devices(pkg, gold, tmp_path):
+    """A storage-streamed handle driving two device contexts (here both on GPU 0), each with its own
+    reader threads and slot ring over the same file, splits the samples and returns the resident
+    handle's rows."""
+    mb = O.load_npz_mps(np.load(f"{gold}/c1b.npz"))
+    path = str(tmp_path / "c1b.mpsb")
+    O.ref_save_mps(mb, path, O.F32)
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    res = pkg.GpuSampler.from_file(path, pol, pass_samples=256)
+    st = pkg.GpuSampler.from_file(path, pol, devices=[0, 0], pass_samples=256, streamed=True)
+    assert np.array_equal(st.sample(0, 1500, 11), res.sample(0, 1500, 11))
+    res.close()
+    st.close()
+
+
 def test_mpsb_file_streamed_corrupt_payload(pkg, gold, tmp_path):
     """A payload whose checksum fails surfaces as IoError from the sampling call that reads it."""
     mb = O.load_npz_mps(np.load(f"{gold}/c1b.npz"))
