@@ -341,3 +341,26 @@ def test_tp_partition_block_aligned():
                 last = max(i for i, w in enumerate(widths) if w > 0)  # the last non-empty shard
                 assert all(w == full for w in widths[:last]) and 0 < widths[last] <= full
                 assert all(w == 0 for w in widths[last + 1:])
+
+
+def test_grid_mode_config_checks_precede_device():
+    """MPSG_MODE_GRID reproduces the TF32 / F16 compute policies only: with compute F64 / F32, with
+    tensor parallelism, GlobalMax scaling or the decay trace it is a ConfigError (checked before any
+    device is touched); a valid GRID request reaches the device check (MPSG_ERR_CUDA here)."""
+    L = _lib.lib()
+    if L.mpsg_device_count() != 0:
+        pytest.skip("device present: the no-device code path is not reachable")
+    bd = (C.c_uint64 * 3)(1, 4, 1)
+
+    def begin(compute, scaling=2, tp=1, trace=0):
+        h = C.c_void_p()
+        pol = _lib.Policy(compute, 0, scaling)
+        opt = _lib.Options(4, 0, 0, tp, 0, 0, trace, 0, 0)
+        return L.mpsg_builder_begin(2, 2, bd, C.byref(pol), C.byref(opt), None, 0, C.byref(h))
+
+    assert begin(0) == _lib.MPSG_ERR_CONFIG            # F64 compute
+    assert begin(1) == _lib.MPSG_ERR_CONFIG            # F32 compute
+    assert begin(3, tp=2) == _lib.MPSG_ERR_CONFIG      # tensor parallelism
+    assert begin(3, scaling=1) == _lib.MPSG_ERR_CONFIG  # GlobalMax
+    assert begin(2, trace=1) == _lib.MPSG_ERR_CONFIG   # decay trace
+    assert begin(3) == _lib.MPSG_ERR_CUDA and begin(2) == _lib.MPSG_ERR_CUDA
