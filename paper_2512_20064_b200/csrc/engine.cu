@@ -103,6 +103,21 @@ static CUtensorMap make_tma_2d(const void* base, uint64_t cols, uint64_t rows,
   return m;
 }
 
+// temp [rows][d][chirp] float2 as a 3-D tensor {chirp, d, rows} of 8-byte elements: box 32 columns x
+// 1 outcome x 8 samples (the K1 epilogue's TMA tensor stores, 256 B contiguous per sample).
+static CUtensorMap make_tma_temp(const void* base, uint64_t chirp, uint64_t d, uint64_t rows) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {chirp, d, rows};
+  cuuint64_t strides[2] = {chirp * 8, d * chirp * 8};
+  cuuint32_t box[3] = {32, 1, 8};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(MPSG_ERR_CUDA, "cuTensorMapEncodeTiled (temp) failed");
+  return m;
+}
+
 // Shard-major env [shards][planes * cap rows][kshard]: box 32 k x box_rows rows x 1 shard.
 static CUtensorMap make_tma_env(const void* base, uint64_t kshard, uint64_t rows, uint64_t shards,
                                 uint32_t box_rows = kBM, uint32_t box_k = kBK) {
@@ -492,6 +507,7 @@ struct Lane {
   uint8_t* host_rows = nullptr;   // pinned [cap][M]
   std::vector<CUtensorMap> tma_env;    // per site: the shard-major env map over this lane's env
   std::vector<CUtensorMap> tma_env64;  // same with a 64-row box (3M kernel: env is the B operand)
+  std::vector<CUtensorMap> tma_temp;   // per site: temp as {chirp, d, cap} (K1's TMA tensor stores)
   // slice-recompute path (3M, tp = 1): rows bucketed by outcome each site
   __half* env_perm = nullptr;     // the environment rows in bucket order (slice GEMM B operand)
   int* perm = nullptr;            // [cap] row -> sample of the pass
@@ -765,6 +781,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     CUDA_OK(cudaEventCreateWithFlags(&ln.seldone, cudaEventDisableTiming));
     ln.tma_env.resize(h.M);
     ln.tma_env64.resize(h.M);
+    ln.tma_temp.resize(h.M);
     if (h.slice_rc) {
       CUDA_OK(cudaMalloc(&ln.env_perm, 2ull * h.env_comp * ln.cap * kmax * sizeof(__half)));
       CUDA_OK(cudaMalloc(&ln.perm, ln.cap * sizeof(int)));
@@ -950,6 +967,7 @@ static void site_maps(mpsg_handle_s& h, DevCtx& dc, uint64_t i) {
     const uint64_t env_rows = 2ull * h.env_comp * ln.cap;
     ln.tma_env[i] = make_tma_env(ln.env, s.kshard, env_rows, h.tp);
     if (h.m3) ln.tma_env64[i] = make_tma_env(ln.env, s.kshard, env_rows, h.tp, kBM / 2, kBK3);
+    if (h.m3) ln.tma_temp[i] = make_tma_temp(ln.temp, s.chirp, h.d, ln.cap);
     if (ln.env_perm) ln.tma_envp64[i] = make_tma_env(ln.env_perm, s.kshard, env_rows, h.tp, kBM / 2, kBK3);
   }
   if (dc.slots) {
@@ -1331,9 +1349,15 @@ static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const S
       const char* v = std::getenv("MPSG_3M_QUAD");
       return v && std::atoi(v) != 0;
     }();
+    // temp through TMA tensor stores (MPSG_3M_TMA_STORE=1: A/B switch)
+    static const bool env_tma = [] {
+      const char* v = std::getenv("MPSG_3M_TMA_STORE");
+      return v && std::atoi(v) != 0;
+    }();
+    const bool tma_store = env_tma && slice == 0 && !h.precise;
     launch_site_gemm_3m(h.split, slice == 1 || epilogue_max(h, s), env_epi, env_quad && slice == 0, h.precise,
                         slice == 2 ? ln.tma_envp64[i] : ln.tma_env64[i], *tma_g128, ga, std::min(ctas, dc.num_sms),
-                        stream, slice == 2);
+                        stream, slice == 2, tma_store ? &ln.tma_temp[i] : nullptr);
     return;
   }
   const int mrow = h.pair ? 2 * kBM : kBM;

@@ -36,7 +36,11 @@ namespace mpsg {
 
 // kGlo (MPSG_MODE_PRECISE): Gamma carries a lo plane per component too; stage = [A_hi | A_lo | B_hi |
 // B_lo] and three MMAs per K16 step (A_hi x B_hi, A_hi x B_lo through the A collector, A_lo x B_hi).
-template <bool kSplit, bool kGlo = false>
+// kTma: temp leaves through TMA tensor stores from a per-warp double-buffered staging area (8 samples
+// x 32 columns of float2 per buffer) instead of per-thread 8 B global stores -- the store instructions
+// cost ~40% of the epilogue at chi <= 512 (clock64 probes with the stores removed: 7.0k -> 4.1k cycles
+// per unit, profiles/r2_prof3m/); one operand stage is given up for the staging area.
+template <bool kSplit, bool kGlo = false, bool kTma = false>
 struct Cfg3M {
   static constexpr int kHalves = kSplit ? 2 : 1;
   static constexpr int kAHalves = kGlo ? 2 : 1;
@@ -44,11 +48,13 @@ struct Cfg3M {
   static constexpr int kBTile = (kBM / 2) * kBK3 * 2;  // 8 KiB: this SM's 64 sample rows
   static constexpr int kBOff = kAHalves * kATile;      // B tiles after the A tile(s)
   static constexpr int kStageBytes = kAHalves * kATile + kHalves * kBTile;
-  static constexpr int kStages = kGlo ? 4 : (kSplit ? 6 : 8);
+  static constexpr int kStages = kGlo ? 4 : (kSplit ? (kTma ? 5 : 6) : (kTma ? 7 : 8));
   static constexpr int kRedBytes = 4 * kBM * 8;        // [4 lane quarters][128 samples] float2
   static constexpr int kBarBytes = 512;
   static constexpr int kOffBytes = 256;                // slice GEMM: bucket offsets
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + kBarBytes + kRedBytes + kOffBytes;
+  static constexpr int kTmaBufFloat2 = 8 * 32;         // one staging buffer: 8 samples x 32 columns
+  static constexpr int kTmaBytes = kTma ? 8 * 2 * kTmaBufFloat2 * 8 : 0;  // 8 epilogue warps x 2 buffers
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + kBarBytes + kRedBytes + kOffBytes + kTmaBytes;
 };
 
 int gemm_3m_smem_bytes(bool split) { return split ? Cfg3M<true>::kSmem : Cfg3M<false>::kSmem; }
@@ -95,7 +101,8 @@ __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
   return kMax ? fmaxf(v[0], other) : v[0] + other;
 }
 
-// Timing probes (flags & 32): [0] epilogue cycles waiting for the accumulators, [1] epilogue busy
+// Timing probes (flags & 32; flags & 64 additionally skips the temp stores -- a timing experiment,
+// the results are then wrong): [0] epilogue cycles waiting for the accumulators, [1] epilogue busy
 // cycles, [2] MMA cycles waiting for a free TMEM slot, [3] MMA cycles waiting for operands,
 // [4] units, [5] epilogue cycles from accumulator-ready to slot release.
 __device__ unsigned long long g_prof3m[8];
@@ -109,11 +116,14 @@ __device__ unsigned long long g_prof3m[8];
 // kSlice: the slice GEMM of the slice-recompute path (Gemm3MArgs::bcount): units whose sample tile
 // misses the bucket of their outcome are skipped by every role alike, and the epilogue writes the
 // next environment's hi / lo planes exactly as the select kernel would from temp.
-template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad, bool kGlo = false, bool kSlice = false>
+template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad, bool kGlo = false, bool kSlice = false,
+          bool kTma = false>
 __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
     site_gemm_3m_kernel(const __grid_constant__ CUtensorMap tma_env64,
-                        const __grid_constant__ CUtensorMap tma_g, const Gemm3MArgs a) {
-  using C = Cfg3M<kSplit, kGlo>;
+                        const __grid_constant__ CUtensorMap tma_g, const Gemm3MArgs a,
+                        const __grid_constant__ CUtensorMap tma_temp) {
+  static_assert(!kTma || (kEpiWarps == 8 && !kGlo && !kSlice && !kQuad), "TMA temp stores: 8-warp K1 only");
+  using C = Cfg3M<kSplit, kGlo, kTma>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -124,6 +134,8 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
   float2* red = reinterpret_cast<float2*>(smem + C::kStages * C::kStageBytes + C::kBarBytes);
   int* boff = reinterpret_cast<int*>(smem + C::kStages * C::kStageBytes + C::kBarBytes + C::kRedBytes);
+  float2* tbuf = reinterpret_cast<float2*>(smem + C::kStages * C::kStageBytes + C::kBarBytes + C::kRedBytes +
+                                           C::kOffBytes);  // 128 B aligned (kTma staging)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -300,6 +312,8 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
     const int ec = q * 32 + lane;  // column within the SM's 128
     uint32_t gp = 0;
     int unit = 0;
+    int tst = 0;  // kTma: this warp's staging-buffer sequence number
+    const uint64_t pol_temp = kTma ? ptx::l2_policy_evict_first() : 0;
     for (int u = cluster; u < units; u += num_clusters) {
       int m, t;
       unit_coords_3m(u, a, g_units, m, t);
@@ -366,15 +380,46 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
             }
           }
         } else if (valid) {
+          if constexpr (kTma) {
+            // two 8-sample halves through this warp's double-buffered staging area: lane = column,
+            // one 8 x 32 float2 TMA tensor store per half (256 B contiguous per sample in temp)
+            float2* wbuf = tbuf + (warp - 4) * 2 * C::kTmaBufFloat2;
 #pragma unroll
-          for (int i = 0; i < kEpiSamples; ++i) {
-            const float re = (pr[i] - pi[i]) * ci.x;
-            const float im = (ps[i] - pr[i] - pi[i]) * ci.x;
-            // streaming store: temp (1.6 GB per c3 site) must not evict the Gamma group from L2;
-            // no temp at all on the slice-recompute path (weights only)
-            if (a.temp != nullptr) __stcs(dst + (ch * kEpiSamples + i) * row_stride, make_float2(re, im));
-            pr[i] = ci.y * fmaf(re, re, im * im);
-            if constexpr (kMax) pi[i] = fmaxf(fabsf(re), fabsf(im));
+            for (int hf = 0; hf < kEpiSamples / 8; ++hf) {
+              float2* buf = wbuf + (tst & 1) * C::kTmaBufFloat2;
+              if (tst >= 2 && lane == 0) ptx::bulk_wait_group_read<1>();  // this buffer's last store read it
+              __syncwarp();
+#pragma unroll
+              for (int i8 = 0; i8 < 8; ++i8) {
+                const int i = hf * 8 + i8;
+                const float re = (pr[i] - pi[i]) * ci.x;
+                const float im = (ps[i] - pr[i] - pi[i]) * ci.x;
+                buf[i8 * 32 + lane] = make_float2(re, im);
+                pr[i] = ci.y * fmaf(re, re, im * im);
+                if constexpr (kMax) pi[i] = fmaxf(fabsf(re), fabsf(im));
+              }
+              ptx::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                ptx::tma_store_3d(&tma_temp, buf, col0 - k * a.chirp + q * 32, k,
+                                  t * kBM + static_cast<int>(c0) + ch * kEpiSamples + hf * 8, pol_temp);
+                ptx::bulk_commit_group();
+              }
+              ++tst;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < kEpiSamples; ++i) {
+              const float re = (pr[i] - pi[i]) * ci.x;
+              const float im = (ps[i] - pr[i] - pi[i]) * ci.x;
+              // streaming store: temp (1.6 GB per c3 site) must not evict the Gamma group from L2;
+              // no temp at all on the slice-recompute path (weights only)
+              // (flags & 64: diagnostic -- skip the stores, to time the epilogue without them)
+              if (a.temp != nullptr && !(a.flags & 64))
+                __stcs(dst + (ch * kEpiSamples + i) * row_stride, make_float2(re, im));
+              pr[i] = ci.y * fmaf(re, re, im * im);
+              if constexpr (kMax) pi[i] = fmaxf(fabsf(re), fabsf(im));
+            }
           }
           const float w = transpose_reduce16<false>(pr, lane);
           float mx = 0.f;
@@ -406,6 +451,9 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
       ++unit;
       gp += 3;
     }
+    if constexpr (kTma) {
+      if (lane == 0) ptx::bulk_wait_group<0>();  // this warp's temp stores performed
+    }
   }
 
   ptx::tc_fence_before();
@@ -417,11 +465,12 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
   }
 }
 
-template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad, bool kGlo = false, bool kSlice = false>
+template <bool kSplit, bool kMax, int kEpiWarps, bool kQuad, bool kGlo = false, bool kSlice = false,
+          bool kTma = false>
 static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
-                        int grid, cudaStream_t s) {
-  auto kern = site_gemm_3m_kernel<kSplit, kMax, kEpiWarps, kQuad, kGlo, kSlice>;
-  using Cf = Cfg3M<kSplit, kGlo>;
+                        int grid, cudaStream_t s, const CUtensorMap* tma_temp = nullptr) {
+  auto kern = site_gemm_3m_kernel<kSplit, kMax, kEpiWarps, kQuad, kGlo, kSlice, kTma>;
+  using Cf = Cfg3M<kSplit, kGlo, kTma>;
   constexpr int kCl = kQuad ? 4 : 2;
   static PerDevice clusters;  // per device: smem opt-in + occupancy query
   cudaLaunchConfig_t cfg = {};
@@ -448,17 +497,23 @@ static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, 
     return mc;
   });
   cfg.gridDim = dim3(kCl * std::max(1, std::min(max_clusters, grid / kCl)));
-  check_launch(cudaLaunchKernelEx(&cfg, kern, tma_env64, tma_g, a), "site_gemm_3m_kernel");
+  // kernels without TMA temp stores never read the map: pass any valid one
+  check_launch(cudaLaunchKernelEx(&cfg, kern, tma_env64, tma_g, a, tma_temp ? *tma_temp : tma_g),
+               "site_gemm_3m_kernel");
 }
 
 template <bool kSplit, bool kMax>
 static void launch_3m_w(int epi_warps, bool quad, bool glo, const CUtensorMap& e, const CUtensorMap& g,
-                        const Gemm3MArgs& a, int grid, cudaStream_t s) {
+                        const Gemm3MArgs& a, int grid, cudaStream_t s, const CUtensorMap* tma_temp) {
   if constexpr (kSplit) {
     if (glo) {
       launch_3m_t<kSplit, kMax, 8, false, true>(e, g, a, grid, s);
       return;
     }
+  }
+  if (tma_temp && !quad && epi_warps == 8) {
+    launch_3m_t<kSplit, kMax, 8, false, false, false, true>(e, g, a, grid, s, tma_temp);
+    return;
   }
   if (quad)
     launch_3m_t<kSplit, kMax, 8, true>(e, g, a, grid, s);
@@ -472,7 +527,7 @@ static void launch_3m_w(int epi_warps, bool quad, bool glo, const CUtensorMap& e
 
 void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, bool glo,
                          const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
-                         int grid, cudaStream_t s, bool slice) {
+                         int grid, cudaStream_t s, bool slice, const CUtensorMap* tma_temp) {
   if (slice) {  // slice GEMM: 8 epilogue warps, CTA pairs
     if (split)
       glo ? launch_3m_t<true, false, 8, false, true, true>(tma_env64, tma_g, a, grid, s)
@@ -481,12 +536,13 @@ void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, bo
       launch_3m_t<false, false, 8, false, false, true>(tma_env64, tma_g, a, grid, s);
     return;
   }
+  if (a.temp == nullptr) tma_temp = nullptr;  // weights only: nothing to store
   if (split)
-    with_max ? launch_3m_w<true, true>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s)
-             : launch_3m_w<true, false>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s);
+    with_max ? launch_3m_w<true, true>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s, tma_temp)
+             : launch_3m_w<true, false>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s, tma_temp);
   else
-    with_max ? launch_3m_w<false, true>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s)
-             : launch_3m_w<false, false>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s);
+    with_max ? launch_3m_w<false, true>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s, tma_temp)
+             : launch_3m_w<false, false>(epi_warps, quad, glo, tma_env64, tma_g, a, grid, s, tma_temp);
 }
 
 }  // namespace mpsg

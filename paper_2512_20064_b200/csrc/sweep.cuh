@@ -232,9 +232,11 @@ int gemm_pair_smem_bytes(bool split);
 // quad: 4-CTA clusters sharing the environment tiles by multicast (see site_gemm_3m.cu).
 // glo: Gamma lo planes present (MPSG_MODE_PRECISE, split only).
 // slice = true: the slice GEMM of the slice-recompute path (Gemm3MArgs::bcount / scale / env_next)
+// tma_temp: a 3-D map of temp ({chirp, d, rows} float2, box 32 x 1 x 8) -> the epilogue stores temp
+// with TMA tensor stores (8-warp SPLIT / SINGLE K1); null -> per-thread global stores
 void launch_site_gemm_3m(bool split, bool with_max, int epi_warps, bool quad, bool glo,
                          const CUtensorMap& tma_env64, const CUtensorMap& tma_g, const Gemm3MArgs& a,
-                         int grid, cudaStream_t s, bool slice = false);
+                         int grid, cudaStream_t s, bool slice = false, const CUtensorMap* tma_temp = nullptr);
 int gemm_3m_smem_bytes(bool split);
 void launch_select(const SelectArgs& a, cudaStream_t s);
 // env [shards][6][env_cap][kshard] (3M): planes 2, 5 (s = re + im, hi / lo) of rows [0, rows) of every
