@@ -37,6 +37,7 @@ import paper_2512_20064_b200 as P  # noqa: E402
 from paper_2512_20064_b200.synthetic import build_synthetic  # noqa: E402
 
 CONFIGS = {"c2": (256, 512, 6), "c3": (1024, 2048, 6), "c5_256": (512, 256, 4), "c5_1024": (512, 1024, 4),
+           "c5_4096": (512, 4096, 4),
            "c4": (8176, 10000, 4)}  # c4 with --sites N: an N-site chain of the c4 shape (chi = 1e4 in the middle)
 EPS = 1e-6
 
