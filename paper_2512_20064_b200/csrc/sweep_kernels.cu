@@ -1007,53 +1007,55 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
       }
       return;
     }
-    for (int r = lane * 4; r < a.kp_next; r += 128) {  // kp_next is a multiple of 32
-      float4 v01 = make_float4(0.f, 0.f, 0.f, 0.f), v23 = v01;
-      if (kDisp && r < live_cols) {  // displaced: row `outcome` of D applied on the fly
-        float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int q = 0; q < a.d; ++q) {  // chirp is a multiple of 128: the 4 columns stay in the row
-          const float2 dk = D[outcome * a.d + q];
-          const float2* src_q = a.temp + (static_cast<size_t>(n) * a.d + q) * a.chirp + r;
-          const float4 x01 = *reinterpret_cast<const float4*>(src_q);
-          const float4 x23 = *reinterpret_cast<const float4*>(src_q + 2);
-          const float xs[8] = {x01.x, x01.y, x01.z, x01.w, x23.x, x23.y, x23.z, x23.w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            o[2 * j] = fmaf(dk.x, xs[2 * j], fmaf(-dk.y, xs[2 * j + 1], o[2 * j]));
-            o[2 * j + 1] = fmaf(dk.x, xs[2 * j + 1], fmaf(dk.y, xs[2 * j], o[2 * j + 1]));
+    if constexpr (kDisp) {  // (the undisplaced path returned above)
+      for (int r = lane * 4; r < a.kp_next; r += 128) {  // kp_next is a multiple of 32
+        float4 v01 = make_float4(0.f, 0.f, 0.f, 0.f), v23 = v01;
+        if (kDisp && r < live_cols) {  // displaced: row `outcome` of D applied on the fly
+          float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          for (int q = 0; q < a.d; ++q) {  // chirp is a multiple of 128: the 4 columns stay in the row
+            const float2 dk = D[outcome * a.d + q];
+            const float2* src_q = a.temp + (static_cast<size_t>(n) * a.d + q) * a.chirp + r;
+            const float4 x01 = *reinterpret_cast<const float4*>(src_q);
+            const float4 x23 = *reinterpret_cast<const float4*>(src_q + 2);
+            const float xs[8] = {x01.x, x01.y, x01.z, x01.w, x23.x, x23.y, x23.z, x23.w};
+  #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              o[2 * j] = fmaf(dk.x, xs[2 * j], fmaf(-dk.y, xs[2 * j + 1], o[2 * j]));
+              o[2 * j + 1] = fmaf(dk.x, xs[2 * j + 1], fmaf(dk.y, xs[2 * j], o[2 * j + 1]));
+            }
           }
+  #pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (r + j >= live_cols) o[2 * j] = o[2 * j + 1] = 0.f;
+          v01 = make_float4(o[0], o[1], o[2], o[3]);
+          v23 = make_float4(o[4], o[5], o[6], o[7]);
+        } else if (r + 3 < live_cols) {  // chirp is a multiple of 128: these loads stay inside the row
+          v01 = *reinterpret_cast<const float4*>(src + r);
+          v23 = *reinterpret_cast<const float4*>(src + r + 2);
+        } else if (r < live_cols) {
+          const float2 z = make_float2(0.f, 0.f);
+          const float2 c0 = src[r];
+          const float2 c1 = r + 1 < live_cols ? src[r + 1] : z;
+          const float2 c2 = r + 2 < live_cols ? src[r + 2] : z;
+          v01 = make_float4(c0.x, c0.y, c1.x, c1.y);
+          v23 = make_float4(c2.x, c2.y, 0.f, 0.f);
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (r + j >= live_cols) o[2 * j] = o[2 * j + 1] = 0.f;
-        v01 = make_float4(o[0], o[1], o[2], o[3]);
-        v23 = make_float4(o[4], o[5], o[6], o[7]);
-      } else if (r + 3 < live_cols) {  // chirp is a multiple of 128: these loads stay inside the row
-        v01 = *reinterpret_cast<const float4*>(src + r);
-        v23 = *reinterpret_cast<const float4*>(src + r + 2);
-      } else if (r < live_cols) {
-        const float2 z = make_float2(0.f, 0.f);
-        const float2 c0 = src[r];
-        const float2 c1 = r + 1 < live_cols ? src[r + 1] : z;
-        const float2 c2 = r + 2 < live_cols ? src[r + 2] : z;
-        v01 = make_float4(c0.x, c0.y, c1.x, c1.y);
-        v23 = make_float4(c2.x, c2.y, 0.f, 0.f);
-      }
-      const float cre[4] = {v01.x * scale, v01.z * scale, v23.x * scale, v23.z * scale};
-      const float cim[4] = {v01.y * scale, v01.w * scale, v23.y * scale, v23.w * scale};
-      __align__(8) __half hv[3][4], lv[3][4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        __half h3[3], l3[3];
-        env_split(cre[j], cim[j], h3, l3);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) hv[c][j] = h3[c], lv[c][j] = l3[c];
-      }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        if (c >= C) break;
-        *reinterpret_cast<uint2*>(e0 + c * plane + r) = *reinterpret_cast<const uint2*>(hv[c]);
-        *reinterpret_cast<uint2*>(e0 + (C + c) * plane + r) = *reinterpret_cast<const uint2*>(lv[c]);
+        const float cre[4] = {v01.x * scale, v01.z * scale, v23.x * scale, v23.z * scale};
+        const float cim[4] = {v01.y * scale, v01.w * scale, v23.y * scale, v23.w * scale};
+        __align__(8) __half hv[3][4], lv[3][4];
+  #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          __half h3[3], l3[3];
+          env_split(cre[j], cim[j], h3, l3);
+  #pragma unroll
+          for (int c = 0; c < 3; ++c) hv[c][j] = h3[c], lv[c][j] = l3[c];
+        }
+  #pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (c >= C) break;
+          *reinterpret_cast<uint2*>(e0 + c * plane + r) = *reinterpret_cast<const uint2*>(hv[c]);
+          *reinterpret_cast<uint2*>(e0 + (C + c) * plane + r) = *reinterpret_cast<const uint2*>(lv[c]);
+        }
       }
     }
   }
