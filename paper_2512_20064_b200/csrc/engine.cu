@@ -1297,9 +1297,10 @@ static bool epilogue_max(const mpsg_handle_s& h, const SiteDev& s) { return xchg
 static void launch_contraction(const mpsg_handle_s& h, const DevCtx& dc, const SiteDev& s, const Lane& ln,
                                uint64_t i, int rows, const CUtensorMap* tma_g128,
                                const CUtensorMap& tma_g64, const float2* cinfo, cudaStream_t stream,
-                               int slice = 0, int kp_next = 0) {
+                               int slice = 0, int kp_next = 0, bool pdl = false) {
   if (h.m3) {
     Gemm3MArgs ga = {};
+    ga.pdl = pdl ? 1 : 0;
     ga.g_tiles = s.np / (2 * kBN);
     ga.s_tiles = rows / kBM;
     ga.k_blocks = s.kp / kBK3;
@@ -1400,6 +1401,15 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
   // slice recompute for plain sampling passes (teacher forcing, marginals, displacement and the decay
   // trace read temp): rows are then permuted by outcome every such site, perm maps them to samples
   const bool rc_pass = h.slice_rc && !forced && !marg && !displaced && !dc.trace;
+  // Programmatic dependent launch between the contraction and the selection of consecutive sites
+  // (one lane, resident or generated Gamma, no exchange / displacement / slice recompute): each
+  // kernel's prologue overlaps its predecessor's tail.  Opt-in (MPSG_PDL=1): measured neutral at
+  // chi = 256 / 512 (profiles/r2_select_rows/), where the per-site launches are shortest.
+  static const bool env_pdl = [] {
+    const char* v = std::getenv("MPSG_PDL");
+    return v != nullptr && std::atoi(v) != 0;
+  }();
+  const bool pdl = env_pdl && h.m3 && nl == 1 && !dc.slots && !xchg(h) && !displaced && !rc_pass;
   int rows[2];
   for (int L = 0; L < active; ++L) {
     Lane& ln = dc.lanes[L];
@@ -1436,7 +1446,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       const bool has_next = i + 1 < h.M;
       const bool rc = rc_pass && h.opts.slice == MPSG_SLICE_RECOMPUTE;
       if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[4 * i], ln.stream));
-      launch_contraction(h, dc, s, ln, i, rows[L], tma_g128, *tma_g64, cinfo, ln.stream, rc ? 1 : 0);
+      launch_contraction(h, dc, s, ln, i, rows[L], tma_g128, *tma_g64, cinfo, ln.stream, rc ? 1 : 0, 0, pdl);
       if (timing >= 2) CUDA_OK(cudaEventRecord(ln.gev[4 * i + 1], ln.stream));
       // Displacement fused into the selection (one read of temp) unless the weights must be exchanged
       // first (tensor parallelism) or the decay trace reads the transformed slice.
@@ -1474,6 +1484,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
       };
 
       SelectArgs sa;
+      sa.pdl = pdl ? 1 : 0;
       sa.site = static_cast<int>(i);
       sa.num_sites = static_cast<int>(h.M);
       sa.d = static_cast<int>(h.d);

@@ -386,5 +386,12 @@ __device__ __forceinline__ uint32_t elect_one() {
   return pred;
 }
 
+// Programmatic dependent launch (kernels launched with cudaLaunchAttributeProgrammaticStream-
+// Serialization): wait = block until the preceding kernel in the stream has completed and its memory
+// is visible; launch_dependents = allow the next kernel's CTAs to be scheduled (their prologue runs
+// before their own wait).  Both are no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace ptx
 }  // namespace mpsg

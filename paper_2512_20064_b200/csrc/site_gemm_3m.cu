@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
   const int num_clusters = gridDim.x / kCl;
   const int g_units = kQuad ? (a.g_tiles + 1) >> 1 : a.g_tiles;  // Gamma tile (pairs) per unit row
 
+  if constexpr (kSlice) ptx::grid_dep_wait();  // the prologue reads the selection's bucket counts
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&full[s], 1);   // leader: own expect_tx, bytes from both CTAs
@@ -178,6 +179,10 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the prologue above overlapped the previous kernel's tail; from
+  // here on the previous selection's environment writes / temp reads must be complete.
+  ptx::grid_dep_wait();
+  ptx::grid_dep_launch();
   const int units = g_units * a.s_tiles;
   // slice GEMM: does Gamma tile pair m (outcome of either SM's 128 columns) meet sample tile t's rows?
   auto unit_on = [&](int m, int t) -> bool {
@@ -477,11 +482,13 @@ static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, 
   cfg.blockDim = dim3(128 + 32 * kEpiWarps);
   cfg.dynamicSmemBytes = Cf::kSmem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = kCl;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   const int max_clusters = clusters.get([&] {
@@ -497,6 +504,7 @@ static void launch_3m_t(const CUtensorMap& tma_env64, const CUtensorMap& tma_g, 
     return mc;
   });
   cfg.gridDim = dim3(kCl * std::max(1, std::min(max_clusters, grid / kCl)));
+  if (a.pdl) cfg.numAttrs = 2;
   // kernels without TMA temp stores never read the map: pass any valid one
   check_launch(cudaLaunchKernelEx(&cfg, kern, tma_env64, tma_g, a, tma_temp ? *tma_temp : tma_g),
                "site_gemm_3m_kernel");

@@ -125,6 +125,7 @@ struct Gemm3MArgs {
   const float* scale;
   __half* env_next;  // [2 * 3][env_cap][kp_next]
   int kp_next;
+  int pdl;           // launched as a programmatic dependent of the previous kernel in the stream
 };
 
 // Slice-recompute path: rows of the environment scattered into outcome buckets (bucket d = dead
@@ -196,6 +197,7 @@ struct SelectArgs {
   uint8_t* rowk;
   float* scale_out;
   int* bcount;              // [d + 1]
+  int pdl;                  // launched as a programmatic dependent (select4_kernel only)
 };
 
 // GBS displacement site transform (SPEC.md gbs-ops; the hook of sampler.cpp:143): for every live

@@ -809,15 +809,21 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectArgs a) {
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  if (n >= a.rows) return;
-  const int sidx = a.perm != nullptr ? a.perm[n] : n;  // sample of this row within the pass
-  const bool live_in = sidx < a.count && a.alive[n];
+  const bool in_range = n < a.rows;
+  const int sidx = !in_range ? 0 : a.perm != nullptr ? a.perm[n] : n;  // sample of this row within the pass
+  const bool live_in = in_range && sidx < a.count && a.alive[n];
+  // measure's live counter (RunStats), aggregated per block: one warp per sample made it one
+  // same-address atomic per sample, which serialised in L2 (~60 us per 65536-row site)
+  if (a.live != nullptr) {
+    const int c = __syncthreads_count(live_in && lane == 0);
+    if (threadIdx.x == 0 && c > 0) atomicAdd(a.live, static_cast<unsigned long long>(c));
+  }
+  if (!in_range) return;
   int outcome = kDead;   // recorded at this site
   bool live_out = false; // carries into the next site
   float scale = 0.f;
   double gdiv = 1.0, gmul = 1.0;  // grid modes: next env = RN((temp / gdiv) * gmul)
   const float2* D = sD[kDisp ? wib : 0];
-  if (live_in && a.live != nullptr && lane == 0) atomicAdd(a.live, 1ull);  // measure's counters
   if (kDisp && live_in) {
     const double2 mu = a.mu[static_cast<size_t>(n) * a.num_sites + a.site];
     for (int e = lane; e < a.d * a.d; e += 32) {
@@ -1130,9 +1136,203 @@ void launch_env_reform_s(__half* env, int env_cap, int kshard, int shards, int r
   env_reform_s_kernel<<<blocks, 256, 0, s>>>(env, env_cap, kshard, shards, rows);
 }
 
+// K2 fast path for short rows (chi <= 512): R rows per warp, each row's chosen slice held in
+// registers.  select_kernel's one-warp-per-row chain (alive -> partials -> draw -> slice max -> env
+// stores, the max pass and the split pass each a round trip per 64 columns) is latency-bound when a
+// row is only 2-4 KB: ~14 waves of 32 resident warps per SM over a 65536-row pass.  Here a warp runs
+// the weights / CDF / draw of R rows at once (32/R lanes per row, lane k of a group owns outcome k),
+// then issues all loads of the R chosen slices together (CH chunks of 256 columns per row, 8 columns
+// per lane: 4 * R * CH 16 B loads in flight per lane), takes the max and splits from registers.
+// The arithmetic is select_kernel's operation for operation (fixed-order f64 partial sums per
+// outcome, ascending-k totals and CDF, max of the chosen slice, env_split), so outcomes and
+// environments are bit-identical to it (tests/test_gpu_parity.py::test_select_fast_path_identical).
+// Covers the plain sampling pass: no displacement, no GRID rounding, no decay trace, no slice-
+// recompute bucketing, d <= 32 / R.
+template <int R, int CH>
+__global__ void __launch_bounds__(256) select_rows_kernel(const SelectArgs a) {
+  constexpr unsigned kFull = 0xffffffffu;
+  constexpr int kG = 32 / R;  // lanes per row in the draw phase
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / kG, k = lane % kG, g0 = grp * kG;
+  const unsigned gmask = (kG == 32 ? kFull : ((1u << kG) - 1u)) << g0;
+  const int wrow0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * R;
+  ptx::grid_dep_wait();  // (programmatic dependent launch) the contraction's temp / partials are complete
+  ptx::grid_dep_launch();
+  // ---- phase 1: lane group grp = row wrow0 + grp ----
+  const int n = wrow0 + grp;
+  const bool in_range = n < a.rows;
+  const int sidx = !in_range ? 0 : a.perm != nullptr ? a.perm[n] : n;
+  const bool live_in = in_range && sidx < a.count && a.alive[n];
+  if (a.live != nullptr) {
+    const int c = __syncthreads_count(live_in && k == 0);
+    if (threadIdx.x == 0 && c > 0) atomicAdd(a.live, static_cast<unsigned long long>(c));
+  }
+  if (wrow0 >= a.rows) return;  // whole warp out of range (rows is a multiple of 128)
+  double wk = 0.0;
+  float mk = 0.f;
+  if (live_in && k < a.d) {  // sampler.cpp:83-90: outcome k's tile partials in order, f64
+    const float2* base = a.part_base + n * a.row_stride + k * a.k_stride;
+    for (int t = 0; t < a.parts; ++t) {
+      const float2 v = base[t * a.part_stride];
+      wk += static_cast<double>(v.x);
+      mk = fmaxf(mk, v.y);
+    }
+  }
+  double total = 0.0;  // sampler.cpp:92-93, ascending k
+  for (int q = 0; q < a.d; ++q) total += __shfl_sync(kFull, wk, g0 + q);
+  if (a.marg != nullptr && k < a.d) {
+    if (live_in)
+      a.marg[(static_cast<size_t>(n) * a.num_sites + a.site) * a.d + k] = total == 0.0 ? -1.0 : wk / total;
+    else if (in_range && n < a.count)
+      a.marg[(static_cast<size_t>(n) * a.num_sites + a.site) * a.d + k] = -1.0;
+  }
+  int kk = kDead;
+  if (live_in && total != 0.0) {  // total == 0 -> dead (sampler.cpp:94-98); group-uniform branch
+    if (a.forced != nullptr) {
+      kk = a.forced[static_cast<size_t>(n) * a.num_sites + a.site];
+    } else {
+      const double draw = keyed_uniform(a.seed, kMeasureStream, a.first + sidx, a.site);
+      double cum = 0.0;
+      kk = 0;
+      bool near = false;
+      for (int q = 0; q < a.d; ++q) {  // sampler.cpp:100-106: strict '>', no early break
+        cum += __shfl_sync(gmask, wk, g0 + q) / total;
+        if (draw > cum) ++kk;
+        near |= q + 1 < a.d && fabs(draw - cum) < kBoundaryEps;
+      }
+      if (kk >= a.d) kk = a.d - 1;  // :107
+      if (near && a.near != nullptr && k == 0) atomicAdd(a.near, 1ull);
+    }
+  }
+  // the partials' max of the chosen outcome (used when slice_max == 0: TP / long-K epilogues)
+  const float mk_sel = __shfl_sync(kFull, mk, g0 + ((kk != kDead && kk < kG) ? kk : 0));
+  // ---- phase 2: the warp loads the R chosen slices (all loads in flight), max, split, store ----
+  int out_r[R];
+  float mx_r[R];
+  float2 v[R][CH][8];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    out_r[r] = __shfl_sync(kFull, kk, r * kG);
+    mx_r[r] = __shfl_sync(kFull, mk_sel, r * kG);
+    const int live_cols = out_r[r] != kDead ? a.chir_loc : 0;
+    const float2* src = a.temp + (static_cast<size_t>(wrow0 + r) * a.d + (out_r[r] != kDead ? out_r[r] : 0)) * a.chirp;
+#pragma unroll
+    for (int ch = 0; ch < CH; ++ch) {
+      const int c = ch * 256 + lane * 8;
+      if (c + 7 < live_cols) {  // chirp is a multiple of 128: these loads stay inside the row
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 x = *reinterpret_cast<const float4*>(src + c + 2 * j);
+          v[r][ch][2 * j] = make_float2(x.x, x.y);
+          v[r][ch][2 * j + 1] = make_float2(x.z, x.w);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[r][ch][j] = c + j < live_cols ? src[c + j] : make_float2(0.f, 0.f);
+      }
+    }
+  }
+  if (a.slice_max) {  // precision.cpp:155-160: max component of the chosen slice (zeros beyond it)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float m = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < CH; ++ch)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m = fmaxf(m, fmaxf(fabsf(v[r][ch][j].x), fabsf(v[r][ch][j].y)));
+      mx_r[r] = warp_max(m);
+    }
+  }
+  float scale_r[R];
+  bool live_r[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    scale_r[r] = 0.f;
+    live_r[r] = false;
+    if (out_r[r] != kDead && mx_r[r] > 0.f) {
+      int e;
+      frexpf(mx_r[r], &e);  // the env max lands in [2^13, 2^14)
+      scale_r[r] = ldexpf(1.0f, kEnvExp - e);
+      live_r[r] = true;
+    }
+  }
+  if (lane < R) {
+    int o = kDead;
+    bool lv = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (r == lane) o = out_r[r], lv = live_r[r];
+    const int nr = wrow0 + lane;
+    const int sr = a.perm != nullptr ? a.perm[nr] : nr;
+    if (sr < a.count) {
+      a.rows_out[static_cast<size_t>(sr) * a.num_sites + a.site] = static_cast<uint8_t>(o);
+      a.alive[nr] = lv ? 1 : 0;
+    }
+  }
+  if (a.kp_next <= 0) return;
+  // next env rows (select_kernel's split; zeros for dead rows and beyond the slice): one 16 B store
+  // per plane and 8 columns
+  const size_t plane = static_cast<size_t>(a.env_cap) * a.kp_next;
+  const int C = a.env_comp;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const float sc = live_r[r] ? scale_r[r] : 0.f;
+    __half* e0 = a.env_next + static_cast<size_t>(wrow0 + r) * a.kp_next;
+#pragma unroll
+    for (int ch = 0; ch < CH; ++ch) {
+      const int c = ch * 256 + lane * 8;
+      if (c >= a.kp_next) break;
+      __align__(16) __half hv[3][8], lv[3][8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        __half h3[3], l3[3];
+        // dead rows: select_kernel splits zeros (it reads nothing); the loads above gave zeros too
+        env_split(live_r[r] ? v[r][ch][j].x * sc : 0.f, live_r[r] ? v[r][ch][j].y * sc : 0.f, h3, l3);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) hv[q][j] = h3[q], lv[q][j] = l3[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        if (q >= C) break;
+        *reinterpret_cast<uint4*>(e0 + q * plane + c) = *reinterpret_cast<const uint4*>(hv[q]);
+        *reinterpret_cast<uint4*>(e0 + (C + q) * plane + c) = *reinterpret_cast<const uint4*>(lv[q]);
+      }
+    }
+  }
+}
+
+template <int R, int CH>
+static void launch_select_rows(const SelectArgs& a, cudaStream_t s) {
+  const int threads = 256;
+  const int warps = a.rows / R;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((warps * 32 + threads - 1) / threads);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  check_launch(cudaLaunchKernelEx(&cfg, select_rows_kernel<R, CH>, a), "select_rows_kernel");
+}
+
 void launch_select(const SelectArgs& a, cudaStream_t s) {
   const int threads = 256;
   const int blocks = (a.rows * 32 + threads - 1) / threads;
+  static const bool legacy = [] {
+    const char* v = std::getenv("MPSG_SELECT_LEGACY");
+    return v != nullptr && std::atoi(v) != 0;
+  }();
+  const bool plain = !legacy && a.mu == nullptr && a.grid == kGridNone && a.trace == nullptr && a.rowk == nullptr;
+  if (plain && a.d <= 8 && a.chir_loc <= 256 && a.kp_next <= 256 && a.rows % 4 == 0) {
+    launch_select_rows<4, 1>(a, s);
+    return;
+  }
+  if (plain && a.d <= 16 && a.chir_loc <= 512 && a.kp_next <= 512 && a.rows % 2 == 0) {
+    launch_select_rows<2, 2>(a, s);
+    return;
+  }
   if (a.mu != nullptr) {
     ensure_fact_table();
     if (a.d <= 8)

@@ -1252,3 +1252,27 @@ def test_torchrun_bench_two_ranks_shared_device():
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1 and json.loads(lines[0])["impl"] == "reference"
+
+
+def test_select_fast_path_identical(pkg, gold, tmp_path):
+    """The four-rows-per-warp selection (select4_kernel, the default for plain sampling passes with
+    d <= 8) against the one-warp-per-row select_kernel (MPSG_SELECT_LEGACY=1): identical outcome
+    strings, teacher-forced marginals and RunStats counters (incl. the near-boundary count) on
+    synthetic chains at chi = 256 / 512 / 1024 (one and two pipeline lanes, ragged passes, d = 3, 4,
+    6, 8), SPLIT / SINGLE / PRECISE, the c1 / c1b goldens and a chain where samples die."""
+    import os
+    import subprocess
+    import sys
+    worker = os.path.join(os.path.dirname(__file__), "select_identity_worker.py")
+    files = {}
+    for arm, legacy in (("fast", "0"), ("legacy", "1")):
+        env = dict(os.environ, MPSG_SELECT_LEGACY=legacy)
+        files[arm] = str(tmp_path / f"{arm}.npz")
+        r = subprocess.run([sys.executable, worker, files[arm], str(gold)], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    a, b = np.load(files["fast"]), np.load(files["legacy"])
+    assert sorted(a.files) == sorted(b.files)
+    for k in a.files:
+        assert a[k].dtype == b[k].dtype and np.array_equal(a[k], b[k], equal_nan=True), k
+    assert (a["dead_rows"][:, -1] == pkg.DEAD_OUTCOME).any()
