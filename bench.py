@@ -113,6 +113,21 @@ def chain_macs(M, chi, d):
 # ---------------------------------------------------------------------------------------------
 # clocks during the timed region
 # ---------------------------------------------------------------------------------------------
+def fp16_context(achieved, issued_tflops):
+    """cuBLAS fp16 dense sustained throughput measured on a B200 of this pool with the
+    MEASURED_PEAKS.json method (profiles/r2_gemm_peak/probe.log): fp16 runs ~5% slower than bf16
+    under the 1000 W cap (lower clock), and K1 issues fp16 MMAs."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_gemm_peak", "probe.log")
+    try:
+        rec = json.loads(open(path).read().strip().splitlines()[-1])["fp16"]
+    except Exception:
+        return None
+    pk = rec["tflops_sustained"]
+    return {"peak": pk, "sm_mhz": rec["clocks"]["sm_mhz"], "source": "profiles/r2_gemm_peak/probe.log",
+            "frac": achieved / pk if achieved else None,
+            "issued_frac": issued_tflops / pk if issued_tflops else None}
+
+
 class ClockSampler:
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -568,6 +583,9 @@ def main():
                                                         if gemm_s > 0 and pclk and clocks and clocks.get("sm_mhz")
                                                         else None),
                          "peak_sm_mhz": pclk,
+                         # the contraction's MMAs are fp16 (kind::f16): the same-method cuBLAS fp16
+                         # figure under the same power cap, for context (frac above stays on bf16)
+                         "fp16_sustained": fp16_context(achieved, issued / gemm_s / 1e12 if gemm_s > 0 else None),
                          "gemm_share_of_step": gemm_s / dev_s if dev_s > 0 else None},
             "cpu_baseline": cpu,
             "host_link": link,
