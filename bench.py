@@ -563,7 +563,11 @@ def main():
                                            f"({smp.state_bytes / 1e9:.1f} GB of Gamma scalars) re-read by a reader "
                                            "thread into pinned staging, uploaded and compressed on the device "
                                            f"into 3 slots ({h2d / t_max / 1e9:.1f} GB/s from the file)")
-                                          if file_path else "HBM",
+                                          if file_path else
+                                          (f"HBM, compact 3M: the [Gr, Gi] planes ({smp.state_bytes / 1e9:.1f} GB) "
+                                           "resident, each site copied into 3 device slots and its Gs plane "
+                                           "re-formed there on the copy stream (the 3-plane state does not fit)")
+                                          if smp.gamma_store == "compact" else "HBM",
                        "build_seconds": round(build_s, 1)},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
                          "frac": achieved / sustained if achieved else None, "traffic": traffic,

@@ -194,13 +194,26 @@ void mpsg_destroy(mpsg_handle h);
 
 /* Bytes of the compressed state held per device: in HBM, or for a host-streamed handle in pinned
  * host memory (there the 3M sum planes are re-formed on the device after each copy, so a 3M
- * host-streamed state holds 2/3 of the resident state's bytes); for a generated handle the bytes of
- * its base isometries in HBM. */
+ * host-streamed state holds 2/3 of the resident state's bytes, as does a compact-3M state in HBM);
+ * for a generated handle the bytes of its base isometries in HBM. */
 uint64_t mpsg_state_bytes(mpsg_handle h);
 /* The contraction scheme the handle runs: MPSG_SCHEME_3M or MPSG_SCHEME_4M (0 for a null handle). */
 int mpsg_scheme(mpsg_handle h);
 /* The precision mode the handle runs: MPSG_MODE_SPLIT, _SINGLE or _PRECISE (0 for a null handle). */
 int mpsg_mode(mpsg_handle h);
+/* Where the handle's compressed Gamma lives (0 for a null handle):
+ *   MPSG_STORE_RESIDENT  all planes in HBM
+ *   MPSG_STORE_COMPACT   3M with only [Gr, Gi] in HBM; each site is copied into a ring of device slots
+ *                        and its Gs plane re-formed there (AUTO when only the 2-plane state fits)
+ *   MPSG_STORE_HOST      pinned host memory, streamed per site (host_stream_slots)
+ *   MPSG_STORE_GENERATED regenerated on the device every pass (mpsg_generated_*)
+ *   MPSG_STORE_FILE      re-read from an MPSB file every pass (mpsg_create_from_file_streamed) */
+#define MPSG_STORE_RESIDENT 1
+#define MPSG_STORE_COMPACT 2
+#define MPSG_STORE_HOST 3
+#define MPSG_STORE_GENERATED 4
+#define MPSG_STORE_FILE 5
+int mpsg_gamma_store(mpsg_handle h);
 
 /* The Gamma values the GPU actually samples (decoded compressed format), reference layout:
  * complex128 interleaved (chiL, chiR, d).  The CPU oracle consumes these.  A tensor-parallel

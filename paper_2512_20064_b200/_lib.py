@@ -57,6 +57,7 @@ SIGNATURES = [
     ("mpsg_state_bytes", _u64, [C.c_void_p]),
     ("mpsg_scheme", _int, [C.c_void_p]),
     ("mpsg_mode", _int, [C.c_void_p]),
+    ("mpsg_gamma_store", _int, [C.c_void_p]),
     ("mpsg_decoded_gamma", _int, [C.c_void_p, _u64, _pd]),
     ("mpsg_sample", _int, [C.c_void_p, _u64, _u64, _u64, _pu8, C.POINTER(Stats)]),
     ("mpsg_sample_device", _int, [C.c_void_p, _u64, _u64, _u64, C.c_void_p, C.POINTER(Stats)]),

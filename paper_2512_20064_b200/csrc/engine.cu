@@ -587,6 +587,10 @@ struct mpsg_handle_s {
   bool generated = false;                  // Gamma regenerated on the device every pass (synthetic chains)
   uint64_t gen_seed = 0;
   bool file = false;                       // Gamma streamed from an MPSB file every pass
+  // 3M with only [Gr, Gi] resident in HBM (the 3-plane state does not fit, the 2-plane one does):
+  // every site is copied device-to-device into the slot ring and its Gs plane re-formed there
+  // (the host-streamed machinery with device memory as the store)
+  bool dev_store = false;
   mpsg::FileMeta fmeta;
   std::unique_ptr<mpsg::Comm> comm;
   std::mutex mu;
@@ -629,21 +633,36 @@ static void choose_scheme(mpsg_handle_s& h) {
     m3 = h.pair;  // regenerated / streamed into device slots: no state to fit
   } else if (h.opts.scheme == MPSG_SCHEME_AUTO) {
     if (!h.pair) m3 = false;
-    double state3 = 0.0;
+    double state3 = 0.0, max_site3 = 0.0;
     for (uint64_t i = 0; i < h.M; ++i) {
       const double kp = static_cast<double>(h.tp) * kshard_of(h, h.bonds[i]);
       const double np = round_up(static_cast<int>(h.d) * chirp_of(h, h.bonds[i + 1]), 2 * kBN);
       state3 += 3.0 * 2.0 * np * kp;
+      max_site3 = std::max(max_site3, 3.0 * 2.0 * np * kp);
     }
     if (h.opts.host_stream_slots != 0) {
       const double host = static_cast<double>(sysconf(_SC_PHYS_PAGES)) * sysconf(_SC_PAGE_SIZE);
       if (state3 * (2.0 / 3.0) * h.devs.size() > 0.8 * host) m3 = false;  // host keeps Gr, Gi only
     } else {
+      bool compact = m3;
       for (auto& dc : h.devs) {
         size_t free_b = 0, total_b = 0;
         CUDA_OK(cudaSetDevice(dc.device));
         CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
         if (state3 + 10.0e9 > static_cast<double>(free_b)) m3 = false;  // pass buffers + headroom
+        // [Gr, Gi] resident + a 3-slot ring of 3-plane sites (MPSG_COMPACT_3M=0 disables)
+        if (state3 * (2.0 / 3.0) + 3.0 * max_site3 + 12.0e9 > static_cast<double>(free_b)) compact = false;
+      }
+      // MPSG_COMPACT_3M: 0 = never, 1 = when only the 2-plane state fits (default), 2 = always (tests)
+      static const int env_compact = [] {
+        const char* v = std::getenv("MPSG_COMPACT_3M");
+        return v == nullptr ? 1 : std::atoi(v);
+      }();
+      if (h.pair && (!m3 || env_compact == 2) && compact && env_compact != 0 && !h.precise_auto && h.tp == 1 &&
+          h.opts.mode != MPSG_MODE_PRECISE) {
+        m3 = true;
+        h.dev_store = true;
+        h.opts.host_stream_slots = 3;
       }
     }
   }
@@ -907,8 +926,14 @@ static void free_device(DevCtx& dc) {
   if (dc.pass_end) cudaEventDestroy(dc.pass_end);
   if (dc.copy_stream) cudaStreamSynchronize(dc.copy_stream);
   for (auto& s : dc.sites) {
-    if (s.g_host) cudaFreeHost(s.g_host);
-    if (s.cinfo_host) cudaFreeHost(s.cinfo_host);
+    for (void* p : {static_cast<void*>(s.g_host), static_cast<void*>(s.cinfo_host)}) {
+      if (!p) continue;
+      cudaPointerAttributes at = {};  // the store: pinned host memory, or device memory (compact 3M)
+      if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice)
+        cudaFree(p);
+      else
+        cudaFreeHost(p);
+    }
     if (dc.slots) s.g = nullptr, s.cinfo = nullptr;  // slot buffers, freed below
   }
   for (auto p : dc.slot_g) cudaFree(p);
@@ -1027,18 +1052,23 @@ static void compress_site(mpsg_handle_s& h, DevCtx& dc, uint64_t i, const void* 
   check_err_flag(dc, dc.stream, "site " + std::to_string(i));
   if (dc.slots) {
     const size_t pe = static_cast<size_t>(s.np) * s.kp;  // elements per plane
-    if (!s.g_host) {
-      CUDA_OK(cudaMallocHost(&s.g_host, h.hplanes * pe * sizeof(__half)));
-      CUDA_OK(cudaMallocHost(&s.cinfo_host, 1ull * s.np * sizeof(float2)));
+    if (!s.g_host) {  // the store: pinned host memory, or device memory for the compact-3M state
+      if (h.dev_store) {
+        CUDA_OK(cudaMalloc(&s.g_host, h.hplanes * pe * sizeof(__half)));
+        CUDA_OK(cudaMalloc(&s.cinfo_host, 1ull * s.np * sizeof(float2)));
+      } else {
+        CUDA_OK(cudaMallocHost(&s.g_host, h.hplanes * pe * sizeof(__half)));
+        CUDA_OK(cudaMallocHost(&s.cinfo_host, 1ull * s.np * sizeof(float2)));
+      }
     }
     if (h.hplanes == h.gplanes) {
-      CUDA_OK(cudaMemcpyAsync(s.g_host, s.g, h.gplanes * pe * sizeof(__half), cudaMemcpyDeviceToHost, dc.stream));
-    } else {  // 3M: [Gr, Gi] of each precision half (the Gs planes are re-formed after the H2D copy)
+      CUDA_OK(cudaMemcpyAsync(s.g_host, s.g, h.gplanes * pe * sizeof(__half), cudaMemcpyDefault, dc.stream));
+    } else {  // 3M: [Gr, Gi] of each precision half (the Gs planes are re-formed after the slot copy)
       for (int hf = 0; hf < h.gplanes / 3; ++hf)
         CUDA_OK(cudaMemcpyAsync(s.g_host + 2ull * hf * pe, s.g + 3ull * hf * pe, 2 * pe * sizeof(__half),
-                                cudaMemcpyDeviceToHost, dc.stream));
+                                cudaMemcpyDefault, dc.stream));
     }
-    CUDA_OK(cudaMemcpyAsync(s.cinfo_host, s.cinfo, 1ull * s.np * sizeof(float2), cudaMemcpyDeviceToHost, dc.stream));
+    CUDA_OK(cudaMemcpyAsync(s.cinfo_host, s.cinfo, 1ull * s.np * sizeof(float2), cudaMemcpyDefault, dc.stream));
     CUDA_OK(cudaStreamSynchronize(dc.stream));
     s.g = nullptr;
     s.cinfo = nullptr;
@@ -1134,19 +1164,19 @@ static void issue_loads(mpsg_handle_s& h, DevCtx& dc, uint64_t upto) {
     const size_t pe = static_cast<size_t>(s.np) * s.kp;
     const size_t gb = h.hplanes * pe * sizeof(__half);
     if (h.hplanes == h.gplanes) {
-      CUDA_OK(cudaMemcpyAsync(dc.slot_g[slot], s.g_host, gb, cudaMemcpyHostToDevice, dc.copy_stream));
+      CUDA_OK(cudaMemcpyAsync(dc.slot_g[slot], s.g_host, gb, cudaMemcpyDefault, dc.copy_stream));
     } else {
       for (int hf = 0; hf < h.gplanes / 3; ++hf) {
         __half* dst = dc.slot_g[slot] + 3ull * hf * pe;
         CUDA_OK(cudaMemcpyAsync(dst, s.g_host + 2ull * hf * pe, 2 * pe * sizeof(__half),
-                                cudaMemcpyHostToDevice, dc.copy_stream));
+                                cudaMemcpyDefault, dc.copy_stream));
         launch_sum_plane(dst, pe, dc.copy_stream);  // Gs = Gr + Gi (exact fp16 sums)
       }
     }
     CUDA_OK(cudaMemcpyAsync(dc.slot_cinfo[slot], s.cinfo_host, 1ull * s.np * sizeof(float2),
-                            cudaMemcpyHostToDevice, dc.copy_stream));
+                            cudaMemcpyDefault, dc.copy_stream));
     CUDA_OK(cudaEventRecord(dc.loaded[slot], dc.copy_stream));
-    dc.h2d_bytes += gb + 1ull * s.np * sizeof(float2);
+    if (!h.dev_store) dc.h2d_bytes += gb + 1ull * s.np * sizeof(float2);
     ++dc.issued;
   }
 }
@@ -1437,7 +1467,11 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
     for (int L = 0; L < active; ++L) {
       Lane& ln = dc.lanes[L];
       const uint64_t lfirst = first + off[L];
-      if (active == 2) {  // contraction kernels alternate A_i, B_i, A_i+1, ...
+      static const bool lane_sync = [] {  // MPSG_LANE_SYNC=0: A/B switch (no cross-lane ordering)
+        const char* v = std::getenv("MPSG_LANE_SYNC");
+        return v == nullptr || std::atoi(v) != 0;
+      }();
+      if (active == 2 && (lane_sync || dc.slots)) {  // contraction kernels alternate A_i, B_i, A_i+1, ...
         if (L == 1)
           CUDA_OK(cudaStreamWaitEvent(ln.stream, dc.lanes[0].k1done, 0));
         else if (i > 0)
@@ -2177,6 +2211,14 @@ uint64_t mpsg_state_bytes(mpsg_handle h) {
 
 int mpsg_scheme(mpsg_handle h) { return h ? (h->m3 ? MPSG_SCHEME_3M : MPSG_SCHEME_4M) : 0; }
 
+int mpsg_gamma_store(mpsg_handle h) {
+  if (!h || h->devs.empty()) return 0;
+  if (h->generated) return MPSG_STORE_GENERATED;
+  if (h->file) return MPSG_STORE_FILE;
+  if (h->dev_store) return MPSG_STORE_COMPACT;
+  return h->devs[0].slots ? MPSG_STORE_HOST : MPSG_STORE_RESIDENT;
+}
+
 int mpsg_mode(mpsg_handle h) {
   if (!h) return 0;
   if (h->grid) return MPSG_MODE_GRID;
@@ -2235,9 +2277,10 @@ int mpsg_decoded_gamma(mpsg_handle h, uint64_t site, double* out) {
       cudaFree(tg);
       cudaFree(tc);
       CUDA_OK(e);
-    } else if (dc.slots) {  // host planes [Gr, Gi] per precision half: place them at their device plane
+    } else if (dc.slots) {  // stored planes [Gr, Gi] per precision half: place them at their device plane
       for (int hf = 0; hf < h->hplanes / 2; ++hf)
-        std::memcpy(g.data() + (h->m3 ? 3 : 2) * hf * pe, s.g_host + 2 * hf * pe, 2 * pe * sizeof(__half));
+        CUDA_OK(cudaMemcpy(g.data() + (h->m3 ? 3 : 2) * hf * pe, s.g_host + 2 * hf * pe, 2 * pe * sizeof(__half),
+                           cudaMemcpyDefault));
     } else {
       CUDA_OK(cudaMemcpy(g.data(), s.g, g.size() * sizeof(__half), cudaMemcpyDeviceToHost));
     }

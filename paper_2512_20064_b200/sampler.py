@@ -418,6 +418,13 @@ class GpuSampler:
         """The contraction scheme this handle runs (3M or 4M)."""
         return Scheme(_lib.lib().mpsg_scheme(self._h))
 
+    @property
+    def gamma_store(self) -> str:
+        """Where the compressed Gamma lives: resident / compact (3M, [Gr, Gi] in HBM, Gs re-formed per
+        site in device slots) / host / generated / file (mpsg_gamma_store)."""
+        return {1: "resident", 2: "compact", 3: "host", 4: "generated", 5: "file"}.get(
+            _lib.lib().mpsg_gamma_store(self._h), "none")
+
     def decoded_gamma(self, site: int) -> np.ndarray:
         b = self.bond_dims
         out = np.empty((b[site], b[site + 1], self.phys_dim), np.complex128)

@@ -1,6 +1,7 @@
-"""Worker for test_select_fast_path_identical: samples a set of chains and writes rows, marginals and
-counters to an npz.  Run once with MPSG_SELECT_LEGACY=1 (one warp per row) and once without (the
-four-rows-per-warp fast path); the test asserts the two files are identical bit for bit."""
+"""Worker for the engine A/B identity tests (test_select_fast_path_identical,
+test_compact_3m_store_identical): samples a set of chains and writes rows, teacher-forced marginals,
+counters and state sizes to an npz.  The tests run it under two settings of an engine switch
+(MPSG_SELECT_LEGACY, MPSG_COMPACT_3M -- read once per process) and compare the files bit for bit."""
 import os
 import sys
 
@@ -33,6 +34,7 @@ for m, chi, d, n, ps, mode in [(10, 256, 4, 2000, 0, P.Mode.SPLIT), (8, 512, 6, 
                                (6, 256, 3, 600, 256, P.Mode.PRECISE)]:
     smp, _ = build_synthetic(m, chi, d, seed=13, policy=pol, mode=mode, pass_samples=ps)
     record(f"syn_{m}_{chi}_{d}_{int(mode)}", smp, n, 7, first=5)
+    res[f"syn_{m}_{chi}_{d}_{int(mode)}_state_bytes"] = np.array([smp.state_bytes], dtype=np.uint64)
     smp.close()
 g0 = np.zeros((1, 2, 2), complex)  # a chain where some samples die (test_gpu_parity._dead_chain)
 g0[0, 0, 0], g0[0, 1, 1] = 1.0, 0.8

@@ -1276,3 +1276,39 @@ def test_select_fast_path_identical(pkg, gold, tmp_path):
     for k in a.files:
         assert a[k].dtype == b[k].dtype and np.array_equal(a[k], b[k], equal_nan=True), k
     assert (a["dead_rows"][:, -1] == pkg.DEAD_OUTCOME).any()
+
+
+def _worker_arms(gold, tmp_path, var, arms):
+    import os
+    import subprocess
+    import sys
+    worker = os.path.join(os.path.dirname(__file__), "select_identity_worker.py")
+    out = {}
+    for arm, val in arms:
+        f = str(tmp_path / f"{arm}.npz")
+        r = subprocess.run([sys.executable, worker, f, str(gold)], env=dict(os.environ, **{var: val}),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        out[arm] = np.load(f)
+    return out
+
+
+def test_compact_3m_store_identical(pkg, gold, tmp_path):
+    """Compact 3M (only [Gr, Gi] resident in HBM; every site copied into the slot ring and its Gs
+    plane re-formed there -- AUTO's choice when the 3-plane state does not fit but the 2-plane one
+    does, e.g. c5 chi = 4096) forced on every chain (MPSG_COMPACT_3M=2) against the resident
+    3-plane state (=0): identical rows, marginals and counters; the resident store is 2/3 of the
+    3-plane one for the SPLIT / SINGLE synthetic chains (PRECISE and the AUTO c1 chains keep their
+    own state)."""
+    r = _worker_arms(gold, tmp_path, "MPSG_COMPACT_3M", (("compact", "2"), ("resident", "0")))
+    a, b = r["compact"], r["resident"]
+    assert sorted(a.files) == sorted(b.files)
+    compacted = 0
+    for k in a.files:
+        if k.endswith("_state_bytes"):
+            if int(a[k][0]) != int(b[k][0]):
+                assert 3 * int(a[k][0]) == 2 * int(b[k][0]), k
+                compacted += 1
+            continue
+        assert a[k].dtype == b[k].dtype and np.array_equal(a[k], b[k], equal_nan=True), k
+    assert compacted >= 4
