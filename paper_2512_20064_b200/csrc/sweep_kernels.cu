@@ -1459,7 +1459,9 @@ struct ArraySrc {  // complex T interleaved, (chiL, chiR * d) row-major
   __device__ __forceinline__ static double wide(double x) { return x; }
   __device__ __forceinline__ static double wide(float x) { return static_cast<double>(x); }
   __device__ __forceinline__ static double wide(__half x) { return static_cast<double>(__half2float(x)); }
-  __device__ __forceinline__ void load(int l, size_t j, double& re, double& im) const {
+  struct Col {};  // nothing per column
+  __device__ __forceinline__ Col col(size_t) const { return {}; }
+  __device__ __forceinline__ void load(int l, size_t j, const Col&, double& re, double& im) const {
     const T* q = p + 2 * (static_cast<size_t>(l) * stride + j);
     re = wide(q[0]);
     im = wide(q[1]);
@@ -1470,19 +1472,27 @@ struct ArraySrc {  // complex T interleaved, (chiL, chiR * d) row-major
 //   Gamma_i[l, j] = B[l, j] * phase_i[j] * (lambda_{i-1}[l] * (1 / lambda_i[r])),  j = r * d + k
 // with explicitly rounded fp32 operations, so every kernel that evaluates it (the compression of a
 // regenerated site, mpsg_synthetic_site) produces the same bits.
-__device__ __forceinline__ float2 synth_value(const SynthSite& g, int l, size_t j) {
+// (ph = phase_i[j], il = 1 / lambda_i[r]: per column, hoisted out of the compression kernels' row loops)
+__device__ __forceinline__ float2 synth_value_c(const SynthSite& g, int l, size_t j, float2 ph, float il) {
   const float2 b = g.base[static_cast<size_t>(l) * g.ld + j];
-  const float2 ph = g.phase[j];
   const float tr = __fsub_rn(__fmul_rn(b.x, ph.x), __fmul_rn(b.y, ph.y));
   const float ti = __fadd_rn(__fmul_rn(b.x, ph.y), __fmul_rn(b.y, ph.x));
-  const float sc = __fmul_rn(g.lam_prev[l], g.inv_lam[j / g.d]);
+  const float sc = __fmul_rn(g.lam_prev[l], il);
   return make_float2(__fmul_rn(tr, sc), __fmul_rn(ti, sc));
+}
+__device__ __forceinline__ float2 synth_value(const SynthSite& g, int l, size_t j) {
+  return synth_value_c(g, l, j, g.phase[j], g.inv_lam[j / g.d]);
 }
 struct SynthSrc {
   static constexpr bool kExactF32 = true;  // fp32 generator values
   SynthSite g;
-  __device__ __forceinline__ void load(int l, size_t j, double& re, double& im) const {
-    const float2 v = synth_value(g, l, j);
+  struct Col {
+    float2 ph;
+    float il;
+  };
+  __device__ __forceinline__ Col col(size_t j) const { return {g.phase[j], g.inv_lam[j / g.d]}; }
+  __device__ __forceinline__ void load(int l, size_t j, const Col& c, double& re, double& im) const {
+    const float2 v = synth_value_c(g, l, j, c.ph, c.il);
     re = static_cast<double>(v.x);
     im = static_cast<double>(v.y);
   }
@@ -1533,11 +1543,14 @@ __global__ void colmax_kernel(const Src src, int chil, int d, int b0, int width,
   const int l0 = blockIdx.y * 64, l1 = min(chil, l0 + 64);
   double mx = 0.0;
   bool finite = true;
+  // per-column operands loaded once per thread (the row loop is load-instruction bound otherwise)
+  const typename Src::Col cj = src.col(j);
+  const double grr = gr[r];
   for (int l = l0; l < l1; ++l) {
     double re, im;
-    src.load(l, j, re, im);
+    src.load(l, j, cj, re, im);
     if (!isfinite(re) || !isfinite(im)) finite = false;
-    const double f = gr[r] * inv_pow2(gl[l]);
+    const double f = grr * inv_pow2(gl[l]);
     mx = fmax(mx, fmax(fabs(re * f), fabs(im * f)));
   }
   if (!finite) atomicExch(err, 3);  // NumericError: non-finite Gamma (contract.cpp:117-119)
@@ -1622,16 +1635,27 @@ __global__ void pack_kernel(const Src src, int chil, int d, int b0, int width, i
   const int wcols = width * d;
   const int j0 = blockIdx.x * 32, l0 = blockIdx.y * 64;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  // this thread's column: its per-column operands are loaded once, outside the row loop
+  const int jc = j0 + tx;
+  const bool col_ok = jc < wcols;
+  const int rc = col_ok ? jc / d : 0, kc = col_ok ? jc - rc * d : 0;
+  const size_t jsrc = static_cast<size_t>(b0 + rc) * d + kc;
+  typename Src::Col cj{};
+  double grr = 0.0, ics = 0.0;
+  if (col_ok) {
+    cj = src.col(jsrc);
+    grr = gr[b0 + rc];
+    ics = inv_pow2(cs[jc]);
+  }
   for (int yy = ty; yy < 64; yy += 8) {
-    const int l = l0 + yy, jl = j0 + tx;
+    const int l = l0 + yy;
     __half h[6];
 #pragma unroll
     for (int p = 0; p < 6; ++p) h[p] = __float2half_rn(0.f);
-    if (l < chil && jl < wcols) {
-      const int rl = jl / d, k = jl - rl * d;
+    if (l < chil && col_ok) {
       double re, im;
-      src.load(l, static_cast<size_t>(b0 + rl) * d + k, re, im);
-      const double f = gr[b0 + rl] * inv_pow2(gl[l]) * inv_pow2(cs[jl]);
+      src.load(l, jsrc, cj, re, im);
+      const double f = grr * inv_pow2(gl[l]) * ics;
       if (grid != kGridNone) {  // round_scalar per component (precision.cpp:23-50): IEEE RNE
         h[0] = __double2half(re * f);
         h[1] = __double2half(im * f);

@@ -1312,3 +1312,23 @@ def test_compact_3m_store_identical(pkg, gold, tmp_path):
             continue
         assert a[k].dtype == b[k].dtype and np.array_equal(a[k], b[k], equal_nan=True), k
     assert compacted >= 4
+
+
+@pytest.mark.parametrize("chi,d", [(256, 4), (512, 6)])
+def test_generated_compression_equals_array_compression(pkg, chi, d):
+    """The regenerated supply's compression (SynthSrc: generator values straight into colmax / pack,
+    fp32 quantize_pair) against the array path (the same site values materialised as complex128 by
+    mpsg_generated_site_values, compressed with the f64 quantize_pair): identical decoded Gamma at
+    every site, so hoisting the generator's per-column operands out of the row loops changed no bit."""
+    from paper_2512_20064_b200.synthetic import build_synthetic
+    pol = pkg.PrecisionPolicy(scaling=pkg.ScalingMode.PER_SAMPLE_MAX)
+    m = 8
+    gen, lams = build_synthetic(m, chi, d, seed=21, policy=pol, generated=True, pass_samples=512)
+    gammas = [gen.original_gamma(i) for i in range(m)]
+    st = pkg.MpsState(m, d, list(gen.bond_dims), gammas, [np.asarray(x, float) for x in lams])
+    arr = pkg.GpuSampler(st, pol, mode=pkg.Mode.SPLIT, pass_samples=512)
+    for i in range(m):
+        assert np.array_equal(gen.decoded_gamma(i), arr.decoded_gamma(i)), i
+    assert np.array_equal(gen.sample(0, 700, 7), arr.sample(0, 700, 7))
+    gen.close()
+    arr.close()
