@@ -1527,7 +1527,15 @@ void launch_synth_values(const SynthSite& g, int rows, float2* out, cudaStream_t
 // 1 / x for a power of two x (the bond and column scales): exact, and a few integer ops instead of an
 // f64 division (the divisions made the compression kernels FP64-bound: pack 1.5 ms per chi = 8192
 // site, the regenerated supply's main overhead).
-__device__ __forceinline__ double inv_pow2(double x) { return ldexp(1.0, -ilogb(x)); }
+// Fast path on the exponent bits (2^-floor(log2 x) for a positive normal x whose reciprocal power is
+// normal -- every scale the engine forms); ilogb / ldexp otherwise.  Bit-identical to the original
+// (the library calls made the compression kernels issue-bound: ~200 instructions per element).
+__device__ __forceinline__ double inv_pow2(double x) {
+  const long long b = __double_as_longlong(x);
+  const int e = static_cast<int>((b >> 52) & 0x7ff);
+  if (b > 0 && e >= 1 && e <= 2045) return __longlong_as_double(static_cast<long long>(2046 - e) << 52);
+  return ldexp(1.0, -ilogb(x));
+}
 
 // Per local column jl = r_loc * d + k: max over l of max(|re|, |im|) * gr[r] / gl[l] (f64), as an
 // order-independent atomic max of the nonnegative doubles' bit patterns.  A 2-D grid (64-row chunks
@@ -1613,10 +1621,11 @@ __device__ __forceinline__ void quantize_pair_f32(float a, float b, __half& ha, 
     ha = hb = hs = __float2half_rn(0.f);
     return;
   }
-  int e;
-  frexpf(m, &e);
-  const int ue = max(e - 11, -24);
-  const float u = ldexpf(1.f, ue), iu = ldexpf(1.f, -ue);
+  // frexpf's exponent from the bits (m = f 2^e, f in [0.5, 1)); a subnormal m has e <= -126, so
+  // ue = -24 for it either way; u = 2^ue and 1/u are built from their exponent fields
+  const int eb = (__float_as_int(m) >> 23) & 0xff;
+  const int ue = eb == 0 ? -24 : max(eb - 126 - 11, -24);
+  const float u = __int_as_float((ue + 127) << 23), iu = __int_as_float((127 - ue) << 23);
   const float qa = rintf(a * iu) * u, qb = rintf(b * iu) * u;
   ha = __float2half_rn(qa);
   hb = __float2half_rn(qb);
