@@ -444,11 +444,12 @@ def main():
     # e2e through the C ABI with host buffers: rows D2H inside the timed region and, in the
     # streamed arm, the whole compressed MPS H2D from pinned host memory every step
     state_bytes = smp.state_bytes
+    gamma_store = smp.gamma_store  # of the timed handle (the streamed e2e arm replaces smp below)
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     e2e_mode = args.e2e
     if e2e_mode == "auto":
         # a 3M state streams its Gr, Gi planes only (Gs is re-formed on the device): 2/3 of the bytes
-        host_need = state_bytes * (2 / 3 if smp.scheme == P.Scheme.M3 else 1)
+        host_need = state_bytes * (2 / 3 if smp.scheme == P.Scheme.M3 and gamma_store == "resident" else 1)
         # several ranks pin their states at once: keep 40% of the host memory free then
         room = host_mem_available() * (1 / 1.15 if local_world == 1 else 0.6)
         e2e_mode = "stream" if (not args.stream_slots and room > host_need * local_world) \
@@ -549,7 +550,7 @@ def main():
                        "bond_schedule": sched_note,
                        "displacement": (f"GBS displacement D(mu) per (sample, site), mu ~ CN(0, {args.displace}^2)"
                                         if args.displace > 0 else None),
-                       "l2": (f"inputs larger than L2 (compressed MPS {smp.state_bytes / 1e9:.1f} GB)" if not generated
+                       "l2": (f"inputs larger than L2 (compressed MPS {state_bytes / 1e9:.1f} GB)" if not generated
                               else "inputs larger than L2 (every site regenerated into 3 device slots of up to "
                                    f"{max(6 * cfg['chi'] * cfg['chi'] * cfg['d'], 1) / 1e9:.1f} GB)"),
                        "warmup_pass_samples": min(warm_pass, P_pass),
@@ -564,10 +565,10 @@ def main():
                                            "thread into pinned staging, uploaded and compressed on the device "
                                            f"into 3 slots ({h2d / t_max / 1e9:.1f} GB/s from the file)")
                                           if file_path else
-                                          (f"HBM, compact 3M: the [Gr, Gi] planes ({smp.state_bytes / 1e9:.1f} GB) "
+                                          (f"HBM, compact 3M: the [Gr, Gi] planes ({state_bytes / 1e9:.1f} GB) "
                                            "resident, each site copied into 3 device slots and its Gs plane "
                                            "re-formed there on the copy stream (the 3-plane state does not fit)")
-                                          if smp.gamma_store == "compact" else "HBM",
+                                          if gamma_store == "compact" else "HBM",
                        "build_seconds": round(build_s, 1)},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
                          "frac": achieved / sustained if achieved else None, "traffic": traffic,

@@ -1496,6 +1496,9 @@ struct SynthSrc {
     re = static_cast<double>(v.x);
     im = static_cast<double>(v.y);
   }
+  __device__ __forceinline__ float2 load_f(int l, size_t j, const Col& c) const {
+    return synth_value_c(g, l, j, c.ph, c.il);
+  }
 };
 
 // phase_i[j] = exp(2 pi i u), u = keyed uniform of (seed, kPhaseStream, site, j) (rng.hpp:22-37)
@@ -1555,6 +1558,13 @@ __global__ void colmax_kernel(const Src src, int chil, int d, int b0, int width,
   const typename Src::Col cj = src.col(j);
   const double grr = gr[r];
   for (int l = l0; l < l1; ++l) {
+    if constexpr (std::is_same<Src, SynthSrc>::value) {
+      // max(|re f|, |im f|) = max(|re|, |im|) f: f > 0 and both f64 products are exact
+      const float2 v = src.load_f(l, j, cj);
+      if (!isfinite(v.x) || !isfinite(v.y)) finite = false;
+      mx = fmax(mx, static_cast<double>(fmaxf(fabsf(v.x), fabsf(v.y))) * (grr * inv_pow2(gl[l])));
+      continue;
+    }
     double re, im;
     src.load(l, j, cj, re, im);
     if (!isfinite(re) || !isfinite(im)) finite = false;
@@ -1662,9 +1672,25 @@ __global__ void pack_kernel(const Src src, int chil, int d, int b0, int width, i
 #pragma unroll
     for (int p = 0; p < 6; ++p) h[p] = __float2half_rn(0.f);
     if (l < chil && col_ok) {
+      const double f = grr * inv_pow2(gl[l]) * ics;
+      if constexpr (std::is_same<Src, SynthSrc>::value) {
+        // fp32 generator values scaled by a power of two that is a normal float: v * f in fp32 is one
+        // rounding of the same exact product as float(double(v) * f) -- identical bits, no f64 work
+        if (grid == kGridNone && f >= 0x1p-126 && f <= 0x1p127) {
+          const float ff = static_cast<float>(f);
+          const float2 v = src.load_f(l, jsrc, cj);
+          const float a = __fmul_rn(v.x, ff), b = __fmul_rn(v.y, ff);
+          quantize_pair_f32(a, b, h[0], h[1], h[2]);
+          if (gplanes == 6)
+            quantize_pair_f32(a - __half2float(h[0]), b - __half2float(h[1]), h[3], h[4], h[5]);
+#pragma unroll
+          for (int p = 0; p < 6; ++p)
+            if (p < gplanes) tp[p][yy][tx] = h[p];
+          continue;
+        }
+      }
       double re, im;
       src.load(l, jsrc, cj, re, im);
-      const double f = grr * inv_pow2(gl[l]) * ics;
       if (grid != kGridNone) {  // round_scalar per component (precision.cpp:23-50): IEEE RNE
         h[0] = __double2half(re * f);
         h[1] = __double2half(im * f);
