@@ -1473,12 +1473,15 @@ struct ArraySrc {  // complex T interleaved, (chiL, chiR * d) row-major
 // with explicitly rounded fp32 operations, so every kernel that evaluates it (the compression of a
 // regenerated site, mpsg_synthetic_site) produces the same bits.
 // (ph = phase_i[j], il = 1 / lambda_i[r]: per column, hoisted out of the compression kernels' row loops)
-__device__ __forceinline__ float2 synth_value_c(const SynthSite& g, int l, size_t j, float2 ph, float il) {
-  const float2 b = g.base[static_cast<size_t>(l) * g.ld + j];
+// (b = B[l, j] and lp = lambda_{i-1}[l] already loaded: the compression kernels batch these loads)
+__device__ __forceinline__ float2 synth_from_base(float2 b, float2 ph, float lp, float il) {
   const float tr = __fsub_rn(__fmul_rn(b.x, ph.x), __fmul_rn(b.y, ph.y));
   const float ti = __fadd_rn(__fmul_rn(b.x, ph.y), __fmul_rn(b.y, ph.x));
-  const float sc = __fmul_rn(g.lam_prev[l], il);
+  const float sc = __fmul_rn(lp, il);
   return make_float2(__fmul_rn(tr, sc), __fmul_rn(ti, sc));
+}
+__device__ __forceinline__ float2 synth_value_c(const SynthSite& g, int l, size_t j, float2 ph, float il) {
+  return synth_from_base(g.base[static_cast<size_t>(l) * g.ld + j], ph, g.lam_prev[l], il);
 }
 __device__ __forceinline__ float2 synth_value(const SynthSite& g, int l, size_t j) {
   return synth_value_c(g, l, j, g.phase[j], g.inv_lam[j / g.d]);
@@ -1557,14 +1560,29 @@ __global__ void colmax_kernel(const Src src, int chil, int d, int b0, int width,
   // per-column operands loaded once per thread (the row loop is load-instruction bound otherwise)
   const typename Src::Col cj = src.col(j);
   const double grr = gr[r];
-  for (int l = l0; l < l1; ++l) {
-    if constexpr (std::is_same<Src, SynthSrc>::value) {
-      // max(|re f|, |im f|) = max(|re|, |im|) f: f > 0 and both f64 products are exact
-      const float2 v = src.load_f(l, j, cj);
-      if (!isfinite(v.x) || !isfinite(v.y)) finite = false;
-      mx = fmax(mx, static_cast<double>(fmaxf(fabsf(v.x), fabsf(v.y))) * (grr * inv_pow2(gl[l])));
-      continue;
+  if constexpr (std::is_same<Src, SynthSrc>::value) {
+    // max(|re f|, |im f|) = max(|re|, |im|) f: f > 0 and both f64 products are exact; rows in groups
+    // of 8 with their loads issued together
+    for (int lb = l0; lb < l1; lb += 8) {
+      float2 bv[8];
+      float lp[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int l = lb + i;
+        bv[i] = l < l1 ? src.g.base[static_cast<size_t>(l) * src.g.ld + j] : make_float2(0.f, 0.f);
+        lp[i] = l < l1 ? src.g.lam_prev[l] : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int l = lb + i;
+        if (l >= l1) break;
+        const float2 v = synth_from_base(bv[i], cj.ph, lp[i], cj.il);
+        if (!isfinite(v.x) || !isfinite(v.y)) finite = false;
+        mx = fmax(mx, static_cast<double>(fmaxf(fabsf(v.x), fabsf(v.y))) * (grr * inv_pow2(gl[l])));
+      }
     }
+  }
+  for (int l = l0; l < l1 && !std::is_same<Src, SynthSrc>::value; ++l) {
     double re, im;
     src.load(l, j, cj, re, im);
     if (!isfinite(re) || !isfinite(im)) finite = false;
@@ -1666,29 +1684,60 @@ __global__ void pack_kernel(const Src src, int chil, int d, int b0, int width, i
     grr = gr[b0 + rc];
     ics = inv_pow2(cs[jc]);
   }
-  for (int yy = ty; yy < 64; yy += 8) {
+  bool done = false;
+  if constexpr (std::is_same<Src, SynthSrc>::value) {
+    if (grid == kGridNone) {
+      // generator source: the thread's 8 rows' operands are loaded up front (8 base loads in flight per
+      // thread -- one at a time left the kernel waiting on DRAM latency), then each value is scaled by
+      // its power of two in fp32 when that is a normal float: v * f in fp32 is one rounding of the
+      // same exact product as float(double(v) * f), i.e. the generic path's bits without f64 work
+      float2 bv[8];
+      float lp[8];
+      double ig[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int l = l0 + ty + 8 * i;
+        const bool ok = l < chil && col_ok;
+        bv[i] = ok ? src.g.base[static_cast<size_t>(l) * src.g.ld + jsrc] : make_float2(0.f, 0.f);
+        lp[i] = ok ? src.g.lam_prev[l] : 0.f;
+        ig[i] = ok ? inv_pow2(gl[l]) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int yy = ty + 8 * i, l = l0 + yy;
+        __half h[6];
+#pragma unroll
+        for (int p = 0; p < 6; ++p) h[p] = __float2half_rn(0.f);
+        if (l < chil && col_ok) {
+          const double f = grr * ig[i] * ics;
+          const float2 v = synth_from_base(bv[i], cj.ph, lp[i], cj.il);
+          float a, b;
+          if (f >= 0x1p-126 && f <= 0x1p127) {
+            const float ff = static_cast<float>(f);
+            a = __fmul_rn(v.x, ff);
+            b = __fmul_rn(v.y, ff);
+          } else {
+            a = static_cast<float>(static_cast<double>(v.x) * f);
+            b = static_cast<float>(static_cast<double>(v.y) * f);
+          }
+          quantize_pair_f32(a, b, h[0], h[1], h[2]);
+          if (gplanes == 6)
+            quantize_pair_f32(a - __half2float(h[0]), b - __half2float(h[1]), h[3], h[4], h[5]);
+        }
+#pragma unroll
+        for (int p = 0; p < 6; ++p)
+          if (p < gplanes) tp[p][yy][tx] = h[p];
+      }
+      done = true;
+    }
+  }
+  for (int yy = ty; yy < 64 && !done; yy += 8) {
     const int l = l0 + yy;
     __half h[6];
 #pragma unroll
     for (int p = 0; p < 6; ++p) h[p] = __float2half_rn(0.f);
     if (l < chil && col_ok) {
       const double f = grr * inv_pow2(gl[l]) * ics;
-      if constexpr (std::is_same<Src, SynthSrc>::value) {
-        // fp32 generator values scaled by a power of two that is a normal float: v * f in fp32 is one
-        // rounding of the same exact product as float(double(v) * f) -- identical bits, no f64 work
-        if (grid == kGridNone && f >= 0x1p-126 && f <= 0x1p127) {
-          const float ff = static_cast<float>(f);
-          const float2 v = src.load_f(l, jsrc, cj);
-          const float a = __fmul_rn(v.x, ff), b = __fmul_rn(v.y, ff);
-          quantize_pair_f32(a, b, h[0], h[1], h[2]);
-          if (gplanes == 6)
-            quantize_pair_f32(a - __half2float(h[0]), b - __half2float(h[1]), h[3], h[4], h[5]);
-#pragma unroll
-          for (int p = 0; p < 6; ++p)
-            if (p < gplanes) tp[p][yy][tx] = h[p];
-          continue;
-        }
-      }
       double re, im;
       src.load(l, jsrc, cj, re, im);
       if (grid != kGridNone) {  // round_scalar per component (precision.cpp:23-50): IEEE RNE
