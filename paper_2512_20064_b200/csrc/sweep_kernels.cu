@@ -1499,9 +1499,6 @@ struct SynthSrc {
     re = static_cast<double>(v.x);
     im = static_cast<double>(v.y);
   }
-  __device__ __forceinline__ float2 load_f(int l, size_t j, const Col& c) const {
-    return synth_value_c(g, l, j, c.ph, c.il);
-  }
 };
 
 // phase_i[j] = exp(2 pi i u), u = keyed uniform of (seed, kPhaseStream, site, j) (rng.hpp:22-37)
