@@ -1432,7 +1432,7 @@ static void run_pass(mpsg_handle_s& h, DevCtx& dc, uint64_t seed, uint64_t first
   // trace read temp): rows are then permuted by outcome every such site, perm maps them to samples
   const bool rc_pass = h.slice_rc && !forced && !marg && !displaced && !dc.trace;
   // Programmatic dependent launch between the contraction and the selection of consecutive sites
-  // (one lane, resident or generated Gamma, no exchange / displacement / slice recompute): each
+  // (one lane, HBM-resident Gamma, no exchange / displacement / slice recompute): each
   // kernel's prologue overlaps its predecessor's tail.  Opt-in (MPSG_PDL=1): measured neutral at
   // chi = 256 / 512 (profiles/r2_select_rows/), where the per-site launches are shortest.
   static const bool env_pdl = [] {
@@ -2443,7 +2443,7 @@ int mpsg_contract_site(mpsg_handle h, uint64_t site, const double* env, uint64_t
     config_check(h != nullptr && env != nullptr && temp != nullptr, "null argument");
     config_check(site < h->M && h->finished, "bad site / unfinished state");
     config_check(h->tp == 1, "mpsg_contract_site: not available on a tensor-parallel handle");
-    config_check(h->devs[0].slots == 0, "mpsg_contract_site: not available in host-streamed mode");
+    config_check(h->devs[0].slots == 0, "mpsg_contract_site: not available with a slot-streamed Gamma store (host / compact 3M)");
     DevCtx& dc = h->devs[0];
     config_check(count >= 1 && count <= static_cast<uint64_t>(dc.lanes[0].cap), "count exceeds pass capacity");
     CUDA_OK(cudaSetDevice(dc.device));
