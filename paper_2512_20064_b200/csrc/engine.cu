@@ -755,7 +755,12 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
   CUDA_OK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dc.device));
   if (major != 10) throw Error(MPSG_ERR_CUDA, "device is not sm_100 (B200)");
   CUDA_OK(cudaDeviceGetAttribute(&dc.num_sms, cudaDevAttrMultiProcessorCount, dc.device));
-  CUDA_OK(cudaStreamCreateWithFlags(&dc.stream, cudaStreamNonBlocking));
+  // Stream priorities: the lanes' streams (contraction, selection) run at the device's greatest
+  // priority and the copy stream (slot copies, Gs re-formation, side-stream compression) at its
+  // least, so the block scheduler places a persistent contraction's CTAs before further supply blocks
+  int prio_least = 0, prio_greatest = 0;
+  CUDA_OK(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+  CUDA_OK(cudaStreamCreateWithPriority(&dc.stream, cudaStreamNonBlocking, prio_greatest));
   const int kmax = h.tp * kshard_max_of(h), chirpm = chirp_max_of(h);
   const size_t nt_max = h.d * (chirpm / kBN) + 1;  // + the pair-padding tile
   const size_t row_bytes = 4ull * h.env_comp * kmax + 8ull * h.d * chirpm + 8ull * nt_max + 1 + h.M +
@@ -787,7 +792,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
     if (L == 0)
       ln.stream = dc.stream;
     else
-      CUDA_OK(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking));
+      CUDA_OK(cudaStreamCreateWithPriority(&ln.stream, cudaStreamNonBlocking, prio_greatest));
     CUDA_OK(cudaMalloc(&ln.env, 2ull * h.env_comp * ln.cap * kmax * sizeof(__half)));
     CUDA_OK(cudaMalloc(&ln.temp, 1ull * ln.cap * h.d * chirpm * sizeof(float2)));
     CUDA_OK(cudaMalloc(&ln.pstat, 1ull * ln.cap * nt_max * sizeof(float2)));
@@ -833,7 +838,7 @@ static void alloc_device(mpsg_handle_s& h, DevCtx& dc) {
       gmax = std::max(gmax, static_cast<size_t>(h.gplanes) * np * kp);
       nmax = std::max(nmax, np);
     }
-    CUDA_OK(cudaStreamCreateWithFlags(&dc.copy_stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithPriority(&dc.copy_stream, cudaStreamNonBlocking, prio_least));
     dc.slot_g.resize(dc.slots);
     dc.slot_cinfo.resize(dc.slots);
     dc.loaded.resize(dc.slots);
