@@ -1332,3 +1332,17 @@ def test_generated_compression_equals_array_compression(pkg, chi, d):
     assert np.array_equal(gen.sample(0, 700, 7), arr.sample(0, 700, 7))
     gen.close()
     arr.close()
+
+
+def test_gamma_store_reported(pkg):
+    """mpsg_gamma_store names where each handle's compressed Gamma lives (resident in HBM, pinned host
+    memory streamed per site, regenerated on the device); the compact store is covered by
+    test_compact_3m_store_identical (its state is 2/3 of the 3-plane bytes)."""
+    from paper_2512_20064_b200.synthetic import build_synthetic
+    res, _ = build_synthetic(6, 256, 4, seed=3)
+    host, _ = build_synthetic(6, 256, 4, seed=3, host_stream_slots=2)
+    gen, _ = build_synthetic(6, 256, 4, seed=3, generated=True)
+    assert (res.gamma_store, host.gamma_store, gen.gamma_store) == ("resident", "host", "generated")
+    assert np.array_equal(host.sample(0, 300, 7), res.sample(0, 300, 7))
+    for s in (res, host, gen):
+        s.close()
